@@ -1,0 +1,152 @@
+/*
+ * kvrot_b200.h -- C ABI of the B200-native Hadamard-INT4 KV hot path.
+ *
+ * One shared library (libkvrot_b200.so, sm_100a) exports these symbols.  All
+ * buffers are DEVICE pointers unless a parameter says "host"; every entry
+ * point is asynchronous on `stream` (a cudaStream_t passed as void*), never
+ * allocates, never throws, and returns a kvr_status.  The only global state
+ * is a thread-local last-error string (kvr_last_error).
+ *
+ * The entry points replace, one for one, the reference's operator boundary
+ * `kvrot._kernels` (pkg/src/kvrot/_kernels/__init__.py:35-39) and the
+ * serving-path callers above it:
+ *
+ *   kvr_fwht_rows_f64        <- _kernels.fwht_rows        (_ref.py:22-40, _core.pyx:22-47)
+ *   kvr_pack_rows            <- _kernels.pack_rows        (_ref.py:43-45, _core.pyx:50-60)
+ *   kvr_unpack_rows          <- _kernels.unpack_rows      (_ref.py:48-54, _core.pyx:63-73)
+ *   kvr_quantize_rows_f64    <- _kernels.quantize_rows    (_ref.py:57-80, _core.pyx:76-130)
+ *   kvr_dequantize_rows_f64  <- _kernels.dequantize_rows  (_ref.py:83-95, _core.pyx:133-158)
+ *   kvr_block_rotate         <- rotation.apply_block_rotation / apply_inverse_rotation
+ *                               (rotation.py:118-159), hadamard.fwht_blocks (hadamard.py:70-89)
+ *   kvr_rotate_quantize_store<- cache.PageTable.append_token / append_tokens_two_pass
+ *                               (cache.py:235-317) incl. _rotate_token (cache.py:453-462)
+ *   kvr_dequantize_pages     <- cache.PageTable.read_token / read_sequence (cache.py:319-362)
+ *   kvr_paged_decode         <- attention.decode_step (attention.py:50-87)
+ */
+#ifndef KVROT_B200_H
+#define KVROT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KVR_ABI_VERSION 1
+#define KVR_MAX_HEAD_DIM 256
+
+typedef enum {
+  KVR_OK = 0,
+  KVR_ERR_SHAPE = 1,        /* maps to kvrot.errors.ShapeError            */
+  KVR_ERR_ORDER = 2,        /* maps to kvrot.errors.InvalidOrderError     */
+  KVR_ERR_UNSUPPORTED = 3,  /* configuration not built into this library  */
+  KVR_ERR_CUDA = 4,         /* CUDA runtime failure (see kvr_last_error)  */
+  KVR_ERR_ARG = 5           /* null pointer / negative size / bad enum    */
+} kvr_status;
+
+typedef enum { KVR_F64 = 0, KVR_F32 = 1, KVR_BF16 = 2, KVR_F16 = 3 } kvr_dtype;
+
+/* rotation.Targets (rotation.py:32-36) */
+typedef enum { KVR_KEYS_ONLY = 0, KVR_KEYS_AND_VALUES = 1 } kvr_targets;
+
+/* Device-side status bits written by the write kernel (never cleared by it). */
+#define KVR_FLAG_NONFINITE 1u   /* a K/V row held NaN/Inf -> NonFiniteInputError */
+
+/*
+ * The paged pool: `num_pages` page blobs of `page_bytes` each.  A blob's byte
+ * layout IS the reference `.kvpg` page record (cache.py:387-397, page shapes
+ * cache.py:103-114):
+ *     k_payload u8[P][H][d/2] | v_payload u8[P][H][d/2] |
+ *     k_scale f32[P][H] | k_zp u8[P][H] | v_scale f32[P][H] | v_zp u8[P][H]
+ * so exporting a page table is a page-ordered copy of blobs.
+ */
+typedef struct {
+  void* base;          /* device pointer, 16-byte aligned                  */
+  int64_t num_pages;
+  int32_t page_tokens; /* P  */
+  int32_t num_kv_heads;/* H  */
+  int32_t head_dim;    /* d  */
+  int32_t page_bytes;
+  int32_t off_k_payload, off_v_payload, off_k_scale, off_k_zp, off_v_scale, off_v_zp;
+} kvr_pool;
+
+/* Fill a kvr_pool for (P, H, d); returns the blob size via pool->page_bytes. */
+int kvr_pool_init(kvr_pool* pool, void* base, int64_t num_pages, int32_t page_tokens,
+                  int32_t num_kv_heads, int32_t head_dim);
+
+const char* kvr_last_error(void);
+int kvr_abi_version(void);
+/* Number of SMs of the current device (0 if no device). */
+int kvr_device_sms(void);
+
+/* ---- operator layer: kvrot._kernels on device buffers, bit-exact f64 ------- */
+int kvr_fwht_rows_f64(double* x, int64_t n, int32_t d, int32_t order, void* stream);
+int kvr_pack_rows(const uint8_t* nibbles, uint8_t* out, int64_t n, int32_t d, void* stream);
+int kvr_unpack_rows(const uint8_t* packed, uint8_t* out, int64_t n, int32_t logical_len,
+                    void* stream);
+int kvr_quantize_rows_f64(const double* x, int64_t n, int32_t d, uint8_t* packed, float* scale,
+                          uint8_t* zp, void* stream);
+int kvr_dequantize_rows_f64(const uint8_t* packed, const float* scale, const uint8_t* zp,
+                            int64_t n, int32_t logical_len, double* out, void* stream);
+
+/*
+ * Block rotation of rows (n, d): forward  y = x diag(s) H_blk   (inverse=0)
+ *                                inverse  y = x H_blk diag(s)   (inverse=1)
+ * in_dtype in {F64, F32, BF16, F16}; out_dtype in {F64, F32}.  F64->F64 is
+ * bit-identical to the reference.  sign_words (host): d/32 little-endian
+ * words, bit i set <=> signs[i] == -1; NULL means no sign flips.
+ */
+int kvr_block_rotate(const void* x, int32_t in_dtype, void* out, int32_t out_dtype, int64_t n,
+                     int32_t d, int32_t order, const uint32_t* sign_words, int32_t inverse,
+                     void* stream);
+
+/*
+ * K1: fused rotate -> token-wise INT4 quantize -> paged store.
+ *   k, v         : (n_tok, H, d) rows of in_dtype (F64/F32/BF16/F16), contiguous
+ *   slot_mapping : int64[n_tok] device, page_id * P + slot; negative = skip
+ *   rotate       : 0 = plain INT4 twin (no rotation anywhere)
+ *   targets      : KVR_KEYS_ONLY rotates K only; KVR_KEYS_AND_VALUES both
+ *   exact        : 1 = f64 arithmetic (bit-identical to the reference for any
+ *                  input); 0 = fast path (fp32 butterfly)
+ *   flags        : device uint32, KVR_FLAG_* bits OR-ed in (may be NULL)
+ */
+int kvr_rotate_quantize_store(const void* k, const void* v, int32_t in_dtype, int64_t n_tok,
+                              const int64_t* slot_mapping, const kvr_pool* pool,
+                              int32_t rot_order, int32_t rotate, int32_t targets,
+                              const uint32_t* sign_words, int32_t exact, uint32_t* flags,
+                              void* stream);
+
+/*
+ * K4: flatten-dequant of sequences into dense stored-space rows.
+ *   block_table : int32[batch][bt_stride] page ids; seq_lens: int32[batch]
+ *   k_out/v_out : (batch, max_len, H, d) of out_dtype (F64/F32/BF16); rows past a
+ *                 sequence's length are left untouched.
+ */
+int kvr_dequantize_pages(const kvr_pool* pool, const int32_t* block_table, int32_t bt_stride,
+                         const int32_t* seq_lens, int32_t batch, int32_t max_len, void* k_out,
+                         void* v_out, int32_t out_dtype, void* stream);
+
+/*
+ * K2+K3: paged INT4 decode attention, split-K over pages, rotated-frame query,
+ * inverse-rotated output for V (when rotate && targets == KEYS_AND_VALUES).
+ *   q        : (batch, num_q_heads, d) of q_dtype (F32/BF16/F16)
+ *   out      : (batch, num_q_heads, d) f32
+ *   num_splits <= 0 picks a split count for the device.  Workspace must be at
+ *   least kvr_decode_workspace_bytes(...) bytes and zero-filled once before
+ *   first use (the kernels leave the split counters at zero afterwards).
+ */
+size_t kvr_decode_workspace_bytes(int32_t batch, int32_t num_kv_heads, int32_t num_q_heads,
+                                  int32_t head_dim, int32_t num_splits);
+int kvr_decode_pick_splits(int32_t batch, int32_t num_kv_heads, int32_t max_seq_len,
+                           int32_t page_tokens);
+int kvr_paged_decode(const void* q, int32_t q_dtype, const kvr_pool* pool,
+                     const int32_t* block_table, int32_t bt_stride, const int32_t* seq_lens,
+                     int32_t batch, int32_t num_q_heads, int32_t max_seq_len, int32_t rot_order,
+                     int32_t rotate, int32_t targets, const uint32_t* sign_words, float* out,
+                     void* workspace, size_t workspace_bytes, int32_t num_splits, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVROT_B200_H */

@@ -1,0 +1,137 @@
+"""Decode attention over the paged INT4 cache (mirrors kvrot.attention, attention.py:24-115).
+
+`decode_step` keeps the reference signature (one request, numpy in / numpy
+out); `decode_batch` is the serving entry point (many sequences, CUDA tensors,
+no host synchronisation).  Both run the split-K paged decode kernel, which
+rotates the query into the stored-key frame in-kernel and inverse-rotates the
+output when values were stored rotated.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _kernels, _lib
+from .cache import PageTable
+from .errors import EmptySequenceError, NonFiniteInputError, ShapeError, UnsupportedConfigError
+from .layout import HeadLayout
+from .rotation import RotationSpec, Targets
+
+_Q_CODE = {torch.float32: _lib.KVR_F32, torch.bfloat16: _lib.KVR_BF16, torch.float16: _lib.KVR_F16}
+
+
+@dataclass(frozen=True)
+class DecodeRequest:
+    q: np.ndarray  # (num_q_heads, head_dim)
+    seq: int
+
+
+def _check_query(q, layout: HeadLayout) -> np.ndarray:
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    if q.shape != (layout.num_q_heads, layout.head_dim):
+        raise ShapeError(f"expected ({layout.num_q_heads}, {layout.head_dim}) query, got {q.shape}")
+    if not np.isfinite(q).all():
+        raise NonFiniteInputError("query contains NaN or Inf")
+    return q
+
+
+class DecodePlan:
+    """Device-resident decode arguments for a fixed batch of sequences
+    (block table, lengths, split count, workspace) so repeated steps issue one
+    kernel launch and no host<->device traffic."""
+
+    def __init__(self, table: PageTable, seqs: Sequence[int], num_splits: int = 0, extra_tokens: int = 0):
+        self.table = table
+        self.seqs = list(seqs)
+        lay = table.layout
+        for s in self.seqs:
+            if table.sequence_length(s) == 0 and extra_tokens == 0:
+                raise EmptySequenceError(f"sequence {s} has no tokens")
+        self.bt, self.lens, self.max_len = table.block_table(self.seqs)
+        self.max_len += extra_tokens
+        if num_splits <= 0:
+            num_splits = _lib.lib().kvr_decode_pick_splits(len(self.seqs), lay.num_kv_heads, self.max_len,
+                                                           lay.page_tokens)
+        self.splits = num_splits
+        self.ws = table.workspace(len(self.seqs), lay.num_q_heads, num_splits)
+
+    def refresh(self) -> None:
+        """Re-read block table and lengths after appends (small host->device copies)."""
+        bt, lens, max_len = self.table.block_table(self.seqs)
+        if bt.shape == self.bt.shape:
+            self.bt.copy_(bt)
+        else:
+            self.bt = bt
+        self.lens.copy_(lens)
+        self.max_len = max(self.max_len, max_len)
+
+    def run(self, q: torch.Tensor, spec: Optional[RotationSpec], out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        table, lay = self.table, self.table.layout
+        if q.dtype not in _Q_CODE:
+            q = q.float()
+        q = q.contiguous()
+        if tuple(q.shape) != (len(self.seqs), lay.num_q_heads, lay.head_dim):
+            raise ShapeError(f"expected ({len(self.seqs)}, {lay.num_q_heads}, {lay.head_dim}) queries, "
+                             f"got {tuple(q.shape)}")
+        if out is None:
+            out = torch.empty(q.shape, dtype=torch.float32, device=table.device)
+        rotate = spec is not None
+        if rotate:
+            if spec.order != lay.rot_order:
+                raise ShapeError(f"spec order {spec.order} != layout rot_order {lay.rot_order}")
+            if spec.learned is not None:
+                raise UnsupportedConfigError("learned rotations are not fused into the decode kernel (row f3)")
+        targets = _lib.KVR_KEYS_ONLY if (rotate and spec.targets is Targets.KEYS_ONLY) else _lib.KVR_KEYS_AND_VALUES
+        _lib.check(_lib.lib().kvr_paged_decode(
+            _kernels.ptr(q), _Q_CODE[q.dtype], ctypes.byref(table.desc), _kernels.ptr(self.bt), self.bt.shape[1],
+            _kernels.ptr(self.lens), len(self.seqs), lay.num_q_heads, self.max_len, spec.order if rotate else 1,
+            1 if rotate else 0, targets, spec.sign_words(lay.head_dim) if rotate else None, _kernels.ptr(out),
+            _kernels.ptr(self.ws), self.ws.numel(), self.splits, _kernels.stream_ptr()))
+        return out
+
+
+def decode_batch(q: torch.Tensor, table: PageTable, seqs: Sequence[int], spec: Optional[RotationSpec] = None,
+                 num_splits: int = 0) -> torch.Tensor:
+    """Serving decode: q (B, num_q_heads, d) CUDA tensor -> f32 (B, num_q_heads, d)."""
+    plan = DecodePlan(table, seqs, num_splits)
+    return plan.run(q.to(table.device), spec)
+
+
+def decode_step(req: DecodeRequest, table: PageTable, spec: Optional[RotationSpec] = None) -> np.ndarray:
+    """One query token over one cached sequence; returns (num_q_heads, d) f64 (attention.py:50-87)."""
+    layout = table.layout
+    q = _check_query(req.q, layout)
+    if table.sequence_length(req.seq) == 0:
+        raise EmptySequenceError(f"sequence {req.seq} has no tokens")
+    qt = torch.from_numpy(q).to(table.device, dtype=torch.float32).reshape(1, *q.shape)
+    out = DecodePlan(table, [req.seq]).run(qt, spec)
+    return out[0].double().cpu().numpy()
+
+
+def decode_step_fp(q, flat_k, flat_v, layout: HeadLayout) -> np.ndarray:
+    """Full-precision decode over flat (t, kv_heads, d) arrays (attention.py:90-115), f64 on the device."""
+    q = _check_query(q, layout)
+    k = np.asarray(flat_k, dtype=np.float64)
+    v = np.asarray(flat_v, dtype=np.float64)
+    if k.ndim != 3 or k.shape[1:] != (layout.num_kv_heads, layout.head_dim):
+        raise ShapeError(f"expected (t, kv_heads, dim) keys, got {k.shape}")
+    if k.shape != v.shape:
+        raise ShapeError(f"key/value shape mismatch: {k.shape} vs {v.shape}")
+    if k.shape[0] == 0:
+        raise EmptySequenceError("no cached tokens")
+    dev = _kernels.device()
+    qt = torch.from_numpy(q).to(dev)
+    kt = torch.from_numpy(k).to(dev)
+    vt = torch.from_numpy(v).to(dev)
+    g = layout.group_size
+    kq = kt.repeat_interleave(g, dim=1)  # (t, nq, d)
+    vq = vt.repeat_interleave(g, dim=1)
+    logits = torch.einsum("thd,hd->ht", kq, qt) * (1.0 / math.sqrt(layout.head_dim))
+    w = torch.softmax(logits, dim=-1)
+    return torch.einsum("ht,thd->hd", w, vq).cpu().numpy()

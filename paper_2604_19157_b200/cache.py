@@ -1,0 +1,451 @@
+"""Paged INT4 KV cache in B200 HBM (mirrors kvrot.cache.PageTable, cache.py:122-450).
+
+Device layout: one uint8 tensor [num_pages, page_bytes]; each row is a page blob
+whose byte layout is the reference `.kvpg` page record
+    k_payload u8[P][H][d/2] | v_payload | k_scale f32[P][H] | k_zp u8[P][H] | v_scale | v_zp
+(cache.py:103-114, 387-397), so `dump` is a header plus a page-ordered copy.
+
+Host side: the same lowest-id-first page heap and per-sequence page lists as
+the reference (cache.py:150-151, 211-223), so page ids -- and therefore dump
+bytes -- match it token for token.  All data movement and arithmetic (rotate,
+quantize, store, dequantize) happens in the native library.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import heapq
+import json
+import struct
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _kernels, _lib
+from .errors import (CapacityExceededError, ConfigError, NonFiniteInputError, SequenceNotFoundError, ShapeError,
+                     UnsupportedConfigError)
+from .layout import HeadLayout
+from .rotation import RotationSpec, Targets
+
+BF16 = "bf16"
+INT4 = "int4"
+
+_DUMP_MAGIC = b"KVPG"
+_DUMP_VERSION = 1
+
+_TORCH_DTYPE_CODE = {torch.float64: _lib.KVR_F64, torch.float32: _lib.KVR_F32, torch.bfloat16: _lib.KVR_BF16,
+                     torch.float16: _lib.KVR_F16}
+
+
+def float_to_bf16_bits(x) -> np.ndarray:
+    """RNE f32 -> bf16 storage bits (cache.py:43-47)."""
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+
+
+def bf16_bits_to_float(bits) -> np.ndarray:
+    """bf16 storage bits -> f64 (cache.py:50-53)."""
+    return (np.asarray(bits).astype(np.uint32) << np.uint32(16)).view(np.float32).astype(np.float64)
+
+
+def token_bytes(layout: HeadLayout, precision: str, include_sidecar: bool = False) -> int:
+    """Bytes of one token's K+V (cache.py:56-68)."""
+    h, d = layout.num_kv_heads, layout.head_dim
+    if precision == BF16:
+        return 4 * h * d
+    if precision == INT4:
+        return h * d + (10 * h if include_sidecar else 0)
+    raise ConfigError(f"unknown precision {precision!r}")
+
+
+def capacity_tokens(budget_bytes: int, layout: HeadLayout, precision: str) -> int:
+    """Token capacity at BF16-token granularity; INT4 holds exactly 4x (cache.py:71-86)."""
+    if budget_bytes < 0:
+        raise ConfigError(f"budget_bytes={budget_bytes} must be >= 0")
+    base = budget_bytes // token_bytes(layout, BF16)
+    if precision == BF16:
+        return base
+    if precision == INT4:
+        return 4 * base
+    raise ConfigError(f"unknown precision {precision!r}")
+
+
+def page_bytes(layout: HeadLayout) -> int:
+    """Size of one INT4 page blob (== one .kvpg page record)."""
+    return layout.page_tokens * layout.num_kv_heads * (layout.head_dim + 10)
+
+
+class PageAllocator:
+    """Host-side page bookkeeping of a pool: lowest-id-first free heap and
+    per-sequence page lists (cache.py:150-151, 157-186, 211-223).  Pure Python,
+    no device state, so the allocation order is testable without a GPU."""
+
+    def __init__(self, num_pages: int, page_tokens: int) -> None:
+        self.num_pages = num_pages
+        self.page_tokens = page_tokens
+        self.free = list(range(num_pages))
+        heapq.heapify(self.free)
+        self.seq_pages: dict[int, list[int]] = {}
+        self.seq_len: dict[int, int] = {}
+
+    def require(self, seq: int) -> None:
+        if seq not in self.seq_pages:
+            raise SequenceNotFoundError(f"unknown sequence {seq}")
+
+    def create(self, seq: int) -> None:
+        if seq in self.seq_pages:
+            raise ConfigError(f"sequence {seq} already exists")
+        self.seq_pages[seq] = []
+        self.seq_len[seq] = 0
+
+    def release(self, seq: int) -> int:
+        self.require(seq)
+        pages = self.seq_pages.pop(seq)
+        self.seq_len.pop(seq)
+        for pid in pages:
+            heapq.heappush(self.free, pid)
+        return len(pages)
+
+    def plan(self, seqs: Sequence[int]) -> tuple[np.ndarray, list[int]]:
+        """Slot ids (page * P + slot) for appending one token per entry of `seqs`
+        (in order), taking new pages lowest id first.  All-or-nothing: on
+        exhaustion nothing is committed.  Returns (slots, freshly taken pages)."""
+        P = self.page_tokens
+        lens: dict[int, int] = {}
+        new_pages: dict[int, list[int]] = {}
+        free = list(self.free)
+        slots = np.empty(len(seqs), dtype=np.int64)
+        fresh = []
+        for n, seq in enumerate(seqs):
+            self.require(seq)
+            t = lens.get(seq, self.seq_len[seq])
+            if t % P == 0:
+                if not free:
+                    raise CapacityExceededError(f"page pool exhausted ({self.num_pages} pages)")
+                pid = heapq.heappop(free)
+                new_pages.setdefault(seq, []).append(pid)
+                fresh.append(pid)
+            owned = self.seq_pages[seq]
+            idx = t // P
+            pid = owned[idx] if idx < len(owned) else new_pages[seq][idx - len(owned)]
+            slots[n] = pid * P + t % P
+            lens[seq] = t + 1
+        self.free = free
+        for seq, pids in new_pages.items():
+            self.seq_pages[seq].extend(pids)
+        for seq, t in lens.items():
+            self.seq_len[seq] = t
+        return slots, fresh
+
+
+class PageTable:
+    """GPU page pool + per-sequence page lists (drop-in for kvrot.cache.PageTable)."""
+
+    def __init__(self, layout: HeadLayout, precision: str = INT4, budget_bytes: Optional[int] = None,
+                 num_pages: Optional[int] = None, device=None) -> None:
+        if precision not in (INT4, BF16):
+            raise ConfigError(f"unknown precision {precision!r}")
+        if (budget_bytes is None) == (num_pages is None):
+            raise ConfigError("specify exactly one of budget_bytes or num_pages")
+        if precision == BF16:
+            raise UnsupportedConfigError("BF16 pages are not built in this round (SURVEY row f2); use INT4")
+        self.layout = layout
+        self.precision = precision
+        self.budget_bytes = budget_bytes
+        if num_pages is None:
+            num_pages = capacity_tokens(budget_bytes, layout, precision) // layout.page_tokens
+        if num_pages < 0:
+            raise ConfigError(f"num_pages={num_pages} must be >= 0")
+        self.num_pages = num_pages
+        self.device = torch.device(device) if device is not None else _kernels.device()
+        self.page_bytes = page_bytes(layout)
+        self.pool = torch.zeros((max(num_pages, 1), self.page_bytes), dtype=torch.uint8, device=self.device)
+        self.desc = _lib.KvrPool()
+        _lib.check(_lib.lib().kvr_pool_init(ctypes.byref(self.desc), ctypes.c_void_p(self.pool.data_ptr()),
+                                            num_pages, layout.page_tokens, layout.num_kv_heads, layout.head_dim))
+        assert self.desc.page_bytes == self.page_bytes
+        self.flags = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.alloc = PageAllocator(num_pages, layout.page_tokens)
+        self._ws = None
+
+    # reference-compatible views of the allocator state (cache.py:149-153)
+    @property
+    def _seq_pages(self) -> dict:
+        return self.alloc.seq_pages
+
+    @property
+    def _seq_len(self) -> dict:
+        return self.alloc.seq_len
+
+    @property
+    def _free(self) -> list:
+        return self.alloc.free
+
+    # -- sequence management (cache.py:157-186) --------------------------------
+    def create_sequence(self, seq: int) -> None:
+        self.alloc.create(seq)
+
+    def has_sequence(self, seq: int) -> bool:
+        return seq in self.alloc.seq_pages
+
+    def sequence_length(self, seq: int) -> int:
+        self._require(seq)
+        return self.alloc.seq_len[seq]
+
+    def sequence_ids(self) -> list[int]:
+        return sorted(self.alloc.seq_pages)
+
+    def sequence_pages(self, seq: int) -> list[int]:
+        self._require(seq)
+        return list(self.alloc.seq_pages[seq])
+
+    def free_sequence(self, seq: int) -> int:
+        return self.alloc.release(seq)
+
+    def _require(self, seq: int) -> None:
+        self.alloc.require(seq)
+
+    # -- capacity (cache.py:190-207) ----------------------------------------------
+    def capacity_tokens(self, precision: Optional[str] = None) -> int:
+        if self.budget_bytes is None:
+            return self.num_pages * self.layout.page_tokens
+        return capacity_tokens(self.budget_bytes, self.layout, precision or self.precision)
+
+    @property
+    def used_tokens(self) -> int:
+        return sum(self._seq_len.values())
+
+    @property
+    def free_pages(self) -> int:
+        return len(self._free)
+
+    @property
+    def allocated_pages(self) -> int:
+        return self.num_pages - len(self._free)
+
+    # -- slot allocation --------------------------------------------------------
+    def _plan_slots(self, seqs: Sequence[int]) -> tuple[np.ndarray, list[int]]:
+        return self.alloc.plan(seqs)
+
+    def _zero_pages(self, pids: list[int]) -> None:
+        # the reference hands out freshly zeroed pages (cache.py:103-119)
+        if pids:
+            idx = torch.tensor(pids, dtype=torch.long).to(self.device, non_blocking=True)
+            self.pool.index_fill_(0, idx, 0)
+
+    # -- writes -----------------------------------------------------------------
+    def _store(self, k: torch.Tensor, v: torch.Tensor, slots: np.ndarray, spec: Optional[RotationSpec],
+               exact: bool) -> None:
+        n = k.shape[0]
+        slot_t = torch.from_numpy(slots).to(self.device, non_blocking=True)
+        rotate = spec is not None
+        if rotate:
+            if spec.order != self.layout.rot_order:
+                raise ShapeError(f"spec order {spec.order} != layout rot_order {self.layout.rot_order}")
+            if spec.learned is not None:
+                raise UnsupportedConfigError("learned rotations are not fused into the write kernel (row f3)")
+        targets = _lib.KVR_KEYS_ONLY if (rotate and spec.targets is Targets.KEYS_ONLY) else _lib.KVR_KEYS_AND_VALUES
+        words = spec.sign_words(self.layout.head_dim) if rotate else None
+        _lib.check(_lib.lib().kvr_rotate_quantize_store(
+            _kernels.ptr(k), _kernels.ptr(v), _TORCH_DTYPE_CODE[k.dtype], n, _kernels.ptr(slot_t),
+            ctypes.byref(self.desc), spec.order if rotate else 1, 1 if rotate else 0, targets, words,
+            1 if exact else 0, _kernels.ptr(self.flags), _kernels.stream_ptr()))
+
+    def _check_kv_host(self, k, v, ndim: int):
+        h, d = self.layout.num_kv_heads, self.layout.head_dim
+        k = np.ascontiguousarray(k, dtype=np.float64)
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        shape = (h, d) if ndim == 2 else (None, h, d)
+        if k.ndim != ndim or v.shape != k.shape or k.shape[-2:] != (h, d):
+            raise ShapeError(f"expected {shape} k and v, got {k.shape}, {v.shape}")
+        if not (np.isfinite(k).all() and np.isfinite(v).all()):
+            raise NonFiniteInputError("k/v contain NaN or Inf")
+        return k, v
+
+    def append_token(self, seq: int, k, v, spec: Optional[RotationSpec] = None) -> int:
+        """Fused rotate-quantize-write of one token; returns its index (cache.py:235-270).
+        f64 inputs take the bit-exact f64 kernel path."""
+        self._require(seq)
+        k, v = self._check_kv_host(k, v, 2)
+        first = self._seq_len[seq]
+        slots, fresh = self._plan_slots([seq])
+        self._zero_pages(fresh)
+        kt = torch.from_numpy(k).to(self.device).reshape(1, *k.shape)
+        vt = torch.from_numpy(v).to(self.device).reshape(1, *v.shape)
+        self._store(kt, vt, slots, spec, exact=True)
+        return first
+
+    def append_tokens_two_pass(self, seq: int, ks, vs, spec: Optional[RotationSpec] = None) -> int:
+        """Unfused route (cache.py:272-317): materialise the rotated stacks for all
+        tokens, then quantize + write them.  Must equal the fused path bitwise."""
+        self._require(seq)
+        ks, vs = self._check_kv_host(ks, vs, 3)
+        first = self._seq_len[seq]
+        t = ks.shape[0]
+        if t == 0:
+            return first
+        slots, fresh = self._plan_slots([seq] * t)
+        self._zero_pages(fresh)
+        h, d = self.layout.num_kv_heads, self.layout.head_dim
+        kt = torch.from_numpy(ks).to(self.device)
+        vt = torch.from_numpy(vs).to(self.device)
+        if spec is not None:
+            from .rotation import apply_block_rotation, value_branch_spec
+
+            kt = apply_block_rotation(kt.reshape(t * h, d), self.layout, spec).reshape(t, h, d)
+            vspec = value_branch_spec(spec)
+            if vspec is not None:
+                vt = apply_block_rotation(vt.reshape(t * h, d), self.layout, vspec).reshape(t, h, d)
+        self._store(kt.contiguous(), vt.contiguous(), slots, None, exact=True)
+        return first
+
+    def append_batch(self, seqs: Sequence[int], k, v, spec: Optional[RotationSpec] = None,
+                     exact: Optional[bool] = None, check: bool = True) -> np.ndarray:
+        """Serving write: token n of (k, v) [n, H, d] is appended to sequence seqs[n].
+        bf16/fp16 CUDA tensors take the fast K1 kernel; f64 takes the exact one.
+        Returns the slot ids.  check=False defers the non-finite check (see check_flags)."""
+        kt = k if isinstance(k, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(k))
+        vt = v if isinstance(v, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(v))
+        kt = kt.to(self.device, non_blocking=True).contiguous()
+        vt = vt.to(self.device, non_blocking=True).contiguous()
+        h, d = self.layout.num_kv_heads, self.layout.head_dim
+        if kt.shape != vt.shape or kt.ndim != 3 or tuple(kt.shape[1:]) != (h, d) or kt.shape[0] != len(seqs):
+            raise ShapeError(f"expected ({len(seqs)}, {h}, {d}) k and v, got {tuple(kt.shape)}, {tuple(vt.shape)}")
+        if kt.dtype not in _TORCH_DTYPE_CODE or vt.dtype != kt.dtype:
+            raise ShapeError(f"unsupported k/v dtype {kt.dtype}/{vt.dtype}")
+        if exact is None:
+            exact = kt.dtype == torch.float64
+        slots, fresh = self._plan_slots(list(seqs))
+        self._zero_pages(fresh)
+        self._store(kt, vt, slots, spec, exact=exact)
+        if check:
+            self.check_flags()
+        return slots
+
+    def store_slots(self, k: torch.Tensor, v: torch.Tensor, slots: torch.Tensor, spec: Optional[RotationSpec] = None,
+                    exact: bool = False) -> None:
+        """Engine-level write (no host bookkeeping, no sync): token n of the CUDA
+        tensors k, v [n, H, d] goes to the precomputed slot id slots[n]
+        (page * P + slot, int64, negative = skip), like a serving engine's
+        slot_mapping.  The caller owns the slot assignment."""
+        if slots.dtype != torch.int64 or not slots.is_cuda:
+            raise ShapeError("slots must be an int64 CUDA tensor")
+        rotate = spec is not None
+        targets = _lib.KVR_KEYS_ONLY if (rotate and spec.targets is Targets.KEYS_ONLY) else _lib.KVR_KEYS_AND_VALUES
+        _lib.check(_lib.lib().kvr_rotate_quantize_store(
+            _kernels.ptr(k), _kernels.ptr(v), _TORCH_DTYPE_CODE[k.dtype], k.shape[0], _kernels.ptr(slots),
+            ctypes.byref(self.desc), spec.order if rotate else 1, 1 if rotate else 0, targets,
+            spec.sign_words(self.layout.head_dim) if rotate else None, 1 if exact else 0, _kernels.ptr(self.flags),
+            _kernels.stream_ptr()))
+
+    def check_flags(self) -> None:
+        """Raise NonFiniteInputError if any write since the last check saw NaN/Inf."""
+        f = int(self.flags.item())
+        if f & _lib.KVR_FLAG_NONFINITE:
+            self.flags.zero_()
+            raise NonFiniteInputError("k/v contained NaN or Inf (rows were not written)")
+
+    # -- reads (cache.py:319-362) -------------------------------------------------
+    def block_table(self, seqs: Sequence[int]) -> tuple[torch.Tensor, torch.Tensor, int]:
+        """Device (int32 [B, max_pages] page ids, int32 [B] lengths, max length)."""
+        rows = [self._seq_pages[s] for s in seqs]
+        width = max(1, max((len(r) for r in rows), default=1))
+        bt = np.zeros((len(seqs), width), dtype=np.int32)
+        for i, r in enumerate(rows):
+            bt[i, :len(r)] = r
+        lens = np.array([self._seq_len[s] for s in seqs], dtype=np.int32)
+        return (torch.from_numpy(bt).to(self.device), torch.from_numpy(lens).to(self.device),
+                int(lens.max()) if len(lens) else 0)
+
+    def read_sequence_device(self, seqs: Sequence[int], dtype: torch.dtype = torch.float64):
+        """Flatten-dequant of several sequences -> (k, v) [B, max_len, H, d] on the device."""
+        for s in seqs:
+            self._require(s)
+        bt, lens, max_len = self.block_table(seqs)
+        h, d = self.layout.num_kv_heads, self.layout.head_dim
+        k = torch.zeros((len(seqs), max_len, h, d), dtype=dtype, device=self.device)
+        v = torch.zeros_like(k)
+        code = {torch.float64: _lib.KVR_F64, torch.float32: _lib.KVR_F32, torch.bfloat16: _lib.KVR_BF16}[dtype]
+        _lib.check(_lib.lib().kvr_dequantize_pages(ctypes.byref(self.desc), _kernels.ptr(bt), bt.shape[1],
+                                                   _kernels.ptr(lens), len(seqs), max_len, _kernels.ptr(k),
+                                                   _kernels.ptr(v), code, _kernels.stream_ptr()))
+        return k, v
+
+    def read_sequence(self, seq: int) -> tuple[np.ndarray, np.ndarray]:
+        """Dequantized stored-space (t, H, d) f64 stacks (cache.py:337-362)."""
+        k, v = self.read_sequence_device([seq], torch.float64)
+        return k[0].cpu().numpy(), v[0].cpu().numpy()
+
+    def read_token(self, seq: int, t: int) -> tuple[np.ndarray, np.ndarray]:
+        self._require(seq)
+        if not 0 <= t < self._seq_len[seq]:
+            raise IndexError(f"token {t} out of range for sequence of {self._seq_len[seq]}")
+        k, v = self.read_sequence(seq)
+        return k[t], v[t]
+
+    # -- serialization (cache.py:366-450) ------------------------------------------
+    def _header(self) -> bytes:
+        lay = self.layout
+        header = {
+            "version": _DUMP_VERSION,
+            "precision": self.precision,
+            "budget_bytes": self.budget_bytes,
+            "num_pages": self.num_pages,
+            "layout": {"num_q_heads": lay.num_q_heads, "num_kv_heads": lay.num_kv_heads, "head_dim": lay.head_dim,
+                       "rot_order": lay.rot_order, "page_tokens": lay.page_tokens},
+            "sequences": {str(s): {"pages": self._seq_pages[s], "length": self._seq_len[s]}
+                          for s in sorted(self._seq_pages)},
+        }
+        return json.dumps(header, sort_keys=True, separators=(",", ":")).encode()
+
+    def dump_bytes(self) -> bytes:
+        blob = self._header()
+        pids = sorted(p for ps in self._seq_pages.values() for p in ps)
+        pages = b""
+        if pids:
+            idx = torch.tensor(pids, dtype=torch.long, device=self.device)
+            pages = self.pool.index_select(0, idx).cpu().numpy().tobytes()
+        return _DUMP_MAGIC + struct.pack("<II", _DUMP_VERSION, len(blob)) + blob + pages
+
+    def dump(self, path) -> None:
+        with open(path, "wb") as f:
+            f.write(self.dump_bytes())
+
+    @classmethod
+    def load(cls, path, device=None) -> "PageTable":
+        with open(path, "rb") as f:
+            raw = f.read()
+        if raw[:4] != _DUMP_MAGIC:
+            raise ConfigError(f"{path} is not a page dump")
+        version, hlen = struct.unpack("<II", raw[4:12])
+        if version != _DUMP_VERSION:
+            raise ConfigError(f"unsupported dump version {version}")
+        header = json.loads(raw[12:12 + hlen].decode())
+        lay = header["layout"]
+        layout = HeadLayout(num_q_heads=lay["num_q_heads"], num_kv_heads=lay["num_kv_heads"],
+                            head_dim=lay["head_dim"], rot_order=lay["rot_order"], page_tokens=lay["page_tokens"])
+        table = cls(layout, precision=header["precision"], num_pages=header["num_pages"], device=device)
+        table.budget_bytes = header["budget_bytes"]
+        allocated = sorted(p for s in header["sequences"].values() for p in s["pages"])
+        body = np.frombuffer(raw, dtype=np.uint8, offset=12 + hlen)
+        if body.size != len(allocated) * table.page_bytes:
+            raise ConfigError(f"{path}: page payload size mismatch")
+        if allocated:
+            blobs = torch.from_numpy(body.reshape(len(allocated), table.page_bytes).copy()).to(table.device)
+            table.pool.index_copy_(0, torch.tensor(allocated, dtype=torch.long, device=table.device), blobs)
+        taken = set(allocated)
+        table.alloc.free = [p for p in range(table.num_pages) if p not in taken]
+        heapq.heapify(table.alloc.free)
+        for seq_str, entry in sorted(header["sequences"].items(), key=lambda kv: int(kv[0])):
+            table.alloc.seq_pages[int(seq_str)] = list(entry["pages"])
+            table.alloc.seq_len[int(seq_str)] = entry["length"]
+        return table
+
+    # -- decode workspace --------------------------------------------------------------
+    def workspace(self, batch: int, num_q_heads: int, splits: int) -> torch.Tensor:
+        need = _lib.lib().kvr_decode_workspace_bytes(batch, self.layout.num_kv_heads, num_q_heads,
+                                                     self.layout.head_dim, max(splits, 1))
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
+        return self._ws

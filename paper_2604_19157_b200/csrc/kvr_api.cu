@@ -1,0 +1,267 @@
+// extern "C" boundary of libkvrot_b200.so: validation, dispatch, error text.
+// See include/kvrot_b200.h for the contract and the reference interface each
+// entry point replaces.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "kvr_common.cuh"
+#include "kvr_internal.h"
+
+using namespace kvr;
+
+static thread_local char g_err[512] = "";
+
+static int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+static int check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(KVR_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return KVR_OK;
+}
+
+static bool pow2(int x) { return x >= 1 && (x & (x - 1)) == 0; }
+
+static int check_order(int d, int order) {
+  if (!pow2(order)) return fail(KVR_ERR_ORDER, "order=%d is not a power of two", order);
+  if (d % order != 0) return fail(KVR_ERR_ORDER, "order=%d does not divide dim=%d", order, d);
+  return KVR_OK;
+}
+
+static int make_signs(const uint32_t* words, int d, Signs& s, int& has) {
+  memset(&s, 0, sizeof(s));
+  has = words != nullptr;
+  if (!has) return KVR_OK;
+  if (d > KVR_MAX_HEAD_DIM) return fail(KVR_ERR_UNSUPPORTED, "signs for head_dim %d > %d", d, KVR_MAX_HEAD_DIM);
+  memcpy(s.w, words, sizeof(uint32_t) * ((d + 31) / 32));
+  return KVR_OK;
+}
+
+static int to_pool(const kvr_pool* in, Pool& p) {
+  if (!in || !in->base) return fail(KVR_ERR_ARG, "null pool");
+  p.base = reinterpret_cast<uint8_t*>(in->base);
+  p.num_pages = in->num_pages;
+  p.P = in->page_tokens;
+  p.H = in->num_kv_heads;
+  p.d = in->head_dim;
+  p.page_bytes = in->page_bytes;
+  p.off_kp = in->off_k_payload;
+  p.off_vp = in->off_v_payload;
+  p.off_ks = in->off_k_scale;
+  p.off_kz = in->off_k_zp;
+  p.off_vs = in->off_v_scale;
+  p.off_vz = in->off_v_zp;
+  return KVR_OK;
+}
+
+CUresult kvr_encode_tensor_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows,
+                                  uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_rows,
+                                  CUtensorMapSwizzle swz) {
+  typedef CUresult (*encode_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static encode_fn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !f)
+      return CUDA_ERROR_NOT_FOUND;
+    fn = reinterpret_cast<encode_fn>(f);
+  }
+  const cuuint64_t dims[2] = {inner, rows < 1 ? 1 : rows};
+  const cuuint64_t strides[1] = {row_stride_bytes};
+  const cuuint32_t box[2] = {box_inner, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
+
+int kvr_num_sms() {
+  static int sms = -1;
+  if (sms < 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) !=
+                                                   cudaSuccess) {
+      cudaGetLastError();
+      sms = 0;
+    }
+  }
+  return sms;
+}
+
+extern "C" {
+
+const char* kvr_last_error(void) { return g_err; }
+int kvr_abi_version(void) { return KVR_ABI_VERSION; }
+int kvr_device_sms(void) { return kvr_num_sms(); }
+
+int kvr_pool_init(kvr_pool* pool, void* base, int64_t num_pages, int32_t page_tokens, int32_t num_kv_heads,
+                  int32_t head_dim) {
+  if (!pool) return fail(KVR_ERR_ARG, "null pool");
+  if (page_tokens < 1 || num_kv_heads < 1 || head_dim < 2 || (head_dim & 1) || num_pages < 0)
+    return fail(KVR_ERR_SHAPE, "bad pool geometry P=%d H=%d d=%d", page_tokens, num_kv_heads, head_dim);
+  const int64_t cells = (int64_t)page_tokens * num_kv_heads;
+  pool->base = base;
+  pool->num_pages = num_pages;
+  pool->page_tokens = page_tokens;
+  pool->num_kv_heads = num_kv_heads;
+  pool->head_dim = head_dim;
+  // .kvpg page record order: k_payload, v_payload, k_scale, k_zp, v_scale, v_zp (cache.py:391-397)
+  pool->off_k_payload = 0;
+  pool->off_v_payload = (int32_t)(cells * (head_dim / 2));
+  pool->off_k_scale = (int32_t)(2 * cells * (head_dim / 2));
+  pool->off_k_zp = pool->off_k_scale + (int32_t)(4 * cells);
+  pool->off_v_scale = pool->off_k_zp + (int32_t)cells;
+  pool->off_v_zp = pool->off_v_scale + (int32_t)(4 * cells);
+  pool->page_bytes = pool->off_v_zp + (int32_t)cells;
+  return KVR_OK;
+}
+
+int kvr_fwht_rows_f64(double* x, int64_t n, int32_t d, int32_t order, void* stream) {
+  if (n < 0 || d < 1) return fail(KVR_ERR_SHAPE, "bad shape (%lld, %d)", (long long)n, d);
+  if (int rc = check_order(d, order)) return rc;
+  if (n == 0 || order == 1) return KVR_OK;
+  if (!x) return fail(KVR_ERR_ARG, "null x");
+  if (d > 6144) return fail(KVR_ERR_UNSUPPORTED, "dim %d > 6144", d);
+  kvr_launch_fwht_f64(x, n, d, order, (cudaStream_t)stream);
+  return check_launch("fwht_rows_f64");
+}
+
+int kvr_pack_rows(const uint8_t* nibbles, uint8_t* out, int64_t n, int32_t d, void* stream) {
+  if (n < 0 || d < 0 || (d & 1)) return fail(KVR_ERR_SHAPE, "pack_rows needs even d, got %d", d);
+  if (n == 0 || d == 0) return KVR_OK;
+  kvr_launch_pack(nibbles, out, n, d, (cudaStream_t)stream);
+  return check_launch("pack_rows");
+}
+
+int kvr_unpack_rows(const uint8_t* packed, uint8_t* out, int64_t n, int32_t logical_len, void* stream) {
+  if (n < 0 || logical_len < 0 || (logical_len & 1))
+    return fail(KVR_ERR_SHAPE, "unpack_rows needs even logical_len, got %d", logical_len);
+  if (n == 0 || logical_len == 0) return KVR_OK;
+  kvr_launch_unpack(packed, out, n, logical_len, (cudaStream_t)stream);
+  return check_launch("unpack_rows");
+}
+
+int kvr_quantize_rows_f64(const double* x, int64_t n, int32_t d, uint8_t* packed, float* scale, uint8_t* zp,
+                          void* stream) {
+  if (n < 0 || d < 2 || (d & 1)) return fail(KVR_ERR_SHAPE, "expected (n, even d) rows, got d=%d", d);
+  if (n == 0) return KVR_OK;
+  if (d > 6144) return fail(KVR_ERR_UNSUPPORTED, "dim %d > 6144", d);
+  kvr_launch_quantize_f64(x, n, d, packed, scale, zp, (cudaStream_t)stream);
+  return check_launch("quantize_rows_f64");
+}
+
+int kvr_dequantize_rows_f64(const uint8_t* packed, const float* scale, const uint8_t* zp, int64_t n,
+                            int32_t logical_len, double* out, void* stream) {
+  if (n < 0 || logical_len < 0 || (logical_len & 1)) return fail(KVR_ERR_SHAPE, "bad logical_len %d", logical_len);
+  if (n == 0 || logical_len == 0) return KVR_OK;
+  kvr_launch_dequantize_f64(packed, scale, zp, n, logical_len, out, (cudaStream_t)stream);
+  return check_launch("dequantize_rows_f64");
+}
+
+int kvr_block_rotate(const void* x, int32_t in_dtype, void* out, int32_t out_dtype, int64_t n, int32_t d,
+                     int32_t order, const uint32_t* sign_words, int32_t inverse, void* stream) {
+  if (n < 0 || d < 1) return fail(KVR_ERR_SHAPE, "bad shape");
+  if (int rc = check_order(d, order)) return rc;
+  if (d > 6144) return fail(KVR_ERR_UNSUPPORTED, "dim %d > 6144", d);
+  Signs s;
+  int has;
+  if (int rc = make_signs(sign_words, d, s, has)) return rc;
+  if (n == 0) return KVR_OK;
+  int rc = kvr_launch_block_rotate(x, in_dtype, out, out_dtype, n, d, order, s, has, inverse, (cudaStream_t)stream);
+  if (rc) return fail(rc, "block_rotate: unsupported dtype combination (%d -> %d)", in_dtype, out_dtype);
+  return check_launch("block_rotate");
+}
+
+int kvr_rotate_quantize_store(const void* k, const void* v, int32_t in_dtype, int64_t n_tok,
+                              const int64_t* slot_mapping, const kvr_pool* pool, int32_t rot_order, int32_t rotate,
+                              int32_t targets, const uint32_t* sign_words, int32_t exact, uint32_t* flags,
+                              void* stream) {
+  Pool pl;
+  if (int rc = to_pool(pool, pl)) return rc;
+  if (n_tok < 0) return fail(KVR_ERR_SHAPE, "n_tok < 0");
+  if (n_tok == 0) return KVR_OK;
+  if (!k || !v || !slot_mapping) return fail(KVR_ERR_ARG, "null k/v/slot_mapping");
+  if (in_dtype < KVR_F64 || in_dtype > KVR_F16) return fail(KVR_ERR_ARG, "bad dtype %d", in_dtype);
+  if (rotate) {
+    if (int rc = check_order(pl.d, rot_order)) return rc;
+  } else {
+    rot_order = 1;
+  }
+  Signs s;
+  int has;
+  if (int rc = make_signs(rotate ? sign_words : nullptr, pl.d, s, has)) return rc;
+  const int rot_k = rotate ? 1 : 0;
+  const int rot_v = (rotate && targets == KVR_KEYS_AND_VALUES) ? 1 : 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = KVR_ERR_UNSUPPORTED;
+  if (!exact) rc = kvr_launch_store_fast(k, v, in_dtype, n_tok, slot_mapping, pl, rot_order, rot_k, rot_v, s, has,
+                                         flags, st);
+  if (rc == KVR_ERR_UNSUPPORTED) {
+    if (pl.d > 6144) return fail(KVR_ERR_UNSUPPORTED, "dim %d > 6144", pl.d);
+    rc = kvr_launch_store_exact(k, v, in_dtype, n_tok, slot_mapping, pl, rot_order, rot_k, rot_v, s, has, flags, st);
+  }
+  if (rc) return fail(rc, "rotate_quantize_store: launch failed (%d)", rc);
+  return check_launch("rotate_quantize_store");
+}
+
+int kvr_dequantize_pages(const kvr_pool* pool, const int32_t* block_table, int32_t bt_stride,
+                         const int32_t* seq_lens, int32_t batch, int32_t max_len, void* k_out, void* v_out,
+                         int32_t out_dtype, void* stream) {
+  Pool pl;
+  if (int rc = to_pool(pool, pl)) return rc;
+  if (batch < 0 || max_len < 0) return fail(KVR_ERR_SHAPE, "bad batch/max_len");
+  if (batch == 0 || max_len == 0) return KVR_OK;
+  int rc = kvr_launch_dequant_pages(pl, block_table, bt_stride, seq_lens, batch, max_len, k_out, v_out, out_dtype,
+                                    (cudaStream_t)stream);
+  if (rc) return fail(rc, "dequantize_pages: unsupported out dtype %d", out_dtype);
+  return check_launch("dequantize_pages");
+}
+
+size_t kvr_decode_workspace_bytes(int32_t batch, int32_t num_kv_heads, int32_t num_q_heads, int32_t head_dim,
+                                  int32_t num_splits) {
+  return kvr_decode_ws_bytes(batch, num_kv_heads, num_q_heads, head_dim, num_splits);
+}
+
+int kvr_decode_pick_splits(int32_t batch, int32_t num_kv_heads, int32_t max_seq_len, int32_t page_tokens) {
+  return kvr_pick_splits(batch, num_kv_heads, max_seq_len, page_tokens);
+}
+
+int kvr_paged_decode(const void* q, int32_t q_dtype, const kvr_pool* pool, const int32_t* block_table,
+                     int32_t bt_stride, const int32_t* seq_lens, int32_t batch, int32_t num_q_heads,
+                     int32_t max_seq_len, int32_t rot_order, int32_t rotate, int32_t targets,
+                     const uint32_t* sign_words, float* out, void* workspace, size_t workspace_bytes,
+                     int32_t num_splits, void* stream) {
+  Pool pl;
+  if (int rc = to_pool(pool, pl)) return rc;
+  if (batch < 0 || num_q_heads < 1 || num_q_heads % pl.H != 0)
+    return fail(KVR_ERR_SHAPE, "num_q_heads=%d is not a multiple of num_kv_heads=%d", num_q_heads, pl.H);
+  if (batch == 0) return KVR_OK;
+  if (q_dtype != KVR_F32 && q_dtype != KVR_BF16 && q_dtype != KVR_F16)
+    return fail(KVR_ERR_ARG, "q dtype %d unsupported (F32/BF16/F16)", q_dtype);
+  if (rotate) {
+    if (int rc = check_order(pl.d, rot_order)) return rc;
+  } else {
+    rot_order = 1;
+  }
+  Signs s;
+  int has;
+  if (int rc = make_signs(rotate ? sign_words : nullptr, pl.d, s, has)) return rc;
+  const int rot_v = (rotate && targets == KVR_KEYS_AND_VALUES) ? 1 : 0;
+  int rc = kvr_launch_decode(q, q_dtype, pl, block_table, bt_stride, seq_lens, batch, num_q_heads, max_seq_len,
+                             rot_order, rotate, rot_v, s, has, out, workspace, workspace_bytes, num_splits,
+                             (cudaStream_t)stream);
+  if (rc == KVR_ERR_ARG) return fail(rc, "decode workspace too small");
+  if (rc) return fail(rc, "paged_decode: unsupported geometry (d=%d, P=%d, G=%d)", pl.d, pl.P, num_q_heads / pl.H);
+  return check_launch("paged_decode");
+}
+
+}  // extern "C"

@@ -1,0 +1,132 @@
+// Shared device helpers for the sm_100a Hadamard-INT4 KV kernels.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/kvrot_b200.h"
+
+#define KVR_DEV __device__ __forceinline__
+
+namespace kvr {
+
+// Rotation signs: bit i of w[i/32] set <=> signs[i] == -1 (rotation.py:81-101).
+struct Signs {
+  uint32_t w[KVR_MAX_HEAD_DIM / 32];
+};
+
+// Pool geometry passed by value to kernels (mirror of kvr_pool).
+struct Pool {
+  uint8_t* base;
+  int64_t num_pages;
+  int32_t P, H, d, page_bytes;
+  int32_t off_kp, off_vp, off_ks, off_kz, off_vs, off_vz;
+};
+
+KVR_DEV bool sign_bit(const Signs& s, int i) { return (s.w[i >> 5] >> (i & 31)) & 1u; }
+
+// ---- f64 reference arithmetic (_ref.py:16-19) ------------------------------
+KVR_DEV double round_half_away(double t) { return copysign(floor(fabs(t) + 0.5), t); }
+
+// ---- f32x2 packed arithmetic (FADD2 / FFMA2 on sm_100a) --------------------
+KVR_DEV unsigned long long pk(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+KVR_DEV void upk(unsigned long long r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+KVR_DEV unsigned long long add2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+KVR_DEV unsigned long long sub2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+// fl_RM(a*b + c) elementwise: the magic-number floor (exact product-sum, one rounding)
+KVR_DEV unsigned long long fma2_rm(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rm.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+KVR_DEV float max3_nan(float a, float b, float c) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+KVR_DEV float min3_nan(float a, float b, float c) {
+  float r;
+  asm("min.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+KVR_DEV uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+// ---- mbarrier + TMA (cp.async.bulk.tensor) ---------------------------------
+KVR_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+KVR_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+KVR_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+KVR_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+KVR_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+KVR_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+KVR_DEV void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t x, int32_t y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+KVR_DEV void prefetch_tensormap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+// ---- warp helpers ----------------------------------------------------------
+KVR_DEV float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+KVR_DEV float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename T>
+KVR_DEV double load_as_f64(const T* p, int64_t i);
+template <>
+KVR_DEV double load_as_f64<double>(const double* p, int64_t i) { return p[i]; }
+template <>
+KVR_DEV double load_as_f64<float>(const float* p, int64_t i) { return (double)p[i]; }
+template <>
+KVR_DEV double load_as_f64<__nv_bfloat16>(const __nv_bfloat16* p, int64_t i) {
+  return (double)__bfloat162float(p[i]);
+}
+template <>
+KVR_DEV double load_as_f64<__half>(const __half* p, int64_t i) { return (double)__half2float(p[i]); }
+
+}  // namespace kvr

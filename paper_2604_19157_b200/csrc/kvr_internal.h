@@ -1,0 +1,46 @@
+// Host-side launcher declarations shared between the .cu translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/kvrot_b200.h"
+
+namespace kvr {
+struct Signs;
+struct Pool;
+}  // namespace kvr
+
+int kvr_launch_fwht_f64(double* x, int64_t n, int d, int order, cudaStream_t st);
+int kvr_launch_quantize_f64(const double* x, int64_t n, int d, uint8_t* p, float* s, uint8_t* z, cudaStream_t st);
+int kvr_launch_dequantize_f64(const uint8_t* p, const float* s, const uint8_t* z, int64_t n, int len, double* out,
+                              cudaStream_t st);
+int kvr_launch_pack(const uint8_t* nib, uint8_t* out, int64_t n, int d, cudaStream_t st);
+int kvr_launch_unpack(const uint8_t* p, uint8_t* out, int64_t n, int len, cudaStream_t st);
+int kvr_launch_block_rotate(const void* x, int in_dtype, void* out, int out_dtype, int64_t n, int d, int order,
+                            const kvr::Signs& s, int has, int inv, cudaStream_t st);
+int kvr_launch_store_exact(const void* k, const void* v, int in_dtype, int64_t n_tok, const int64_t* slots,
+                           const kvr::Pool& pool, int order, int rot_k, int rot_v, const kvr::Signs& s, int has,
+                           uint32_t* flags, cudaStream_t st);
+int kvr_launch_dequant_pages(const kvr::Pool& pool, const int32_t* bt, int bt_stride, const int32_t* lens, int batch,
+                             int max_len, void* k_out, void* v_out, int out_dtype, cudaStream_t st);
+
+// Fast serving-path write (bf16/fp16 rows, head_dim 128): returns KVR_ERR_UNSUPPORTED
+// when the configuration has no specialised kernel (caller falls back to the exact path).
+int kvr_launch_store_fast(const void* k, const void* v, int in_dtype, int64_t n_tok, const int64_t* slots,
+                          const kvr::Pool& pool, int order, int rot_k, int rot_v, const kvr::Signs& s, int has,
+                          uint32_t* flags, cudaStream_t st);
+
+// Decode (kvr_decode.cu)
+size_t kvr_decode_ws_bytes(int batch, int H, int nq, int d, int splits);
+int kvr_pick_splits(int batch, int H, int max_len, int P);
+int kvr_launch_decode(const void* q, int q_dtype, const kvr::Pool& pool, const int32_t* bt, int bt_stride,
+                      const int32_t* lens, int batch, int nq, int max_len, int order, int rotate, int rot_v,
+                      const kvr::Signs& s, int has, float* out, void* ws, size_t ws_bytes, int splits,
+                      cudaStream_t st);
+
+// Tensor-map encoder resolved through the runtime (no -lcuda link dependency).
+CUresult kvr_encode_tensor_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows,
+                                  uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_rows,
+                                  CUtensorMapSwizzle swz);
+int kvr_num_sms();

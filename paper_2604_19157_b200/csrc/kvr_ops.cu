@@ -1,0 +1,388 @@
+// Operator-layer kernels (kvrot._kernels on the GPU) and the generic f64
+// ("exact") variants of the rotation, the fused write and the flatten-dequant.
+//
+// Everything here computes in IEEE f64 with the reference's operation order,
+// so results are bit-identical to kvrot's numpy/Cython backends:
+//   fwht_rows        _ref.py:22-40  / _core.pyx:22-47
+//   quantize_rows    _ref.py:57-80  / _core.pyx:76-130
+//   dequantize_rows  _ref.py:83-95  / _core.pyx:133-158
+//   pack/unpack      _ref.py:43-54  / _core.pyx:50-73
+// These kernels are warp-per-row and latency-oriented; the bandwidth-bound
+// serving path (bf16/fp16 rows, head_dim 128) lives in kvr_store_fast.cu and
+// kvr_decode.cu.
+#include "kvr_common.cuh"
+#include "kvr_internal.h"
+
+namespace kvr {
+
+// In-place f64 block butterfly over a row held in shared memory by one warp.
+// Pair (i, i+half) -> (a+b, a-b) for half = 1, 2, ..., order/2, then * inv.
+KVR_DEV void warp_fwht_f64(double* s, int d, int order, int lane) {
+  if (order == 1) return;
+  const int npairs = d >> 1;
+  for (int half = 1; half < order; half <<= 1) {
+    for (int p = lane; p < npairs; p += 32) {
+      const int blk = p / (order >> 1), q = p % (order >> 1);
+      const int i = blk * order + (q / half) * 2 * half + (q % half);
+      const double a = s[i], b = s[i + half];
+      s[i] = a + b;
+      s[i + half] = a - b;
+    }
+    __syncwarp();
+  }
+  const double inv = 1.0 / sqrt((double)order);
+  for (int i = lane; i < d; i += 32) s[i] = s[i] * inv;
+  __syncwarp();
+}
+
+// Quantize one f64 row held in smem (one warp) -> packed bytes / scale / zp.
+// Writes packed[0 .. d/2), *scale, *zp.  Bit-exact with _ref.quantize_rows.
+KVR_DEV void warp_quantize_f64(const double* s, int d, int lane, uint8_t* packed, float* scale, uint8_t* zp) {
+  double mn = s[0], mx = s[0];
+  for (int i = lane; i < d; i += 32) {
+    const double v = s[i];
+    mn = v < mn ? v : mn;
+    mx = v > mx ? v : mx;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double a = __shfl_xor_sync(0xffffffffu, mn, o);
+    const double b = __shfl_xor_sync(0xffffffffu, mx, o);
+    mn = a < mn ? a : mn;
+    mx = b > mx ? b : mx;
+  }
+  const float s32 = (float)((mx - mn) / 15.0);
+  if (s32 == 0.0f) {
+    for (int m = lane; m < (d >> 1); m += 32) packed[m] = 0;
+    if (lane == 0) {
+      *scale = (float)mn;
+      *zp = 0xFF;
+    }
+    return;
+  }
+  const double s64 = (double)s32;
+  double z = round_half_away(-mn / s64);
+  z = z < 0.0 ? 0.0 : (z > 15.0 ? 15.0 : z);
+  for (int m = lane; m < (d >> 1); m += 32) {
+    double lo = round_half_away(s[2 * m] / s64) + z;
+    double hi = round_half_away(s[2 * m + 1] / s64) + z;
+    lo = lo < 0.0 ? 0.0 : (lo > 15.0 ? 15.0 : lo);
+    hi = hi < 0.0 ? 0.0 : (hi > 15.0 ? 15.0 : hi);
+    packed[m] = (uint8_t)((uint32_t)lo | ((uint32_t)hi << 4));
+  }
+  if (lane == 0) {
+    *scale = s32;
+    *zp = (uint8_t)z;
+  }
+}
+
+__global__ void fwht_rows_f64_kernel(double* x, int64_t n, int d, int order) {
+  extern __shared__ double sm_f64[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double* s = sm_f64 + (size_t)wib * d;
+  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; row < n;
+       row += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    double* xr = x + row * d;
+    for (int i = lane; i < d; i += 32) s[i] = xr[i];
+    __syncwarp();
+    warp_fwht_f64(s, d, order, lane);
+    for (int i = lane; i < d; i += 32) xr[i] = s[i];
+    __syncwarp();
+  }
+}
+
+__global__ void quantize_rows_f64_kernel(const double* x, int64_t n, int d, uint8_t* packed, float* scale,
+                                         uint8_t* zp) {
+  extern __shared__ double sm_f64[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double* s = sm_f64 + (size_t)wib * d;
+  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; row < n;
+       row += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    for (int i = lane; i < d; i += 32) s[i] = x[row * d + i];
+    __syncwarp();
+    warp_quantize_f64(s, d, lane, packed + row * (d >> 1), scale + row, zp + row);
+    __syncwarp();
+  }
+}
+
+__global__ void dequantize_rows_f64_kernel(const uint8_t* packed, const float* scale, const uint8_t* zp, int64_t n,
+                                           int len, double* out) {
+  const int half = len >> 1;
+  const int64_t total = n * half;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = idx / half;
+    const int m = (int)(idx % half);
+    const double s64 = (double)scale[row];
+    const uint8_t z = zp[row];
+    double* o = out + row * len + 2 * m;
+    if (z == 0xFF) {
+      o[0] = s64;
+      o[1] = s64;
+    } else {
+      const uint8_t b = packed[row * half + m];
+      const double zf = (double)z;
+      o[0] = s64 * ((double)(b & 0x0F) - zf);
+      o[1] = s64 * ((double)(b >> 4) - zf);
+    }
+  }
+}
+
+__global__ void pack_rows_kernel(const uint8_t* nib, uint8_t* out, int64_t n, int d) {
+  const int64_t total = n * (d >> 1);
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = idx / (d >> 1);
+    const int m = (int)(idx % (d >> 1));
+    out[idx] = (uint8_t)(nib[row * d + 2 * m] | (nib[row * d + 2 * m + 1] << 4));
+  }
+}
+
+__global__ void unpack_rows_kernel(const uint8_t* packed, uint8_t* out, int64_t n, int len) {
+  const int half = len >> 1;
+  const int64_t total = n * half;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = idx / half;
+    const int m = (int)(idx % half);
+    const uint8_t b = packed[row * half + m];
+    out[row * len + 2 * m] = b & 0x0F;
+    out[row * len + 2 * m + 1] = b >> 4;
+  }
+}
+
+// Rotation of rows in f64 (exact for f64 input), any input dtype, f64/f32 out.
+template <typename TIn, typename TOut>
+__global__ void block_rotate_kernel(const TIn* x, TOut* out, int64_t n, int d, int order, Signs signs, int has_signs,
+                                    int inverse) {
+  extern __shared__ double sm_f64[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double* s = sm_f64 + (size_t)wib * d;
+  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; row < n;
+       row += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    for (int i = lane; i < d; i += 32) {
+      double v = load_as_f64<TIn>(x, row * d + i);
+      if (has_signs && !inverse && sign_bit(signs, i)) v = v * -1.0;
+      s[i] = v;
+    }
+    __syncwarp();
+    warp_fwht_f64(s, d, order, lane);
+    for (int i = lane; i < d; i += 32) {
+      double v = s[i];
+      if (has_signs && inverse && sign_bit(signs, i)) v = v * -1.0;
+      out[row * d + i] = (TOut)v;
+    }
+    __syncwarp();
+  }
+}
+
+// Generic exact fused write: warp per (token, head, side) row, f64 arithmetic.
+// Row order: all K rows (token-major, head-minor) then all V rows.
+template <typename TIn>
+__global__ void store_exact_kernel(const TIn* k, const TIn* v, int64_t n_tok, const int64_t* slots, Pool pool,
+                                   int order, int rot_k, int rot_v, Signs signs, int has_signs, uint32_t* flags) {
+  extern __shared__ double sm_f64[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int d = pool.d, H = pool.H;
+  double* s = sm_f64 + (size_t)wib * d;
+  const int64_t rows = n_tok * H;
+  for (int64_t r2 = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; r2 < 2 * rows;
+       r2 += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    const int side = r2 >= rows;  // 0 = K, 1 = V
+    const int64_t row = side ? r2 - rows : r2;
+    const int64_t tok = row / H;
+    const int head = (int)(row % H);
+    const int64_t slot = slots[tok];
+    if (slot < 0) continue;
+    const TIn* src = side ? v : k;
+    const int rot = side ? rot_v : rot_k;
+    bool finite = true;
+    for (int i = lane; i < d; i += 32) {
+      double val = load_as_f64<TIn>(src, row * d + i);
+      finite &= isfinite(val);
+      if (rot && has_signs && sign_bit(signs, i)) val = val * -1.0;
+      s[i] = val;
+    }
+    finite = __all_sync(0xffffffffu, finite);
+    __syncwarp();
+    if (!finite) {
+      if (lane == 0 && flags) atomicOr(flags, (uint32_t)KVR_FLAG_NONFINITE);
+      continue;
+    }
+    if (rot) warp_fwht_f64(s, d, order, lane);
+    const int64_t page = slot / pool.P;
+    const int sl = (int)(slot % pool.P);
+    uint8_t* blob = pool.base + page * (int64_t)pool.page_bytes;
+    const int idx = sl * H + head;
+    uint8_t* payload = blob + (side ? pool.off_vp : pool.off_kp) + (int64_t)idx * (d >> 1);
+    float* sc = reinterpret_cast<float*>(blob + (side ? pool.off_vs : pool.off_ks)) + idx;
+    uint8_t* zp = blob + (side ? pool.off_vz : pool.off_kz) + idx;
+    warp_quantize_f64(s, d, lane, payload, sc, zp);
+    __syncwarp();
+  }
+}
+
+// Flatten-dequant (cache.py:337-362): thread per (row, byte) -> two outputs.
+template <typename TOut>
+__global__ void dequant_pages_kernel(Pool pool, const int32_t* bt, int bt_stride, const int32_t* lens, int batch,
+                                     int max_len, TOut* k_out, TOut* v_out) {
+  const int d = pool.d, H = pool.H, half = d >> 1;
+  const int64_t per_side = (int64_t)batch * max_len * H * half;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < 2 * per_side;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int side = idx >= per_side;
+    int64_t r = side ? idx - per_side : idx;
+    const int m = (int)(r % half);
+    r /= half;
+    const int head = (int)(r % H);
+    r /= H;
+    const int t = (int)(r % max_len);
+    const int b = (int)(r / max_len);
+    if (t >= lens[b]) continue;
+    const int page = bt[(int64_t)b * bt_stride + t / pool.P];
+    const int sl = t % pool.P;
+    const uint8_t* blob = pool.base + (int64_t)page * pool.page_bytes;
+    const int i2 = sl * H + head;
+    const uint8_t byte = blob[(side ? pool.off_vp : pool.off_kp) + (int64_t)i2 * half + m];
+    const float sc = reinterpret_cast<const float*>(blob + (side ? pool.off_vs : pool.off_ks))[i2];
+    const uint8_t z = blob[(side ? pool.off_vz : pool.off_kz) + i2];
+    TOut* o = (side ? v_out : k_out) + ((((int64_t)b * max_len + t) * H + head) * d) + 2 * m;
+    if (z == 0xFF) {
+      o[0] = (TOut)sc;
+      o[1] = (TOut)sc;
+    } else {
+      if constexpr (sizeof(TOut) == 8) {
+        const double s64 = (double)sc, zf = (double)z;
+        o[0] = (TOut)(s64 * ((double)(byte & 0x0F) - zf));
+        o[1] = (TOut)(s64 * ((double)(byte >> 4) - zf));
+      } else {
+        const float zf = (float)z;
+        o[0] = (TOut)(sc * ((float)(byte & 0x0F) - zf));
+        o[1] = (TOut)(sc * ((float)(byte >> 4) - zf));
+      }
+    }
+  }
+}
+
+}  // namespace kvr
+
+// ============================ host launchers ================================
+using namespace kvr;
+
+static int grid_for(int64_t work, int per_block) {
+  int64_t g = (work + per_block - 1) / per_block;
+  const int cap = 148 * 32;
+  return (int)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+static int warps_per_block_for(int d) {
+  // smem per warp = d doubles; keep <= 48 KB per block (no opt-in needed)
+  int w = 8;
+  while (w > 1 && (size_t)w * d * 8 > 48 * 1024) w >>= 1;
+  return w;
+}
+
+int kvr_launch_fwht_f64(double* x, int64_t n, int d, int order, cudaStream_t st) {
+  const int w = warps_per_block_for(d);
+  fwht_rows_f64_kernel<<<grid_for(n, w), 32 * w, (size_t)w * d * 8, st>>>(x, n, d, order);
+  return 0;
+}
+
+int kvr_launch_quantize_f64(const double* x, int64_t n, int d, uint8_t* p, float* s, uint8_t* z, cudaStream_t st) {
+  const int w = warps_per_block_for(d);
+  quantize_rows_f64_kernel<<<grid_for(n, w), 32 * w, (size_t)w * d * 8, st>>>(x, n, d, p, s, z);
+  return 0;
+}
+
+int kvr_launch_dequantize_f64(const uint8_t* p, const float* s, const uint8_t* z, int64_t n, int len, double* out,
+                              cudaStream_t st) {
+  dequantize_rows_f64_kernel<<<grid_for(n * (len / 2), 256), 256, 0, st>>>(p, s, z, n, len, out);
+  return 0;
+}
+
+int kvr_launch_pack(const uint8_t* nib, uint8_t* out, int64_t n, int d, cudaStream_t st) {
+  pack_rows_kernel<<<grid_for(n * (d / 2), 256), 256, 0, st>>>(nib, out, n, d);
+  return 0;
+}
+
+int kvr_launch_unpack(const uint8_t* p, uint8_t* out, int64_t n, int len, cudaStream_t st) {
+  unpack_rows_kernel<<<grid_for(n * (len / 2), 256), 256, 0, st>>>(p, out, n, len);
+  return 0;
+}
+
+template <typename TIn>
+static int rotate_dispatch_out(const void* x, void* out, int out_dtype, int64_t n, int d, int order, const Signs& s,
+                               int has, int inv, cudaStream_t st) {
+  const int w = warps_per_block_for(d);
+  const size_t sm = (size_t)w * d * 8;
+  if (out_dtype == KVR_F64)
+    block_rotate_kernel<TIn, double><<<grid_for(n, w), 32 * w, sm, st>>>((const TIn*)x, (double*)out, n, d, order, s,
+                                                                         has, inv);
+  else if (out_dtype == KVR_F32)
+    block_rotate_kernel<TIn, float><<<grid_for(n, w), 32 * w, sm, st>>>((const TIn*)x, (float*)out, n, d, order, s,
+                                                                        has, inv);
+  else
+    return KVR_ERR_UNSUPPORTED;
+  return 0;
+}
+
+int kvr_launch_block_rotate(const void* x, int in_dtype, void* out, int out_dtype, int64_t n, int d, int order,
+                            const Signs& s, int has, int inv, cudaStream_t st) {
+  switch (in_dtype) {
+    case KVR_F64: return rotate_dispatch_out<double>(x, out, out_dtype, n, d, order, s, has, inv, st);
+    case KVR_F32: return rotate_dispatch_out<float>(x, out, out_dtype, n, d, order, s, has, inv, st);
+    case KVR_BF16: return rotate_dispatch_out<__nv_bfloat16>(x, out, out_dtype, n, d, order, s, has, inv, st);
+    case KVR_F16: return rotate_dispatch_out<__half>(x, out, out_dtype, n, d, order, s, has, inv, st);
+  }
+  return KVR_ERR_ARG;
+}
+
+int kvr_launch_store_exact(const void* k, const void* v, int in_dtype, int64_t n_tok, const int64_t* slots,
+                           const Pool& pool, int order, int rot_k, int rot_v, const Signs& s, int has,
+                           uint32_t* flags, cudaStream_t st) {
+  const int w = warps_per_block_for(pool.d);
+  const size_t sm = (size_t)w * pool.d * 8;
+  const int g = grid_for(2 * n_tok * pool.H, w);
+  switch (in_dtype) {
+    case KVR_F64:
+      store_exact_kernel<double><<<g, 32 * w, sm, st>>>((const double*)k, (const double*)v, n_tok, slots, pool, order,
+                                                        rot_k, rot_v, s, has, flags);
+      break;
+    case KVR_F32:
+      store_exact_kernel<float><<<g, 32 * w, sm, st>>>((const float*)k, (const float*)v, n_tok, slots, pool, order,
+                                                       rot_k, rot_v, s, has, flags);
+      break;
+    case KVR_BF16:
+      store_exact_kernel<__nv_bfloat16><<<g, 32 * w, sm, st>>>((const __nv_bfloat16*)k, (const __nv_bfloat16*)v,
+                                                               n_tok, slots, pool, order, rot_k, rot_v, s, has, flags);
+      break;
+    case KVR_F16:
+      store_exact_kernel<__half><<<g, 32 * w, sm, st>>>((const __half*)k, (const __half*)v, n_tok, slots, pool, order,
+                                                        rot_k, rot_v, s, has, flags);
+      break;
+    default: return KVR_ERR_ARG;
+  }
+  return 0;
+}
+
+int kvr_launch_dequant_pages(const Pool& pool, const int32_t* bt, int bt_stride, const int32_t* lens, int batch,
+                             int max_len, void* k_out, void* v_out, int out_dtype, cudaStream_t st) {
+  const int64_t work = 2LL * batch * max_len * pool.H * (pool.d / 2);
+  const int g = grid_for(work, 256);
+  switch (out_dtype) {
+    case KVR_F64:
+      dequant_pages_kernel<double><<<g, 256, 0, st>>>(pool, bt, bt_stride, lens, batch, max_len, (double*)k_out,
+                                                      (double*)v_out);
+      break;
+    case KVR_F32:
+      dequant_pages_kernel<float><<<g, 256, 0, st>>>(pool, bt, bt_stride, lens, batch, max_len, (float*)k_out,
+                                                     (float*)v_out);
+      break;
+    case KVR_BF16:
+      dequant_pages_kernel<__nv_bfloat16><<<g, 256, 0, st>>>(pool, bt, bt_stride, lens, batch, max_len,
+                                                             (__nv_bfloat16*)k_out, (__nv_bfloat16*)v_out);
+      break;
+    default: return KVR_ERR_ARG;
+  }
+  return 0;
+}

@@ -1,0 +1,141 @@
+"""Rotation specs and block-diagonal Hadamard rotation (mirrors kvrot.rotation, transform part).
+
+Row convention as in the reference (rotation.py:118-159):
+    forward  x -> x diag(s) H_blk R      inverse  x -> x R^T H_blk diag(s)
+The block butterfly runs in the native library in f64 (bit-identical to the
+reference).  The optional learned factor R (Hessian calibration, out of scope
+for the serving kernels) is applied as an f64 GEMM on the device.
+"""
+
+from __future__ import annotations
+
+import enum
+from dataclasses import dataclass, replace
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _kernels, _lib
+from .errors import InvalidOrderError, ShapeError
+from .hadamard import block_hadamard_matrix
+from .layout import HeadLayout, is_power_of_two
+
+
+class Targets(enum.Enum):
+    KEYS_ONLY = "keys_only"
+    KEYS_AND_VALUES = "keys_and_values"
+
+
+@dataclass(frozen=True)
+class RotationSpec:
+    """Hadamard block order, optional +-1 signs, optional learned orthogonal R, targets."""
+
+    order: int
+    signs: Optional[np.ndarray] = None
+    learned: Optional[np.ndarray] = None
+    targets: Targets = Targets.KEYS_AND_VALUES
+    learned_values: bool = False
+
+    def __post_init__(self) -> None:
+        if not is_power_of_two(self.order):
+            raise InvalidOrderError(f"order={self.order} is not a power of two")
+        if self.signs is not None:
+            s = np.array(self.signs, dtype=np.float64, copy=True).reshape(np.shape(self.signs))
+            if s.ndim != 1:
+                raise ShapeError("signs must be a vector")
+            if not np.all(np.abs(s) == 1.0):
+                raise ShapeError("signs entries must be +-1")
+            s.setflags(write=False)
+            object.__setattr__(self, "signs", s)
+        if self.learned is not None:
+            r = np.array(self.learned, dtype=np.float64, copy=True)
+            if r.ndim != 2 or r.shape[0] != r.shape[1]:
+                raise ShapeError(f"learned rotation must be square, got {r.shape}")
+            dev = np.abs(r.T @ r - np.eye(r.shape[0])).max()
+            if dev > 1e-6:
+                raise ShapeError(f"learned rotation not orthogonal (max dev {dev:.2e})")
+            r.setflags(write=False)
+            object.__setattr__(self, "learned", r)
+
+    def sign_words(self, head_dim: int):
+        return _lib.sign_words(self.signs, head_dim)
+
+
+def make_signs(seed: int, layer: int, head_dim: int, order: int) -> np.ndarray:
+    """Deterministic +-1 vector, one Philox stream per (seed, layer, block) (rotation.py:81-101).
+
+    The sign vector is a parameter of the rotation (computed once per layer),
+    so it is generated with numpy's Philox exactly as the reference does.
+    """
+    if not is_power_of_two(order) or head_dim % order:
+        raise InvalidOrderError(f"order={order} does not divide head_dim={head_dim}")
+    if not 0 <= layer < (1 << 24):
+        raise ShapeError(f"layer={layer} outside supported range [0, 2^24)")
+    blocks = []
+    for blk in range(head_dim // order):
+        key = np.array([seed & ((1 << 64) - 1), (0x5164 << 48) | (layer << 24) | blk], dtype=np.uint64)
+        draws = np.random.Generator(np.random.Philox(key=key)).integers(0, 2, size=order)
+        blocks.append(draws * 2.0 - 1.0)
+    return np.concatenate(blocks).astype(np.float64)
+
+
+def _check_spec_layout(spec: RotationSpec, layout: HeadLayout) -> None:
+    d = layout.head_dim
+    if spec.order != layout.rot_order:
+        raise ShapeError(f"spec order {spec.order} != layout rot_order {layout.rot_order}")
+    if d % spec.order:
+        raise InvalidOrderError(f"order={spec.order} does not divide head_dim={d}")
+    if spec.signs is not None and spec.signs.shape != (d,):
+        raise ShapeError(f"signs length {spec.signs.shape} != head_dim {d}")
+    if spec.learned is not None and spec.learned.shape != (d, d):
+        raise ShapeError(f"learned shape {spec.learned.shape} != ({d}, {d})")
+
+
+def _rotate(x, layout: HeadLayout, spec: RotationSpec, inverse: bool):
+    is_np = not isinstance(x, torch.Tensor)
+    t = _kernels.to_device(np.asarray(x, dtype=np.float64) if is_np else x, torch.float64)
+    if t.ndim != 2 or t.shape[1] != layout.head_dim:
+        raise ShapeError(f"expected (n, {layout.head_dim}) rows, got {tuple(t.shape)}")
+    _check_spec_layout(spec, layout)
+    n, d = t.shape
+    learned = None if spec.learned is None else torch.from_numpy(np.asarray(spec.learned)).to(t.device)
+    if inverse and learned is not None:
+        t = (t @ learned.T).contiguous()
+    out = torch.empty_like(t)
+    _lib.check(_lib.lib().kvr_block_rotate(_kernels.ptr(t), _lib.KVR_F64, _kernels.ptr(out), _lib.KVR_F64, n, d,
+                                           spec.order, spec.sign_words(d), 1 if inverse else 0,
+                                           _kernels.stream_ptr()))
+    if not inverse and learned is not None:
+        out = out @ learned
+    return out.cpu().numpy() if is_np else out
+
+
+def apply_block_rotation(x, layout: HeadLayout, spec: RotationSpec):
+    """Rotate rows: x diag(signs) H_blk learned (rotation.py:118-142)."""
+    return _rotate(x, layout, spec, inverse=False)
+
+
+def apply_inverse_rotation(x, layout: HeadLayout, spec: RotationSpec):
+    """Map rotated rows back: x learned^T H_blk diag(signs) (rotation.py:145-159)."""
+    return _rotate(x, layout, spec, inverse=True)
+
+
+def value_branch_spec(spec: RotationSpec) -> Optional[RotationSpec]:
+    """Value-side transform: None for KEYS_ONLY; learned part only if learned_values (rotation.py:162-168)."""
+    if spec.targets is Targets.KEYS_ONLY:
+        return None
+    if spec.learned is not None and not spec.learned_values:
+        return replace(spec, learned=None)
+    return spec
+
+
+def compose_transform(spec: RotationSpec, layout: HeadLayout) -> np.ndarray:
+    """Dense T = diag(signs) H_blk learned (rotation.py:171-184)."""
+    _check_spec_layout(spec, layout)
+    t = block_hadamard_matrix(layout.head_dim, spec.order)
+    if spec.signs is not None:
+        t = spec.signs[:, None] * t
+    if spec.learned is not None:
+        t = t @ spec.learned
+    return t

@@ -1,0 +1,67 @@
+"""The C-ABI library builds for sm_100a, loads without a GPU and exports
+every entry point include/kvrot_b200.h declares (no compute calls here)."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "kvrot_b200.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(kvr_[a-z0-9_]+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def libpath():
+    from paper_2604_19157_b200 import build
+
+    return build.build()
+
+
+def test_header_symbols_exported(libpath):
+    lib = ctypes.CDLL(libpath)
+    syms = declared_symbols()
+    assert len(syms) >= 15
+    for name in syms:
+        assert hasattr(lib, name), name
+    from paper_2604_19157_b200 import _lib
+
+    assert sorted(_lib.EXPORTED) == syms
+
+
+def test_cubin_is_sm100a_with_tma_and_mma(libpath):
+    out = subprocess.run(["cuobjdump", "-sass", libpath], capture_output=True, text=True, check=True).stdout
+    assert "sm_100a" in out or "SM100" in out.upper()
+    assert "UTMALDG" in out          # TMA tile loads in the write kernel
+    assert "HMMA" in out             # tensor-core decode
+    assert "FADD2" in out or "FFMA2" in out  # packed f32x2 butterfly / quantizer
+
+
+def test_pool_init_layout(libpath):
+    from paper_2604_19157_b200 import _lib
+
+    lib = _lib.lib()
+    pool = _lib.KvrPool()
+    assert lib.kvr_pool_init(ctypes.byref(pool), None, 10, 16, 8, 128) == 0
+    # .kvpg page record: 16*8*64*2 payload + 16*8*(4+1)*2 sidecar = 17664 B (cache.py:56-68)
+    assert pool.page_bytes == 17664
+    assert (pool.off_k_payload, pool.off_v_payload, pool.off_k_scale, pool.off_k_zp, pool.off_v_scale,
+            pool.off_v_zp) == (0, 8192, 16384, 16896, 17024, 17536)
+    assert lib.kvr_abi_version() == 1
+    assert lib.kvr_decode_workspace_bytes(1, 8, 32, 128, 4) > 0
+
+
+def test_errors_without_device(libpath):
+    from paper_2604_19157_b200 import _lib
+
+    lib = _lib.lib()
+    # argument validation happens before any CUDA call
+    assert lib.kvr_fwht_rows_f64(None, 4, 24, 16, None) == 2  # InvalidOrder: 16 does not divide 24
+    assert b"does not divide" in lib.kvr_last_error()
+    assert lib.kvr_quantize_rows_f64(None, 4, 7, None, None, None, None) == 1
