@@ -134,7 +134,8 @@ def run_ours(args, rank, world, local_rank):
     sets = []
     chunk = 8192
     for r in range(R):
-        t = PageTable(layout, num_pages=(L + 1 + P - 1) // P, device=dev)
+        # headroom for the e2e steps (which append real tokens through the API)
+        t = PageTable(layout, num_pages=(L + 1 + P - 1) // P + 64, device=dev)
         t.create_sequence(0)
         for c0 in range(0, L, chunk):
             n = min(chunk, L - c0)
@@ -159,10 +160,11 @@ def run_ours(args, rank, world, local_rank):
     def k2(s, sp=spec):
         s["plan"].run(s["q"], sp, out=s["out"])
 
+    def fused(s, sp=spec):
+        s["plan"].run_step(s["q"], s["k"], s["v"], s["slot"], sp, out=s["out"])
+
     def step(i):
-        s = sets[i % R]
-        k1(s)
-        k2(s)
+        fused(sets[i % R])
 
     def graph_of(fn, n):
         g = torch.cuda.CUDAGraph()
@@ -215,23 +217,28 @@ def run_ours(args, rank, world, local_rank):
             timed(step, 256)
             extra += 1
     ms_per_step = ms / args.steps
+    print(f"[bench] step {ms_per_step * 1e3:.2f} us", file=sys.stderr, flush=True)
     Lstep = L + 1
     per_rank_bytes = step_bytes(Lstep)
     value = world * per_rank_bytes / (ms_per_step * 1e-3) / 1e9
 
     # ---- per-kernel timings (rotated and plain twins)
     n_k = max(args.steps, 512)
+    t_fused = ms_per_step
     t_k1 = timed(lambda i: k1(sets[i % R]), n_k) / n_k
     t_k2 = timed(lambda i: k2(sets[i % R]), n_k) / n_k
     t_k1p = timed(lambda i: k1(sets[i % R], None), n_k) / n_k
     t_k2p = timed(lambda i: k2(sets[i % R], None), n_k) / n_k
+    t_fp = timed(lambda i: fused(sets[i % R], None), n_k) / n_k
     # restore the rotated token in every set (the plain twin overwrote slot L)
     for s in sets:
         k1(s)
     torch.cuda.synchronize()
+    print(f"[bench] k1 {t_k1 * 1e3:.2f} us, k2 {t_k2 * 1e3:.2f} us, k1 plain {t_k1p * 1e3:.2f}, k2 plain "
+          f"{t_k2p * 1e3:.2f}, fused {t_fused * 1e3:.2f}, fused plain {t_fp * 1e3:.2f}", file=sys.stderr, flush=True)
     peak, peak_kind = hbm_peak()
-    dbytes = decode_bytes(Lstep)
-    ach = dbytes / (t_k2 * 1e-3) / 1e9
+    dbytes = step_bytes(Lstep)
+    ach = dbytes / (t_fused * 1e-3) / 1e9
     traffic = None
     try:
         with open(NCU_SUMMARY) as f:
@@ -278,17 +285,20 @@ def run_ours(args, rank, world, local_rank):
             "parallelism": f"dp{world} (independent sequences per GPU, no data-path collective)",
             "algorithmic_bytes_per_step": per_rank_bytes,
         },
-        "roofline": {"bound": "hbm", "kernel": "K2 paged_decode (decode_mma_kernel)", "achieved": round(ach, 1),
-                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(ach / peak, 4),
-                     "traffic": traffic, "algorithmic_bytes": dbytes, "avg_launch_us": round(t_k2 * 1e3, 3)},
+        "roofline": {"bound": "hbm", "kernel": "decode_tma_kernel (fused append + split-K decode, kvr_decode_step)",
+                     "achieved": round(ach, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": round(ach / peak, 4), "traffic": traffic, "algorithmic_bytes": dbytes,
+                     "avg_launch_us": round(t_fused * 1e3, 3)},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": args.steps,
         "clocks": clocks,
         "detail": {
             "k1_write_1tok_us": round(t_k1 * 1e3, 3), "k1_plain_1tok_us": round(t_k1p * 1e3, 3),
             "k2_decode_us": round(t_k2 * 1e3, 3), "k2_plain_us": round(t_k2p * 1e3, 3),
             "k2_overhead_vs_plain": round(t_k2 / t_k2p - 1.0, 4),
+            "fused_step_us": round(t_fused * 1e3, 3), "fused_step_plain_us": round(t_fp * 1e3, 3),
+            "fused_step_overhead_vs_plain": round(t_fused / t_fp - 1.0, 4),
             "c1_quantize_store": c1,
         },
     }
@@ -321,7 +331,8 @@ def c1_quantize_store(torch, layout, spec, dev, gen, timed):
 
 
 def e2e_api(torch, layout, spec, dev, table, args, world):
-    """Public-API step with host buffers: H2D new K/V + q, append_batch + decode, D2H output."""
+    """Public-API step with host buffers: H2D of the new K/V and q, DecodePlan.step
+    (slot allocation + one fused append+decode launch), D2H of the output."""
     from paper_2604_19157_b200 import DecodePlan
 
     steps = min(args.steps, 200)
@@ -330,20 +341,18 @@ def e2e_api(torch, layout, spec, dev, table, args, world):
     qh = torch.randn((1, NQ, D)).to(torch.bfloat16).pin_memory()
     oh = torch.empty((1, NQ, D), dtype=torch.float32).pin_memory()
     kd, vd, qd = kh.to(dev), vh.to(dev), qh.to(dev)
-    # a private copy of the sequence state so the bench's sets stay intact
-    plan = DecodePlan(table, [0], extra_tokens=steps + 8)
+    od = torch.empty((1, NQ, D), dtype=torch.float32, device=dev)
     free_before = list(table.alloc.free)
     base_len = table.alloc.seq_len[0]
     base_pages = list(table.alloc.seq_pages[0])
+    plan = DecodePlan(table, [0], extra_tokens=steps + 8)
 
     def one():
         kd.copy_(kh, non_blocking=True)
         vd.copy_(vh, non_blocking=True)
         qd.copy_(qh, non_blocking=True)
-        table.append_batch([0], kd, vd, spec=spec, check=False)
-        plan.refresh()
-        out = plan.run(qd, spec)
-        oh.copy_(out, non_blocking=True)
+        plan.step(qd, kd, vd, spec, out=od)
+        oh.copy_(od, non_blocking=True)
 
     for _ in range(3):
         one()
@@ -367,7 +376,7 @@ def e2e_api(torch, layout, spec, dev, table, args, world):
     byts = step_bytes(L)
     return {"value": round(world * byts / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "ms_per_step": round(ms, 4),
             "h2d_bytes_per_step": kh.numel() * 2 + vh.numel() * 2 + qh.numel() * 2,
-            "d2h_bytes_per_step": oh.numel() * 4, "api": "PageTable.append_batch + DecodePlan.refresh/run",
+            "d2h_bytes_per_step": oh.numel() * 4, "api": "DecodePlan.step (fused append + decode) with host buffers",
             "steps": steps}
 
 

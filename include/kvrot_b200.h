@@ -22,6 +22,8 @@
  *                               (cache.py:235-317) incl. _rotate_token (cache.py:453-462)
  *   kvr_dequantize_pages     <- cache.PageTable.read_token / read_sequence (cache.py:319-362)
  *   kvr_paged_decode         <- attention.decode_step (attention.py:50-87)
+ *   kvr_decode_step          <- PageTable.append_token + decode_step fused: one serving
+ *                               decode step (cache.py:235-270 then attention.py:50-87)
  */
 #ifndef KVROT_B200_H
 #define KVROT_B200_H
@@ -145,6 +147,19 @@ int kvr_paged_decode(const void* q, int32_t q_dtype, const kvr_pool* pool,
                      int32_t batch, int32_t num_q_heads, int32_t max_seq_len, int32_t rot_order,
                      int32_t rotate, int32_t targets, const uint32_t* sign_words, float* out,
                      void* workspace, size_t workspace_bytes, int32_t num_splits, void* stream);
+
+/*
+ * One serving decode step, fused into a single launch: for every sequence b the
+ * new token's K/V rows (new_k/new_v: (batch, H, d) of kv_dtype) are rotated and
+ * INT4-quantized reference-exactly (f64) into slot new_slot[b], and the decode
+ * attends over seq_lens[b] tokens -- which must already count that token (the
+ * host allocator's slot).  Same output/workspace contract as kvr_paged_decode.
+ */
+int kvr_decode_step(const void* q, int32_t q_dtype, const void* new_k, const void* new_v, int32_t kv_dtype,
+                    const int64_t* new_slot, const kvr_pool* pool, const int32_t* block_table, int32_t bt_stride,
+                    const int32_t* seq_lens, int32_t batch, int32_t num_q_heads, int32_t max_seq_len,
+                    int32_t rot_order, int32_t rotate, int32_t targets, const uint32_t* sign_words, float* out,
+                    void* workspace, size_t workspace_bytes, int32_t num_splits, uint32_t* flags, void* stream);
 
 #ifdef __cplusplus
 }

@@ -24,7 +24,7 @@ EXPORTED = (
     "kvr_fwht_rows_f64", "kvr_pack_rows", "kvr_unpack_rows", "kvr_quantize_rows_f64",
     "kvr_dequantize_rows_f64", "kvr_block_rotate", "kvr_rotate_quantize_store",
     "kvr_dequantize_pages", "kvr_decode_workspace_bytes", "kvr_decode_pick_splits",
-    "kvr_paged_decode",
+    "kvr_paged_decode", "kvr_decode_step",
 )
 
 
@@ -69,6 +69,8 @@ def _declare(lib):
         "kvr_decode_pick_splits": (_I32, [_I32, _I32, _I32, _I32]),
         "kvr_paged_decode": (_I32, [_P, _I32, ctypes.POINTER(KvrPool), _P, _I32, _P, _I32, _I32, _I32, _I32, _I32,
                                     _I32, _P, _P, _P, _SZ, _I32, _P]),
+        "kvr_decode_step": (_I32, [_P, _I32, _P, _P, _I32, _P, ctypes.POINTER(KvrPool), _P, _I32, _P, _I32, _I32,
+                                   _I32, _I32, _I32, _I32, _P, _P, _P, _SZ, _I32, _P, _P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -96,6 +96,41 @@ class DecodePlan:
         return out
 
 
+    def run_step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, slots: torch.Tensor,
+                 spec: Optional[RotationSpec], out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Fused serving step on device buffers (no host bookkeeping): write token b's
+        K/V rows (B, H, d) into slot slots[b] (rotated + INT4-quantized bit-exactly
+        in f64) and decode over the plan's lengths, which must already include it."""
+        table, lay = self.table, self.table.layout
+        q = q.contiguous()
+        if out is None:
+            out = torch.empty(q.shape, dtype=torch.float32, device=table.device)
+        rotate = spec is not None
+        if rotate and spec.learned is not None:
+            raise UnsupportedConfigError("learned rotations are not fused into the decode kernel (row f3)")
+        targets = _lib.KVR_KEYS_ONLY if (rotate and spec.targets is Targets.KEYS_ONLY) else _lib.KVR_KEYS_AND_VALUES
+        from .cache import _TORCH_DTYPE_CODE
+        _lib.check(_lib.lib().kvr_decode_step(
+            _kernels.ptr(q), _Q_CODE[q.dtype], _kernels.ptr(k_new), _kernels.ptr(v_new), _TORCH_DTYPE_CODE[k_new.dtype],
+            _kernels.ptr(slots), ctypes.byref(table.desc), _kernels.ptr(self.bt), self.bt.shape[1],
+            _kernels.ptr(self.lens), len(self.seqs), lay.num_q_heads, self.max_len, spec.order if rotate else 1,
+            1 if rotate else 0, targets, spec.sign_words(lay.head_dim) if rotate else None, _kernels.ptr(out),
+            _kernels.ptr(self.ws), self.ws.numel(), self.splits, _kernels.ptr(table.flags), _kernels.stream_ptr()))
+        return out
+
+    def step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, spec: Optional[RotationSpec],
+             out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """One serving decode step for every sequence of the plan: allocate the new
+        token's slot (reference page order), then one fused append + decode launch."""
+        table = self.table
+        slots, fresh = table.alloc.plan(self.seqs)
+        table._zero_pages(fresh)
+        self.refresh()
+        slot_t = torch.from_numpy(slots).to(table.device, non_blocking=True)
+        dev = table.device
+        return self.run_step(q.to(dev), k_new.to(dev).contiguous(), v_new.to(dev).contiguous(), slot_t, spec, out)
+
+
 def decode_batch(q: torch.Tensor, table: PageTable, seqs: Sequence[int], spec: Optional[RotationSpec] = None,
                  num_splits: int = 0) -> torch.Tensor:
     """Serving decode: q (B, num_q_heads, d) CUDA tensor -> f32 (B, num_q_heads, d)."""

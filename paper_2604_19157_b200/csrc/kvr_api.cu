@@ -264,4 +264,35 @@ int kvr_paged_decode(const void* q, int32_t q_dtype, const kvr_pool* pool, const
   return check_launch("paged_decode");
 }
 
+int kvr_decode_step(const void* q, int32_t q_dtype, const void* new_k, const void* new_v, int32_t kv_dtype,
+                    const int64_t* new_slot, const kvr_pool* pool, const int32_t* block_table, int32_t bt_stride,
+                    const int32_t* seq_lens, int32_t batch, int32_t num_q_heads, int32_t max_seq_len,
+                    int32_t rot_order, int32_t rotate, int32_t targets, const uint32_t* sign_words, float* out,
+                    void* workspace, size_t workspace_bytes, int32_t num_splits, uint32_t* flags, void* stream) {
+  Pool pl;
+  if (int rc = to_pool(pool, pl)) return rc;
+  if (batch < 0 || num_q_heads < 1 || num_q_heads % pl.H != 0)
+    return fail(KVR_ERR_SHAPE, "num_q_heads=%d is not a multiple of num_kv_heads=%d", num_q_heads, pl.H);
+  if (batch == 0) return KVR_OK;
+  if (!new_k || !new_v || !new_slot) return fail(KVR_ERR_ARG, "decode_step needs new_k, new_v and new_slot");
+  if (kv_dtype < KVR_F64 || kv_dtype > KVR_F16) return fail(KVR_ERR_ARG, "bad kv dtype %d", kv_dtype);
+  if (q_dtype != KVR_F32 && q_dtype != KVR_BF16 && q_dtype != KVR_F16)
+    return fail(KVR_ERR_ARG, "q dtype %d unsupported (F32/BF16/F16)", q_dtype);
+  if (rotate) {
+    if (int rc = check_order(pl.d, rot_order)) return rc;
+  } else {
+    rot_order = 1;
+  }
+  Signs s;
+  int has;
+  if (int rc = make_signs(rotate ? sign_words : nullptr, pl.d, s, has)) return rc;
+  const int rot_v = (rotate && targets == KVR_KEYS_AND_VALUES) ? 1 : 0;
+  int rc = kvr_launch_decode(q, q_dtype, pl, block_table, bt_stride, seq_lens, batch, num_q_heads, max_seq_len,
+                             rot_order, rotate, rot_v, s, has, out, workspace, workspace_bytes, num_splits,
+                             (cudaStream_t)stream, new_k, new_v, kv_dtype, new_slot, flags);
+  if (rc == KVR_ERR_ARG) return fail(rc, "decode workspace too small");
+  if (rc) return fail(rc, "decode_step: unsupported geometry (needs d=128, page_tokens>=16, G in 1/2/4/8)");
+  return check_launch("decode_step");
+}
+
 }  // extern "C"

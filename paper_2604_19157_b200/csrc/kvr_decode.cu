@@ -30,7 +30,6 @@
 
 namespace kvr {
 
-constexpr int DEC_WARPS = 4;
 constexpr float LOG2E = 1.4426950408889634f;
 
 struct DecodeParams {
@@ -42,9 +41,15 @@ struct DecodeParams {
   const int32_t* lens;
   int batch, nq, G, splits, order, rotate, rot_v, has_signs, log2P;
   float* out;
-  float* ws_o;    // [B][H][S][G][128]
-  float* ws_lse;  // [B][H][S][G]
+  float* ws_o;       // [B][H][S][8][128]
+  float* ws_lse;     // [B][H][S][8]
   uint32_t* ws_cnt;  // [B][H]
+  // fused decode-step append (kvr_decode_step): one token per sequence
+  const void* new_k;
+  const void* new_v;
+  int new_dtype;
+  const int64_t* new_slot;  // [B] slot id of the appended token (it is the last of seq_lens[b])
+  uint32_t* flags;
 };
 
 KVR_DEV uint32_t pack_h2(float a, float b) {
@@ -60,6 +65,12 @@ KVR_DEV void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+KVR_DEV float ex2f(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 KVR_DEV uint32_t movtrans(uint32_t x) {
   uint32_t r;
   asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(r) : "r"(x));
@@ -72,162 +83,309 @@ KVR_DEV float load_q(const void* q, int dtype, int64_t i) {
   return reinterpret_cast<const float*>(q)[i];
 }
 
-// fp32 block FWHT on rows of 128 held in shared memory, whole CTA cooperating.
-// rows*64 butterflies per stage; inv = 1/sqrt(order).
-KVR_DEV void cta_fwht128(float* s, int rows, int order) {
-  for (int half = 1; half < order; half <<= 1) {
-    for (int p = threadIdx.x; p < rows * 64; p += blockDim.x) {
-      const int r = p >> 6, q = p & 63;
-      const int blk = q / (order >> 1), w = q % (order >> 1);
-      const int i = r * 128 + blk * order + (w / half) * 2 * half + (w % half);
-      const float a = s[i], b = s[i + half];
-      s[i] = a + b;
-      s[i + half] = a - b;
-    }
-    __syncthreads();
-  }
-  const float inv = (float)(1.0 / sqrt((double)order));
-  for (int i = threadIdx.x; i < rows * 128; i += blockDim.x) s[i] *= inv;
-  __syncthreads();
-}
-
-struct TileRegs {
-  uint4 k0, k1;          // K codes, tokens r and r+8 (16 B each: dims 32i..32i+31)
-  uint2 v[4];            // V codes, tokens 2i, 2i+1, 2i+8, 2i+9 (8 B each: dims 16r..16r+15)
-  float ks0, ks1, vs0, vs1;
-  uint32_t kz0, kz1, vz0, vz1;
-};
-
 KVR_DEV const uint8_t* token_blob(const DecodeParams& p, int b, int t, int& slot) {
   const int page = p.bt[(int64_t)b * p.bt_stride + (t >> p.log2P)];
   slot = t & ((1 << p.log2P) - 1);
   return p.pool.base + (int64_t)page * p.pool.page_bytes;
 }
 
-KVR_DEV void load_tile(const DecodeParams& p, int b, int h, int t0, int len, int lane, TileRegs& R) {
-  const int r = lane >> 2, i = lane & 3;
-  const int H = p.pool.H;
-  const int ta = t0 + r, tb = t0 + r + 8;
-  R.k0 = make_uint4(0, 0, 0, 0);
-  R.k1 = make_uint4(0, 0, 0, 0);
-  R.ks0 = R.ks1 = R.vs0 = R.vs1 = 0.f;
-  R.kz0 = R.kz1 = R.vz0 = R.vz1 = 0u;
-  if (ta < len) {
-    int sl;
-    const uint8_t* blob = token_blob(p, b, ta, sl);
-    const int idx = sl * H + h;
-    R.k0 = __ldg(reinterpret_cast<const uint4*>(blob + p.pool.off_kp + (int64_t)idx * 64 + 16 * i));
-    R.ks0 = __ldg(reinterpret_cast<const float*>(blob + p.pool.off_ks) + idx);
-    R.kz0 = __ldg(blob + p.pool.off_kz + idx);
-    R.vs0 = __ldg(reinterpret_cast<const float*>(blob + p.pool.off_vs) + idx);
-    R.vz0 = __ldg(blob + p.pool.off_vz + idx);
-  }
-  if (tb < len) {
-    int sl;
-    const uint8_t* blob = token_blob(p, b, tb, sl);
-    const int idx = sl * H + h;
-    R.k1 = __ldg(reinterpret_cast<const uint4*>(blob + p.pool.off_kp + (int64_t)idx * 64 + 16 * i));
-    R.ks1 = __ldg(reinterpret_cast<const float*>(blob + p.pool.off_ks) + idx);
-    R.kz1 = __ldg(blob + p.pool.off_kz + idx);
-    R.vs1 = __ldg(reinterpret_cast<const float*>(blob + p.pool.off_vs) + idx);
-    R.vz1 = __ldg(blob + p.pool.off_vz + idx);
-  }
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int t = t0 + 2 * i + (u & 1) + 8 * (u >> 1);
-    R.v[u] = make_uint2(0, 0);
-    if (t < len) {
-      int sl;
-      const uint8_t* blob = token_blob(p, b, t, sl);
-      R.v[u] = __ldg(reinterpret_cast<const uint2*>(blob + p.pool.off_vp + (int64_t)(sl * H + h) * 64 + 8 * r));
-    }
-  }
-}
-
 // dims held by A-operand register (k-step s, lane group i, slot R0/R2, half e)
 KVR_DEV int qk_dim(int s, int i, int slot2, int e) { return 32 * i + 8 * (s >> 1) + 2 * (s & 1) + slot2 + 4 * e; }
 
-template <int NT>  // number of 8-column MMA tiles: G <= 4 -> 1, G == 8 -> 2
-__global__ void __launch_bounds__(DEC_WARPS * 32, 3) decode_mma_kernel(const __grid_constant__ DecodeParams p,
-                                                                        const __grid_constant__ Signs signs) {
-  __shared__ float sq[8 * 128];                  // rotated query of this kv head's group
-  __shared__ float sred[DEC_WARPS][8][128 + 2];  // per-warp (o_unnorm, M, l) for the CTA merge
-  __shared__ uint32_t s_last;
+// fp32 block FWHT of `rows` rows of 128 in shared memory, whole CTA, then * 1/sqrt(ORDER).
+template <int ORDER>
+KVR_DEV void cta_fwht_rows(float* s, int rows) {
+#pragma unroll
+  for (int half = 1; half < ORDER; half <<= 1) {
+    for (int p = threadIdx.x; p < rows * 64; p += blockDim.x) {
+      const int r = p >> 6, q = p & 63;
+      const int i = r * 128 + ((q / half) * 2 * half) + (q % half);  // half is a power-of-two constant
+      const float a = s[i], b = s[i + half];
+      s[i] = a + b;
+      s[i + half] = a - b;
+    }
+    __syncthreads();
+  }
+  const float inv = (float)(1.0 / sqrt((double)ORDER));
+  for (int i = threadIdx.x; i < rows * 128; i += blockDim.x) s[i] *= inv;
+  __syncthreads();
+}
+
+// ---- the fused decode-step append: one token's K or V row of head h, computed
+// reference-exactly in f64 by one warp (lane l owns elements 4l..4l+3): sign
+// flip, butterfly stages half = 1, 2 in registers and 4..ORDER/2 via shuffles
+// (pairs combined lowest index first, exactly _ref.fwht_rows), * 1/sqrt(ORDER),
+// then _ref.quantize_rows (_ref.py:22-40, 57-80) and the paged store.
+template <int ORDER>
+KVR_DEV void append_row_exact(const DecodeParams& p, const Signs& sg, int b, int h, int side) {
+  const int lane = threadIdx.x & 31;
+  const int64_t slot = p.new_slot[b];
+  const int64_t base = ((int64_t)b * p.pool.H + h) * 128 + 4 * lane;
+  const void* src = side ? p.new_v : p.new_k;
+  double x[4];
+  bool fin = true;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (p.new_dtype == KVR_BF16) x[u] = (double)__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(src)[base + u]);
+    else if (p.new_dtype == KVR_F16) x[u] = (double)__half2float(reinterpret_cast<const __half*>(src)[base + u]);
+    else if (p.new_dtype == KVR_F32) x[u] = (double)reinterpret_cast<const float*>(src)[base + u];
+    else x[u] = reinterpret_cast<const double*>(src)[base + u];
+    fin &= (bool)isfinite(x[u]);
+  }
+  fin = __all_sync(0xffffffffu, fin);
+  if (!fin) {
+    if (lane == 0 && p.flags) atomicOr(p.flags, (uint32_t)KVR_FLAG_NONFINITE);
+    return;
+  }
+  const bool rot = side ? (p.rotate && p.rot_v) : p.rotate;
+  if (rot) {
+    if (p.has_signs) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (sign_bit(sg, 4 * lane + u)) x[u] = x[u] * -1.0;
+    }
+    double a0 = x[0] + x[1], a1 = x[0] - x[1], a2 = x[2] + x[3], a3 = x[2] - x[3];  // half = 1
+    x[0] = a0 + a2;                                                               // half = 2
+    x[1] = a1 + a3;
+    x[2] = a0 - a2;
+    x[3] = a1 - a3;
+#pragma unroll
+    for (int k = 0; (4 << k) < ORDER; ++k) {  // half = 4 << k: partner lane = lane ^ (1 << k)
+      const bool upper = (lane >> k) & 1;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double o = __shfl_xor_sync(0xffffffffu, x[u], 1 << k);
+        x[u] = upper ? o - x[u] : x[u] + o;
+      }
+    }
+    const double inv = 1.0 / sqrt((double)ORDER);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = x[u] * inv;
+  }
+  double mn = x[0], mx = x[0];
+#pragma unroll
+  for (int u = 1; u < 4; ++u) {
+    mn = x[u] < mn ? x[u] : mn;
+    mx = x[u] > mx ? x[u] : mx;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double a = __shfl_xor_sync(0xffffffffu, mn, o), c = __shfl_xor_sync(0xffffffffu, mx, o);
+    mn = a < mn ? a : mn;
+    mx = c > mx ? c : mx;
+  }
+  const int P = 1 << p.log2P;
+  uint8_t* blob = p.pool.base + (slot >> p.log2P) * (int64_t)p.pool.page_bytes;
+  const int idx = (int)(slot & (P - 1)) * p.pool.H + h;
+  const float s32 = (float)((mx - mn) / 15.0);
+  uint32_t bytes2 = 0u, zpv = 0xFFu;
+  float scv = (float)mn;
+  if (s32 != 0.0f) {
+    const double s64 = (double)s32;
+    double z = round_half_away(-mn / s64);
+    z = z < 0.0 ? 0.0 : (z > 15.0 ? 15.0 : z);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      double q = round_half_away(x[u] / s64) + z;
+      q = q < 0.0 ? 0.0 : (q > 15.0 ? 15.0 : q);
+      bytes2 |= (uint32_t)q << (4 * u);
+    }
+    scv = s32;
+    zpv = (uint32_t)z;
+  }
+  *reinterpret_cast<uint16_t*>(blob + (side ? p.pool.off_vp : p.pool.off_kp) + (int64_t)idx * 64 + 2 * lane) =
+      (uint16_t)bytes2;
+  if (lane == 0) {
+    reinterpret_cast<float*>(blob + (side ? p.pool.off_vs : p.pool.off_ks))[idx] = scv;
+    blob[(side ? p.pool.off_vz : p.pool.off_kz) + idx] = (uint8_t)zpv;
+  }
+}
+
+KVR_DEV void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+KVR_DEV void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+KVR_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+KVR_DEV void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+KVR_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+constexpr int DW = 16;           // warps per CTA (one CTA per SM)
+constexpr int NSTG = 4;          // TMA pipeline depth per warp
+constexpr int STG = 2560;        // stage: K codes 1 KB | V codes 1 KB | sidecars 256 B | pad
+constexpr int MAX_CTA_TILES = 8192;
+
+size_t decode_smem_bytes() { return 1024 + DW * NSTG * STG + (DW * NSTG + 1) * 8 + 2 * 1024 * 4 + 16 + MAX_CTA_TILES * 4; }
+
+template <int NT, int ORDER>
+__global__ void __launch_bounds__(DW * 32, 1)
+    decode_tma_kernel(const __grid_constant__ DecodeParams p, const __grid_constant__ Signs signs,
+                      const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v) {
+  // dynamic smem starts 1024-aligned (no static smem in this kernel); indexing the
+  // __shared__ array directly keeps every access in the shared window (LDS/STS)
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = sm_raw + ((1024u - (smem_u32(sm_raw) & 1023u)) & 1023u);
+  uint8_t* ring = sm;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + DW * NSTG * STG);
+  uint64_t* app_bar = bars + DW * NSTG;
+  float* sq = reinterpret_cast<float*>(app_bar + 1);
+  float* sqlo = sq + 1024;
+  uint32_t* s_last = reinterpret_cast<uint32_t*>(sqlo + 1024);
+  int32_t* sbt = reinterpret_cast<int32_t*>(s_last + 4);
+
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = lane >> 2, i = lane & 3;
-  const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int h = blockIdx.x, split = blockIdx.y, b = blockIdx.z;
   const int G = p.G, H = p.pool.H;
   const int len = p.lens[b];
-
-  // ---- query: load, rotate into the stored-key frame, normalise, split hi/lo
-  for (int x = threadIdx.x; x < 8 * 128; x += blockDim.x) {
-    const int j = x >> 7, dd = x & 127;
-    float v = 0.f;
-    if (j < G) {
-      v = load_q(p.q, p.q_dtype, ((int64_t)b * p.nq + (int64_t)h * G + j) * 128 + dd);
-      if (p.rotate && p.has_signs && sign_bit(signs, dd)) v = -v;
-    }
-    sq[x] = v;
-  }
-  __syncthreads();
-  if (p.rotate) cta_fwht128(sq, G, p.order);
-  float amax = 0.f;
-  for (int x = lane; x < G * 128; x += 32) amax = fmaxf(amax, fabsf(sq[x]));
-  amax = warp_max(amax);
-  // q' = q * 2^-e with max|q'| in [2^13, 2^14): fp16 hi/lo keep ~22 bits
-  int e2 = 0;
-  if (amax > 0.f) e2 = ilogbf(amax) - 13;
-  const float qscale = ldexpf(1.0f, -e2);
-  __syncthreads();  // every warp has read sq for amax
-  // hi/lo split in place: sq[x] <- hi, sred used as scratch for lo
-  float* sqlo = &sred[0][0][0];
-  for (int x = threadIdx.x; x < G * 128; x += blockDim.x) {
-    const float v = sq[x] * qscale;
-    const float hi = __half2float(__float2half_rn(v));
-    sq[x] = hi;
-    sqlo[x] = __half2float(__float2half_rn(v - hi));
-  }
-  __syncthreads();
-
-  uint32_t bq[NT][8][2];
-  float sumq[2] = {0.f, 0.f};  // per head owned by this lane: j = 4*nt + i
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    const int col = r;  // B-fragment column = lane / 4
-    const int j = 4 * nt + (col >> 1), part = col & 1;
-    const float* src = part ? sqlo : sq;
-#pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      float v4[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int slot2 = k >> 1, e = k & 1;
-        const float v = (j < G) ? src[j * 128 + qk_dim(s, i, slot2, e)] : 0.f;
-        v4[k] = slot2 ? v * (1.0f / 16.0f) : v;
-      }
-      bq[nt][s][0] = pack_h2(v4[0], v4[1]);
-      bq[nt][s][1] = pack_h2(v4[2], v4[3]);
-    }
-  }
-  // sum over d of (hi + lo) per head, in MMA units (x 2^-24)
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    for (int jj = 4 * nt; jj < min(G, 4 * nt + 4); ++jj) {
-      float a = 0.f;
-      for (int dd = lane; dd < 128; dd += 32) a += sq[jj * 128 + dd] + sqlo[jj * 128 + dd];
-      a = warp_sum(a);
-      if (jj == 4 * nt + i) sumq[nt] = a * 5.9604644775390625e-08f;  // 2^-24
-    }
-  }
-  __syncthreads();  // sred scratch is reused by the merge below
-  // logit (log2 units) = (D - z * sumq) * s_k * kscale
-  const float kscale = ldexpf(1.0f, e2 + 24) * LOG2E * (float)(1.0 / sqrt(128.0));
-
-  // ---- split range in 16-token tiles
   const int n_tiles = (len + 15) >> 4;
   const int per = (n_tiles + p.splits - 1) / p.splits;
-  const int tile_lo = split * per;
-  const int tile_hi = min(n_tiles, tile_lo + per);
+  const int lo = min(n_tiles, split * per);
+  const int hi = min(n_tiles, lo + per);
+  const int t_new = (len - 1) >> 4;
+  const bool has_app = p.new_slot != nullptr && len > 0 && p.new_slot[b] >= 0 && t_new >= lo && t_new < hi;
+
+  // ---- setup: barriers, block-table slice, query --------------------------------
+  if (threadIdx.x < DW * NSTG) mbar_init(&bars[threadIdx.x], 1 + 16);
+  if (threadIdx.x == DW * NSTG) mbar_init(app_bar, 2);
+  if (threadIdx.x == 0) {
+    prefetch_tensormap(&tm_k);
+    prefetch_tensormap(&tm_v);
+  }
+  for (int t = lo + threadIdx.x; t < hi; t += blockDim.x)
+    sbt[t - lo] = p.bt[(int64_t)b * p.bt_stride + ((t << 4) >> p.log2P)];
+  fence_mbar_init();
+  __syncthreads();
+
+  // ---- the fused append (writer warps DW-1: K, DW-2: V) -------------------------
+  if (has_app && warp >= DW - 2) {
+    append_row_exact<ORDER>(p, signs, b, h, warp == DW - 1 ? 0 : 1);
+    fence_proxy_async_global();
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(app_bar);
+  }
+
+  // ---- per-warp TMA pipeline ------------------------------------------------------
+  const uint8_t* pb = p.pool.base;
+  const int pmask = (1 << p.log2P) - 1;
+  auto issue = [&](int k) {
+    const int t = lo + warp + DW * k;
+    const int stg = k % NSTG;
+    uint8_t* st = ring + (warp * NSTG + stg) * STG;
+    uint64_t* bar = &bars[warp * NSTG + stg];
+    if (has_app && t == t_new) mbar_wait(app_bar, 0);
+    const int page = sbt[t - lo];
+    const int slot0 = (t << 4) & pmask;
+    if (lane == 0) {
+      fence_proxy_async();
+      mbar_expect_tx(bar, 2048);
+      tma_load_4d(st, &tm_k, bar, 0, h, slot0, page);
+      tma_load_4d(st + 1024, &tm_v, bar, 0, h, slot0, page);
+    }
+    if (lane < 16) {
+      const int tok = (t << 4) + lane;
+      if (tok < len) {
+        const uint8_t* blob = pb + (int64_t)page * p.pool.page_bytes;
+        const int idx = (slot0 + lane) * H + h;
+        float* sc = reinterpret_cast<float*>(st + 2048);
+        cp_async4(sc + lane, blob + p.pool.off_ks + 4 * idx);
+        cp_async4(sc + 16 + lane, blob + p.pool.off_vs + 4 * idx);
+        cp_async4(sc + 32 + lane, blob + ((p.pool.off_kz + idx) & ~3));
+        cp_async4(sc + 48 + lane, blob + ((p.pool.off_vz + idx) & ~3));
+      }
+      cp_async_arrive_noinc(bar);
+    }
+  };
+  const int my_tiles = (hi - lo - warp + DW - 1) / DW > 0 ? (hi - lo - warp + DW - 1) / DW : 0;
+#pragma unroll 1
+  for (int k = 0; k < NSTG && k < my_tiles; ++k) issue(k);
+
+  // ---- query prep (overlaps the TMA fill): warp j < 4*NT owns q head j of this kv
+  // head: sign flip + fp32 butterfly in registers/shuffles, per-head power-of-two
+  // normalisation, fp16 hi/lo split, scattered straight into MMA-fragment order
+  uint16_t* sfrag = reinterpret_cast<uint16_t*>(sq);        // [NT][8 k-steps][2 regs][32 lanes][2 halves]
+  float* s_sumq = sqlo;                                     // [8]
+  float* s_ksc = sqlo + 8;                                  // [8]
+  if (warp < 4 * NT) {
+    const int j = warp;
+    float x[4] = {0.f, 0.f, 0.f, 0.f};
+    if (j < G) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        x[u] = load_q(p.q, p.q_dtype, ((int64_t)b * p.nq + (int64_t)h * G + j) * 128 + 4 * lane + u);
+        if (p.rotate && p.has_signs && sign_bit(signs, 4 * lane + u)) x[u] = -x[u];
+      }
+      if (p.rotate) {
+        const float a0 = x[0] + x[1], a1 = x[0] - x[1], a2 = x[2] + x[3], a3 = x[2] - x[3];
+        x[0] = a0 + a2;
+        x[1] = a1 + a3;
+        x[2] = a0 - a2;
+        x[3] = a1 - a3;
+#pragma unroll
+        for (int k = 0; (4 << k) < ORDER; ++k) {
+          const bool upper = (lane >> k) & 1;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float o = __shfl_xor_sync(0xffffffffu, x[u], 1 << k);
+            x[u] = upper ? o - x[u] : x[u] + o;
+          }
+        }
+        const float inv = (float)(1.0 / sqrt((double)ORDER));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] *= inv;
+      }
+    }
+    float amax = fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])), fmaxf(fabsf(x[2]), fabsf(x[3])));
+    amax = warp_max(amax);
+    const int e2 = amax > 0.f ? ilogbf(amax) - 13 : 0;  // q' = q 2^-e2, max|q'| in [2^13, 2^14)
+    const float qs = ldexpf(1.0f, -e2);
+    float hs = 0.f;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int d = 4 * lane + u, rem = d & 31;
+      const int ii = d >> 5, s = 2 * (rem >> 3) + ((rem & 3) >> 1), slot2 = rem & 1, e = (rem >> 2) & 1;
+      const float v = x[u] * qs;
+      const float hi = __half2float(__float2half_rn(v));
+      const float lo = __half2float(__float2half_rn(v - hi));
+      hs += hi + lo;
+      const float f = slot2 ? (1.0f / 16.0f) : 1.0f;  // x16 nibble slots
+      const int nt = j >> 2, col = 2 * (j & 3);
+      const int base = (((nt * 8 + s) * 2 + slot2) * 32) * 2 + e;
+      sfrag[base + ((col + 0) * 4 + ii) * 2] = __half_as_ushort(__float2half_rn(hi * f));
+      sfrag[base + ((col + 1) * 4 + ii) * 2] = __half_as_ushort(__float2half_rn(lo * f));
+    }
+    hs = warp_sum(hs);
+    if (lane == 0) {
+      s_sumq[j] = hs * 5.9604644775390625e-08f;  // x 2^-24 (MMA units)
+      s_ksc[j] = ldexpf(1.0f, e2 + 24) * LOG2E * (float)(1.0 / sqrt(128.0));
+    }
+  }
+  __syncthreads();
+  uint32_t bq[NT][8][2];
+  float sumq[NT], kscale[NT];
+  {
+    const uint32_t* f32 = reinterpret_cast<const uint32_t*>(sfrag);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        bq[nt][s][0] = f32[((nt * 8 + s) * 2 + 0) * 32 + lane];
+        bq[nt][s][1] = f32[((nt * 8 + s) * 2 + 1) * 32 + lane];
+      }
+      sumq[nt] = s_sumq[4 * nt + i];
+      kscale[nt] = s_ksc[4 * nt + i];
+    }
+  }
 
   float M[NT], lsum[NT], Zs[NT];
   float acc[NT][8][4];
@@ -242,19 +400,38 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 3) decode_mma_kernel(const __g
       for (int c = 0; c < 4; ++c) acc[nt][m][c] = 0.f;
   }
 
-  TileRegs cur, nxt;
-  int tile = tile_lo + warp;
-  if (tile < tile_hi) load_tile(p, b, h, tile * 16, len, lane, cur);
-  for (; tile < tile_hi; tile += DEC_WARPS) {
-    const int tnext = tile + DEC_WARPS;
-    if (tnext < tile_hi) load_tile(p, b, h, tnext * 16, len, lane, nxt);
+  // ---- main loop over this warp's tiles ---------------------------------------------
+#pragma unroll 1
+  for (int k = 0; k < my_tiles; ++k) {
+    const int t = lo + warp + DW * k;
+    const int stg = k % NSTG;
+    const uint8_t* st = ring + (warp * NSTG + stg) * STG;
+    mbar_wait(&bars[warp * NSTG + stg], (uint32_t)((k / NSTG) & 1));
+    // fragments out of the swizzled (64B) stage
+    const uint4 ka = *reinterpret_cast<const uint4*>(st + r * 64 + ((i ^ ((r >> 1) & 3)) << 4));
+    const uint4 kb = *reinterpret_cast<const uint4*>(st + (r + 8) * 64 + ((i ^ (((r + 8) >> 1) & 3)) << 4));
+    uint2 vw[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int tok = 2 * i + (u & 1) + 8 * (u >> 1);
+      vw[u] = *reinterpret_cast<const uint2*>(st + 1024 + tok * 64 + (((r >> 1) ^ ((tok >> 1) & 3)) << 4) + 8 * (r & 1));
+    }
+    const float* sc = reinterpret_cast<const float*>(st + 2048);
+    const uint32_t* zw = reinterpret_cast<const uint32_t*>(st + 2048);
+    float sk0 = sc[r], sk1 = sc[r + 8], sv0 = sc[16 + r], sv1 = sc[16 + r + 8];
+    const int slot0 = (t << 4) & pmask;
+    const int sh0 = 8 * (((slot0 + r) * H + h) & 3), sh1 = 8 * (((slot0 + r + 8) * H + h) & 3);
+    const uint32_t kz0 = (zw[32 + r] >> sh0) & 0xFFu, kz1 = (zw[32 + r + 8] >> sh1) & 0xFFu;
+    const uint32_t vz0 = (zw[48 + r] >> sh0) & 0xFFu, vz1 = (zw[48 + r + 8] >> sh1) & 0xFFu;
+    __syncwarp();
+    if (k + NSTG < my_tiles) issue(k + NSTG);
 
     // ---- S = C_k q : 8 k-steps of m16n8k16 per 8-column tile
-    float sc[NT][4];
+    float scv[NT][4];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
-    const uint32_t kw0[4] = {cur.k0.x, cur.k0.y, cur.k0.z, cur.k0.w};
-    const uint32_t kw1[4] = {cur.k1.x, cur.k1.y, cur.k1.z, cur.k1.w};
+    for (int nt = 0; nt < NT; ++nt) scv[nt][0] = scv[nt][1] = scv[nt][2] = scv[nt][3] = 0.f;
+    const uint32_t kw0[4] = {ka.x, ka.y, ka.z, ka.w};
+    const uint32_t kw1[4] = {kb.x, kb.y, kb.z, kb.w};
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
       const uint32_t wa = kw0[s >> 1], wb = kw1[s >> 1];
@@ -262,60 +439,65 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 3) decode_mma_kernel(const __g
       const uint32_t a0 = xa & 0x000F000Fu, a2 = xa & 0x00F000F0u;
       const uint32_t a1 = xb & 0x000F000Fu, a3 = xb & 0x00F000F0u;
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) mma16816(sc[nt], a0, a1, a2, a3, bq[nt][s][0], bq[nt][s][1]);
+      for (int nt = 0; nt < NT; ++nt) mma16816(scv[nt], a0, a1, a2, a3, bq[nt][s][0], bq[nt][s][1]);
     }
 
-    // ---- sidecars (sentinel rows: scale slot holds the offset, codes are 0)
-    float sk0 = cur.ks0, sk1 = cur.ks1, zk0 = (float)cur.kz0, zk1 = (float)cur.kz1;
-    if (cur.kz0 == 0xFFu) { zk0 = -sk0; sk0 = 1.f; }
-    if (cur.kz1 == 0xFFu) { zk1 = -sk1; sk1 = 1.f; }
-    float sv0 = cur.vs0, sv1 = cur.vs1, zv0 = (float)cur.vz0, zv1 = (float)cur.vz1;
-    if (cur.vz0 == 0xFFu) { zv0 = -sv0; sv0 = 1.f; }
-    if (cur.vz1 == 0xFFu) { zv1 = -sv1; sv1 = 1.f; }
-    const int t0 = tile * 16 + r, t1 = t0 + 8;
+    // ---- sidecars (sentinel rows: the scale slot holds the offset, codes are 0)
+    float zk0 = (float)kz0, zk1 = (float)kz1, zv0 = (float)vz0, zv1 = (float)vz1;
+    if (kz0 == 0xFFu) { zk0 = -sk0; sk0 = 1.f; }
+    if (kz1 == 0xFFu) { zk1 = -sk1; sk1 = 1.f; }
+    if (vz0 == 0xFFu) { zv0 = -sv0; sv0 = 1.f; }
+    if (vz1 == 0xFFu) { zv1 = -sv1; sv1 = 1.f; }
+    const int t0 = (t << 4) + r, t1 = t0 + 8;
     const bool ok0 = t0 < len, ok1 = t1 < len;
     const float lgv0 = ok0 ? __log2f(sv0) : 0.f, lgv1 = ok1 ? __log2f(sv1) : 0.f;
 
-    uint32_t wb_lo[NT], wb_hi[NT];
+    uint32_t wlo[NT], whi[NT];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
-      const float l0 = ok0 ? (sc[nt][0] + sc[nt][1] - zk0 * sumq[nt]) * (sk0 * kscale) : -INFINITY;
-      const float l1 = ok1 ? (sc[nt][2] + sc[nt][3] - zk1 * sumq[nt]) * (sk1 * kscale) : -INFINITY;
-      const float b0 = l0 + lgv0, b1 = l1 + lgv1;  // log2(p * s_v) up to the running max
+      const float l0 = ok0 ? (scv[nt][0] + scv[nt][1] - zk0 * sumq[nt]) * (sk0 * kscale[nt]) : -INFINITY;
+      const float l1 = ok1 ? (scv[nt][2] + scv[nt][3] - zk1 * sumq[nt]) * (sk1 * kscale[nt]) : -INFINITY;
+      const float b0 = l0 + lgv0, b1 = l1 + lgv1;  // log2(p * s_v)
       float tm = fmaxf(b0, b1);
       tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 4));
       tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 8));
       tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 16));
-      const float mnew = fmaxf(M[nt], tm);
-      const float alpha = (mnew == -INFINITY) ? 1.f : exp2f(M[nt] - mnew);
-      M[nt] = mnew;
-      const float ms = (mnew == -INFINITY) ? 0.f : mnew;
-      const float w0 = exp2f(b0 - ms), w1 = exp2f(b1 - ms);   // = p_t * s_v <= 1
-      const float p0 = exp2f(l0 - ms), p1 = exp2f(l1 - ms);   // = p_t
-      lsum[nt] = lsum[nt] * alpha + p0 + p1;
-      Zs[nt] = Zs[nt] * alpha + w0 * zv0 + w1 * zv1;
-      if (__any_sync(0xffffffffu, alpha != 1.f)) {
+      // lazy rescaling: the reference point M only moves when a logit exceeds it by
+      // > 2^7, so w = 2^(b - M) <= 128 and w * 2^8 stays inside fp16 range
+      if (__any_sync(0xffffffffu, tm > M[nt] + 7.0f)) {
+        const float mnew = fmaxf(M[nt], tm);
+        const float alpha = (M[nt] == -INFINITY) ? 0.f : ex2f(M[nt] - mnew);
+        if (mnew != -INFINITY) {
+          lsum[nt] *= alpha;
+          Zs[nt] *= alpha;
 #pragma unroll
-        for (int m = 0; m < 8; ++m)
+          for (int m = 0; m < 8; ++m)
 #pragma unroll
-          for (int c = 0; c < 4; ++c) acc[nt][m][c] *= alpha;
+            for (int c = 0; c < 4; ++c) acc[nt][m][c] *= alpha;
+          M[nt] = mnew;
+        }
       }
-      // fp16 hi/lo of w * 2^15 (w <= 1): keeps the lo half out of fp16 subnormals
-      // for weights down to ~2^-28 of the running max
-      const float w0s = w0 * 32768.0f, w1s = w1 * 32768.0f;
+      const float ms = (M[nt] == -INFINITY) ? 0.f : M[nt];
+      const float w0 = ex2f(b0 - ms), w1 = ex2f(b1 - ms);  // = p_t * s_v * 2^(.)
+      const float p0 = ex2f(l0 - ms), p1 = ex2f(l1 - ms);  // = p_t * 2^(.)
+      lsum[nt] += p0 + p1;
+      Zs[nt] += w0 * zv0 + w1 * zv1;
+      // fp16 hi/lo of w * 2^8 (w <= 2^7): 22-bit weights, the lo half out of fp16
+      // subnormals for weights down to ~2^-21 of the reference point
+      const float w0s = w0 * 256.0f, w1s = w1 * 256.0f;
       const float w0h = __half2float(__float2half_rn(w0s)), w1h = __half2float(__float2half_rn(w1s));
-      wb_lo[nt] = movtrans(pack_h2(w0h, w0s - w0h));  // tokens 0..7  -> b0,b1
-      wb_hi[nt] = movtrans(pack_h2(w1h, w1s - w1h));  // tokens 8..15 -> b2,b3
+      wlo[nt] = movtrans(pack_h2(w0h, w0s - w0h));  // tokens 0..7  -> b0,b1
+      whi[nt] = movtrans(pack_h2(w1h, w1s - w1h));  // tokens 8..15 -> b2,b3
     }
 
     // ---- O^T += C_v^T W : 8 m-tiles (16 dims each) of m16n8k16
-    uint32_t xr[2][2][8];  // [token pair (2i,2i+1)|(2i+8,2i+9)][word q][dim e]
+    uint32_t xr[2][2][8];  // [token pair (2i,2i+1)|(2i+8,2i+9)][word][dim e]
 #pragma unroll
     for (int tp = 0; tp < 2; ++tp)
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
-        const uint32_t wa = q ? cur.v[2 * tp].y : cur.v[2 * tp].x;
-        const uint32_t wb = q ? cur.v[2 * tp + 1].y : cur.v[2 * tp + 1].x;
+        const uint32_t wa = q ? vw[2 * tp].y : vw[2 * tp].x;
+        const uint32_t wb = q ? vw[2 * tp + 1].y : vw[2 * tp + 1].x;
         const uint32_t t0w = prmt(wa, wb, 0x5410u), t1w = prmt(wa, wb, 0x7632u);
         const uint32_t t0s = t0w >> 8, t1s = t1w >> 8;
         xr[tp][q][0] = t0w & 0x000F000Fu;
@@ -331,11 +513,12 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 3) decode_mma_kernel(const __g
     for (int m = 0; m < 8; ++m)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
-        mma16816(acc[nt][m], xr[0][0][m], xr[0][1][m], xr[1][0][m], xr[1][1][m], wb_lo[nt], wb_hi[nt]);
-    cur = nxt;
+        mma16816(acc[nt][m], xr[0][0][m], xr[0][1][m], xr[1][0][m], xr[1][1][m], wlo[nt], whi[nt]);
   }
 
-  // ---- per-warp finalisation: reduce l and Z over the 8 lanes of a head
+  // ---- per-warp finalisation into shared memory (the ring is free now)
+  __syncthreads();
+  float* sred = reinterpret_cast<float*>(ring);  // [DW][8][130]
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
@@ -345,36 +528,37 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 3) decode_mma_kernel(const __g
     }
     const int j = 4 * nt + i;
     if (j < G) {
+      float* row = sred + (warp * 8 + j) * 130;
 #pragma unroll
       for (int m = 0; m < 8; ++m) {
-        const float f = (m & 1) ? 512.0f / 16.0f : 512.0f;  // undo 2^-24 (codes), 2^15 (w) and the x16 nibble
-        sred[warp][j][16 * r + m] = (acc[nt][m][0] + acc[nt][m][1]) * f - Zs[nt];
-        sred[warp][j][16 * r + 8 + m] = (acc[nt][m][2] + acc[nt][m][3]) * f - Zs[nt];
+        const float f = (m & 1) ? 65536.0f / 16.0f : 65536.0f;  // undo 2^-24 (codes), 2^8 (w), x16 nibble
+        row[16 * r + m] = (acc[nt][m][0] + acc[nt][m][1]) * f - Zs[nt];
+        row[16 * r + 8 + m] = (acc[nt][m][2] + acc[nt][m][3]) * f - Zs[nt];
       }
       if (r == 0) {
-        sred[warp][j][128] = M[nt];
-        sred[warp][j][129] = lsum[nt];
+        row[128] = M[nt];
+        row[129] = lsum[nt];
       }
     }
   }
   __syncthreads();
 
-  // ---- CTA merge over warps -> (o, lse) for this split
-  float* obuf = sq;  // reuse: [G][128] merged normalised output
+  // ---- CTA merge over warps -> (o, lse) of this split
+  float* obuf = sq;
   for (int x = threadIdx.x; x < G * 128; x += blockDim.x) {
     const int j = x >> 7, dd = x & 127;
     float mmax = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < DEC_WARPS; ++w) mmax = fmaxf(mmax, sred[w][j][128]);
+    for (int w = 0; w < DW; ++w) mmax = fmaxf(mmax, sred[(w * 8 + j) * 130 + 128]);
     float lt = 0.f, ot = 0.f;
     if (mmax != -INFINITY) {
 #pragma unroll
-      for (int w = 0; w < DEC_WARPS; ++w) {
-        const float mw = sred[w][j][128];
+      for (int w = 0; w < DW; ++w) {
+        const float mw = sred[(w * 8 + j) * 130 + 128];
         if (mw == -INFINITY) continue;
         const float f = exp2f(mw - mmax);
-        lt += f * sred[w][j][129];
-        ot += f * sred[w][j][dd];
+        lt += f * sred[(w * 8 + j) * 130 + 129];
+        ot += f * sred[(w * 8 + j) * 130 + dd];
       }
     }
     const float o = (lt > 0.f) ? ot / lt : 0.f;
@@ -392,33 +576,44 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 3) decode_mma_kernel(const __g
     __syncthreads();
     if (threadIdx.x == 0) {
       const uint32_t prev = atomicAdd(&p.ws_cnt[(int64_t)b * H + h], 1u);
-      s_last = (prev == (uint32_t)p.splits - 1) ? 1u : 0u;
+      *s_last = (prev == (uint32_t)p.splits - 1) ? 1u : 0u;
     }
     __syncthreads();
-    if (!s_last) return;
+    if (!*s_last) return;
     __threadfence();
-    // last CTA of (b, h): LSE-merge all splits
+    // last CTA of (b, h): LSE-merge all splits; weights once per (split, head)
+    float* wts = sqlo;  // [S][8] weights, S <= 128
+    for (int x = threadIdx.x; x < G; x += blockDim.x) {
+      const int64_t base0 = (((int64_t)b * H + h) * p.splits) * 8 + x;
+      float lmax = -INFINITY;
+      for (int s = 0; s < p.splits; ++s) lmax = fmaxf(lmax, __ldcg(&p.ws_lse[base0 + (int64_t)s * 8]));
+      float tot = 0.f;
+      for (int s = 0; s < p.splits; ++s) {
+        const float ls = __ldcg(&p.ws_lse[base0 + (int64_t)s * 8]);
+        const float f = (ls == -INFINITY) ? 0.f : exp2f(ls - lmax);
+        wts[s * 8 + x] = f;
+        tot += f;
+      }
+      for (int s = 0; s < p.splits; ++s) wts[s * 8 + x] = tot > 0.f ? wts[s * 8 + x] / tot : 0.f;
+    }
+    __syncthreads();
     for (int x = threadIdx.x; x < G * 128; x += blockDim.x) {
       const int j = x >> 7, dd = x & 127;
       const int64_t base0 = (((int64_t)b * H + h) * p.splits) * 8 + j;
-      float lmax = -INFINITY;
-      for (int s = 0; s < p.splits; ++s) lmax = fmaxf(lmax, __ldcg(&p.ws_lse[base0 + (int64_t)s * 8]));
-      float wt = 0.f, ot = 0.f;
+      float ot = 0.f;
+#pragma unroll 4
       for (int s = 0; s < p.splits; ++s) {
-        const float ls = __ldcg(&p.ws_lse[base0 + (int64_t)s * 8]);
-        if (ls == -INFINITY) continue;
-        const float f = exp2f(ls - lmax);
-        wt += f;
-        ot += f * __ldcg(&p.ws_o[(base0 + (int64_t)s * 8) * 128 + dd]);
+        const float f = wts[s * 8 + j];
+        if (f != 0.f) ot += f * __ldcg(&p.ws_o[(base0 + (int64_t)s * 8) * 128 + dd]);
       }
-      obuf[x] = wt > 0.f ? ot / wt : 0.f;
+      obuf[x] = ot;
     }
     if (threadIdx.x == 0) p.ws_cnt[(int64_t)b * H + h] = 0u;  // re-arm for the next launch
   }
   __syncthreads();
   // ---- inverse rotation of the value branch: o @ H_blk @ diag(signs)
   if (p.rotate && p.rot_v) {
-    cta_fwht128(obuf, G, p.order);
+    cta_fwht_rows<ORDER>(obuf, G);
     if (p.has_signs)
       for (int x = threadIdx.x; x < G * 128; x += blockDim.x)
         if (sign_bit(signs, x & 127)) obuf[x] = -obuf[x];
@@ -553,18 +748,69 @@ int kvr_pick_splits(int batch, int H, int max_len, int P) {
   (void)P;
   const int sms = kvr_num_sms() > 0 ? kvr_num_sms() : 148;
   const int tiles = (max_len + 15) / 16;
-  const int target = sms * 3;  // resident CTAs
   const int units = batch * H;
-  int s = (target + units - 1) / units;
-  const int max_s = (tiles + 2 * DEC_WARPS - 1) / (2 * DEC_WARPS);  // >= 2 tiles per warp
+  int s = sms / units;  // one CTA per SM, a single wave
+  const int min_tiles_per_cta = 2 * DW;
+  const int max_s = tiles / min_tiles_per_cta;
   if (s > max_s) s = max_s;
+  if (s > 128) s = 128;
   if (s < 1) s = 1;
+  while ((tiles + s - 1) / s > MAX_CTA_TILES && s < 128) ++s;
   return s;
+}
+
+template <int NT>
+static int launch_tma(const DecodeParams& p, const Signs& sg, const CUtensorMap& mk, const CUtensorMap& mv,
+                      dim3 grid, size_t smem, int order, cudaStream_t st) {
+#define KVR_DEC_CASE(ORD)                                                                               \
+  case ORD: {                                                                                           \
+    auto kern = decode_tma_kernel<NT, ORD>;                                                             \
+    static bool set = false;                                                                            \
+    if (!set) {                                                                                         \
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);               \
+      set = true;                                                                                       \
+    }                                                                                                   \
+    kern<<<grid, DW * 32, smem, st>>>(p, sg, mk, mv);                                                   \
+    return 0;                                                                                           \
+  }
+  switch (order) {
+    KVR_DEC_CASE(128)
+    KVR_DEC_CASE(64)
+    KVR_DEC_CASE(32)
+    KVR_DEC_CASE(16)
+  }
+#undef KVR_DEC_CASE
+  return KVR_ERR_UNSUPPORTED;
+}
+
+static CUresult encode_codes_map(CUtensorMap* map, const Pool& pool, int off) {
+  typedef CUresult (*encode_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static encode_fn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !f)
+      return CUDA_ERROR_NOT_FOUND;
+    fn = reinterpret_cast<encode_fn>(f);
+  }
+  // [num_pages][P][H][64 B] codes of one side: dims innermost first
+  const cuuint64_t dims[4] = {64, (cuuint64_t)pool.H, (cuuint64_t)pool.P, (cuuint64_t)pool.num_pages};
+  const cuuint64_t strides[3] = {64, (cuuint64_t)pool.H * 64, (cuuint64_t)pool.page_bytes};
+  const cuuint32_t box[4] = {64, 1, 16, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, pool.base + off, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 
 int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_t* bt, int bt_stride,
                       const int32_t* lens, int batch, int nq, int max_len, int order, int rotate, int rot_v,
-                      const Signs& s, int has, float* out, void* ws, size_t ws_bytes, int splits, cudaStream_t st) {
+                      const Signs& s, int has, float* out, void* ws, size_t ws_bytes, int splits, cudaStream_t st,
+                      const void* new_k, const void* new_v, int new_dtype, const int64_t* new_slot,
+                      uint32_t* flags) {
   DecodeParams p{};
   p.pool = pool;
   p.q = q;
@@ -580,29 +826,41 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
   p.rot_v = rot_v;
   p.has_signs = has;
   p.out = out;
+  p.new_k = new_k;
+  p.new_v = new_v;
+  p.new_dtype = new_dtype;
+  p.new_slot = new_slot;
+  p.flags = flags;
   int l2 = 0;
   while ((1 << l2) < pool.P) ++l2;
   const bool pow2 = (1 << l2) == pool.P;
   p.log2P = l2;
   Signs sg = s;
   if (!has) for (auto& x : sg.w) x = 0u;
-  const bool mma_ok = pool.d == 128 && pow2 && (p.G == 1 || p.G == 2 || p.G == 4 || p.G == 8);
   if (!pow2) return KVR_ERR_UNSUPPORTED;
-  if (mma_ok) {
+  const bool tma_ok = pool.d == 128 && pool.P >= 16 && (p.G == 1 || p.G == 2 || p.G == 4 || p.G == 8) &&
+                      (reinterpret_cast<uintptr_t>(pool.base) & 15) == 0 && (pool.page_bytes & 15) == 0 &&
+                      (pool.off_vp & 15) == 0;
+  if (tma_ok) {
     if (splits <= 0) splits = kvr_pick_splits(batch, pool.H, max_len, pool.P);
+    if (splits > 128) splits = 128;
+    if ((max_len + 15) / 16 > (int64_t)splits * MAX_CTA_TILES) return KVR_ERR_UNSUPPORTED;
     if (splits > 1 && kvr_decode_ws_bytes(batch, pool.H, nq, 128, splits) > ws_bytes) return KVR_ERR_ARG;
     p.splits = splits;
     const size_t units = (size_t)batch * pool.H * splits * 8;
     p.ws_o = reinterpret_cast<float*>(ws);
     p.ws_lse = p.ws_o + units * 128;
     p.ws_cnt = reinterpret_cast<uint32_t*>(p.ws_lse + units);
-    dim3 grid(splits, pool.H, batch);
-    if (p.G == 8)
-      decode_mma_kernel<2><<<grid, DEC_WARPS * 32, 0, st>>>(p, sg);
-    else
-      decode_mma_kernel<1><<<grid, DEC_WARPS * 32, 0, st>>>(p, sg);
-    return 0;
+    CUtensorMap mk, mv;
+    if (encode_codes_map(&mk, pool, pool.off_kp) != CUDA_SUCCESS) return KVR_ERR_CUDA;
+    if (encode_codes_map(&mv, pool, pool.off_vp) != CUDA_SUCCESS) return KVR_ERR_CUDA;
+    dim3 grid(pool.H, splits, batch);
+    const int ord = rotate ? order : 128;
+    const size_t smem = decode_smem_bytes();
+    return p.G == 8 ? launch_tma<2>(p, sg, mk, mv, grid, smem, ord, st)
+                    : launch_tma<1>(p, sg, mk, mv, grid, smem, ord, st);
   }
+  if (new_slot) return KVR_ERR_UNSUPPORTED;  // the fused append lives in the TMA kernel only
   if (pool.d > 256 || (pool.d & 31)) return KVR_ERR_UNSUPPORTED;
   p.splits = 1;
   const int warps = 4;

@@ -37,7 +37,8 @@ int kvr_pick_splits(int batch, int H, int max_len, int P);
 int kvr_launch_decode(const void* q, int q_dtype, const kvr::Pool& pool, const int32_t* bt, int bt_stride,
                       const int32_t* lens, int batch, int nq, int max_len, int order, int rotate, int rot_v,
                       const kvr::Signs& s, int has, float* out, void* ws, size_t ws_bytes, int splits,
-                      cudaStream_t st);
+                      cudaStream_t st, const void* new_k = nullptr, const void* new_v = nullptr, int new_dtype = 0,
+                      const int64_t* new_slot = nullptr, uint32_t* flags = nullptr);
 
 // Tensor-map encoder resolved through the runtime (no -lcuda link dependency).
 CUresult kvr_encode_tensor_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows,

@@ -1,5 +1,5 @@
 // K1 -- fused block-Hadamard rotate -> token-wise INT4 quantize -> paged store,
-// the serving-path write for bf16/fp16 rows with head_dim 128.
+// the serving-path bulk write for bf16/fp16 rows with head_dim 128.
 //
 // Reference semantics: cache.PageTable.append_token (cache.py:235-270) ->
 // _rotate_token (cache.py:453-462) -> apply_block_rotation (rotation.py:118-142)
@@ -9,17 +9,17 @@
 //  * persistent CTAs of 4 warps; each warp streams 32-row tiles (8 KB) through a
 //    private double buffer filled by TMA (cp.async.bulk.tensor.2d, SWIZZLE_128B:
 //    conflict-free row-per-thread shared-memory reads);
-//  * one thread owns one 128-element row in registers: sign flip + unpack in 2
-//    ops per bf16 pair, the 7-stage butterfly as f32x2 (FADD2) except the one
-//    lane-crossing stage, NaN-propagating 3-input min/max (FMNMX3.NAN);
+//  * one thread owns one 128-element row in registers: sign flip + bf16 unpack
+//    fused with the first butterfly stage, the remaining stages as f32x2 (FADD2),
+//    NaN-propagating 3-input min/max (FMNMX3.NAN);
 //  * the row scale / zero point are formed in f64 exactly as the reference does,
 //    from the fp32 butterfly's extreme values;
 //  * codes: one FFMA2.RM per element pair evaluates floor((t + z + 1/2) * 2^16)
 //    as a fixed-point integer (magic 2^23), twice (+-delta) -- if both agree on
-//    the integer part the nibble is provably the reference's round-half-away
-//    code for this y; otherwise (|t| within delta of a half step) the element
-//    is recomputed in f64 from the bf16 inputs with the reference's own
-//    butterfly tree (bit-exact), see exact_code();
+//    the integer part the nibble is the reference's round-half-away code for this
+//    y; a row with an element within delta of a half step is recomputed in f64
+//    from the bf16 inputs with the reference's butterfly order, warp-cooperatively
+//    (warp_exact_row), and its flagged 8-code groups are replaced;
 //  * 8 nibbles are packed with 3 PRMT + 1 IMAD.HI per 4 codes.
 #include "kvr_common.cuh"
 #include "kvr_internal.h"
@@ -27,11 +27,14 @@
 namespace kvr {
 
 constexpr int FS_WARPS = 4;
+#ifndef KVR_FS_MINB
+#define KVR_FS_MINB 2
+#endif
 constexpr int FS_TILE_ROWS = 32;
-constexpr int FS_TILE_BYTES = FS_TILE_ROWS * 256;  // 128 bf16 per row
+constexpr int FS_TILE_BYTES = FS_TILE_ROWS * 256;  // 128 x 16-bit per row
 constexpr float FS_MAGIC = 8388608.0f;            // 2^23
 constexpr float FS_FIX = 65536.0f;                // 16 fraction bits
-constexpr float FS_D = 2.0f;                      // +-delta in units of 2^-16 (delta ~ 3.1e-5)
+constexpr float FS_D = 1.0f;                      // +-delta in units of 2^-16 (delta ~ 1.5e-5)
 
 struct FastStoreParams {
   Pool pool;
@@ -44,64 +47,75 @@ struct FastStoreParams {
   uint32_t sgn_lo[64];  // word j: 0x80000000 <=> element 2j negated (added to w << 16)
 };
 
-template <bool F16>
-KVR_DEV void unpack_pair(uint32_t w, uint32_t s_hi, uint32_t s_lo, bool rot, float& e, float& o) {
+template <bool F16, bool ROT>
+KVR_DEV void unpack_pair(uint32_t w, uint32_t s_hi, uint32_t s_lo, float& e, float& o) {
   if constexpr (!F16) {
     // bf16 pair -> two f32 (exact); the sign flip is folded into the same ops
-    const uint32_t lo = rot ? (w << 16) + s_lo : (w << 16);
-    const uint32_t hi = rot ? ((w ^ s_hi) & 0xFFFF0000u) : (w & 0xFFFF0000u);
-    e = __uint_as_float(lo);
-    o = __uint_as_float(hi);
+    e = __uint_as_float(ROT ? (w << 16) + s_lo : (w << 16));
+    o = __uint_as_float(ROT ? ((w ^ s_hi) & 0xFFFF0000u) : (w & 0xFFFF0000u));
   } else {
-    const uint32_t ws = rot ? (w ^ ((s_lo >> 16) | s_hi)) : w;
-    const __half2 h = *reinterpret_cast<const __half2*>(&ws);
-    const float2 f = __half22float2(h);
+    const uint32_t ws = ROT ? (w ^ ((s_lo >> 16) | s_hi)) : w;
+    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&ws));
     e = f.x;
     o = f.y;
   }
 }
 
-// Element `e` (0..127) of the row staged in the swizzled TMA tile, as f64.
+// Elements 4l..4l+3 of the row staged for lane `src` in the swizzled tile, as f64.
 template <bool F16>
-KVR_DEV double tile_elem(const uint8_t* buf, int lane, int e) {
+KVR_DEV void tile_quad(const uint8_t* buf, int src, int l, double (&x)[4]) {
+  const int e = 4 * l;
   const int h = e >> 6, c = (e >> 3) & 7, within = e & 7;
-  const uint8_t* p = buf + h * 4096 + lane * 128 + ((c ^ (lane & 7)) << 4) + within * 2;
-  const uint16_t bits = *reinterpret_cast<const uint16_t*>(p);
-  if constexpr (F16) return (double)__half2float(__ushort_as_half(bits));
-  return (double)__uint_as_float((uint32_t)bits << 16);
+  const uint2 q = *reinterpret_cast<const uint2*>(buf + h * 4096 + src * 128 + ((c ^ (src & 7)) << 4) + within * 2);
+  const uint32_t w[2] = {q.x, q.y};
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const uint32_t bits = (u & 1) ? (w[u >> 1] >> 16) : (w[u >> 1] & 0xFFFFu);
+    if constexpr (F16) x[u] = (double)__half2float(__ushort_as_half((unsigned short)bits));
+    else x[u] = (double)__uint_as_float(bits << 16);
+  }
 }
 
-// Reference-exact code for element e: the f64 butterfly tree that produces
-// output e in _ref.fwht_rows (pairs combined lowest-index-first, stage by
-// stage, sign by the bits of e), then * inv, / s64, round-half-away, + z, clip.
-template <int ORDER, bool F16>
-__device__ __noinline__ uint32_t exact_code(const uint8_t* buf, int lane, int e, bool rot, const Signs* sg,
-                                            double inv, double s64, double z) {
-  double y;
-  if (rot) {
-    double acc[ORDER];
-    const int base = (e / ORDER) * ORDER, j = e % ORDER;
-#pragma unroll 1
-    for (int i = 0; i < ORDER; ++i) {
-      double x = tile_elem<F16>(buf, lane, base + i);
-      if (sign_bit(*sg, base + i)) x = x * -1.0;
-      acc[i] = x;
+// Reference-exact codes of the row staged for lane `src`, computed by the whole
+// warp: lane l owns elements 4l..4l+3; f64 butterfly in _ref.fwht_rows order
+// (stages half = 1, 2 in registers, 4..ORDER/2 by shuffles, lowest index first),
+// * 1/sqrt(ORDER), then round-half-away(y / s64) + z, clip (_ref.py:22-40, 57-80).
+// Returns the 4 codes of lane l as a 16-bit group (element 4l in the low nibble).
+template <int ORDER, bool F16, bool ROT>
+__device__ __noinline__ uint32_t warp_exact_row(const uint8_t* buf, int src, const Signs& sg, double s64, double z) {
+  const int lane = threadIdx.x & 31;
+  double x[4];
+  tile_quad<F16>(buf, src, lane, x);
+  if constexpr (ROT) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (sign_bit(sg, 4 * lane + u)) x[u] = x[u] * -1.0;
+    const double a0 = x[0] + x[1], a1 = x[0] - x[1], a2 = x[2] + x[3], a3 = x[2] - x[3];  // half = 1
+    x[0] = a0 + a2;                                                                     // half = 2
+    x[1] = a1 + a3;
+    x[2] = a0 - a2;
+    x[3] = a1 - a3;
+#pragma unroll
+    for (int k = 0; (4 << k) < ORDER; ++k) {
+      const bool upper = (lane >> k) & 1;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double o = __shfl_xor_sync(0xffffffffu, x[u], 1 << k);
+        x[u] = upper ? o - x[u] : x[u] + o;
+      }
     }
-    int n = ORDER;
-#pragma unroll 1
-    for (int lvl = 0; (1 << lvl) < ORDER; ++lvl) {
-      const bool minus = (j >> lvl) & 1;
-#pragma unroll 1
-      for (int m = 0; m < (n >> 1); ++m) acc[m] = minus ? acc[2 * m] - acc[2 * m + 1] : acc[2 * m] + acc[2 * m + 1];
-      n >>= 1;
-    }
-    y = acc[0] * inv;
-  } else {
-    y = tile_elem<F16>(buf, lane, e);
+    const double inv = 1.0 / sqrt((double)ORDER);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = x[u] * inv;
   }
-  double q = round_half_away(y / s64) + z;
-  q = q < 0.0 ? 0.0 : (q > 15.0 ? 15.0 : q);
-  return (uint32_t)q;
+  uint32_t g = 0u;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    double q = round_half_away(x[u] / s64) + z;
+    q = q < 0.0 ? 0.0 : (q > 15.0 ? 15.0 : q);
+    g |= (uint32_t)q << (4 * u);
+  }
+  return g;
 }
 
 KVR_DEV uint32_t pack4(uint32_t m0, uint32_t m1, uint32_t m2, uint32_t m3) {
@@ -110,19 +124,179 @@ KVR_DEV uint32_t pack4(uint32_t m0, uint32_t m1, uint32_t m2, uint32_t m3) {
   return __umulhi(c, 1u << 28) + c;  // c | c >> 4: bytes 0 and 2 hold k0|k1<<4, k2|k3<<4
 }
 
+// Quantize this lane's staged row: packed codes, scale, zero point; returns write flag.
+template <int ORDER, bool F16, bool ROT>
+KVR_DEV bool row_codes(const uint8_t* buf, int lane, const FastStoreParams& p, const Signs& signs, bool valid,
+                       uint32_t (&packed)[16], float& scale_out, uint32_t& zp_out) {
+  // ---- stage the row: 16 x 16 B swizzled reads; unpack fused with stage half = 1
+  unsigned long long v[64];  // v[j] = (y_{2j}, y_{2j+1})
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint4 q = *reinterpret_cast<const uint4*>(buf + h * 4096 + lane * 128 + ((c ^ (lane & 7)) << 4));
+      const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = h * 32 + c * 4 + u;
+        float e, o;
+        unpack_pair<F16, ROT>(w4[u], p.sgn_hi[j], p.sgn_lo[j], e, o);
+        v[j] = ROT ? pk(e + o, e - o) : pk(e, o);
+      }
+    }
+  if constexpr (ROT) {
+    // stages half = 2 .. ORDER/2: pairs (j, j + hh) of (y_{2j}, y_{2j+1}) vectors
+#pragma unroll
+    for (int hh = 1; hh < ORDER / 2; hh <<= 1) {
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        if ((j & hh) == 0) {
+          const unsigned long long a = v[j], c = v[j + hh];
+          v[j] = add2(a, c);
+          v[j + hh] = sub2(a, c);
+        }
+      }
+    }
+  }
+  // ---- row extremes (NaN-propagating)
+  float mx0, mn0, mx1, mn1;
+  {
+    float a0, a1, b0, b1;
+    upk(v[0], a0, a1);
+    upk(v[1], b0, b1);
+    mx0 = max3_nan(a0, a1, a1);
+    mn0 = min3_nan(a0, a1, a1);
+    mx1 = max3_nan(b0, b1, b1);
+    mn1 = min3_nan(b0, b1, b1);
+#pragma unroll
+    for (int j = 2; j < 64; j += 2) {
+      float x0, x1, y0, y1;
+      upk(v[j], x0, x1);
+      upk(v[j + 1], y0, y1);
+      mx0 = max3_nan(mx0, x0, x1);
+      mn0 = min3_nan(mn0, x0, x1);
+      mx1 = max3_nan(mx1, y0, y1);
+      mn1 = min3_nan(mn1, y0, y1);
+    }
+  }
+  const float mxf = max3_nan(mx0, mx1, mx1), mnf = min3_nan(mn0, mn1, mn1);
+
+#pragma unroll
+  for (int i = 0; i < 16; ++i) packed[i] = 0u;
+  scale_out = 0.f;
+  zp_out = 0u;
+  bool write = valid;
+  if (valid && !(isfinite(mxf) && isfinite(mnf))) {
+    if (p.flags) atomicOr(p.flags, (uint32_t)KVR_FLAG_NONFINITE);
+    write = false;
+  }
+  // ---- row scale / zero point in f64, exactly as _ref.quantize_rows
+  const double inv64 = 1.0 / sqrt((double)ORDER);
+  bool do_codes = false, clamp_row = false;
+  double s64 = 1.0, z = 0.0, cst = 0.0;
+  if (write) {
+    const double scl = ROT ? inv64 : 1.0;
+    const double mx = (double)mxf * scl, mn = (double)mnf * scl;  // == fl64(S * inv) of the reference
+    const float s32 = (float)((mx - mn) / 15.0);
+    if (s32 == 0.0f) {
+      scale_out = (float)mn;  // sentinel row: offset in the scale slot, zp 0xFF, codes 0
+      zp_out = 0xFFu;
+    } else {
+      s64 = (double)s32;
+      z = round_half_away(-mn / s64);
+      z = z < 0.0 ? 0.0 : (z > 15.0 ? 15.0 : z);
+      scale_out = s32;
+      zp_out = (uint32_t)z;
+      cst = scl / s64;
+      const double ulo = mn * (1.0 / s64) + z + 0.5, uhi = mx * (1.0 / s64) + z + 0.5;
+      // rows whose codes may leave [0, 15] (z clipped / boundary ties) clamp u first;
+      // clamping is exact at both ends because floor-then-clip agrees on either side
+      clamp_row = !((ulo > 1e-3) && (uhi < 16.0 - 1e-3));
+      do_codes = true;
+    }
+  }
+  const bool clamp = __any_sync(0xffffffffu, do_codes && clamp_row);
+  uint32_t gflags = 0u;  // bit q: an element of 8q..8q+7 is within delta of a rounding boundary
+  if (do_codes) {
+    if (!clamp) {
+      // U = floor((y*c + z + 1/2 (+-delta)) * 2^16) + 2^23, one FFMA2.RM per pair and sign
+      const float cf = (float)(cst * (double)FS_FIX);
+      const float bias = (float)((z + 0.5) * (double)FS_FIX) + FS_MAGIC;
+      const unsigned long long c2 = pk(cf, cf);
+      const unsigned long long bp = pk(bias + FS_D, bias + FS_D), bm = pk(bias - FS_D, bias - FS_D);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        uint32_t mp[8], dq = 0u;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const unsigned long long up = fma2_rm(v[q * 4 + r], c2, bp);
+          const unsigned long long um = fma2_rm(v[q * 4 + r], c2, bm);
+          const uint32_t p0 = (uint32_t)up, p1 = (uint32_t)(up >> 32);
+          dq |= (p0 ^ (uint32_t)um) | (p1 ^ (uint32_t)(um >> 32));
+          mp[2 * r] = p0;
+          mp[2 * r + 1] = p1;
+        }
+        packed[q] = prmt(pack4(mp[0], mp[1], mp[2], mp[3]), pack4(mp[4], mp[5], mp[6], mp[7]), 0x6420u);
+        gflags |= (dq >= 0x10000u ? 1u : 0u) << q;
+      }
+    } else {
+      // clamped variant: u in f32 (error <= 2^-20), clamped to [2^-13, 15.99], then the magic floor
+      const float zb = (float)(z + 0.5), cu = (float)cst;
+      const unsigned long long fix2 = pk(FS_FIX, FS_FIX);
+      const unsigned long long mgp = pk(FS_MAGIC + FS_D, FS_MAGIC + FS_D), mgm = pk(FS_MAGIC - FS_D, FS_MAGIC - FS_D);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        uint32_t mp[8], dq = 0u;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          float a0, a1;
+          upk(v[q * 4 + r], a0, a1);
+          const float u0 = fminf(fmaxf(fmaf(a0, cu, zb), 1.0f / 8192.0f), 15.99f);
+          const float u1 = fminf(fmaxf(fmaf(a1, cu, zb), 1.0f / 8192.0f), 15.99f);
+          const unsigned long long uu = pk(u0, u1);
+          const unsigned long long up = fma2_rm(uu, fix2, mgp);
+          const unsigned long long um = fma2_rm(uu, fix2, mgm);
+          mp[2 * r] = (uint32_t)up;
+          mp[2 * r + 1] = (uint32_t)(up >> 32);
+          dq |= ((uint32_t)up ^ (uint32_t)um) | ((uint32_t)(up >> 32) ^ (uint32_t)(um >> 32));
+        }
+        packed[q] = prmt(pack4(mp[0], mp[1], mp[2], mp[3]), pack4(mp[4], mp[5], mp[6], mp[7]), 0x6420u);
+        gflags |= (dq >= 0x10000u ? 1u : 0u) << q;
+      }
+    }
+  }
+  // ---- rare: reference-exact recomputation of flagged rows, warp-cooperative
+  uint32_t todo = __ballot_sync(0xffffffffu, gflags != 0u);
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const uint32_t gf = __shfl_sync(0xffffffffu, gflags, src);
+    const double sb = __shfl_sync(0xffffffffu, s64, src), zb = __shfl_sync(0xffffffffu, z, src);
+    const uint32_t g16 = warp_exact_row<ORDER, F16, ROT>(buf, src, signs, sb, zb);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      if ((gf >> q) & 1u) {  // warp-uniform
+        const uint32_t lo = __shfl_sync(0xffffffffu, g16, 2 * q), hi = __shfl_sync(0xffffffffu, g16, 2 * q + 1);
+        if (lane == src) packed[q] = lo | (hi << 16);
+      }
+    }
+  }
+  return write;
+}
+
 template <int ORDER, bool F16>
-__global__ void __launch_bounds__(FS_WARPS * 32, 3)
+__global__ void __launch_bounds__(FS_WARPS * 32, KVR_FS_MINB)
     store_fast_kernel(const __grid_constant__ FastStoreParams p, const __grid_constant__ CUtensorMap map_k,
                       const __grid_constant__ CUtensorMap map_v, const __grid_constant__ Signs signs) {
-  extern __shared__ uint8_t fs_smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(fs_smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint8_t* bufs = smem + wib * 2 * FS_TILE_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + FS_WARPS * 2 * FS_TILE_BYTES) + wib * 2;
 
   const int total_tiles = 2 * p.tiles_per_side;
-  const int warp_global = blockIdx.x * FS_WARPS + wib;
   const int warp_stride = gridDim.x * FS_WARPS;
+  const int H = p.pool.H;
 
   if (lane == 0) {
     prefetch_tensormap(&map_k);
@@ -143,214 +317,51 @@ __global__ void __launch_bounds__(FS_WARPS * 32, 3)
     tma_load_2d(dst, m, &bars[b], 0, row0);
     tma_load_2d(dst + 4096, m, &bars[b], 64, row0);
   };
+  auto row_of = [&](int tile) -> int64_t {
+    const int side = tile >= p.tiles_per_side;
+    return (int64_t)(side ? tile - p.tiles_per_side : tile) * FS_TILE_ROWS + lane;
+  };
+  auto slot_of = [&](int tile) -> int64_t {  // slot id of this lane's row (or -1)
+    if (tile >= total_tiles) return -1;
+    const int64_t row = row_of(tile);
+    return row < p.n_rows ? __ldg(&p.slots[row / H]) : -1;
+  };
 
-  int tile = warp_global;
+  int tile = blockIdx.x * FS_WARPS + wib;
   if (tile < total_tiles && lane == 0) issue(tile, 0);
   uint32_t phase[2] = {0u, 0u};
-  const double inv64 = 1.0 / sqrt((double)ORDER);
+  int64_t slot_cur = slot_of(tile);
 
   for (int it = 0; tile < total_tiles; ++it, tile += warp_stride) {
     const int b = it & 1;
     const int next = tile + warp_stride;
     if (next < total_tiles && lane == 0) issue(next, b ^ 1);
+    const int64_t slot = slot_cur;
+    slot_cur = slot_of(next);  // prefetch: consumed one tile later
     mbar_wait(&bars[b], phase[b]);
     phase[b] ^= 1u;
     const uint8_t* buf = bufs + b * FS_TILE_BYTES;
-
     const int side = tile >= p.tiles_per_side;
-    const int64_t row = (int64_t)(side ? tile - p.tiles_per_side : tile) * FS_TILE_ROWS + lane;
-    const bool rot = side ? p.rot_v : p.rot_k;
-    bool valid = row < p.n_rows;
-    int64_t slot = -1;
-    if (valid) {
-      slot = p.slots[row / p.pool.H];
-      valid = slot >= 0;
-    }
-
-    // ---- stage the row: 16 x 16 B swizzled reads -> 64 packed words --------
-    uint32_t w[64];
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const uint4 q = *reinterpret_cast<const uint4*>(buf + h * 4096 + lane * 128 + ((c ^ (lane & 7)) << 4));
-        w[h * 32 + c * 4 + 0] = q.x;
-        w[h * 32 + c * 4 + 1] = q.y;
-        w[h * 32 + c * 4 + 2] = q.z;
-        w[h * 32 + c * 4 + 3] = q.w;
-      }
-
-    // ---- unpack (+ signs) and butterfly: v[j] = (y_{2j}, y_{2j+1}) -----------
-    unsigned long long v[64];
-#pragma unroll
-    for (int j = 0; j < 64; ++j) {
-      float e, o;
-      unpack_pair<F16>(w[j], p.sgn_hi[j], p.sgn_lo[j], rot, e, o);
-      v[j] = pk(e, o);
-    }
-    if (rot) {
-      // stages half = 2 .. ORDER/2 act on (E_j, O_j) pairs vertically
-#pragma unroll
-      for (int hh = 1; hh < ORDER / 2; hh <<= 1) {
-#pragma unroll
-        for (int j = 0; j < 64; ++j) {
-          if ((j & hh) == 0) {
-            const unsigned long long a = v[j], c = v[j + hh];
-            v[j] = add2(a, c);
-            v[j + hh] = sub2(a, c);
-          }
-        }
-      }
-      // stage half = 1 pairs the two lanes of each f32x2
-#pragma unroll
-      for (int j = 0; j < 64; ++j) {
-        float e, o;
-        upk(v[j], e, o);
-        v[j] = pk(e + o, e - o);
-      }
-    }
-
-    // ---- row extremes (NaN-propagating) --------------------------------------
-    float mx0, mn0, mx1, mn1;
-    {
-      float a0, a1, b0, b1;
-      upk(v[0], a0, a1);
-      upk(v[1], b0, b1);
-      mx0 = fmaxf(a0, a1);
-      mn0 = fminf(a0, a1);
-      mx1 = fmaxf(b0, b1);
-      mn1 = fminf(b0, b1);
-#pragma unroll
-      for (int j = 2; j < 64; j += 2) {
-        float x0, x1, y0, y1;
-        upk(v[j], x0, x1);
-        upk(v[j + 1], y0, y1);
-        mx0 = max3_nan(mx0, x0, x1);
-        mn0 = min3_nan(mn0, x0, x1);
-        mx1 = max3_nan(mx1, y0, y1);
-        mn1 = min3_nan(mn1, y0, y1);
-      }
-    }
-    const float mxf = max3_nan(mx0, mx1, mx1), mnf = min3_nan(mn0, mn1, mn1);
+    const int64_t row = row_of(tile);
+    const bool valid = row < p.n_rows;  // codes are computed whatever the slot; the store is predicated
 
     uint32_t packed[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) packed[i] = 0u;
-    float scale_out = 0.f;
-    uint32_t zp_out = 0;
-    bool write = valid;
-    if (valid && !(isfinite(mxf) && isfinite(mnf))) {
-      if (p.flags) atomicOr(p.flags, (uint32_t)KVR_FLAG_NONFINITE);
-      write = false;
-    }
-    // ---- row scale / zero point in f64, exactly as _ref.quantize_rows --------
-    bool do_codes = false, clamp_row = false;
-    double s64 = 1.0, z = 0.0, cst = 0.0;
-    if (write) {
-      const double scl = rot ? inv64 : 1.0;
-      const double mx = (double)mxf * scl, mn = (double)mnf * scl;  // == fl64(S * inv) of the reference
-      const float s32 = (float)((mx - mn) / 15.0);
-      if (s32 == 0.0f) {
-        scale_out = (float)mn;  // sentinel row: offset in the scale slot, zp 0xFF, codes 0
-        zp_out = 0xFFu;
-      } else {
-        s64 = (double)s32;
-        z = round_half_away(-mn / s64);
-        z = z < 0.0 ? 0.0 : (z > 15.0 ? 15.0 : z);
-        scale_out = s32;
-        zp_out = (uint32_t)z;
-        cst = scl / s64;
-        const double ulo = mn * (1.0 / s64) + z + 0.5, uhi = mx * (1.0 / s64) + z + 0.5;
-        // rows whose codes may leave [0, 15] (z clipped / boundary ties) clamp u first;
-        // clamping is exact at both ends because floor-then-clip agrees on either side
-        clamp_row = !((ulo > 1e-3) && (uhi < 16.0 - 1e-3));
-        do_codes = true;
-      }
-    }
-    const bool clamp = __any_sync(0xffffffffu, do_codes && clamp_row);
-    if (do_codes) {
-      // fixed-point code evaluation: U = floor((y*c + z + 1/2 (+-delta)) * 2^16) + 2^23
-      if (!clamp) {
-        const float cf = (float)(cst * (double)FS_FIX);
-        const float bias = (float)((z + 0.5) * (double)FS_FIX) + FS_MAGIC;
-        const unsigned long long c2 = pk(cf, cf);
-        const unsigned long long bp = pk(bias + FS_D, bias + FS_D), bm = pk(bias - FS_D, bias - FS_D);
-        uint32_t diff = 0u;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          uint32_t mp[8];
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            const unsigned long long up = fma2_rm(v[q * 4 + r], c2, bp);
-            const unsigned long long um = fma2_rm(v[q * 4 + r], c2, bm);
-            const uint32_t p0 = (uint32_t)up, p1 = (uint32_t)(up >> 32);
-            diff |= (p0 ^ (uint32_t)um) | (p1 ^ (uint32_t)(um >> 32));
-            mp[2 * r] = p0;
-            mp[2 * r + 1] = p1;
-          }
-          packed[q] = prmt(pack4(mp[0], mp[1], mp[2], mp[3]), pack4(mp[4], mp[5], mp[6], mp[7]), 0x6420u);
-        }
-        if (diff & 0xFFFF0000u) {
-          // rare: an element within delta of a rounding boundary -> reference-exact recomputation
-#pragma unroll
-          for (int j = 0; j < 64; ++j) {
-            const unsigned long long up = fma2_rm(v[j], c2, bp);
-            const unsigned long long um = fma2_rm(v[j], c2, bm);
-            if (((uint32_t)up ^ (uint32_t)um) & 0xFFFF0000u) {
-              const uint32_t code = exact_code<ORDER, F16>(buf, lane, 2 * j, rot, &signs, inv64, s64, z);
-              const int sh = 4 * ((2 * j) & 7);
-              packed[j >> 2] = (packed[j >> 2] & ~(0xFu << sh)) | (code << sh);
-            }
-            if (((uint32_t)(up >> 32) ^ (uint32_t)(um >> 32)) & 0xFFFF0000u) {
-              const uint32_t code = exact_code<ORDER, F16>(buf, lane, 2 * j + 1, rot, &signs, inv64, s64, z);
-              const int sh = 4 * ((2 * j + 1) & 7);
-              packed[j >> 2] = (packed[j >> 2] & ~(0xFu << sh)) | (code << sh);
-            }
-          }
-        }
-      } else {
-        // clamped variant: u in f32 (error <= 2^-20), clamp to [2^-13, 15.99] (both ends are
-        // exact: floor-then-clip agrees on either side of 0 and 16), then the magic floor
-        const float zb = (float)(z + 0.5), cu = (float)cst;
-        const unsigned long long fix2 = pk(FS_FIX, FS_FIX);
-        const unsigned long long mgp = pk(FS_MAGIC + FS_D, FS_MAGIC + FS_D), mgm = pk(FS_MAGIC - FS_D, FS_MAGIC - FS_D);
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          uint32_t mp[8], mm[8];
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            float a0, a1;
-            upk(v[q * 4 + r], a0, a1);
-            const float u0 = fminf(fmaxf(fmaf(a0, cu, zb), 1.0f / 8192.0f), 15.99f);
-            const float u1 = fminf(fmaxf(fmaf(a1, cu, zb), 1.0f / 8192.0f), 15.99f);
-            const unsigned long long uu = pk(u0, u1);
-            const unsigned long long up = fma2_rm(uu, fix2, mgp);
-            const unsigned long long um = fma2_rm(uu, fix2, mgm);
-            mp[2 * r] = (uint32_t)up;
-            mp[2 * r + 1] = (uint32_t)(up >> 32);
-            mm[2 * r] = (uint32_t)um;
-            mm[2 * r + 1] = (uint32_t)(um >> 32);
-          }
-          packed[q] = prmt(pack4(mp[0], mp[1], mp[2], mp[3]), pack4(mp[4], mp[5], mp[6], mp[7]), 0x6420u);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            if ((mp[e] ^ mm[e]) & 0xFFFF0000u) {
-              const uint32_t code = exact_code<ORDER, F16>(buf, lane, 8 * q + e, rot, &signs, inv64, s64, z);
-              packed[q] = (packed[q] & ~(0xFu << (4 * e))) | (code << (4 * e));
-            }
-          }
-        }
-      }
-    }
+    float scale_out;
+    uint32_t zp_out;
+    bool write;
+    if (side ? p.rot_v : p.rot_k)  // warp-uniform
+      write = row_codes<ORDER, F16, true>(buf, lane, p, signs, valid, packed, scale_out, zp_out);
+    else
+      write = row_codes<128, F16, false>(buf, lane, p, signs, valid, packed, scale_out, zp_out);
     __syncwarp();  // every lane done with the staged tile -> buffer may be refilled
 
-    if (write) {
+    if (write && slot >= 0) {
       const Pool& pl = p.pool;
-      const int head = (int)(row % pl.H);
+      const int head = (int)(row % H);
       const int64_t page = slot / pl.P;
       const int sl = (int)(slot % pl.P);
       uint8_t* blob = pl.base + page * (int64_t)pl.page_bytes;
-      const int idx = sl * pl.H + head;
+      const int idx = sl * H + head;
       uint4* dst = reinterpret_cast<uint4*>(blob + (side ? pl.off_vp : pl.off_kp) + (int64_t)idx * 64);
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -400,7 +411,7 @@ static int launch_fast_impl(const void* k, const void* v, int64_t n_tok, const i
   }
   const int total_tiles = 2 * prm.tiles_per_side;
   int grid = (total_tiles + FS_WARPS - 1) / FS_WARPS;
-  const int cap = kvr_num_sms() * 3;
+  const int cap = kvr_num_sms() * KVR_FS_MINB;
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
   kern<<<grid, FS_WARPS * 32, smem, st>>>(prm, mk, mv, sg);

@@ -47,9 +47,9 @@ def test_decode_step_matches_reference(golden, tag):
     assert err <= TOL
 
 
-def _build(n_seq, lens, H, G, d, order, P, kind, targets, rotate, seed, dtype=torch.bfloat16):
+def _build(n_seq, lens, H, G, d, order, P, kind, targets, rotate, seed, dtype=torch.bfloat16, extra_pages=0):
     layout = HeadLayout(num_q_heads=G * H, num_kv_heads=H, head_dim=d, rot_order=order, page_tokens=P)
-    npages = sum((L + P - 1) // P for L in lens)
+    npages = sum((L + P - 1) // P for L in lens) + extra_pages
     t = PageTable(layout, num_pages=npages)
     signs = make_signs(seed, 0, d, order) if rotate else None
     spec = RotationSpec(order=order, signs=signs, targets=targets) if rotate else None
@@ -186,3 +186,45 @@ def test_decode_step_fp_gqa():
     out = decode_step_fp(np.zeros((4, 32)), k, v, layout)
     np.testing.assert_allclose(out[:2], 1.0)
     np.testing.assert_allclose(out[2:], 2.0)
+
+
+@pytest.mark.parametrize("targets", [Targets.KEYS_AND_VALUES, Targets.KEYS_ONLY, None])
+@pytest.mark.parametrize("G", [4, 8])
+def test_fused_decode_step(targets, G):
+    """One serving step = append the new token (bit-exact f64 rotate + INT4 into its
+    slot) + decode over it, in one launch (kvr_decode_step)."""
+    H, d = 2, 128
+    lens = [15, 16, 300, 1025]
+    rotate = targets is not None
+    t, spec, layout = _build(len(lens), lens, H, G, d, 128, 16, "gaussian",
+                             targets or Targets.KEYS_AND_VALUES, rotate, seed=31, extra_pages=len(lens))
+    seqs = list(range(len(lens)))
+    rng = np.random.default_rng(77)
+    k_new = rng.standard_normal((len(lens), H, d))
+    v_new = rng.standard_normal((len(lens), H, d))
+    q = rng.standard_normal((len(lens), G * H, d))
+    plan = DecodePlan(t, seqs, extra_tokens=1)
+    kb = torch.tensor(k_new, dtype=torch.bfloat16)
+    vb = torch.tensor(v_new, dtype=torch.bfloat16)
+    out = plan.step(torch.tensor(q, dtype=torch.float32).cuda(), kb.cuda(), vb.cuda(), spec)
+    # 1) the appended slots are bit-identical to the reference append of the same bf16 values
+    signs = None if spec is None else spec.signs
+    for b, s in enumerate(seqs):
+        L = t.sequence_length(s) - 1
+        page = t.sequence_pages(s)[L // 16]
+        blob = t.pool[page].cpu().numpy()
+        from kvtest_util import page_fields
+        f = page_fields(blob, 16, H, d)
+        kk = O.rotate_rows(kb[b].double().numpy(), 128, signs) if rotate else kb[b].double().numpy()
+        vrot = rotate and targets is Targets.KEYS_AND_VALUES
+        vv = O.rotate_rows(vb[b].double().numpy(), 128, signs) if vrot else vb[b].double().numpy()
+        for side, x in (("k", kk), ("v", vv)):
+            pk, sk, zk = O.quantize_rows(x)
+            np.testing.assert_array_equal(f[f"{side}_payload"][0, L % 16], pk)
+            np.testing.assert_array_equal(f[f"{side}_scale"][0, L % 16], sk)
+            np.testing.assert_array_equal(f[f"{side}_zp"][0, L % 16], zk)
+    # 2) the decode saw the new token
+    refo = _oracle_decode(t, layout, spec, q, seqs)
+    err = rel_err(out.double().cpu().numpy(), refo)
+    print("fused step", G, targets, err)
+    assert err <= TOL
