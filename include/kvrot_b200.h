@@ -54,30 +54,43 @@ typedef enum { KVR_KEYS_ONLY = 0, KVR_KEYS_AND_VALUES = 1 } kvr_targets;
 
 /* Device-side status bits written by the write kernel (never cleared by it). */
 #define KVR_FLAG_NONFINITE 1u   /* a K/V row held NaN/Inf -> NonFiniteInputError */
+#define KVR_FLAG_LEN_OVERFLOW 2u /* a decode seq_lens[b] exceeded max_seq_len (tokens past it ignored) */
 
 /*
- * The paged pool: `num_pages` page blobs of `page_bytes` each.  A blob's byte
- * layout IS the reference `.kvpg` page record (cache.py:387-397, page shapes
- * cache.py:103-114):
- *     k_payload u8[P][H][d/2] | v_payload u8[P][H][d/2] |
- *     k_scale f32[P][H] | k_zp u8[P][H] | v_scale f32[P][H] | v_zp u8[P][H]
- * so exporting a page table is a page-ordered copy of blobs.
+ * The paged pool: `num_pages` page blobs of `page_bytes` each.  A page holds
+ * P tokens x H kv heads; inside it, every head owns P / T "cells" of T tokens
+ * (T = cell_tokens = 16 when P is a multiple of 16, else P), and a cell keeps
+ * everything one decode tile of that head needs contiguous:
+ *
+ *     cell = k_scale f32[T] | v_scale f32[T] | k_codes u8[T][d/2] |
+ *            v_codes u8[T][d/2] | k_zp u8[T] | v_zp u8[T]   (padded to 16 B)
+ *     page = cell[h = 0][0 .. P/T) | cell[h = 1][...] | ...
+ *
+ * so a (page, head) tile is ONE bulk copy (2208 B at d = 128, T = 16).  This is
+ * a B200-first re-layout of the reference KvPage (cache.py:103-114); the
+ * `.kvpg` record order (cache.py:387-397) is produced on export (PageTable.dump).
  */
 typedef struct {
-  void* base;          /* device pointer, 16-byte aligned                  */
+  void* base;           /* device pointer, 16-byte aligned                 */
   int64_t num_pages;
-  int32_t page_tokens; /* P  */
-  int32_t num_kv_heads;/* H  */
-  int32_t head_dim;    /* d  */
-  int32_t page_bytes;
-  int32_t off_k_payload, off_v_payload, off_k_scale, off_k_zp, off_v_scale, off_v_zp;
+  int32_t page_tokens;  /* P  */
+  int32_t num_kv_heads; /* H  */
+  int32_t head_dim;     /* d  */
+  int32_t page_bytes;   /* H * (P / T) * cell_bytes                        */
+  int32_t cell_tokens;  /* T                                                */
+  int32_t cell_bytes;   /* roundup16(T * (d + 10))                          */
 } kvr_pool;
 
-/* Fill a kvr_pool for (P, H, d); returns the blob size via pool->page_bytes. */
+/* Fill a kvr_pool for (P, H, d); the page size is returned in pool->page_bytes. */
 int kvr_pool_init(kvr_pool* pool, void* base, int64_t num_pages, int32_t page_tokens,
                   int32_t num_kv_heads, int32_t head_dim);
 
 const char* kvr_last_error(void);
+/* Profiling aid: when non-NULL, decode launches record per-CTA globaltimer
+ * stamps [start, main-loop start, main-loop end, partial written, split counter
+ * returned, merge done, end, 0] (u64 ns) into `trace` (device buffer of
+ * batch * splits * num_kv_heads * 8 entries).  NULL disables. */
+void kvr_debug_decode_trace(void* trace);
 int kvr_abi_version(void);
 /* Number of SMs of the current device (0 if no device). */
 int kvr_device_sms(void);
@@ -134,6 +147,9 @@ int kvr_dequantize_pages(const kvr_pool* pool, const int32_t* block_table, int32
  * inverse-rotated output for V (when rotate && targets == KEYS_AND_VALUES).
  *   q        : (batch, num_q_heads, d) of q_dtype (F32/BF16/F16)
  *   out      : (batch, num_q_heads, d) f32
+ *   seq_lens[b] <= max_seq_len <= bt_stride * page_tokens: the split ranges are
+ *   cut from max_seq_len so the page-id loads do not wait on seq_lens; tokens
+ *   past max_seq_len are ignored (kvr_decode_step sets KVR_FLAG_LEN_OVERFLOW).
  *   num_splits <= 0 picks a split count for the device.  Workspace must be at
  *   least kvr_decode_workspace_bytes(...) bytes and zero-filled once before
  *   first use (the kernels leave the split counters at zero afterwards).

@@ -24,7 +24,7 @@ EXPORTED = (
     "kvr_fwht_rows_f64", "kvr_pack_rows", "kvr_unpack_rows", "kvr_quantize_rows_f64",
     "kvr_dequantize_rows_f64", "kvr_block_rotate", "kvr_rotate_quantize_store",
     "kvr_dequantize_pages", "kvr_decode_workspace_bytes", "kvr_decode_pick_splits",
-    "kvr_paged_decode", "kvr_decode_step",
+    "kvr_paged_decode", "kvr_decode_step", "kvr_debug_decode_trace",
 )
 
 
@@ -36,12 +36,8 @@ class KvrPool(ctypes.Structure):
         ("num_kv_heads", ctypes.c_int32),
         ("head_dim", ctypes.c_int32),
         ("page_bytes", ctypes.c_int32),
-        ("off_k_payload", ctypes.c_int32),
-        ("off_v_payload", ctypes.c_int32),
-        ("off_k_scale", ctypes.c_int32),
-        ("off_k_zp", ctypes.c_int32),
-        ("off_v_scale", ctypes.c_int32),
-        ("off_v_zp", ctypes.c_int32),
+        ("cell_tokens", ctypes.c_int32),
+        ("cell_bytes", ctypes.c_int32),
     ]
 
 
@@ -54,6 +50,7 @@ def _declare(lib):
     sig = {
         "kvr_pool_init": (_I32, [ctypes.POINTER(KvrPool), _P, _I64, _I32, _I32, _I32]),
         "kvr_last_error": (ctypes.c_char_p, []),
+        "kvr_debug_decode_trace": (None, [_P]),
         "kvr_abi_version": (_I32, []),
         "kvr_device_sms": (_I32, []),
         "kvr_fwht_rows_f64": (_I32, [_P, _I64, _I32, _I32, _P]),

@@ -71,9 +71,86 @@ def capacity_tokens(budget_bytes: int, layout: HeadLayout, precision: str) -> in
     raise ConfigError(f"unknown precision {precision!r}")
 
 
+def cell_tokens(layout: HeadLayout) -> int:
+    """Tokens per cell (include/kvrot_b200.h): 16 when page_tokens % 16 == 0, else page_tokens."""
+    return 16 if layout.page_tokens % 16 == 0 else layout.page_tokens
+
+
+def cell_bytes(layout: HeadLayout) -> int:
+    return (cell_tokens(layout) * (layout.head_dim + 10) + 15) & ~15
+
+
 def page_bytes(layout: HeadLayout) -> int:
-    """Size of one INT4 page blob (== one .kvpg page record)."""
+    """Size of one device page blob: H x (P / T) cells."""
+    return layout.num_kv_heads * (layout.page_tokens // cell_tokens(layout)) * cell_bytes(layout)
+
+
+def record_bytes(layout: HeadLayout) -> int:
+    """Size of one reference `.kvpg` page record (cache.py:387-397)."""
     return layout.page_tokens * layout.num_kv_heads * (layout.head_dim + 10)
+
+
+def cells_to_records(blobs: np.ndarray, layout: HeadLayout) -> np.ndarray:
+    """Device page blobs [n, page_bytes] -> reference page records [n, record_bytes]
+    (k_payload [P][H][d/2] | v_payload | k_scale f32[P][H] | k_zp [P][H] | v_scale | v_zp)."""
+    P, H, d = layout.page_tokens, layout.num_kv_heads, layout.head_dim
+    T, cb = cell_tokens(layout), cell_bytes(layout)
+    n = blobs.shape[0]
+    cells = np.ascontiguousarray(blobs, dtype=np.uint8).reshape(n, H, P // T, cb)
+    o = 0
+
+    def take(nbytes, dt, shape):
+        nonlocal o
+        a = cells[..., o:o + nbytes].copy().view(dt).reshape((n, H, P // T) + shape)
+        o += nbytes
+        return a
+
+    ks = take(4 * T, np.float32, (T,))
+    vs = take(4 * T, np.float32, (T,))
+    kc = take(T * d // 2, np.uint8, (T, d // 2))
+    vc = take(T * d // 2, np.uint8, (T, d // 2))
+    kz = take(T, np.uint8, (T,))
+    vz = take(T, np.uint8, (T,))
+
+    def tok_major(a):  # (n, H, P/T, T, ...) -> (n, P, H, ...)
+        a = a.reshape((n, H, P) + a.shape[4:])
+        return np.ascontiguousarray(np.moveaxis(a, 1, 2))
+
+    parts = [tok_major(kc), tok_major(vc), tok_major(ks), tok_major(kz), tok_major(vs), tok_major(vz)]
+    return np.concatenate([p.reshape(n, -1).view(np.uint8) for p in parts], axis=1)
+
+
+def records_to_cells(records: np.ndarray, layout: HeadLayout) -> np.ndarray:
+    """Inverse of cells_to_records (used by PageTable.load)."""
+    P, H, d = layout.page_tokens, layout.num_kv_heads, layout.head_dim
+    T, cb = cell_tokens(layout), cell_bytes(layout)
+    n = records.shape[0]
+    r = np.ascontiguousarray(records, dtype=np.uint8).reshape(n, -1)
+    o = 0
+
+    def take(nbytes, dt, shape):
+        nonlocal o
+        a = r[:, o:o + nbytes].copy().view(dt).reshape((n,) + shape)
+        o += nbytes
+        return a
+
+    kc = take(P * H * d // 2, np.uint8, (P, H, d // 2))
+    vc = take(P * H * d // 2, np.uint8, (P, H, d // 2))
+    ks = take(4 * P * H, np.float32, (P, H))
+    kz = take(P * H, np.uint8, (P, H))
+    vs = take(4 * P * H, np.float32, (P, H))
+    vz = take(P * H, np.uint8, (P, H))
+
+    def cell_major(a):  # (n, P, H, ...) -> (n, H, P/T, T*...) bytes
+        a = np.ascontiguousarray(np.moveaxis(a, 2, 1))  # (n, H, P, ...)
+        return a.reshape(n, H, P // T, -1).view(np.uint8)
+
+    out = np.zeros((n, H, P // T, cb), dtype=np.uint8)
+    o2 = 0
+    for a in (cell_major(ks), cell_major(vs), cell_major(kc), cell_major(vc), cell_major(kz), cell_major(vz)):
+        out[..., o2:o2 + a.shape[-1]] = a
+        o2 += a.shape[-1]
+    return out.reshape(n, -1)
 
 
 class PageAllocator:
@@ -399,13 +476,17 @@ class PageTable:
         }
         return json.dumps(header, sort_keys=True, separators=(",", ":")).encode()
 
+    def page_records(self, pids) -> np.ndarray:
+        """Reference `.kvpg` page records [len(pids), record_bytes] of device pages."""
+        if len(pids) == 0:
+            return np.zeros((0, record_bytes(self.layout)), dtype=np.uint8)
+        idx = torch.tensor(list(pids), dtype=torch.long, device=self.device)
+        return cells_to_records(self.pool.index_select(0, idx).cpu().numpy(), self.layout)
+
     def dump_bytes(self) -> bytes:
         blob = self._header()
         pids = sorted(p for ps in self._seq_pages.values() for p in ps)
-        pages = b""
-        if pids:
-            idx = torch.tensor(pids, dtype=torch.long, device=self.device)
-            pages = self.pool.index_select(0, idx).cpu().numpy().tobytes()
+        pages = self.page_records(pids).tobytes() if pids else b""
         return _DUMP_MAGIC + struct.pack("<II", _DUMP_VERSION, len(blob)) + blob + pages
 
     def dump(self, path) -> None:
@@ -429,10 +510,12 @@ class PageTable:
         table.budget_bytes = header["budget_bytes"]
         allocated = sorted(p for s in header["sequences"].values() for p in s["pages"])
         body = np.frombuffer(raw, dtype=np.uint8, offset=12 + hlen)
-        if body.size != len(allocated) * table.page_bytes:
+        rb = record_bytes(layout)
+        if body.size != len(allocated) * rb:
             raise ConfigError(f"{path}: page payload size mismatch")
         if allocated:
-            blobs = torch.from_numpy(body.reshape(len(allocated), table.page_bytes).copy()).to(table.device)
+            cells = records_to_cells(body.reshape(len(allocated), rb), layout)
+            blobs = torch.from_numpy(cells).to(table.device)
             table.pool.index_copy_(0, torch.tensor(allocated, dtype=torch.long, device=table.device), blobs)
         taken = set(allocated)
         table.alloc.free = [p for p in range(table.num_pages) if p not in taken]

@@ -51,12 +51,10 @@ static int to_pool(const kvr_pool* in, Pool& p) {
   p.H = in->num_kv_heads;
   p.d = in->head_dim;
   p.page_bytes = in->page_bytes;
-  p.off_kp = in->off_k_payload;
-  p.off_vp = in->off_v_payload;
-  p.off_ks = in->off_k_scale;
-  p.off_kz = in->off_k_zp;
-  p.off_vs = in->off_v_scale;
-  p.off_vz = in->off_v_zp;
+  p.T = in->cell_tokens;
+  p.cell_bytes = in->cell_bytes;
+  if (p.T < 1 || p.P % p.T != 0 || p.cell_bytes < p.T * (p.d + 10))
+    return fail(KVR_ERR_SHAPE, "inconsistent pool geometry (P=%d, T=%d, cell=%d)", p.P, p.T, p.cell_bytes);
   return KVR_OK;
 }
 
@@ -100,6 +98,7 @@ int kvr_num_sms() {
 extern "C" {
 
 const char* kvr_last_error(void) { return g_err; }
+void kvr_debug_decode_trace(void* trace) { kvr_set_decode_trace(trace); }
 int kvr_abi_version(void) { return KVR_ABI_VERSION; }
 int kvr_device_sms(void) { return kvr_num_sms(); }
 
@@ -108,20 +107,17 @@ int kvr_pool_init(kvr_pool* pool, void* base, int64_t num_pages, int32_t page_to
   if (!pool) return fail(KVR_ERR_ARG, "null pool");
   if (page_tokens < 1 || num_kv_heads < 1 || head_dim < 2 || (head_dim & 1) || num_pages < 0)
     return fail(KVR_ERR_SHAPE, "bad pool geometry P=%d H=%d d=%d", page_tokens, num_kv_heads, head_dim);
-  const int64_t cells = (int64_t)page_tokens * num_kv_heads;
+  const int T = (page_tokens % 16 == 0) ? 16 : page_tokens;
   pool->base = base;
   pool->num_pages = num_pages;
   pool->page_tokens = page_tokens;
   pool->num_kv_heads = num_kv_heads;
   pool->head_dim = head_dim;
-  // .kvpg page record order: k_payload, v_payload, k_scale, k_zp, v_scale, v_zp (cache.py:391-397)
-  pool->off_k_payload = 0;
-  pool->off_v_payload = (int32_t)(cells * (head_dim / 2));
-  pool->off_k_scale = (int32_t)(2 * cells * (head_dim / 2));
-  pool->off_k_zp = pool->off_k_scale + (int32_t)(4 * cells);
-  pool->off_v_scale = pool->off_k_zp + (int32_t)cells;
-  pool->off_v_zp = pool->off_v_scale + (int32_t)(4 * cells);
-  pool->page_bytes = pool->off_v_zp + (int32_t)cells;
+  pool->cell_tokens = T;
+  pool->cell_bytes = (T * (head_dim + 10) + 15) & ~15;
+  const int64_t pb = (int64_t)num_kv_heads * (page_tokens / T) * pool->cell_bytes;
+  if (pb > 0x7fffffff) return fail(KVR_ERR_SHAPE, "page too large");
+  pool->page_bytes = (int32_t)pb;
   return KVR_OK;
 }
 
@@ -245,6 +241,8 @@ int kvr_paged_decode(const void* q, int32_t q_dtype, const kvr_pool* pool, const
   if (batch < 0 || num_q_heads < 1 || num_q_heads % pl.H != 0)
     return fail(KVR_ERR_SHAPE, "num_q_heads=%d is not a multiple of num_kv_heads=%d", num_q_heads, pl.H);
   if (batch == 0) return KVR_OK;
+  if (max_seq_len < 0 || (int64_t)bt_stride * pl.P < max_seq_len)
+    return fail(KVR_ERR_SHAPE, "max_seq_len=%d exceeds bt_stride=%d pages of %d tokens", max_seq_len, bt_stride, pl.P);
   if (q_dtype != KVR_F32 && q_dtype != KVR_BF16 && q_dtype != KVR_F16)
     return fail(KVR_ERR_ARG, "q dtype %d unsupported (F32/BF16/F16)", q_dtype);
   if (rotate) {
@@ -274,6 +272,8 @@ int kvr_decode_step(const void* q, int32_t q_dtype, const void* new_k, const voi
   if (batch < 0 || num_q_heads < 1 || num_q_heads % pl.H != 0)
     return fail(KVR_ERR_SHAPE, "num_q_heads=%d is not a multiple of num_kv_heads=%d", num_q_heads, pl.H);
   if (batch == 0) return KVR_OK;
+  if (max_seq_len < 0 || (int64_t)bt_stride * pl.P < max_seq_len)
+    return fail(KVR_ERR_SHAPE, "max_seq_len=%d exceeds bt_stride=%d pages of %d tokens", max_seq_len, bt_stride, pl.P);
   if (!new_k || !new_v || !new_slot) return fail(KVR_ERR_ARG, "decode_step needs new_k, new_v and new_slot");
   if (kv_dtype < KVR_F64 || kv_dtype > KVR_F16) return fail(KVR_ERR_ARG, "bad kv dtype %d", kv_dtype);
   if (q_dtype != KVR_F32 && q_dtype != KVR_BF16 && q_dtype != KVR_F16)

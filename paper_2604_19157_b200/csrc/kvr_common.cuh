@@ -18,13 +18,27 @@ struct Signs {
   uint32_t w[KVR_MAX_HEAD_DIM / 32];
 };
 
-// Pool geometry passed by value to kernels (mirror of kvr_pool).
+// Pool geometry passed by value to kernels (mirror of kvr_pool; see the cell
+// layout in include/kvrot_b200.h).
 struct Pool {
   uint8_t* base;
   int64_t num_pages;
-  int32_t P, H, d, page_bytes;
-  int32_t off_kp, off_vp, off_ks, off_kz, off_vs, off_vz;
+  int32_t P, H, d, page_bytes, T, cell_bytes;
 };
+
+// Address of the cell holding (page, head, slot) and the slot's index in it.
+KVR_DEV uint8_t* cell_of(const Pool& p, int64_t page, int h, int slot, int& i) {
+  const int u = slot / p.T;
+  i = slot - u * p.T;
+  return p.base + page * (int64_t)p.page_bytes + (int64_t)(h * (p.P / p.T) + u) * p.cell_bytes;
+}
+// field offsets inside a cell of T tokens
+KVR_DEV int cell_kscale(const Pool& p, int i) { return 4 * i; }
+KVR_DEV int cell_vscale(const Pool& p, int i) { return 4 * p.T + 4 * i; }
+KVR_DEV int cell_kcode(const Pool& p, int i) { return 8 * p.T + i * (p.d >> 1); }
+KVR_DEV int cell_vcode(const Pool& p, int i) { return 8 * p.T + p.T * (p.d >> 1) + i * (p.d >> 1); }
+KVR_DEV int cell_kzp(const Pool& p, int i) { return 8 * p.T + p.T * p.d + i; }
+KVR_DEV int cell_vzp(const Pool& p, int i) { return 9 * p.T + p.T * p.d + i; }
 
 KVR_DEV bool sign_bit(const Signs& s, int i) { return (s.w[i >> 5] >> (i & 31)) & 1u; }
 
@@ -99,6 +113,13 @@ KVR_DEV void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int32
       " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
       "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
       : "memory");
+}
+// 1-D bulk copy global -> shared completing on an mbarrier (16-B aligned, size % 16 == 0)
+KVR_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 KVR_DEV void prefetch_tensormap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");

@@ -39,7 +39,7 @@ struct DecodeParams {
   const int32_t* bt;
   int bt_stride;
   const int32_t* lens;
-  int batch, nq, G, splits, order, rotate, rot_v, has_signs, log2P;
+  int batch, nq, G, splits, order, rotate, rot_v, has_signs, log2P, max_len;
   float* out;
   float* ws_o;       // [B][H][S][8][128]
   float* ws_lse;     // [B][H][S][8]
@@ -50,7 +50,14 @@ struct DecodeParams {
   int new_dtype;
   const int64_t* new_slot;  // [B] slot id of the appended token (it is the last of seq_lens[b])
   uint32_t* flags;
+  unsigned long long* trace;  // optional: per CTA 8 globaltimer stamps (ns), see kvr_debug_decode_trace
 };
+
+KVR_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 KVR_DEV uint32_t pack_h2(float a, float b) {
   __half2 h = __floats2half2_rn(a, b);
@@ -83,10 +90,10 @@ KVR_DEV float load_q(const void* q, int dtype, int64_t i) {
   return reinterpret_cast<const float*>(q)[i];
 }
 
-KVR_DEV const uint8_t* token_blob(const DecodeParams& p, int b, int t, int& slot) {
+// Cell of (sequence b, token t, head h) and the token's index inside it.
+KVR_DEV const uint8_t* token_cell(const DecodeParams& p, int b, int t, int h, int& ci) {
   const int page = p.bt[(int64_t)b * p.bt_stride + (t >> p.log2P)];
-  slot = t & ((1 << p.log2P) - 1);
-  return p.pool.base + (int64_t)page * p.pool.page_bytes;
+  return cell_of(p.pool, page, h, t & ((1 << p.log2P) - 1), ci);
 }
 
 // dims held by A-operand register (k-step s, lane group i, slot R0/R2, half e)
@@ -174,9 +181,8 @@ KVR_DEV void append_row_exact(const DecodeParams& p, const Signs& sg, int b, int
     mn = a < mn ? a : mn;
     mx = c > mx ? c : mx;
   }
-  const int P = 1 << p.log2P;
-  uint8_t* blob = p.pool.base + (slot >> p.log2P) * (int64_t)p.pool.page_bytes;
-  const int idx = (int)(slot & (P - 1)) * p.pool.H + h;
+  int ci;
+  uint8_t* cell = cell_of(p.pool, slot >> p.log2P, h, (int)(slot & ((1 << p.log2P) - 1)), ci);
   const float s32 = (float)((mx - mn) / 15.0);
   uint32_t bytes2 = 0u, zpv = 0xFFu;
   float scv = (float)mn;
@@ -193,43 +199,30 @@ KVR_DEV void append_row_exact(const DecodeParams& p, const Signs& sg, int b, int
     scv = s32;
     zpv = (uint32_t)z;
   }
-  *reinterpret_cast<uint16_t*>(blob + (side ? p.pool.off_vp : p.pool.off_kp) + (int64_t)idx * 64 + 2 * lane) =
+  *reinterpret_cast<uint16_t*>(cell + (side ? cell_vcode(p.pool, ci) : cell_kcode(p.pool, ci)) + 2 * lane) =
       (uint16_t)bytes2;
   if (lane == 0) {
-    reinterpret_cast<float*>(blob + (side ? p.pool.off_vs : p.pool.off_ks))[idx] = scv;
-    blob[(side ? p.pool.off_vz : p.pool.off_kz) + idx] = (uint8_t)zpv;
+    *reinterpret_cast<float*>(cell + (side ? cell_vscale(p.pool, ci) : cell_kscale(p.pool, ci))) = scv;
+    cell[side ? cell_vzp(p.pool, ci) : cell_kzp(p.pool, ci)] = (uint8_t)zpv;
   }
 }
 
-KVR_DEV void cp_async4(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-KVR_DEV void cp_async_arrive_noinc(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 KVR_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-KVR_DEV void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2, int c3) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
-      : "memory");
-}
 KVR_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
-constexpr int DW = 16;           // warps per CTA (one CTA per SM)
+constexpr int DW = 15;  // tile warps per CTA (one CTA per SM) + 1 writer warp for the fused append;
+                       // 16 warps in all: 4 per SM sub-partition keeps the 128-register budget
 constexpr int NSTG = 4;          // TMA pipeline depth per warp
 constexpr int STG = 2560;        // stage: K codes 1 KB | V codes 1 KB | sidecars 256 B | pad
 constexpr int MAX_CTA_TILES = 8192;
 
-size_t decode_smem_bytes() { return 1024 + DW * NSTG * STG + (DW * NSTG + 1) * 8 + 2 * 1024 * 4 + 16 + MAX_CTA_TILES * 4; }
+size_t decode_smem_bytes() { return 1024 + DW * NSTG * STG + (DW * NSTG + 1) * 8 + 2 * 1024 * 4 + 16; }
 
 template <int NT, int ORDER>
-__global__ void __launch_bounds__(DW * 32, 1)
-    decode_tma_kernel(const __grid_constant__ DecodeParams p, const __grid_constant__ Signs signs,
-                      const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v) {
+__global__ void __launch_bounds__((DW + 1) * 32, 1)
+    decode_tma_kernel(const __grid_constant__ DecodeParams p, const __grid_constant__ Signs signs) {
   // dynamic smem starts 1024-aligned (no static smem in this kernel); indexing the
   // __shared__ array directly keeps every access in the shared window (LDS/STS)
   extern __shared__ __align__(1024) uint8_t sm_raw[];
@@ -240,75 +233,101 @@ __global__ void __launch_bounds__(DW * 32, 1)
   float* sq = reinterpret_cast<float*>(app_bar + 1);
   float* sqlo = sq + 1024;
   uint32_t* s_last = reinterpret_cast<uint32_t*>(sqlo + 1024);
-  int32_t* sbt = reinterpret_cast<int32_t*>(s_last + 4);
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = lane >> 2, i = lane & 3;
   const int h = blockIdx.x, split = blockIdx.y, b = blockIdx.z;
   const int G = p.G, H = p.pool.H;
-  const int len = p.lens[b];
+  // split ranges come from max_len, so the page-id loads below do not wait on lens[b]
+  const int len_raw = p.lens[b];
+  const int n_tiles_max = (p.max_len + 15) >> 4;
+  const int per = (n_tiles_max + p.splits - 1) / p.splits;
+  const int lo = min(n_tiles_max, split * per);
+  const int hi_max = min(n_tiles_max, lo + per);
+  const int len = min(len_raw, p.max_len);
   const int n_tiles = (len + 15) >> 4;
-  const int per = (n_tiles + p.splits - 1) / p.splits;
-  const int lo = min(n_tiles, split * per);
-  const int hi = min(n_tiles, lo + per);
+  const int hi = min(n_tiles, hi_max);
   const int t_new = (len - 1) >> 4;
   const bool has_app = p.new_slot != nullptr && len > 0 && p.new_slot[b] >= 0 && t_new >= lo && t_new < hi;
-
-  // ---- setup: barriers, block-table slice, query --------------------------------
-  if (threadIdx.x < DW * NSTG) mbar_init(&bars[threadIdx.x], 1 + 16);
-  if (threadIdx.x == DW * NSTG) mbar_init(app_bar, 2);
+  const int64_t cta_id = ((int64_t)b * p.splits + split) * H + h;
   if (threadIdx.x == 0) {
-    prefetch_tensormap(&tm_k);
-    prefetch_tensormap(&tm_v);
+    if (p.trace) p.trace[cta_id * 8 + 0] = gtimer();
+    if (len_raw > p.max_len && p.flags && h == 0 && split == 0) atomicOr(p.flags, KVR_FLAG_LEN_OVERFLOW);
   }
-  for (int t = lo + threadIdx.x; t < hi; t += blockDim.x)
-    sbt[t - lo] = p.bt[(int64_t)b * p.bt_stride + ((t << 4) >> p.log2P)];
-  fence_mbar_init();
-  __syncthreads();
 
-  // ---- the fused append (writer warps DW-1: K, DW-2: V) -------------------------
-  if (has_app && warp >= DW - 2) {
-    append_row_exact<ORDER>(p, signs, b, h, warp == DW - 1 ? 0 : 1);
+  // ---- setup (latency-ordered): q loads and the page-id windows go out first, the
+  // first NSTG bulk copies right after the one CTA-wide barrier; the query is
+  // prepared while they are in flight.
+  const bool tile_warp = warp < DW;  // warp DW is the append writer
+  const int my_tiles = (tile_warp && hi - lo - warp > 0) ? (hi - lo - warp + DW - 1) / DW : 0;
+  float qx[4] = {0.f, 0.f, 0.f, 0.f};
+  if (warp < 4 * NT && warp < G) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      qx[u] = load_q(p.q, p.q_dtype, ((int64_t)b * p.nq + (int64_t)h * G + warp) * 128 + 4 * lane + u);
+  }
+  if (tile_warp && lane < NSTG) mbar_init(&bars[warp * NSTG + lane], 1);
+  if (warp == DW && lane == 0) mbar_init(app_bar, 1);
+  fence_mbar_init();
+  __syncwarp();
+
+  const int pmask = (1 << p.log2P) - 1;
+  const int32_t* btrow = p.bt + (int64_t)b * p.bt_stride;
+  // one bulk copy per (page, head) tile: the cell holds codes and sidecars of 16 tokens
+  auto issue = [&](int k, int page) {
+    const int t = lo + warp + DW * k;
+    uint8_t* st = ring + (warp * NSTG + (k % NSTG)) * STG;
+    uint64_t* bar = &bars[warp * NSTG + (k % NSTG)];
+    if (lane == 0) {
+      int ci;
+      const uint8_t* cell = cell_of(p.pool, page, h, (t << 4) & pmask, ci);
+      fence_proxy_async();
+      mbar_expect_tx(bar, (uint32_t)p.pool.cell_bytes);
+      bulk_g2s(st, cell, (uint32_t)p.pool.cell_bytes, bar);
+    }
+  };
+  // page ids of this warp's tiles live in registers, 32 tiles per window: lane l
+  // of window w holds the page of tile k = 32 w + l; windows load one ahead
+  auto page_window = [&](int w) -> int {
+    const int t = lo + warp + DW * (32 * w + lane);
+    return (tile_warp && t < hi_max) ? __ldg(&btrow[(t << 4) >> p.log2P]) : 0;
+  };
+  int win_idx = 0;
+  int win0 = page_window(0), win1 = page_window(1);
+  auto page_of = [&](int k) -> int {  // warp-uniform k
+    while ((k >> 5) > win_idx) {
+      win0 = win1;
+      ++win_idx;
+      win1 = page_window(win_idx + 1);
+    }
+    return __shfl_sync(0xffffffffu, win0, k & 31);
+  };
+  __syncthreads();  // barrier inits visible CTA-wide
+  int deferred = -1;  // the tile holding the token appended by this launch waits for the append
+#pragma unroll 1
+  for (int k = 0; k < NSTG && k < my_tiles; ++k) {
+    const int t = lo + warp + DW * k;
+    if (has_app && t == t_new) {
+      deferred = k;
+      continue;
+    }
+    issue(k, page_of(k));
+  }
+
+  // ---- the fused append: the writer warp produces the new token's K and V rows
+  // while the tile warps stream; only the tile holding that token waits for it
+  if (has_app && warp == DW) {
+    append_row_exact<ORDER>(p, signs, b, h, 0);
+    append_row_exact<ORDER>(p, signs, b, h, 1);
     fence_proxy_async_global();
     __threadfence();
     __syncwarp();
     if (lane == 0) mbar_arrive(app_bar);
   }
-
-  // ---- per-warp TMA pipeline ------------------------------------------------------
-  const uint8_t* pb = p.pool.base;
-  const int pmask = (1 << p.log2P) - 1;
-  auto issue = [&](int k) {
-    const int t = lo + warp + DW * k;
-    const int stg = k % NSTG;
-    uint8_t* st = ring + (warp * NSTG + stg) * STG;
-    uint64_t* bar = &bars[warp * NSTG + stg];
-    if (has_app && t == t_new) mbar_wait(app_bar, 0);
-    const int page = sbt[t - lo];
-    const int slot0 = (t << 4) & pmask;
-    if (lane == 0) {
-      fence_proxy_async();
-      mbar_expect_tx(bar, 2048);
-      tma_load_4d(st, &tm_k, bar, 0, h, slot0, page);
-      tma_load_4d(st + 1024, &tm_v, bar, 0, h, slot0, page);
-    }
-    if (lane < 16) {
-      const int tok = (t << 4) + lane;
-      if (tok < len) {
-        const uint8_t* blob = pb + (int64_t)page * p.pool.page_bytes;
-        const int idx = (slot0 + lane) * H + h;
-        float* sc = reinterpret_cast<float*>(st + 2048);
-        cp_async4(sc + lane, blob + p.pool.off_ks + 4 * idx);
-        cp_async4(sc + 16 + lane, blob + p.pool.off_vs + 4 * idx);
-        cp_async4(sc + 32 + lane, blob + ((p.pool.off_kz + idx) & ~3));
-        cp_async4(sc + 48 + lane, blob + ((p.pool.off_vz + idx) & ~3));
-      }
-      cp_async_arrive_noinc(bar);
-    }
-  };
-  const int my_tiles = (hi - lo - warp + DW - 1) / DW > 0 ? (hi - lo - warp + DW - 1) / DW : 0;
-#pragma unroll 1
-  for (int k = 0; k < NSTG && k < my_tiles; ++k) issue(k);
+  if (deferred >= 0) {
+    mbar_wait(app_bar, 0);
+    issue(deferred, page_of(deferred));
+  }
 
   // ---- query prep (overlaps the TMA fill): warp j < 4*NT owns q head j of this kv
   // head: sign flip + fp32 butterfly in registers/shuffles, per-head power-of-two
@@ -322,7 +341,7 @@ __global__ void __launch_bounds__(DW * 32, 1)
     if (j < G) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        x[u] = load_q(p.q, p.q_dtype, ((int64_t)b * p.nq + (int64_t)h * G + j) * 128 + 4 * lane + u);
+        x[u] = qx[u];
         if (p.rotate && p.has_signs && sign_bit(signs, 4 * lane + u)) x[u] = -x[u];
       }
       if (p.rotate) {
@@ -401,30 +420,32 @@ __global__ void __launch_bounds__(DW * 32, 1)
   }
 
   // ---- main loop over this warp's tiles ---------------------------------------------
+  if (p.trace && threadIdx.x == 0) p.trace[cta_id * 8 + 1] = gtimer();
 #pragma unroll 1
   for (int k = 0; k < my_tiles; ++k) {
     const int t = lo + warp + DW * k;
     const int stg = k % NSTG;
     const uint8_t* st = ring + (warp * NSTG + stg) * STG;
     mbar_wait(&bars[warp * NSTG + stg], (uint32_t)((k / NSTG) & 1));
-    // fragments out of the swizzled (64B) stage
-    const uint4 ka = *reinterpret_cast<const uint4*>(st + r * 64 + ((i ^ ((r >> 1) & 3)) << 4));
-    const uint4 kb = *reinterpret_cast<const uint4*>(st + (r + 8) * 64 + ((i ^ (((r + 8) >> 1) & 3)) << 4));
+    // fragments out of the staged cell: k_scale[16] | v_scale[16] | K codes [16][64] |
+    // V codes [16][64] | k_zp[16] | v_zp[16]
+    const uint4 ka = *reinterpret_cast<const uint4*>(st + 128 + r * 64 + 16 * i);
+    const uint4 kb = *reinterpret_cast<const uint4*>(st + 128 + (r + 8) * 64 + 16 * i);
     uint2 vw[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int tok = 2 * i + (u & 1) + 8 * (u >> 1);
-      vw[u] = *reinterpret_cast<const uint2*>(st + 1024 + tok * 64 + (((r >> 1) ^ ((tok >> 1) & 3)) << 4) + 8 * (r & 1));
+      vw[u] = *reinterpret_cast<const uint2*>(st + 1152 + tok * 64 + 8 * r);
     }
-    const float* sc = reinterpret_cast<const float*>(st + 2048);
-    const uint32_t* zw = reinterpret_cast<const uint32_t*>(st + 2048);
+    const float* sc = reinterpret_cast<const float*>(st);
     float sk0 = sc[r], sk1 = sc[r + 8], sv0 = sc[16 + r], sv1 = sc[16 + r + 8];
-    const int slot0 = (t << 4) & pmask;
-    const int sh0 = 8 * (((slot0 + r) * H + h) & 3), sh1 = 8 * (((slot0 + r + 8) * H + h) & 3);
-    const uint32_t kz0 = (zw[32 + r] >> sh0) & 0xFFu, kz1 = (zw[32 + r + 8] >> sh1) & 0xFFu;
-    const uint32_t vz0 = (zw[48 + r] >> sh0) & 0xFFu, vz1 = (zw[48 + r + 8] >> sh1) & 0xFFu;
+    const uint32_t kz0 = st[2176 + r], kz1 = st[2176 + r + 8], vz0 = st[2192 + r], vz1 = st[2192 + r + 8];
     __syncwarp();
-    if (k + NSTG < my_tiles) issue(k + NSTG);
+    if (k + NSTG < my_tiles) {
+      const int tn = t + DW * NSTG;
+      if (has_app && tn == t_new) mbar_wait(app_bar, 0);
+      issue(k + NSTG, page_of(k + NSTG));
+    }
 
     // ---- S = C_k q : 8 k-steps of m16n8k16 per 8-column tile
     float scv[NT][4];
@@ -518,6 +539,7 @@ __global__ void __launch_bounds__(DW * 32, 1)
 
   // ---- per-warp finalisation into shared memory (the ring is free now)
   __syncthreads();
+  if (p.trace && threadIdx.x == 0) p.trace[cta_id * 8 + 2] = gtimer();
   float* sred = reinterpret_cast<float*>(ring);  // [DW][8][130]
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
@@ -527,7 +549,7 @@ __global__ void __launch_bounds__(DW * 32, 1)
       Zs[nt] += __shfl_xor_sync(0xffffffffu, Zs[nt], o);
     }
     const int j = 4 * nt + i;
-    if (j < G) {
+    if (tile_warp && j < G) {
       float* row = sred + (warp * 8 + j) * 130;
 #pragma unroll
       for (int m = 0; m < 8; ++m) {
@@ -545,6 +567,7 @@ __global__ void __launch_bounds__(DW * 32, 1)
 
   // ---- CTA merge over warps -> (o, lse) of this split
   float* obuf = sq;
+  const int64_t hbase = (((int64_t)b * H + h) * p.splits) * 8;
   for (int x = threadIdx.x; x < G * 128; x += blockDim.x) {
     const int j = x >> 7, dd = x & 127;
     float mmax = -INFINITY;
@@ -555,8 +578,7 @@ __global__ void __launch_bounds__(DW * 32, 1)
 #pragma unroll
       for (int w = 0; w < DW; ++w) {
         const float mw = sred[(w * 8 + j) * 130 + 128];
-        if (mw == -INFINITY) continue;
-        const float f = exp2f(mw - mmax);
+        const float f = (mw == -INFINITY) ? 0.f : ex2f(mw - mmax);
         lt += f * sred[(w * 8 + j) * 130 + 129];
         ot += f * sred[(w * 8 + j) * 130 + dd];
       }
@@ -566,63 +588,100 @@ __global__ void __launch_bounds__(DW * 32, 1)
     if (p.splits == 1) {
       obuf[x] = o;
     } else {
-      const int64_t base = (((int64_t)b * H + h) * p.splits + split) * 8 + j;
-      p.ws_o[base * 128 + dd] = o;
-      if (dd == 0) p.ws_lse[base] = lse;
+      p.ws_o[(hbase + (int64_t)split * 8 + j) * 128 + dd] = o;
+      if (dd == 0) p.ws_lse[hbase + (int64_t)split * 8 + j] = lse;
     }
   }
   if (p.splits > 1) {
-    __threadfence();
+    // release the partial: CTA barrier, then one gpu-scope acq_rel atomic by thread 0
+    // (cumulative over the CTA's writes ordered before it by the barrier)
     __syncthreads();
     if (threadIdx.x == 0) {
-      const uint32_t prev = atomicAdd(&p.ws_cnt[(int64_t)b * H + h], 1u);
+      if (p.trace) p.trace[cta_id * 8 + 3] = gtimer();
+      uint32_t prev;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                   : "=r"(prev)
+                   : "l"(&p.ws_cnt[(int64_t)b * H + h])
+                   : "memory");
       *s_last = (prev == (uint32_t)p.splits - 1) ? 1u : 0u;
+      if (p.trace) p.trace[cta_id * 8 + 4] = gtimer();
     }
     __syncthreads();
-    if (!*s_last) return;
-    __threadfence();
-    // last CTA of (b, h): LSE-merge all splits; weights once per (split, head)
-    float* wts = sqlo;  // [S][8] weights, S <= 128
-    for (int x = threadIdx.x; x < G; x += blockDim.x) {
-      const int64_t base0 = (((int64_t)b * H + h) * p.splits) * 8 + x;
-      float lmax = -INFINITY;
-      for (int s = 0; s < p.splits; ++s) lmax = fmaxf(lmax, __ldcg(&p.ws_lse[base0 + (int64_t)s * 8]));
-      float tot = 0.f;
-      for (int s = 0; s < p.splits; ++s) {
-        const float ls = __ldcg(&p.ws_lse[base0 + (int64_t)s * 8]);
-        const float f = (ls == -INFINITY) ? 0.f : exp2f(ls - lmax);
-        wts[s * 8 + x] = f;
-        tot += f;
-      }
-      for (int s = 0; s < p.splits; ++s) wts[s * 8 + x] = tot > 0.f ? wts[s * 8 + x] / tot : 0.f;
+    if (!*s_last) {
+      if (p.trace && threadIdx.x == 0) p.trace[cta_id * 8 + 6] = gtimer();
+      return;
     }
-    __syncthreads();
+    // last CTA of (b, h): LSE-merge all splits.  Every thread re-derives the split
+    // weights of its q head from the lse values (same address across the warp), so
+    // the lse and o loads of a 32-split chunk go out together: one L2 round trip.
     for (int x = threadIdx.x; x < G * 128; x += blockDim.x) {
       const int j = x >> 7, dd = x & 127;
-      const int64_t base0 = (((int64_t)b * H + h) * p.splits) * 8 + j;
-      float ot = 0.f;
-#pragma unroll 4
-      for (int s = 0; s < p.splits; ++s) {
-        const float f = wts[s * 8 + j];
-        if (f != 0.f) ot += f * __ldcg(&p.ws_o[(base0 + (int64_t)s * 8) * 128 + dd]);
+      const float* lsrc = p.ws_lse + hbase + j;
+      const float* osrc = p.ws_o + (hbase + j) * 128 + dd;
+      float lmax = -INFINITY, tot = 0.f, ot = 0.f;
+      for (int s0 = 0; s0 < p.splits; s0 += 32) {
+        float lv[32], ov[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+          const bool in = s0 + u < p.splits;
+          lv[u] = in ? __ldcg(lsrc + (int64_t)(s0 + u) * 8) : -INFINITY;
+          ov[u] = in ? __ldcg(osrc + (int64_t)(s0 + u) * 8 * 128) : 0.f;
+        }
+        float cm = lmax;
+#pragma unroll
+        for (int u = 0; u < 32; ++u) cm = fmaxf(cm, lv[u]);
+        if (cm == -INFINITY) continue;
+        const float a = (lmax == -INFINITY) ? 0.f : exp2f(lmax - cm);
+        tot *= a;
+        ot *= a;
+        lmax = cm;
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+          const float f = (lv[u] == -INFINITY) ? 0.f : exp2f(lv[u] - cm);
+          tot += f;
+          ot += f * ov[u];
+        }
       }
-      obuf[x] = ot;
+      obuf[x] = tot > 0.f ? ot / tot : 0.f;
     }
-    if (threadIdx.x == 0) p.ws_cnt[(int64_t)b * H + h] = 0u;  // re-arm for the next launch
+    if (threadIdx.x == 0) {
+      p.ws_cnt[(int64_t)b * H + h] = 0u;  // re-arm for the next launch
+      if (p.trace) p.trace[cta_id * 8 + 5] = gtimer();
+    }
   }
   __syncthreads();
-  // ---- inverse rotation of the value branch: o @ H_blk @ diag(signs)
-  if (p.rotate && p.rot_v) {
-    cta_fwht_rows<ORDER>(obuf, G);
-    if (p.has_signs)
-      for (int x = threadIdx.x; x < G * 128; x += blockDim.x)
-        if (sign_bit(signs, x & 127)) obuf[x] = -obuf[x];
-    __syncthreads();
+  // ---- output: inverse rotation of the value branch (o @ H_blk @ diag(signs)),
+  // one warp per q head, fp32 butterfly in registers / shuffles
+  if (warp < G) {
+    float x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = obuf[warp * 128 + 4 * lane + u];
+    if (p.rotate && p.rot_v) {
+      const float a0 = x[0] + x[1], a1 = x[0] - x[1], a2 = x[2] + x[3], a3 = x[2] - x[3];
+      x[0] = a0 + a2;
+      x[1] = a1 + a3;
+      x[2] = a0 - a2;
+      x[3] = a1 - a3;
+#pragma unroll
+      for (int k = 0; (4 << k) < ORDER; ++k) {
+        const bool upper = (lane >> k) & 1;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float o = __shfl_xor_sync(0xffffffffu, x[u], 1 << k);
+          x[u] = upper ? o - x[u] : x[u] + o;
+        }
+      }
+      const float inv = (float)(1.0 / sqrt((double)ORDER));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        x[u] *= inv;
+        if (p.has_signs && sign_bit(signs, 4 * lane + u)) x[u] = -x[u];
+      }
+    }
+    float4* dst = reinterpret_cast<float4*>(p.out + ((int64_t)b * p.nq + (int64_t)h * G + warp) * 128) + lane;
+    *dst = make_float4(x[0], x[1], x[2], x[3]);
   }
-  for (int x = threadIdx.x; x < G * 128; x += blockDim.x) {
-    const int j = x >> 7, dd = x & 127;
-    p.out[((int64_t)b * p.nq + (int64_t)h * G + j) * 128 + dd] = obuf[x];
-  }
+  if (p.trace && threadIdx.x == 0) p.trace[cta_id * 8 + 6] = gtimer();
 }
 
 // Generic (any head_dim <= 256, any group) CUDA-core decode: one CTA per
@@ -635,8 +694,8 @@ __global__ void decode_generic_kernel(const __grid_constant__ DecodeParams p, co
   float* sml = gsm + d + (blockDim.x >> 5) * d;  // [warps][2]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int qh = blockIdx.x, b = blockIdx.y;
-  const int G = p.G, H = p.pool.H, h = qh / G;
-  const int len = p.lens[b];
+  const int G = p.G, h = qh / G;
+  const int len = min(p.lens[b], p.max_len);
   for (int x = threadIdx.x; x < d; x += blockDim.x) {
     float v = load_q(p.q, p.q_dtype, ((int64_t)b * p.nq + qh) * d + x);
     if (p.rotate && p.has_signs && sign_bit(signs, x)) v = -v;
@@ -664,16 +723,17 @@ __global__ void decode_generic_kernel(const __grid_constant__ DecodeParams p, co
 #pragma unroll
   for (int k = 0; k < 8; ++k) o[k] = 0.f;
   for (int t = warp; t < len; t += nw) {
-    int sl;
-    const uint8_t* blob = token_blob(p, b, t, sl);
-    const int idx = sl * H + h;
-    const float ks = reinterpret_cast<const float*>(blob + p.pool.off_ks)[idx];
-    const uint8_t kz = blob[p.pool.off_kz + idx];
-    const float vs = reinterpret_cast<const float*>(blob + p.pool.off_vs)[idx];
-    const uint8_t vz = blob[p.pool.off_vz + idx];
+    int ci;
+    const uint8_t* cell = token_cell(p, b, t, h, ci);
+    const float ks = *reinterpret_cast<const float*>(cell + cell_kscale(p.pool, ci));
+    const uint8_t kz = cell[cell_kzp(p.pool, ci)];
+    const float vs = *reinterpret_cast<const float*>(cell + cell_vscale(p.pool, ci));
+    const uint8_t vz = cell[cell_vzp(p.pool, ci)];
+    const uint8_t* kc = cell + cell_kcode(p.pool, ci);
+    const uint8_t* vc = cell + cell_vcode(p.pool, ci);
     float dot = 0.f;
     for (int k = 0, x = lane; x < d; x += 32, ++k) {
-      const uint8_t byte = blob[p.pool.off_kp + (int64_t)idx * (d / 2) + (x >> 1)];
+      const uint8_t byte = kc[x >> 1];
       const float c = (float)((x & 1) ? (byte >> 4) : (byte & 15));
       const float kh = (kz == 0xFF) ? ks : ks * (c - (float)kz);
       dot += kh * sq[x];
@@ -683,7 +743,7 @@ __global__ void decode_generic_kernel(const __grid_constant__ DecodeParams p, co
     const float a = exp2f((m - mn) * LOG2E), pw = exp2f((dot - mn) * LOG2E);
     l = l * a + pw;
     for (int k = 0, x = lane; x < d; x += 32, ++k) {
-      const uint8_t byte = blob[p.pool.off_vp + (int64_t)idx * (d / 2) + (x >> 1)];
+      const uint8_t byte = vc[x >> 1];
       const float c = (float)((x & 1) ? (byte >> 4) : (byte & 15));
       const float vh = (vz == 0xFF) ? vs : vs * (c - (float)vz);
       o[k] = o[k] * a + pw * vh;
@@ -760,8 +820,7 @@ int kvr_pick_splits(int batch, int H, int max_len, int P) {
 }
 
 template <int NT>
-static int launch_tma(const DecodeParams& p, const Signs& sg, const CUtensorMap& mk, const CUtensorMap& mv,
-                      dim3 grid, size_t smem, int order, cudaStream_t st) {
+static int launch_tma(const DecodeParams& p, const Signs& sg, dim3 grid, size_t smem, int order, cudaStream_t st) {
 #define KVR_DEC_CASE(ORD)                                                                               \
   case ORD: {                                                                                           \
     auto kern = decode_tma_kernel<NT, ORD>;                                                             \
@@ -770,7 +829,7 @@ static int launch_tma(const DecodeParams& p, const Signs& sg, const CUtensorMap&
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);               \
       set = true;                                                                                       \
     }                                                                                                   \
-    kern<<<grid, DW * 32, smem, st>>>(p, sg, mk, mv);                                                   \
+    kern<<<grid, (DW + 1) * 32, smem, st>>>(p, sg);                                                     \
     return 0;                                                                                           \
   }
   switch (order) {
@@ -783,28 +842,8 @@ static int launch_tma(const DecodeParams& p, const Signs& sg, const CUtensorMap&
   return KVR_ERR_UNSUPPORTED;
 }
 
-static CUresult encode_codes_map(CUtensorMap* map, const Pool& pool, int off) {
-  typedef CUresult (*encode_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-  static encode_fn fn = nullptr;
-  if (!fn) {
-    cudaDriverEntryPointQueryResult q;
-    void* f = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess || !f)
-      return CUDA_ERROR_NOT_FOUND;
-    fn = reinterpret_cast<encode_fn>(f);
-  }
-  // [num_pages][P][H][64 B] codes of one side: dims innermost first
-  const cuuint64_t dims[4] = {64, (cuuint64_t)pool.H, (cuuint64_t)pool.P, (cuuint64_t)pool.num_pages};
-  const cuuint64_t strides[3] = {64, (cuuint64_t)pool.H * 64, (cuuint64_t)pool.page_bytes};
-  const cuuint32_t box[4] = {64, 1, 16, 1};
-  const cuuint32_t estr[4] = {1, 1, 1, 1};
-  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, pool.base + off, dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-}
+static unsigned long long* g_trace = nullptr;
+void kvr_set_decode_trace(void* trace) { g_trace = reinterpret_cast<unsigned long long*>(trace); }
 
 int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_t* bt, int bt_stride,
                       const int32_t* lens, int batch, int nq, int max_len, int order, int rotate, int rot_v,
@@ -831,6 +870,8 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
   p.new_dtype = new_dtype;
   p.new_slot = new_slot;
   p.flags = flags;
+  p.trace = g_trace;
+  p.max_len = max_len;
   int l2 = 0;
   while ((1 << l2) < pool.P) ++l2;
   const bool pow2 = (1 << l2) == pool.P;
@@ -838,9 +879,8 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
   Signs sg = s;
   if (!has) for (auto& x : sg.w) x = 0u;
   if (!pow2) return KVR_ERR_UNSUPPORTED;
-  const bool tma_ok = pool.d == 128 && pool.P >= 16 && (p.G == 1 || p.G == 2 || p.G == 4 || p.G == 8) &&
-                      (reinterpret_cast<uintptr_t>(pool.base) & 15) == 0 && (pool.page_bytes & 15) == 0 &&
-                      (pool.off_vp & 15) == 0;
+  const bool tma_ok = pool.d == 128 && pool.T == 16 && (p.G == 1 || p.G == 2 || p.G == 4 || p.G == 8) &&
+                      (reinterpret_cast<uintptr_t>(pool.base) & 15) == 0 && (pool.cell_bytes & 15) == 0;
   if (tma_ok) {
     if (splits <= 0) splits = kvr_pick_splits(batch, pool.H, max_len, pool.P);
     if (splits > 128) splits = 128;
@@ -851,14 +891,10 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
     p.ws_o = reinterpret_cast<float*>(ws);
     p.ws_lse = p.ws_o + units * 128;
     p.ws_cnt = reinterpret_cast<uint32_t*>(p.ws_lse + units);
-    CUtensorMap mk, mv;
-    if (encode_codes_map(&mk, pool, pool.off_kp) != CUDA_SUCCESS) return KVR_ERR_CUDA;
-    if (encode_codes_map(&mv, pool, pool.off_vp) != CUDA_SUCCESS) return KVR_ERR_CUDA;
     dim3 grid(pool.H, splits, batch);
     const int ord = rotate ? order : 128;
     const size_t smem = decode_smem_bytes();
-    return p.G == 8 ? launch_tma<2>(p, sg, mk, mv, grid, smem, ord, st)
-                    : launch_tma<1>(p, sg, mk, mv, grid, smem, ord, st);
+    return p.G == 8 ? launch_tma<2>(p, sg, grid, smem, ord, st) : launch_tma<1>(p, sg, grid, smem, ord, st);
   }
   if (new_slot) return KVR_ERR_UNSUPPORTED;  // the fused append lives in the TMA kernel only
   if (pool.d > 256 || (pool.d & 31)) return KVR_ERR_UNSUPPORTED;

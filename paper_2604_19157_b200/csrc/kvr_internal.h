@@ -40,6 +40,8 @@ int kvr_launch_decode(const void* q, int q_dtype, const kvr::Pool& pool, const i
                       cudaStream_t st, const void* new_k = nullptr, const void* new_v = nullptr, int new_dtype = 0,
                       const int64_t* new_slot = nullptr, uint32_t* flags = nullptr);
 
+void kvr_set_decode_trace(void* trace);
+
 // Tensor-map encoder resolved through the runtime (no -lcuda link dependency).
 CUresult kvr_encode_tensor_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows,
                                   uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_rows,

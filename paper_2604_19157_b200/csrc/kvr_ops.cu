@@ -151,12 +151,11 @@ __global__ void store_exact_kernel(const TIn* k, const TIn* v, int64_t n_tok, co
     }
     if (rot) warp_fwht_f64(s, d, order, lane);
     const int64_t page = slot / pool.P;
-    const int sl = (int)(slot % pool.P);
-    uint8_t* blob = pool.base + page * (int64_t)pool.page_bytes;
-    const int idx = sl * H + head;
-    uint8_t* payload = blob + (side ? pool.off_vp : pool.off_kp) + (int64_t)idx * (d >> 1);
-    float* sc = reinterpret_cast<float*>(blob + (side ? pool.off_vs : pool.off_ks)) + idx;
-    uint8_t* zp = blob + (side ? pool.off_vz : pool.off_kz) + idx;
+    int ci;
+    uint8_t* cell = cell_of(pool, page, head, (int)(slot % pool.P), ci);
+    uint8_t* payload = cell + (side ? cell_vcode(pool, ci) : cell_kcode(pool, ci));
+    float* sc = reinterpret_cast<float*>(cell + (side ? cell_vscale(pool, ci) : cell_kscale(pool, ci)));
+    uint8_t* zp = cell + (side ? cell_vzp(pool, ci) : cell_kzp(pool, ci));
     warp_quantize_f64(s, d, lane, payload, sc, zp);
     __syncwarp();
   }
@@ -180,12 +179,11 @@ __global__ void dequant_pages_kernel(Pool pool, const int32_t* bt, int bt_stride
     const int b = (int)(r / max_len);
     if (t >= lens[b]) continue;
     const int page = bt[(int64_t)b * bt_stride + t / pool.P];
-    const int sl = t % pool.P;
-    const uint8_t* blob = pool.base + (int64_t)page * pool.page_bytes;
-    const int i2 = sl * H + head;
-    const uint8_t byte = blob[(side ? pool.off_vp : pool.off_kp) + (int64_t)i2 * half + m];
-    const float sc = reinterpret_cast<const float*>(blob + (side ? pool.off_vs : pool.off_ks))[i2];
-    const uint8_t z = blob[(side ? pool.off_vz : pool.off_kz) + i2];
+    int ci;
+    const uint8_t* cell = cell_of(pool, page, head, t % pool.P, ci);
+    const uint8_t byte = cell[(side ? cell_vcode(pool, ci) : cell_kcode(pool, ci)) + m];
+    const float sc = *reinterpret_cast<const float*>(cell + (side ? cell_vscale(pool, ci) : cell_kscale(pool, ci)));
+    const uint8_t z = cell[side ? cell_vzp(pool, ci) : cell_kzp(pool, ci)];
     TOut* o = (side ? v_out : k_out) + ((((int64_t)b * max_len + t) * H + head) * d) + 2 * m;
     if (z == 0xFF) {
       o[0] = (TOut)sc;

@@ -358,16 +358,14 @@ __global__ void __launch_bounds__(FS_WARPS * 32, KVR_FS_MINB)
     if (write && slot >= 0) {
       const Pool& pl = p.pool;
       const int head = (int)(row % H);
-      const int64_t page = slot / pl.P;
-      const int sl = (int)(slot % pl.P);
-      uint8_t* blob = pl.base + page * (int64_t)pl.page_bytes;
-      const int idx = sl * H + head;
-      uint4* dst = reinterpret_cast<uint4*>(blob + (side ? pl.off_vp : pl.off_kp) + (int64_t)idx * 64);
+      int ci;
+      uint8_t* cell = cell_of(pl, slot / pl.P, head, (int)(slot % pl.P), ci);
+      uint4* dst = reinterpret_cast<uint4*>(cell + (side ? cell_vcode(pl, ci) : cell_kcode(pl, ci)));
 #pragma unroll
       for (int i = 0; i < 4; ++i)
         dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
-      reinterpret_cast<float*>(blob + (side ? pl.off_vs : pl.off_ks))[idx] = scale_out;
-      blob[(side ? pl.off_vz : pl.off_kz) + idx] = (uint8_t)zp_out;
+      *reinterpret_cast<float*>(cell + (side ? cell_vscale(pl, ci) : cell_kscale(pl, ci))) = scale_out;
+      cell[side ? cell_vzp(pl, ci) : cell_kzp(pl, ci)] = (uint8_t)zp_out;
     }
   }
 }
@@ -421,7 +419,7 @@ static int launch_fast_impl(const void* k, const void* v, int64_t n_tok, const i
 int kvr_launch_store_fast(const void* k, const void* v, int in_dtype, int64_t n_tok, const int64_t* slots,
                           const Pool& pool, int order, int rot_k, int rot_v, const Signs& s, int has,
                           uint32_t* flags, cudaStream_t st) {
-  if (pool.d != 128) return KVR_ERR_UNSUPPORTED;
+  if (pool.d != 128 || (pool.T & 1)) return KVR_ERR_UNSUPPORTED;  // 16-B aligned code rows
   if (in_dtype != KVR_BF16 && in_dtype != KVR_F16) return KVR_ERR_UNSUPPORTED;
   if ((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) & 15) return KVR_ERR_UNSUPPORTED;
   if (!(rot_k || rot_v)) order = 128;  // plain twin: order is irrelevant

@@ -49,10 +49,12 @@ def test_pool_init_layout(libpath):
     lib = _lib.lib()
     pool = _lib.KvrPool()
     assert lib.kvr_pool_init(ctypes.byref(pool), None, 10, 16, 8, 128) == 0
-    # .kvpg page record: 16*8*64*2 payload + 16*8*(4+1)*2 sidecar = 17664 B (cache.py:56-68)
+    # B200 cell layout: 8 heads x one 16-token cell of 16*(128+10) = 2208 B per page
+    # (same bytes as a .kvpg record: 17664 B, cache.py:56-68)
     assert pool.page_bytes == 17664
-    assert (pool.off_k_payload, pool.off_v_payload, pool.off_k_scale, pool.off_k_zp, pool.off_v_scale,
-            pool.off_v_zp) == (0, 8192, 16384, 16896, 17024, 17536)
+    assert (pool.cell_tokens, pool.cell_bytes) == (16, 2208)
+    assert lib.kvr_pool_init(ctypes.byref(pool), None, 10, 4, 2, 32) == 0
+    assert (pool.cell_tokens, pool.cell_bytes, pool.page_bytes) == (4, 176, 2 * 176)
     assert lib.kvr_abi_version() == 1
     assert lib.kvr_decode_workspace_bytes(1, 8, 32, 128, 4) > 0
 

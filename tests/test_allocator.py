@@ -62,3 +62,15 @@ def test_byte_accounting_frozen():
     assert capacity_tokens(1 << 20, BIG, "bf16") == 256
     assert capacity_tokens(1 << 20, BIG, "int4") == 1024
     assert page_bytes(BIG) == 16 * 1104
+
+
+@pytest.mark.parametrize("lay", [(32, 8, 128, 128, 16), (4, 2, 32, 16, 4), (4, 1, 128, 64, 32), (4, 2, 32, 16, 3)])
+def test_cell_layout_round_trip(lay):
+    """Device cell layout <-> reference .kvpg page records (cache.py:387-397) is a bijection."""
+    from paper_2604_19157_b200.cache import cells_to_records, records_to_cells, page_bytes, record_bytes
+
+    layout = HeadLayout(*lay)
+    rec = np.random.default_rng(0).integers(0, 256, size=(5, record_bytes(layout)), dtype=np.uint8)
+    cells = records_to_cells(rec, layout)
+    assert cells.shape == (5, page_bytes(layout))
+    np.testing.assert_array_equal(cells_to_records(cells, layout), rec)

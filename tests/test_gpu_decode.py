@@ -212,7 +212,7 @@ def test_fused_decode_step(targets, G):
     for b, s in enumerate(seqs):
         L = t.sequence_length(s) - 1
         page = t.sequence_pages(s)[L // 16]
-        blob = t.pool[page].cpu().numpy()
+        blob = t.page_records([page])
         from kvtest_util import page_fields
         f = page_fields(blob, 16, H, d)
         kk = O.rotate_rows(kb[b].double().numpy(), 128, signs) if rotate else kb[b].double().numpy()

@@ -106,7 +106,7 @@ def _fast_vs_oracle(kind, n_tok, H, d, order, rotate, targets, seed, dtype=torch
     spec = RotationSpec(order=order, signs=signs, targets=targets) if rotate else None
     t.append_batch([0] * n_tok, torch.tensor(k, dtype=dtype).cuda(), torch.tensor(v, dtype=dtype).cuda(), spec=spec,
                    exact=exact)
-    blobs = t.pool[:npages].cpu().numpy()
+    blobs = t.page_records(range(npages))
     f = page_fields(blobs, P, H, d)
     stats = {}
     for side, x, rot in (("k", k, rotate), ("v", v, rotate and targets is Targets.KEYS_AND_VALUES)):
