@@ -86,10 +86,11 @@ int kvr_pool_init(kvr_pool* pool, void* base, int64_t num_pages, int32_t page_to
                   int32_t num_kv_heads, int32_t head_dim);
 
 const char* kvr_last_error(void);
-/* Profiling aid: when non-NULL, decode launches record per-CTA globaltimer
- * stamps [start, main-loop start, main-loop end, partial written, split counter
- * returned, merge done, end, 0] (u64 ns) into `trace` (device buffer of
- * batch * splits * num_kv_heads * 8 entries).  NULL disables. */
+/* Profiling aid: when non-NULL, decode launches record a per-CTA timeline into
+ * `trace` (device buffer of batch * splits * num_kv_heads * 16 u64): [0] the
+ * globaltimer (ns) and [1] clock64 at CTA entry, [k >= 2] clock64 at stamp k
+ * (2 loop start, 3 loop end, 4/5 CTA merge, 6 partial stored, 7 split counter
+ * back, 8 split weights, 9 merged, 10 exit; 0 = not reached).  NULL disables. */
 void kvr_debug_decode_trace(void* trace);
 int kvr_abi_version(void);
 /* Number of SMs of the current device (0 if no device). */

@@ -12,7 +12,7 @@ import os
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libkvrot_b200.so")
+LIB_PATH = os.environ.get("KVR_LIB_PATH") or os.path.join(_HERE, "_lib", "libkvrot_b200.so")  # override: tools only
 
 KVR_F64, KVR_F32, KVR_BF16, KVR_F16 = 0, 1, 2, 3
 KVR_KEYS_ONLY, KVR_KEYS_AND_VALUES = 0, 1

@@ -46,6 +46,8 @@ class DecodePlan:
     (block table, lengths, split count, workspace) so repeated steps issue one
     kernel launch and no host<->device traffic."""
 
+    _RING = 4  # pinned staging buffers in flight (step() inputs + metadata)
+
     def __init__(self, table: PageTable, seqs: Sequence[int], num_splits: int = 0, extra_tokens: int = 0):
         self.table = table
         self.seqs = list(seqs)
@@ -53,23 +55,57 @@ class DecodePlan:
         for s in self.seqs:
             if table.sequence_length(s) == 0 and extra_tokens == 0:
                 raise EmptySequenceError(f"sequence {s} has no tokens")
-        self.bt, self.lens, self.max_len = table.block_table(self.seqs)
-        self.max_len += extra_tokens
+        B, P = len(self.seqs), lay.page_tokens
+        cur = max(table.sequence_length(s) for s in self.seqs)
+        self.max_len = cur + extra_tokens
+        # the block table reserves the pages of `extra_tokens` future steps, so
+        # step() only patches new entries and never reallocates
+        self.bt, lens, _ = table.block_table(self.seqs, width=-(-self.max_len // P))
+        self._known_pages = [len(table._seq_pages[s]) for s in self.seqs]
+        # step metadata lives in one device block: slots int64[B] | lens int32[B];
+        # step() refreshes it (plus the step's q/k/v when given on the host)
+        # with a single pinned host->device copy
+        self._meta_bytes = (12 * B + 255) // 256 * 256
+        self._dev = torch.zeros(self._meta_bytes, dtype=torch.uint8, device=table.device)
+        self.slots = self._dev[:8 * B].view(torch.int64)
+        self.lens = self._dev[8 * B:12 * B].view(torch.int32)
+        self.lens.copy_(lens)
+        self._host = []
+        self._host_i = 0
         if num_splits <= 0:
-            num_splits = _lib.lib().kvr_decode_pick_splits(len(self.seqs), lay.num_kv_heads, self.max_len,
-                                                           lay.page_tokens)
+            num_splits = _lib.lib().kvr_decode_pick_splits(B, lay.num_kv_heads, self.max_len, P)
         self.splits = num_splits
-        self.ws = table.workspace(len(self.seqs), lay.num_q_heads, num_splits)
+        self.ws = table.workspace(B, lay.num_q_heads, num_splits)
+
+    def _patch_pages(self) -> None:
+        """Write block-table entries of pages the sequences gained since the last call."""
+        P = self.table.layout.page_tokens
+        for i, s in enumerate(self.seqs):
+            pages = self.table._seq_pages[s]
+            k0 = self._known_pages[i]
+            if len(pages) > k0:
+                if len(pages) > self.bt.shape[1]:
+                    raise ShapeError(f"sequence {s} grew to {len(pages) * P} tokens, beyond the plan's "
+                                     f"{self.bt.shape[1] * P}-token block table; build a new DecodePlan "
+                                     f"(or pass extra_tokens)")
+                self.bt[i, k0:len(pages)].copy_(torch.tensor(pages[k0:], dtype=torch.int32), non_blocking=False)
+                self._known_pages[i] = len(pages)
 
     def refresh(self) -> None:
         """Re-read block table and lengths after appends (small host->device copies)."""
-        bt, lens, max_len = self.table.block_table(self.seqs)
-        if bt.shape == self.bt.shape:
-            self.bt.copy_(bt)
-        else:
-            self.bt = bt
-        self.lens.copy_(lens)
-        self.max_len = max(self.max_len, max_len)
+        self._patch_pages()
+        lens = [self.table.sequence_length(s) for s in self.seqs]
+        self.lens.copy_(torch.tensor(lens, dtype=torch.int32))
+        self.max_len = max(self.max_len, max(lens))
+
+    def _staging(self, nbytes: int) -> tuple[torch.Tensor, torch.cuda.Event]:
+        if not self._host or self._host[0][0].numel() < nbytes:
+            self._host = [(torch.empty(nbytes, dtype=torch.uint8).pin_memory(), torch.cuda.Event())
+                          for _ in range(self._RING)]
+        buf, ev = self._host[self._host_i]
+        self._host_i = (self._host_i + 1) % self._RING
+        ev.synchronize()  # the copy that last read this buffer has run
+        return buf, ev
 
     def run(self, q: torch.Tensor, spec: Optional[RotationSpec], out: Optional[torch.Tensor] = None) -> torch.Tensor:
         table, lay = self.table, self.table.layout
@@ -121,14 +157,38 @@ class DecodePlan:
     def step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, spec: Optional[RotationSpec],
              out: Optional[torch.Tensor] = None) -> torch.Tensor:
         """One serving decode step for every sequence of the plan: allocate the new
-        token's slot (reference page order), then one fused append + decode launch."""
+        token's slot (reference page order), then one fused append + decode launch.
+        q (B, nq, d) and k_new/v_new (B, H, d) may be host tensors: they travel
+        with the step metadata in one pinned host->device copy."""
         table = self.table
+        B = len(self.seqs)
         slots, fresh = table.alloc.plan(self.seqs)
         table._zero_pages(fresh)
-        self.refresh()
-        slot_t = torch.from_numpy(slots).to(table.device, non_blocking=True)
-        dev = table.device
-        return self.run_step(q.to(dev), k_new.to(dev).contiguous(), v_new.to(dev).contiguous(), slot_t, spec, out)
+        self._patch_pages()
+        lens = np.fromiter((table._seq_len[s] for s in self.seqs), dtype=np.int32, count=B)
+        self.max_len = max(self.max_len, int(lens.max()))
+        host_in = [t for t in (q, k_new, v_new) if not t.is_cuda]
+        sizes = [t.numel() * t.element_size() for t in host_in]
+        offs, o = [], self._meta_bytes
+        for n in sizes:
+            offs.append(o)
+            o += (n + 255) // 256 * 256
+        buf, ev = self._staging(o)
+        buf[:8 * B].view(torch.int64).numpy()[:] = slots
+        buf[8 * B:12 * B].view(torch.int32).numpy()[:] = lens
+        for t, off, n in zip(host_in, offs, sizes):
+            buf[off:off + n].view(t.dtype).view(t.shape).copy_(t)
+        if o > self._dev.numel():
+            dev = torch.zeros(o, dtype=torch.uint8, device=table.device)
+            dev[:self._meta_bytes].copy_(self._dev[:self._meta_bytes])
+            self._dev = dev
+            self.slots = dev[:8 * B].view(torch.int64)
+            self.lens = dev[8 * B:12 * B].view(torch.int32)
+        self._dev[:o].copy_(buf[:o], non_blocking=True)
+        ev.record()
+        dev_in = iter(self._dev[off:off + n].view(t.dtype).view(t.shape) for t, off, n in zip(host_in, offs, sizes))
+        q, k_new, v_new = (t if t.is_cuda else next(dev_in) for t in (q, k_new, v_new))
+        return self.run_step(q, k_new.contiguous(), v_new.contiguous(), self.slots, spec, out)
 
 
 def decode_batch(q: torch.Tensor, table: PageTable, seqs: Sequence[int], spec: Optional[RotationSpec] = None,

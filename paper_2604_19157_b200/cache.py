@@ -189,30 +189,31 @@ class PageAllocator:
         (in order), taking new pages lowest id first.  All-or-nothing: on
         exhaustion nothing is committed.  Returns (slots, freshly taken pages)."""
         P = self.page_tokens
+        # pass 1: validate and count the pages needed (no state touched), so a
+        # step costs O(len(seqs) log free) and never copies the free heap
         lens: dict[int, int] = {}
-        new_pages: dict[int, list[int]] = {}
-        free = list(self.free)
+        need = 0
+        for seq in seqs:
+            self.require(seq)
+            t = lens.get(seq, self.seq_len[seq])
+            if t % P == 0 and t // P >= len(self.seq_pages[seq]):
+                need += 1
+            lens[seq] = t + 1
+        if need > len(self.free):
+            raise CapacityExceededError(f"page pool exhausted ({self.num_pages} pages)")
+        # pass 2: commit
         slots = np.empty(len(seqs), dtype=np.int64)
         fresh = []
         for n, seq in enumerate(seqs):
-            self.require(seq)
-            t = lens.get(seq, self.seq_len[seq])
-            if t % P == 0:
-                if not free:
-                    raise CapacityExceededError(f"page pool exhausted ({self.num_pages} pages)")
-                pid = heapq.heappop(free)
-                new_pages.setdefault(seq, []).append(pid)
-                fresh.append(pid)
+            t = self.seq_len[seq]
             owned = self.seq_pages[seq]
             idx = t // P
-            pid = owned[idx] if idx < len(owned) else new_pages[seq][idx - len(owned)]
-            slots[n] = pid * P + t % P
-            lens[seq] = t + 1
-        self.free = free
-        for seq, pids in new_pages.items():
-            self.seq_pages[seq].extend(pids)
-        for seq, t in lens.items():
-            self.seq_len[seq] = t
+            if idx >= len(owned):
+                pid = heapq.heappop(self.free)
+                owned.append(pid)
+                fresh.append(pid)
+            slots[n] = owned[idx] * P + t % P
+            self.seq_len[seq] = t + 1
         return slots, fresh
 
 
@@ -245,6 +246,7 @@ class PageTable:
         self.flags = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.alloc = PageAllocator(num_pages, layout.page_tokens)
         self._ws = None
+        self._ws_cnt = 0
 
     # reference-compatible views of the allocator state (cache.py:149-153)
     @property
@@ -424,10 +426,11 @@ class PageTable:
             raise NonFiniteInputError("k/v contained NaN or Inf (rows were not written)")
 
     # -- reads (cache.py:319-362) -------------------------------------------------
-    def block_table(self, seqs: Sequence[int]) -> tuple[torch.Tensor, torch.Tensor, int]:
-        """Device (int32 [B, max_pages] page ids, int32 [B] lengths, max length)."""
+    def block_table(self, seqs: Sequence[int], width: int = 0) -> tuple[torch.Tensor, torch.Tensor, int]:
+        """Device (int32 [B, max_pages] page ids, int32 [B] lengths, max length).
+        `width` reserves room for pages a decode plan will append later."""
         rows = [self._seq_pages[s] for s in seqs]
-        width = max(1, max((len(r) for r in rows), default=1))
+        width = max(1, width, max((len(r) for r in rows), default=1))
         bt = np.zeros((len(seqs), width), dtype=np.int32)
         for i, r in enumerate(rows):
             bt[i, :len(r)] = r
@@ -531,4 +534,11 @@ class PageTable:
                                                      self.layout.head_dim, max(splits, 1))
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
+            self._ws_cnt = 0
+        # the split counters sit at the start of the workspace and are left at
+        # zero by every launch; bytes first used as counters are zeroed once here
+        cnt = (batch * self.layout.num_kv_heads * 4 + 255) // 256 * 256
+        if cnt > self._ws_cnt:
+            self._ws[:cnt].zero_()
+            self._ws_cnt = cnt
         return self._ws

@@ -40,6 +40,9 @@ struct DecodeParams {
   int bt_stride;
   const int32_t* lens;
   int batch, nq, G, splits, order, rotate, rot_v, has_signs, log2P, max_len;
+  int cps_log2;       // log2(cells of one head per page) = log2(P / 16) on the TMA path
+  uint32_t mul24;     // = 2^24 (see shr8)
+  int use_cluster;    // 2..16 splits: merge them in a thread-block cluster
   float* out;
   float* ws_o;       // [B][H][S][8][128]
   float* ws_lse;     // [B][H][S][8]
@@ -52,6 +55,18 @@ struct DecodeParams {
   uint32_t* flags;
   unsigned long long* trace;  // optional: per CTA 8 globaltimer stamps (ns), see kvr_debug_decode_trace
 };
+
+KVR_DEV unsigned long long clk64() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %clock64;" : "=l"(t));
+  return t;
+}
+// Debug timeline (kvr_debug_decode_trace): per CTA 16 u64, [0] globaltimer and
+// [1] clock64 at entry, [k >= 2] clock64 at stamp k (written by thread 0).
+#define KVR_STAMP(k)                                                   \
+  do {                                                                 \
+    if (p.trace && threadIdx.x == 0) p.trace[cta_id * 16 + (k)] = clk64(); \
+  } while (0)
 
 KVR_DEV unsigned long long gtimer() {
   unsigned long long t;
@@ -70,6 +85,46 @@ KVR_DEV void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint
       "{%0,%1,%2,%3};"
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// x >> 8 on the FMA pipe (IMAD.HI) instead of the ALU pipe, which the nibble
+// masks already keep busy
+// (m = 2^24 arrives as a kernel parameter so ptxas cannot strength-reduce it)
+#ifndef KVR_MERGE_LD
+#define KVR_MERGE_LD 0
+#endif
+#ifndef KVR_ATOM
+#define KVR_ATOM 0
+#endif
+// loads of other CTAs' split partials (after the acquiring counter atomic)
+KVR_DEV float ld_partial(const float* a) {
+#if KVR_MERGE_LD == 0
+  return __ldcg(a);
+#elif KVR_MERGE_LD == 1
+  return *a;
+#elif KVR_MERGE_LD == 2
+  return __ldg(a);
+#else
+  float v;
+  asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(a));
+  return v;
+#endif
+}
+#ifndef KVR_SHR_IMAD
+#define KVR_SHR_IMAD 0
+#endif
+#ifndef KVR_LATE_V
+#define KVR_LATE_V 1
+#endif
+KVR_DEV uint32_t shr8(uint32_t x, uint32_t m) {
+#if KVR_SHR_IMAD
+  uint32_t r;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(m));
+  return r;
+#else
+  (void)m;
+  return x >> 8;
+#endif
 }
 
 KVR_DEV float ex2f(float x) {
@@ -210,141 +265,614 @@ KVR_DEV void append_row_exact(const DecodeParams& p, const Signs& sg, int b, int
 KVR_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+KVR_DEV bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0u;
+}
 KVR_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+// Programmatic dependent launch: wait for the previous grid in the stream / let
+// the next one start its prologue (griddepcontrol, sm_90+).
+KVR_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+KVR_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-constexpr int DW = 15;  // tile warps per CTA (one CTA per SM) + 1 writer warp for the fused append;
-                       // 16 warps in all: 4 per SM sub-partition keeps the 128-register budget
-constexpr int NSTG = 4;          // TMA pipeline depth per warp
-constexpr int STG = 2560;        // stage: K codes 1 KB | V codes 1 KB | sidecars 256 B | pad
-constexpr int MAX_CTA_TILES = 8192;
+// ---- thread-block cluster helpers (split merge through distributed shared memory)
+KVR_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// final barrier: only says "my remote reads are done" (their values were consumed)
+KVR_DEV void cluster_sync_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+KVR_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// generic address of `local` in the shared memory of cluster CTA `rank`: plain
+// loads through it are independent and pipeline (ordering comes from the barrier)
+KVR_DEV const float* dsmem_ptr(const float* local, uint32_t rank) {
+  const float* r;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(r) : "l"(local), "r"(rank));
+  return r;
+}
 
-size_t decode_smem_bytes() { return 1024 + DW * NSTG * STG + (DW * NSTG + 1) * 8 + 2 * 1024 * 4 + 16; }
+constexpr int NWARPS = 16;       // one CTA per SM, 4 warps per SM sub-partition (128-register budget)
+constexpr int CELL = 2208;       // one cell: T = 16 tokens of one head, d = 128
+constexpr int RING_CELLS = 4;    // cells in flight per warp (NSTG stages of C cells)
+#ifndef KVR_PRE
+#define KVR_PRE 32
+#endif
+constexpr int MERGE_PRELOAD = KVR_PRE;  // split partials whose o-values are loaded before the lse pass
+constexpr int MAX_SPLITS = 256;
 
-template <int NT, int ORDER>
-__global__ void __launch_bounds__((DW + 1) * 32, 1)
+// smem: ring [NWARPS][RING_CELLS][CELL] | bars [NWARPS*RING_CELLS + 1] | q fragments 4 KB | out 4 KB | misc
+constexpr int SM_BARS = NWARPS * RING_CELLS * CELL;
+constexpr int SM_FRAG = SM_BARS + (NWARPS * RING_CELLS + 1) * 8 + 8;  // 16-B aligned
+constexpr int SM_OBUF = SM_FRAG + 4096;
+constexpr int SM_MISC = SM_OBUF + 4096;                               // sumq[8] ksc[8] tot[8] flag lse[8]
+constexpr int SM_TOTAL = SM_MISC + 256;
+size_t decode_smem_bytes() { return 1024 + SM_TOTAL; }
+
+// Fragments of one staged cell: k_scale[16] | v_scale[16] | K codes [16][64] |
+// V codes [16][64] | k_zp[16] | v_zp[16]
+struct CellFrag {
+  uint4 ka, kb;
+  uint2 vw[4];
+  float sk0, sk1, sv0, sv1;
+  uint32_t kz0, kz1, vz0, vz1;
+};
+KVR_DEV void load_cell_k(CellFrag& f, const uint8_t* st, int r, int i) {
+  f.ka = *reinterpret_cast<const uint4*>(st + 128 + r * 64 + 16 * i);
+  f.kb = *reinterpret_cast<const uint4*>(st + 128 + (r + 8) * 64 + 16 * i);
+}
+KVR_DEV void load_cell_rest(CellFrag& f, const uint8_t* st, int r, int i) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int tok = 2 * i + (u & 1) + 8 * (u >> 1);
+    f.vw[u] = *reinterpret_cast<const uint2*>(st + 1152 + tok * 64 + 8 * r);
+  }
+  const float* sc = reinterpret_cast<const float*>(st);
+  f.sk0 = sc[r];
+  f.sk1 = sc[r + 8];
+  f.sv0 = sc[16 + r];
+  f.sv1 = sc[16 + r + 8];
+  f.kz0 = st[2176 + r];
+  f.kz1 = st[2176 + r + 8];
+  f.vz0 = st[2192 + r];
+  f.vz1 = st[2192 + r + 8];
+}
+
+// K2+K3.  grid (kv head, split, sequence); NWARPS warps, one CTA per SM.  With
+// APPEND the last warp writes the step's new K/V token (bit-exact f64) while the
+// other DW warps stream their tiles through private rings of NSTG stages of C
+// cells (one mbarrier per stage, one bulk copy per cell).
+template <int NT, int ORDER, bool APPEND, int C, bool CL>
+__global__ void __launch_bounds__(NWARPS * 32, 1)
     decode_tma_kernel(const __grid_constant__ DecodeParams p, const __grid_constant__ Signs signs) {
-  // dynamic smem starts 1024-aligned (no static smem in this kernel); indexing the
-  // __shared__ array directly keeps every access in the shared window (LDS/STS)
+  constexpr int DW = APPEND ? NWARPS - 1 : NWARPS;
+  constexpr int NSTG = RING_CELLS / C;
+  constexpr int STG = C * CELL;
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = sm_raw + ((1024u - (smem_u32(sm_raw) & 1023u)) & 1023u);
-  uint8_t* ring = sm;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + DW * NSTG * STG);
-  uint64_t* app_bar = bars + DW * NSTG;
-  float* sq = reinterpret_cast<float*>(app_bar + 1);
-  float* sqlo = sq + 1024;
-  uint32_t* s_last = reinterpret_cast<uint32_t*>(sqlo + 1024);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + SM_BARS);
+  uint64_t* app_bar = bars + NWARPS * RING_CELLS;
+  uint16_t* sfrag = reinterpret_cast<uint16_t*>(sm + SM_FRAG);  // [NT][8 k-steps][32 lanes][2 regs][2 halves]
+  float* obuf = reinterpret_cast<float*>(sm + SM_OBUF);         // [G][128]
+  float* s_sumq = reinterpret_cast<float*>(sm + SM_MISC);       // [8]
+  float* s_ksc = s_sumq + 8;                                    // [8]
+  float* s_tot = s_sumq + 16;                                   // [8]
+  uint32_t* s_last = reinterpret_cast<uint32_t*>(s_sumq + 24);
+  float* s_lse = s_sumq + 25;                                   // [8] (cluster merge)
+  float* s_mstar = s_sumq + 40;                                 // [8] CTA reference point per q head
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = lane >> 2, i = lane & 3;
   const int h = blockIdx.x, split = blockIdx.y, b = blockIdx.z;
   const int G = p.G, H = p.pool.H;
-  // split ranges come from max_len, so the page-id loads below do not wait on lens[b]
-  const int len_raw = p.lens[b];
+  const int64_t cta_id = ((int64_t)b * p.splits + split) * H + h;
+  if (p.trace && threadIdx.x == 0) {
+    p.trace[cta_id * 16 + 0] = gtimer();
+    p.trace[cta_id * 16 + 1] = clk64();
+  }
+
+  // ---- prologue (independent of the previous grid): split range from max_len,
+  // the cell addresses of this warp's first 64 tiles, barrier init.
+  // Warp w owns the groups g = w, w + DW, ... of C consecutive tiles of the split;
+  // its j-th tile is t = lo + C (w + DW (j / C)) + j % C.
   const int n_tiles_max = (p.max_len + 15) >> 4;
   const int per = (n_tiles_max + p.splits - 1) / p.splits;
   const int lo = min(n_tiles_max, split * per);
   const int hi_max = min(n_tiles_max, lo + per);
+  const bool tile_warp = warp < DW;
+  const int32_t* btrow = p.bt + (int64_t)b * p.bt_stride;
+  const int cps = p.cps_log2;  // log2(cells of one head per page)
+  auto tile_of = [&](int j) { return lo + C * (warp + DW * (j / C)) + j % C; };
+  // lane l of window w holds the address of this warp's tile j = 32 w + l
+  auto page_window = [&](int w) -> int {
+    const int t = tile_of(32 * w + lane);
+    return (tile_warp && t < hi_max) ? __ldg(&btrow[t >> cps]) : 0;
+  };
+  const uint8_t* head_base = p.pool.base + (int64_t)(h << cps) * p.pool.cell_bytes;
+  const int cmask = (1 << cps) - 1;
+  auto window_addr = [&](int w, int page) -> const uint8_t* {
+    const int t = tile_of(32 * w + lane);
+    return head_base + (int64_t)page * p.pool.page_bytes + (t & cmask) * p.pool.cell_bytes;
+  };
+  int wnext = page_window(1), win_idx = 0;
+  const uint8_t* wcur = window_addr(0, page_window(0));
+  const int len_raw = __ldg(&p.lens[b]);
+  if (threadIdx.x <= NWARPS * RING_CELLS) mbar_init(&bars[threadIdx.x], 1);  // + app_bar
+  fence_mbar_init();
+  __syncthreads();
+
   const int len = min(len_raw, p.max_len);
   const int n_tiles = (len + 15) >> 4;
   const int hi = min(n_tiles, hi_max);
-  const int t_new = (len - 1) >> 4;
-  const bool has_app = p.new_slot != nullptr && len > 0 && p.new_slot[b] >= 0 && t_new >= lo && t_new < hi;
-  const int64_t cta_id = ((int64_t)b * p.splits + split) * H + h;
-  if (threadIdx.x == 0) {
-    if (p.trace) p.trace[cta_id * 8 + 0] = gtimer();
-    if (len_raw > p.max_len && p.flags && h == 0 && split == 0) atomicOr(p.flags, KVR_FLAG_LEN_OVERFLOW);
-  }
+  const int t_new = APPEND ? ((len - 1) >> 4) : -1;  // tile holding the appended token
+  // tiles from `guard` on may hold tokens written by the previous grid (the last
+  // step's append): they are requested only after griddepcontrol.wait
+  const int guard = max(len - 2, 0) >> 4;
+  const int my_groups = (tile_warp && hi - lo - C * warp > 0) ? (hi - lo - C * warp + C * DW - 1) / (C * DW) : 0;
 
-  // ---- setup (latency-ordered): q loads and the page-id windows go out first, the
-  // first NSTG bulk copies right after the one CTA-wide barrier; the query is
-  // prepared while they are in flight.
-  const bool tile_warp = warp < DW;  // warp DW is the append writer
-  const int my_tiles = (tile_warp && hi - lo - warp > 0) ? (hi - lo - warp + DW - 1) / DW : 0;
+  uint8_t* ring_w = sm + warp * RING_CELLS * CELL;
+  uint64_t* bar_w = bars + warp * RING_CELLS;
+  auto advance_to = [&](int j) {  // warp-uniform, non-decreasing j
+    if ((j >> 5) != win_idx) {
+      wcur = window_addr(win_idx + 1, wnext);
+      ++win_idx;
+      wnext = page_window(win_idx + 1);
+    }
+  };
+  // group k -> stage k % NSTG: one expect_tx, one bulk copy per valid cell
+  auto issue = [&](int k) {
+    advance_to(C * k);
+    const uint8_t* src[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+      src[c] = reinterpret_cast<const uint8_t*>(
+          __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(wcur), (C * k + c) & 31));
+    if (lane == 0) {
+      const int t0 = tile_of(C * k);
+      const int nc = min(C, hi - t0);
+      const int s = k % NSTG;
+      fence_proxy_async();
+      mbar_expect_tx(&bar_w[s], (uint32_t)(nc * CELL));
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        if (c < nc) bulk_g2s(ring_w + s * STG + c * CELL, src[c], (uint32_t)CELL, &bar_w[s]);
+    }
+  };
+  auto group_last = [&](int k) { return min(tile_of(C * k) + C, hi) - 1; };
+  // first NSTG groups of this warp: the immutable ones go out before the wait on
+  // the previous grid (programmatic dependent launch overlaps them with its tail)
+  int k0 = 0;
+#pragma unroll 1
+  for (; k0 < NSTG && k0 < my_groups && group_last(k0) < guard; ++k0) issue(k0);
+
+  pdl_wait();  // q, the new token, the workspace and recent pages may come from the previous grid
+  pdl_launch_dependents();
+  if (threadIdx.x == 0 && len_raw > p.max_len && p.flags && h == 0 && split == 0)
+    atomicOr(p.flags, KVR_FLAG_LEN_OVERFLOW);
+
   float qx[4] = {0.f, 0.f, 0.f, 0.f};
-  if (warp < 4 * NT && warp < G) {
+  if (warp < G) {
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       qx[u] = load_q(p.q, p.q_dtype, ((int64_t)b * p.nq + (int64_t)h * G + warp) * 128 + 4 * lane + u);
   }
-  if (tile_warp && lane < NSTG) mbar_init(&bars[warp * NSTG + lane], 1);
-  if (warp == DW && lane == 0) mbar_init(app_bar, 1);
-  fence_mbar_init();
-  __syncwarp();
-
-  const int pmask = (1 << p.log2P) - 1;
-  const int32_t* btrow = p.bt + (int64_t)b * p.bt_stride;
-  // one bulk copy per (page, head) tile: the cell holds codes and sidecars of 16 tokens
-  auto issue = [&](int k, int page) {
-    const int t = lo + warp + DW * k;
-    uint8_t* st = ring + (warp * NSTG + (k % NSTG)) * STG;
-    uint64_t* bar = &bars[warp * NSTG + (k % NSTG)];
-    if (lane == 0) {
-      int ci;
-      const uint8_t* cell = cell_of(p.pool, page, h, (t << 4) & pmask, ci);
-      fence_proxy_async();
-      mbar_expect_tx(bar, (uint32_t)p.pool.cell_bytes);
-      bulk_g2s(st, cell, (uint32_t)p.pool.cell_bytes, bar);
-    }
-  };
-  // page ids of this warp's tiles live in registers, 32 tiles per window: lane l
-  // of window w holds the page of tile k = 32 w + l; windows load one ahead
-  auto page_window = [&](int w) -> int {
-    const int t = lo + warp + DW * (32 * w + lane);
-    return (tile_warp && t < hi_max) ? __ldg(&btrow[(t << 4) >> p.log2P]) : 0;
-  };
-  int win_idx = 0;
-  int win0 = page_window(0), win1 = page_window(1);
-  auto page_of = [&](int k) -> int {  // warp-uniform k
-    while ((k >> 5) > win_idx) {
-      win0 = win1;
-      ++win_idx;
-      win1 = page_window(win_idx + 1);
-    }
-    return __shfl_sync(0xffffffffu, win0, k & 31);
-  };
-  __syncthreads();  // barrier inits visible CTA-wide
-  int deferred = -1;  // the tile holding the token appended by this launch waits for the append
+  // the group holding the new token waits for the writer warp
+  const int k_new = (APPEND && tile_warp && t_new >= lo && t_new < hi && ((t_new - lo) / C) % DW == warp)
+                        ? (t_new - lo) / C / DW
+                        : -1;
+  bool def_pending = false;
 #pragma unroll 1
-  for (int k = 0; k < NSTG && k < my_tiles; ++k) {
-    const int t = lo + warp + DW * k;
-    if (has_app && t == t_new) {
-      deferred = k;
+  for (int k = k0; k < NSTG && k < my_groups; ++k) {
+    if (k == k_new) {
+      def_pending = true;
       continue;
     }
-    issue(k, page_of(k));
+    issue(k);
   }
 
-  // ---- the fused append: the writer warp produces the new token's K and V rows
-  // while the tile warps stream; only the tile holding that token waits for it
-  if (has_app && warp == DW) {
-    append_row_exact<ORDER>(p, signs, b, h, 0);
-    append_row_exact<ORDER>(p, signs, b, h, 1);
-    fence_proxy_async_global();
-    __threadfence();
+  if (APPEND && warp == DW) {  // the writer warp: append, then release the deferred group
+    if (len > 0 && p.new_slot[b] >= 0) {
+      append_row_exact<ORDER>(p, signs, b, h, 0);
+      append_row_exact<ORDER>(p, signs, b, h, 1);
+      fence_proxy_async_global();
+      __threadfence();
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(app_bar);
   }
-  if (deferred >= 0) {
-    mbar_wait(app_bar, 0);
-    issue(deferred, page_of(deferred));
-  }
 
-  // ---- query prep (overlaps the TMA fill): warp j < 4*NT owns q head j of this kv
-  // head: sign flip + fp32 butterfly in registers/shuffles, per-head power-of-two
-  // normalisation, fp16 hi/lo split, scattered straight into MMA-fragment order
-  uint16_t* sfrag = reinterpret_cast<uint16_t*>(sq);        // [NT][8 k-steps][2 regs][32 lanes][2 halves]
-  float* s_sumq = sqlo;                                     // [8]
-  float* s_ksc = sqlo + 8;                                  // [8]
+  // ---- query prep: warp j < 4 NT owns q head j of this kv head (sign flip + fp32
+  // butterfly, power-of-two normalisation, fp16 hi/lo split in MMA-fragment order);
+  // columns j >= G are zero padding (qx = 0)
   if (warp < 4 * NT) {
     const int j = warp;
-    float x[4] = {0.f, 0.f, 0.f, 0.f};
-    if (j < G) {
+    float x[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        x[u] = qx[u];
-        if (p.rotate && p.has_signs && sign_bit(signs, 4 * lane + u)) x[u] = -x[u];
+    for (int u = 0; u < 4; ++u) {
+      x[u] = qx[u];
+      if (p.rotate && p.has_signs && sign_bit(signs, 4 * lane + u)) x[u] = -x[u];
+    }
+    if (p.rotate) {
+      const float a0 = x[0] + x[1], a1 = x[0] - x[1], a2 = x[2] + x[3], a3 = x[2] - x[3];
+      x[0] = a0 + a2;
+      x[1] = a1 + a3;
+      x[2] = a0 - a2;
+      x[3] = a1 - a3;
+#pragma unroll
+      for (int k = 0; (4 << k) < ORDER; ++k) {
+        const bool upper = (lane >> k) & 1;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float o = __shfl_xor_sync(0xffffffffu, x[u], 1 << k);
+          x[u] = upper ? o - x[u] : x[u] + o;
+        }
       }
-      if (p.rotate) {
+      const float inv = (float)(1.0 / sqrt((double)ORDER));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] *= inv;
+    }
+    float amax = fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])), fmaxf(fabsf(x[2]), fabsf(x[3])));
+    amax = warp_max(amax);
+    const int e2 = amax > 0.f ? ilogbf(amax) - 13 : 0;  // q' = q 2^-e2, max|q'| in [2^13, 2^14)
+    const float qs = ldexpf(1.0f, -e2);
+    float hs = 0.f;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int d = 4 * lane + u, rem = d & 31;
+      const int ii = d >> 5, s = 2 * (rem >> 3) + ((rem & 3) >> 1), slot2 = rem & 1, e = (rem >> 2) & 1;
+      const float v = x[u] * qs;
+      const float hi_ = __half2float(__float2half_rn(v));
+      const float lo_ = __half2float(__float2half_rn(v - hi_));
+      hs += hi_ + lo_;
+      const float f = slot2 ? (1.0f / 16.0f) : 1.0f;  // x16 nibble slots
+      const int nt = j >> 2, col = 2 * (j & 3);
+      // sfrag[nt][s][lane'][slot2][e]: lane' = col * 4 + ii owns B-fragment word slot2
+      const int base = (nt * 8 + s) * 128 + slot2 * 2 + e;
+      sfrag[base + ((col + 0) * 4 + ii) * 4] = __half_as_ushort(__float2half_rn(hi_ * f));
+      sfrag[base + ((col + 1) * 4 + ii) * 4] = __half_as_ushort(__float2half_rn(lo_ * f));
+    }
+    hs = warp_sum(hs);
+    if (lane == 0) {
+      s_sumq[j] = hs * 5.9604644775390625e-08f;  // x 2^-24 (MMA units)
+      s_ksc[j] = ldexpf(1.0f, e2 + 24) * LOG2E * (float)(1.0 / sqrt(128.0));
+    }
+  }
+  __syncthreads();
+  // query B fragments: registers for one 8-column tile; with two (G = 8) they stay
+  // in shared memory (one LDS.64 per k-step) to keep the loop inside 128 registers
+  constexpr bool BQ_REG = NT == 1;
+  const uint2* sfrag2 = reinterpret_cast<const uint2*>(sfrag);
+  uint2 bq[BQ_REG ? 8 : 1];
+  float sumq[NT], kscale[NT];
+  if (BQ_REG) {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) bq[BQ_REG ? s : 0] = sfrag2[s * 32 + lane];
+  }
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    sumq[nt] = s_sumq[4 * nt + i];
+    kscale[nt] = s_ksc[4 * nt + i];
+  }
+
+  float M[NT], lsum[NT], Zs[NT];
+  float acc[NT][8][4];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    M[nt] = -INFINITY;
+    lsum[nt] = 0.f;
+    Zs[nt] = 0.f;
+#pragma unroll
+    for (int m = 0; m < 8; ++m)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[nt][m][c] = 0.f;
+  }
+  float Mth = -INFINITY;  // min over columns of M + 7: a logit above it forces a rescale
+  const uint32_t m24 = p.mul24;
+
+  // ---- main loop over this warp's groups of C tiles ----------------------------------
+  KVR_STAMP(2);  // main loop start
+  int stg = 0;
+  uint32_t phase = 0;
+#pragma unroll 1
+  for (int k = 0; k < my_groups; ++k) {
+    const int tg = tile_of(C * k);  // first tile of the group
+    if (APPEND && def_pending) {
+      if (k == k_new) mbar_wait(app_bar, 0);
+      if (k == k_new || mbar_test(app_bar, 0)) {
+        issue(k_new);
+        def_pending = false;
+      }
+    }
+    const uint8_t* st = ring_w + stg * STG;
+    mbar_wait(&bar_w[stg], phase);
+    CellFrag f[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) load_cell_k(f[c], st + c * CELL, r, i);
+    if (!KVR_LATE_V) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) load_cell_rest(f[c], st + c * CELL, r, i);
+    }
+
+    // ---- S = C_k q : 8 k-steps of m16n8k16 per 8-column tile and cell
+    // C * NT independent accumulator chains of 8 HMMAs
+    float scv[C][NT][4];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) scv[c][nt][q] = 0.f;
+      const uint32_t kw0[4] = {f[c].ka.x, f[c].ka.y, f[c].ka.z, f[c].ka.w};
+      const uint32_t kw1[4] = {f[c].kb.x, f[c].kb.y, f[c].kb.z, f[c].kb.w};
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const uint32_t wa = kw0[s >> 1], wb = kw1[s >> 1];
+        const uint32_t xa = (s & 1) ? shr8(wa, m24) : wa, xb = (s & 1) ? shr8(wb, m24) : wb;
+        const uint32_t a0 = xa & 0x000F000Fu, a2 = xa & 0x00F000F0u;
+        const uint32_t a1 = xb & 0x000F000Fu, a3 = xb & 0x00F000F0u;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const uint2 bb = BQ_REG ? bq[BQ_REG ? s : 0] : sfrag2[(nt * 8 + s) * 32 + lane];
+          mma16816(scv[c][nt], a0, a1, a2, a3, bb.x, bb.y);
+        }
+      }
+    }
+
+    // V words and sidecars after the QK MMAs (keeps the register peak down), then
+    // refill this stage with group k + NSTG
+    if (KVR_LATE_V) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) load_cell_rest(f[c], st + c * CELL, r, i);
+    }
+    if (k + NSTG < my_groups) {
+      if (k + NSTG == k_new) {
+        mbar_wait(app_bar, 0);
+        def_pending = false;
+      }
+      __syncwarp();
+      issue(k + NSTG);
+    }
+
+    // ---- logits from the sidecars (sentinel rows: the scale slot holds the
+    // offset and the codes are 0)
+    float l0[C][NT], l1[C][NT], lgv0[C], lgv1[C], zv0[C], zv1[C];
+    bool sentinel = false;
+#pragma unroll
+    for (int c = 0; c < C; ++c) sentinel |= (f[c].kz0 | f[c].kz1 | f[c].vz0 | f[c].vz1) > 15u;
+    const bool rare = __any_sync(0xffffffffu, sentinel);
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      float sk0 = f[c].sk0, sk1 = f[c].sk1, sv0 = f[c].sv0, sv1 = f[c].sv1;
+      float zk0 = (float)f[c].kz0, zk1 = (float)f[c].kz1;
+      zv0[c] = (float)f[c].vz0;
+      zv1[c] = (float)f[c].vz1;
+      if (rare) {
+        if (f[c].kz0 == 0xFFu) { zk0 = -sk0; sk0 = 1.f; }
+        if (f[c].kz1 == 0xFFu) { zk1 = -sk1; sk1 = 1.f; }
+        if (f[c].vz0 == 0xFFu) { zv0[c] = -sv0; sv0 = 1.f; }
+        if (f[c].vz1 == 0xFFu) { zv1[c] = -sv1; sv1 = 1.f; }
+      }
+      lgv0[c] = __log2f(sv0);
+      lgv1[c] = __log2f(sv1);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        l0[c][nt] = (scv[c][nt][0] + scv[c][nt][1] - zk0 * sumq[nt]) * (sk0 * kscale[nt]);
+        l1[c][nt] = (scv[c][nt][2] + scv[c][nt][3] - zk1 * sumq[nt]) * (sk1 * kscale[nt]);
+      }
+    }
+    float b0[C][NT], b1[C][NT];
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        b0[c][nt] = l0[c][nt] + lgv0[c];  // log2(p * s_v)
+        b1[c][nt] = l1[c][nt] + lgv1[c];
+      }
+    if (tg + C > hi || tg + C >= n_tiles) {  // a missing or partial tile in this group
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const int t0 = ((tg + c) << 4) + r;
+        const bool in = tg + c < hi;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          if (!in || t0 >= len) l0[c][nt] = b0[c][nt] = -INFINITY;
+          if (!in || t0 + 8 >= len) l1[c][nt] = b1[c][nt] = -INFINITY;
+        }
+        if (!in) zv0[c] = zv1[c] = 0.f;
+      }
+    }
+    bool over = false;
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) over |= fmaxf(b0[c][nt], b1[c][nt]) > Mth;
+    // lazy rescaling: the reference point M only moves when a logit exceeds it by
+    // > 2^7, so w = 2^(b - M) <= 128 and w * 2^8 stays inside fp16 range
+    if (__any_sync(0xffffffffu, over)) {
+      Mth = INFINITY;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        float tm = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < C; ++c) tm = fmaxf(tm, fmaxf(b0[c][nt], b1[c][nt]));
+        tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 4));
+        tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 8));
+        tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 16));
+        if (tm > M[nt] + 7.0f) {
+          const float alpha = (M[nt] == -INFINITY) ? 0.f : ex2f(M[nt] - tm);
+          lsum[nt] *= alpha;
+          Zs[nt] *= alpha;
+#pragma unroll
+          for (int m = 0; m < 8; ++m)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[nt][m][q] *= alpha;
+          M[nt] = tm;
+        }
+        Mth = fminf(Mth, M[nt] + 7.0f);
+      }
+    }
+
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      uint32_t wlo[NT], whi[NT];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const float ms = (M[nt] == -INFINITY) ? 0.f : M[nt];
+        const float w0 = ex2f(b0[c][nt] - ms), w1 = ex2f(b1[c][nt] - ms);  // = p_t * s_v * 2^(.)
+        const float p0 = ex2f(l0[c][nt] - ms), p1 = ex2f(l1[c][nt] - ms);  // = p_t * 2^(.)
+        lsum[nt] += p0 + p1;
+        Zs[nt] += w0 * zv0[c] + w1 * zv1[c];
+        // fp16 hi/lo of w * 2^8 (w <= 2^7): 22-bit weights, the lo half out of fp16
+        // subnormals for weights down to ~2^-21 of the reference point
+        const float w0s = w0 * 256.0f, w1s = w1 * 256.0f;
+        const float w0h = __half2float(__float2half_rn(w0s)), w1h = __half2float(__float2half_rn(w1s));
+        wlo[nt] = movtrans(pack_h2(w0h, w0s - w0h));  // tokens 0..7  -> b0,b1
+        whi[nt] = movtrans(pack_h2(w1h, w1s - w1h));  // tokens 8..15 -> b2,b3
+      }
+
+      // ---- O^T += C_v^T W : 8 m-tiles (16 dims each) of m16n8k16
+      uint32_t xr[2][2][8];  // [token pair (2i,2i+1)|(2i+8,2i+9)][word][dim e]
+#pragma unroll
+      for (int tp = 0; tp < 2; ++tp)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const uint32_t wa = q ? f[c].vw[2 * tp].y : f[c].vw[2 * tp].x;
+          const uint32_t wb = q ? f[c].vw[2 * tp + 1].y : f[c].vw[2 * tp + 1].x;
+          const uint32_t t0w = prmt(wa, wb, 0x5410u), t1w = prmt(wa, wb, 0x7632u);
+          const uint32_t t0s = shr8(t0w, m24), t1s = shr8(t1w, m24);
+          xr[tp][q][0] = t0w & 0x000F000Fu;
+          xr[tp][q][1] = t0w & 0x00F000F0u;
+          xr[tp][q][2] = t0s & 0x000F000Fu;
+          xr[tp][q][3] = t0s & 0x00F000F0u;
+          xr[tp][q][4] = t1w & 0x000F000Fu;
+          xr[tp][q][5] = t1w & 0x00F000F0u;
+          xr[tp][q][6] = t1s & 0x000F000Fu;
+          xr[tp][q][7] = t1s & 0x00F000F0u;
+        }
+#pragma unroll
+      for (int m = 0; m < 8; ++m)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+          mma16816(acc[nt][m], xr[0][0][m], xr[0][1][m], xr[1][0][m], xr[1][1][m], wlo[nt], whi[nt]);
+    }
+    if (++stg == NSTG) {
+      stg = 0;
+      phase ^= 1u;
+    }
+  }
+
+  // ---- CTA merge: every warp publishes its reference points M and takes the CTA
+  // maximum M*, stores its partial rescaled to M*, and one pass sums the warps.
+  // Dims are stored permuted, p = (d % 16) * 8 + d / 16, with a 136-float head
+  // stride, so both the stores (lane = (r, i)) and the summing reads hit 32 banks.
+  __syncthreads();  // all warps are out of the loop: the rings are free
+  KVR_STAMP(3);  // all warps out of the loop
+  float* s_m = reinterpret_cast<float*>(sm);  // [NWARPS][8] reference points
+  float* s_lw = s_m + NWARPS * 8;             // [NWARPS][8] rescaled softmax sums
+  float* sred = s_lw + NWARPS * 8;            // [NWARPS][8][136] rescaled partials
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      lsum[nt] += __shfl_xor_sync(0xffffffffu, lsum[nt], o);
+      Zs[nt] += __shfl_xor_sync(0xffffffffu, Zs[nt], o);
+    }
+    if (r == 0) s_m[warp * 8 + 4 * nt + i] = tile_warp ? M[nt] : -INFINITY;
+  }
+  __syncthreads();
+  KVR_STAMP(4);  // reference points published
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int j = 4 * nt + i;
+    if (j < G && tile_warp) {
+      float mstar = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < DW; ++w) mstar = fmaxf(mstar, s_m[w * 8 + j]);
+      if (warp == 0 && r == 0) s_mstar[j] = mstar;
+      const float sc = (M[nt] == -INFINITY) ? 0.f : ex2f(M[nt] - mstar);
+      float* dst = sred + (warp * 8 + j) * 136 + r;
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const float f = ((m & 1) ? 65536.0f / 16.0f : 65536.0f) * sc;  // undo 2^-24 (codes), 2^8 (w), x16 nibble
+        dst[m * 8] = (acc[nt][m][0] + acc[nt][m][1]) * f - Zs[nt] * sc;
+        dst[(m + 8) * 8] = (acc[nt][m][2] + acc[nt][m][3]) * f - Zs[nt] * sc;
+      }
+      if (r == 0) s_lw[warp * 8 + j] = lsum[nt] * sc;
+    }
+  }
+  __syncthreads();
+  KVR_STAMP(5);  // rescaled warp partials in smem
+
+  // ---- normalised (o, lse) of this split: thread x sums permuted slot pp of head j
+  const int64_t hbase = (((int64_t)b * H + h) * p.splits) * 8;
+  for (int x = threadIdx.x; x < G * 128; x += blockDim.x) {
+    const int j = x >> 7, pp = x & 127, dd = (pp & 7) * 16 + (pp >> 3);
+    float lt = 0.f, ot = 0.f;
+#pragma unroll
+    for (int w = 0; w < DW; ++w) {
+      lt += s_lw[w * 8 + j];
+      ot += sred[(w * 8 + j) * 136 + pp];
+    }
+    const float o = (lt > 0.f) ? ot / lt : 0.f;
+    const float lse = (lt > 0.f) ? s_mstar[j] + __log2f(lt) : -INFINITY;
+    if (p.splits == 1 || CL) {
+      obuf[j * 128 + dd] = o;
+      if (CL && pp == 0) s_lse[j] = lse;
+    } else {
+      __stcg(&p.ws_o[(hbase + (int64_t)split * 8 + j) * 128 + dd], o);
+      if (pp == 0) __stcg(&p.ws_lse[hbase + (int64_t)split * 8 + j], lse);
+    }
+  }
+  if (CL) {
+    // ---- split merge inside the thread-block cluster (grid.y = splits = cluster
+    // size): CTA r merges the q heads j = r, r + S, ... from every CTA's shared
+    // memory and applies the inverse rotation
+    cluster_sync_all();
+    KVR_STAMP(6);  // cluster barrier passed
+    const int S = p.splits;
+    const int rank = (int)cluster_rank();
+    float* omerge = reinterpret_cast<float*>(sm);  // [8][128] in the (free) rings
+    for (int j = rank; j < G; j += S) {
+      if (threadIdx.x < 128) {
+        const int dd = threadIdx.x;
+        float lv[16], ov[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          lv[u] = u < S ? *dsmem_ptr(s_lse + j, (uint32_t)u) : -INFINITY;
+          ov[u] = u < S ? *dsmem_ptr(obuf + j * 128 + dd, (uint32_t)u) : 0.f;
+        }
+        float mx = -INFINITY;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) mx = fmaxf(mx, lv[u]);
+        float tot = 0.f, ot = 0.f;
+        if (mx != -INFINITY) {
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const float w = (lv[u] == -INFINITY) ? 0.f : ex2f(lv[u] - mx);
+            tot += w;
+            ot += w * ov[u];
+          }
+        }
+        omerge[j * 128 + dd] = tot > 0.f ? ot / tot : 0.f;
+      }
+    }
+    __syncthreads();
+    if (warp < G && warp % S == rank) {
+      float x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = omerge[warp * 128 + 4 * lane + u];
+      if (p.rotate && p.rot_v) {
         const float a0 = x[0] + x[1], a1 = x[0] - x[1], a2 = x[2] + x[3], a3 = x[2] - x[3];
         x[0] = a0 + a2;
         x[1] = a1 + a3;
@@ -361,292 +889,101 @@ __global__ void __launch_bounds__((DW + 1) * 32, 1)
         }
         const float inv = (float)(1.0 / sqrt((double)ORDER));
 #pragma unroll
-        for (int u = 0; u < 4; ++u) x[u] *= inv;
-      }
-    }
-    float amax = fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])), fmaxf(fabsf(x[2]), fabsf(x[3])));
-    amax = warp_max(amax);
-    const int e2 = amax > 0.f ? ilogbf(amax) - 13 : 0;  // q' = q 2^-e2, max|q'| in [2^13, 2^14)
-    const float qs = ldexpf(1.0f, -e2);
-    float hs = 0.f;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int d = 4 * lane + u, rem = d & 31;
-      const int ii = d >> 5, s = 2 * (rem >> 3) + ((rem & 3) >> 1), slot2 = rem & 1, e = (rem >> 2) & 1;
-      const float v = x[u] * qs;
-      const float hi = __half2float(__float2half_rn(v));
-      const float lo = __half2float(__float2half_rn(v - hi));
-      hs += hi + lo;
-      const float f = slot2 ? (1.0f / 16.0f) : 1.0f;  // x16 nibble slots
-      const int nt = j >> 2, col = 2 * (j & 3);
-      const int base = (((nt * 8 + s) * 2 + slot2) * 32) * 2 + e;
-      sfrag[base + ((col + 0) * 4 + ii) * 2] = __half_as_ushort(__float2half_rn(hi * f));
-      sfrag[base + ((col + 1) * 4 + ii) * 2] = __half_as_ushort(__float2half_rn(lo * f));
-    }
-    hs = warp_sum(hs);
-    if (lane == 0) {
-      s_sumq[j] = hs * 5.9604644775390625e-08f;  // x 2^-24 (MMA units)
-      s_ksc[j] = ldexpf(1.0f, e2 + 24) * LOG2E * (float)(1.0 / sqrt(128.0));
-    }
-  }
-  __syncthreads();
-  uint32_t bq[NT][8][2];
-  float sumq[NT], kscale[NT];
-  {
-    const uint32_t* f32 = reinterpret_cast<const uint32_t*>(sfrag);
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-#pragma unroll
-      for (int s = 0; s < 8; ++s) {
-        bq[nt][s][0] = f32[((nt * 8 + s) * 2 + 0) * 32 + lane];
-        bq[nt][s][1] = f32[((nt * 8 + s) * 2 + 1) * 32 + lane];
-      }
-      sumq[nt] = s_sumq[4 * nt + i];
-      kscale[nt] = s_ksc[4 * nt + i];
-    }
-  }
-
-  float M[NT], lsum[NT], Zs[NT];
-  float acc[NT][8][4];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    M[nt] = -INFINITY;
-    lsum[nt] = 0.f;
-    Zs[nt] = 0.f;
-#pragma unroll
-    for (int m = 0; m < 8; ++m)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[nt][m][c] = 0.f;
-  }
-
-  // ---- main loop over this warp's tiles ---------------------------------------------
-  if (p.trace && threadIdx.x == 0) p.trace[cta_id * 8 + 1] = gtimer();
-#pragma unroll 1
-  for (int k = 0; k < my_tiles; ++k) {
-    const int t = lo + warp + DW * k;
-    const int stg = k % NSTG;
-    const uint8_t* st = ring + (warp * NSTG + stg) * STG;
-    mbar_wait(&bars[warp * NSTG + stg], (uint32_t)((k / NSTG) & 1));
-    // fragments out of the staged cell: k_scale[16] | v_scale[16] | K codes [16][64] |
-    // V codes [16][64] | k_zp[16] | v_zp[16]
-    const uint4 ka = *reinterpret_cast<const uint4*>(st + 128 + r * 64 + 16 * i);
-    const uint4 kb = *reinterpret_cast<const uint4*>(st + 128 + (r + 8) * 64 + 16 * i);
-    uint2 vw[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int tok = 2 * i + (u & 1) + 8 * (u >> 1);
-      vw[u] = *reinterpret_cast<const uint2*>(st + 1152 + tok * 64 + 8 * r);
-    }
-    const float* sc = reinterpret_cast<const float*>(st);
-    float sk0 = sc[r], sk1 = sc[r + 8], sv0 = sc[16 + r], sv1 = sc[16 + r + 8];
-    const uint32_t kz0 = st[2176 + r], kz1 = st[2176 + r + 8], vz0 = st[2192 + r], vz1 = st[2192 + r + 8];
-    __syncwarp();
-    if (k + NSTG < my_tiles) {
-      const int tn = t + DW * NSTG;
-      if (has_app && tn == t_new) mbar_wait(app_bar, 0);
-      issue(k + NSTG, page_of(k + NSTG));
-    }
-
-    // ---- S = C_k q : 8 k-steps of m16n8k16 per 8-column tile
-    float scv[NT][4];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) scv[nt][0] = scv[nt][1] = scv[nt][2] = scv[nt][3] = 0.f;
-    const uint32_t kw0[4] = {ka.x, ka.y, ka.z, ka.w};
-    const uint32_t kw1[4] = {kb.x, kb.y, kb.z, kb.w};
-#pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      const uint32_t wa = kw0[s >> 1], wb = kw1[s >> 1];
-      const uint32_t xa = (s & 1) ? (wa >> 8) : wa, xb = (s & 1) ? (wb >> 8) : wb;
-      const uint32_t a0 = xa & 0x000F000Fu, a2 = xa & 0x00F000F0u;
-      const uint32_t a1 = xb & 0x000F000Fu, a3 = xb & 0x00F000F0u;
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) mma16816(scv[nt], a0, a1, a2, a3, bq[nt][s][0], bq[nt][s][1]);
-    }
-
-    // ---- sidecars (sentinel rows: the scale slot holds the offset, codes are 0)
-    float zk0 = (float)kz0, zk1 = (float)kz1, zv0 = (float)vz0, zv1 = (float)vz1;
-    if (kz0 == 0xFFu) { zk0 = -sk0; sk0 = 1.f; }
-    if (kz1 == 0xFFu) { zk1 = -sk1; sk1 = 1.f; }
-    if (vz0 == 0xFFu) { zv0 = -sv0; sv0 = 1.f; }
-    if (vz1 == 0xFFu) { zv1 = -sv1; sv1 = 1.f; }
-    const int t0 = (t << 4) + r, t1 = t0 + 8;
-    const bool ok0 = t0 < len, ok1 = t1 < len;
-    const float lgv0 = ok0 ? __log2f(sv0) : 0.f, lgv1 = ok1 ? __log2f(sv1) : 0.f;
-
-    uint32_t wlo[NT], whi[NT];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const float l0 = ok0 ? (scv[nt][0] + scv[nt][1] - zk0 * sumq[nt]) * (sk0 * kscale[nt]) : -INFINITY;
-      const float l1 = ok1 ? (scv[nt][2] + scv[nt][3] - zk1 * sumq[nt]) * (sk1 * kscale[nt]) : -INFINITY;
-      const float b0 = l0 + lgv0, b1 = l1 + lgv1;  // log2(p * s_v)
-      float tm = fmaxf(b0, b1);
-      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 4));
-      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 8));
-      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 16));
-      // lazy rescaling: the reference point M only moves when a logit exceeds it by
-      // > 2^7, so w = 2^(b - M) <= 128 and w * 2^8 stays inside fp16 range
-      if (__any_sync(0xffffffffu, tm > M[nt] + 7.0f)) {
-        const float mnew = fmaxf(M[nt], tm);
-        const float alpha = (M[nt] == -INFINITY) ? 0.f : ex2f(M[nt] - mnew);
-        if (mnew != -INFINITY) {
-          lsum[nt] *= alpha;
-          Zs[nt] *= alpha;
-#pragma unroll
-          for (int m = 0; m < 8; ++m)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) acc[nt][m][c] *= alpha;
-          M[nt] = mnew;
+        for (int u = 0; u < 4; ++u) {
+          x[u] *= inv;
+          if (p.has_signs && sign_bit(signs, 4 * lane + u)) x[u] = -x[u];
         }
       }
-      const float ms = (M[nt] == -INFINITY) ? 0.f : M[nt];
-      const float w0 = ex2f(b0 - ms), w1 = ex2f(b1 - ms);  // = p_t * s_v * 2^(.)
-      const float p0 = ex2f(l0 - ms), p1 = ex2f(l1 - ms);  // = p_t * 2^(.)
-      lsum[nt] += p0 + p1;
-      Zs[nt] += w0 * zv0 + w1 * zv1;
-      // fp16 hi/lo of w * 2^8 (w <= 2^7): 22-bit weights, the lo half out of fp16
-      // subnormals for weights down to ~2^-21 of the reference point
-      const float w0s = w0 * 256.0f, w1s = w1 * 256.0f;
-      const float w0h = __half2float(__float2half_rn(w0s)), w1h = __half2float(__float2half_rn(w1s));
-      wlo[nt] = movtrans(pack_h2(w0h, w0s - w0h));  // tokens 0..7  -> b0,b1
-      whi[nt] = movtrans(pack_h2(w1h, w1s - w1h));  // tokens 8..15 -> b2,b3
+      float4* dst = reinterpret_cast<float4*>(p.out + ((int64_t)b * p.nq + (int64_t)h * G + warp) * 128) + lane;
+      *dst = make_float4(x[0], x[1], x[2], x[3]);
     }
-
-    // ---- O^T += C_v^T W : 8 m-tiles (16 dims each) of m16n8k16
-    uint32_t xr[2][2][8];  // [token pair (2i,2i+1)|(2i+8,2i+9)][word][dim e]
-#pragma unroll
-    for (int tp = 0; tp < 2; ++tp)
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const uint32_t wa = q ? vw[2 * tp].y : vw[2 * tp].x;
-        const uint32_t wb = q ? vw[2 * tp + 1].y : vw[2 * tp + 1].x;
-        const uint32_t t0w = prmt(wa, wb, 0x5410u), t1w = prmt(wa, wb, 0x7632u);
-        const uint32_t t0s = t0w >> 8, t1s = t1w >> 8;
-        xr[tp][q][0] = t0w & 0x000F000Fu;
-        xr[tp][q][1] = t0w & 0x00F000F0u;
-        xr[tp][q][2] = t0s & 0x000F000Fu;
-        xr[tp][q][3] = t0s & 0x00F000F0u;
-        xr[tp][q][4] = t1w & 0x000F000Fu;
-        xr[tp][q][5] = t1w & 0x00F000F0u;
-        xr[tp][q][6] = t1s & 0x000F000Fu;
-        xr[tp][q][7] = t1s & 0x00F000F0u;
-      }
-#pragma unroll
-    for (int m = 0; m < 8; ++m)
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-        mma16816(acc[nt][m], xr[0][0][m], xr[0][1][m], xr[1][0][m], xr[1][1][m], wlo[nt], whi[nt]);
-  }
-
-  // ---- per-warp finalisation into shared memory (the ring is free now)
-  __syncthreads();
-  if (p.trace && threadIdx.x == 0) p.trace[cta_id * 8 + 2] = gtimer();
-  float* sred = reinterpret_cast<float*>(ring);  // [DW][8][130]
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-#pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {
-      lsum[nt] += __shfl_xor_sync(0xffffffffu, lsum[nt], o);
-      Zs[nt] += __shfl_xor_sync(0xffffffffu, Zs[nt], o);
-    }
-    const int j = 4 * nt + i;
-    if (tile_warp && j < G) {
-      float* row = sred + (warp * 8 + j) * 130;
-#pragma unroll
-      for (int m = 0; m < 8; ++m) {
-        const float f = (m & 1) ? 65536.0f / 16.0f : 65536.0f;  // undo 2^-24 (codes), 2^8 (w), x16 nibble
-        row[16 * r + m] = (acc[nt][m][0] + acc[nt][m][1]) * f - Zs[nt];
-        row[16 * r + 8 + m] = (acc[nt][m][2] + acc[nt][m][3]) * f - Zs[nt];
-      }
-      if (r == 0) {
-        row[128] = M[nt];
-        row[129] = lsum[nt];
-      }
-    }
-  }
-  __syncthreads();
-
-  // ---- CTA merge over warps -> (o, lse) of this split
-  float* obuf = sq;
-  const int64_t hbase = (((int64_t)b * H + h) * p.splits) * 8;
-  for (int x = threadIdx.x; x < G * 128; x += blockDim.x) {
-    const int j = x >> 7, dd = x & 127;
-    float mmax = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < DW; ++w) mmax = fmaxf(mmax, sred[(w * 8 + j) * 130 + 128]);
-    float lt = 0.f, ot = 0.f;
-    if (mmax != -INFINITY) {
-#pragma unroll
-      for (int w = 0; w < DW; ++w) {
-        const float mw = sred[(w * 8 + j) * 130 + 128];
-        const float f = (mw == -INFINITY) ? 0.f : ex2f(mw - mmax);
-        lt += f * sred[(w * 8 + j) * 130 + 129];
-        ot += f * sred[(w * 8 + j) * 130 + dd];
-      }
-    }
-    const float o = (lt > 0.f) ? ot / lt : 0.f;
-    const float lse = (lt > 0.f) ? mmax + __log2f(lt) : -INFINITY;
-    if (p.splits == 1) {
-      obuf[x] = o;
-    } else {
-      p.ws_o[(hbase + (int64_t)split * 8 + j) * 128 + dd] = o;
-      if (dd == 0) p.ws_lse[hbase + (int64_t)split * 8 + j] = lse;
-    }
+    KVR_STAMP(9);  // merged + stored
+    cluster_sync_relaxed();  // every CTA's partial stays readable until all merges are done
+    KVR_STAMP(10);
+    return;
   }
   if (p.splits > 1) {
     // release the partial: CTA barrier, then one gpu-scope acq_rel atomic by thread 0
     // (cumulative over the CTA's writes ordered before it by the barrier)
     __syncthreads();
     if (threadIdx.x == 0) {
-      if (p.trace) p.trace[cta_id * 8 + 3] = gtimer();
+      if (p.trace) p.trace[cta_id * 16 + 6] = clk64();  // partial stored
       uint32_t prev;
+#if KVR_ATOM == 0
       asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
                    : "=r"(prev)
                    : "l"(&p.ws_cnt[(int64_t)b * H + h])
                    : "memory");
+#else
+      __threadfence();
+      prev = atomicAdd(&p.ws_cnt[(int64_t)b * H + h], 1u);
+      __threadfence();
+#endif
       *s_last = (prev == (uint32_t)p.splits - 1) ? 1u : 0u;
-      if (p.trace) p.trace[cta_id * 8 + 4] = gtimer();
+      if (p.trace) p.trace[cta_id * 16 + 7] = clk64();  // counter back
     }
     __syncthreads();
     if (!*s_last) {
-      if (p.trace && threadIdx.x == 0) p.trace[cta_id * 8 + 6] = gtimer();
+      KVR_STAMP(10);
       return;
     }
-    // last CTA of (b, h): LSE-merge all splits.  Every thread re-derives the split
-    // weights of its q head from the lse values (same address across the warp), so
-    // the lse and o loads of a 32-split chunk go out together: one L2 round trip.
-    for (int x = threadIdx.x; x < G * 128; x += blockDim.x) {
+    // last CTA of (b, h): LSE-merge all splits.  The o-values of the first
+    // MERGE_PRELOAD splits are requested together with the lse values, so short
+    // merges take one L2 round trip; warp j < G turns the lse column of q head j
+    // into split weights in shared memory.
+    float* s_w = sred + NWARPS * 8 * 136;  // [8][MAX_SPLITS] (past sred)
+    const int x0 = threadIdx.x;  // G * 128 <= 1024 outputs; blockDim = 512
+    constexpr int PRE = NT == 1 ? MERGE_PRELOAD : (MERGE_PRELOAD / 4 > 0 ? MERGE_PRELOAD / 4 : 1);
+    constexpr int REPS = NT == 1 ? 1 : 2;  // G * 128 outputs over 512 threads
+    float ov[REPS][PRE];
+#pragma unroll
+    for (int rep = 0; rep < REPS; ++rep) {
+      const int x = x0 + rep * 512;
       const int j = x >> 7, dd = x & 127;
-      const float* lsrc = p.ws_lse + hbase + j;
-      const float* osrc = p.ws_o + (hbase + j) * 128 + dd;
-      float lmax = -INFINITY, tot = 0.f, ot = 0.f;
+#pragma unroll
+      for (int u = 0; u < PRE; ++u)
+        ov[rep][u] = (j < G && u < p.splits) ? ld_partial(p.ws_o + (hbase + (int64_t)u * 8 + j) * 128 + dd) : 0.f;
+    }
+    if (warp < G) {
+      const int j = warp;
+      float mx = -INFINITY;
       for (int s0 = 0; s0 < p.splits; s0 += 32) {
-        float lv[32], ov[32];
-#pragma unroll
-        for (int u = 0; u < 32; ++u) {
-          const bool in = s0 + u < p.splits;
-          lv[u] = in ? __ldcg(lsrc + (int64_t)(s0 + u) * 8) : -INFINITY;
-          ov[u] = in ? __ldcg(osrc + (int64_t)(s0 + u) * 8 * 128) : 0.f;
-        }
-        float cm = lmax;
-#pragma unroll
-        for (int u = 0; u < 32; ++u) cm = fmaxf(cm, lv[u]);
-        if (cm == -INFINITY) continue;
-        const float a = (lmax == -INFINITY) ? 0.f : exp2f(lmax - cm);
-        tot *= a;
-        ot *= a;
-        lmax = cm;
-#pragma unroll
-        for (int u = 0; u < 32; ++u) {
-          const float f = (lv[u] == -INFINITY) ? 0.f : exp2f(lv[u] - cm);
-          tot += f;
-          ot += f * ov[u];
-        }
+        const float l = (s0 + lane < p.splits) ? ld_partial(p.ws_lse + hbase + (int64_t)(s0 + lane) * 8 + j) : -INFINITY;
+        s_w[j * MAX_SPLITS + s0 + lane] = l;
+        mx = fmaxf(mx, l);
       }
-      obuf[x] = tot > 0.f ? ot / tot : 0.f;
+      mx = warp_max(mx);
+      float tot = 0.f;
+      for (int s0 = lane; s0 < p.splits; s0 += 32) {
+        const float l = s_w[j * MAX_SPLITS + s0];
+        const float w = (l == -INFINITY) ? 0.f : ex2f(l - mx);
+        s_w[j * MAX_SPLITS + s0] = w;
+        tot += w;
+      }
+      tot = warp_sum(tot);
+      if (lane == 0) s_tot[j] = tot;
+    }
+    __syncthreads();
+    KVR_STAMP(8);  // split weights ready
+#pragma unroll
+    for (int rep = 0; rep < REPS; ++rep) {
+      const int x = x0 + rep * 512;
+      const int j = x >> 7, dd = x & 127;
+      if (j < G) {
+        const float* wj = s_w + j * MAX_SPLITS;
+        float ot = 0.f;
+#pragma unroll
+        for (int u = 0; u < PRE; ++u) ot += (u < p.splits) ? wj[u] * ov[rep][u] : 0.f;
+#pragma unroll 8
+        for (int s = PRE; s < p.splits; ++s)
+          ot += wj[s] * ld_partial(p.ws_o + (hbase + (int64_t)s * 8 + j) * 128 + dd);
+        const float tot = s_tot[j];
+        obuf[x] = tot > 0.f ? ot / tot : 0.f;
+      }
     }
     if (threadIdx.x == 0) {
       p.ws_cnt[(int64_t)b * H + h] = 0u;  // re-arm for the next launch
-      if (p.trace) p.trace[cta_id * 8 + 5] = gtimer();
+      if (p.trace) p.trace[cta_id * 16 + 9] = clk64();  // merged
     }
   }
   __syncthreads();
@@ -681,7 +1018,7 @@ __global__ void __launch_bounds__((DW + 1) * 32, 1)
     float4* dst = reinterpret_cast<float4*>(p.out + ((int64_t)b * p.nq + (int64_t)h * G + warp) * 128) + lane;
     *dst = make_float4(x[0], x[1], x[2], x[3]);
   }
-  if (p.trace && threadIdx.x == 0) p.trace[cta_id * 8 + 6] = gtimer();
+  KVR_STAMP(10);
 }
 
 // Generic (any head_dim <= 256, any group) CUDA-core decode: one CTA per
@@ -795,12 +1132,16 @@ __global__ void decode_generic_kernel(const __grid_constant__ DecodeParams p, co
 
 using namespace kvr;
 
+// Workspace: split counters u32[B][H] first (padded to 256 B, so a workspace reused
+// with another split count still finds them at zero), then lse f32[B][H][S][8],
+// then o f32[B][H][S][8][128].
+static size_t ws_cnt_bytes(int batch, int H) { return ((size_t)batch * H * sizeof(uint32_t) + 255) & ~size_t(255); }
 size_t kvr_decode_ws_bytes(int batch, int H, int nq, int d, int splits) {
   (void)nq;
   (void)d;
   if (splits < 1) splits = 1;
   const size_t units = (size_t)batch * H * splits * 8;
-  size_t bytes = units * 128 * sizeof(float) + units * sizeof(float) + (size_t)batch * H * sizeof(uint32_t);
+  size_t bytes = ws_cnt_bytes(batch, H) + units * sizeof(float) + units * 128 * sizeof(float);
   return (bytes + 255) & ~size_t(255);
 }
 
@@ -810,35 +1151,88 @@ int kvr_pick_splits(int batch, int H, int max_len, int P) {
   const int tiles = (max_len + 15) / 16;
   const int units = batch * H;
   int s = sms / units;  // one CTA per SM, a single wave
-  const int min_tiles_per_cta = 2 * DW;
+  const int min_tiles_per_cta = 2 * NWARPS;
   const int max_s = tiles / min_tiles_per_cta;
   if (s > max_s) s = max_s;
-  if (s > 128) s = 128;
+  if (s > MAX_SPLITS) s = MAX_SPLITS;
   if (s < 1) s = 1;
-  while ((tiles + s - 1) / s > MAX_CTA_TILES && s < 128) ++s;
   return s;
 }
 
-template <int NT>
+// One launch of decode_tma_kernel with programmatic stream serialization (PDL: the
+// prologue may overlap the previous grid) and, for 2..16 splits, a thread-block
+// cluster spanning the splits of one (sequence, kv head) so they merge in DSMEM.
+template <int NT, int ORDER, bool APP, bool CL>
+static int launch_one(dim3 grid, size_t smem, cudaStream_t st, const DecodeParams& p, const Signs& sg) {
+  auto kern = decode_tma_kernel<NT, ORDER, APP, NT == 1 ? 2 : 1, CL>;
+  static bool set = false;  // one flag per instantiation
+  if (!set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return KVR_ERR_CUDA;
+    if (CL && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+      return KVR_ERR_CUDA;
+    set = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(NWARPS * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = 1;
+  attr[1].val.clusterDim.y = grid.y;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = CL ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, p, sg) == cudaSuccess ? 0 : KVR_ERR_CUDA;
+}
+
+// Can clusters of `splits` CTAs of this kernel be co-scheduled? (cached per size)
+template <int NT, int ORDER, bool APP>
+static bool cluster_ok(int splits, size_t smem) {
+  static int cache[17] = {0};  // 0 unknown, 1 yes, 2 no
+  if (splits < 2 || splits > 16) return false;
+  if (!cache[splits]) {
+    auto kern = decode_tma_kernel<NT, ORDER, APP, NT == 1 ? 2 : 1, true>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1, splits, 1);
+    cfg.blockDim = dim3(NWARPS * 32);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = splits;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    const cudaError_t e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+    cache[splits] = (e == cudaSuccess && n >= 1) ? 1 : 2;
+    if (e != cudaSuccess) (void)cudaGetLastError();
+  }
+  return cache[splits] == 1;
+}
+
+template <int NT, int ORDER, bool APP>
+static int launch_sel(dim3 grid, size_t smem, cudaStream_t st, const DecodeParams& p, const Signs& sg) {
+  if (p.use_cluster && cluster_ok<NT, ORDER, APP>((int)grid.y, smem))
+    return launch_one<NT, ORDER, APP, true>(grid, smem, st, p, sg);
+  return launch_one<NT, ORDER, APP, false>(grid, smem, st, p, sg);
+}
+
+template <int NT, bool APP>
 static int launch_tma(const DecodeParams& p, const Signs& sg, dim3 grid, size_t smem, int order, cudaStream_t st) {
-#define KVR_DEC_CASE(ORD)                                                                               \
-  case ORD: {                                                                                           \
-    auto kern = decode_tma_kernel<NT, ORD>;                                                             \
-    static bool set = false;                                                                            \
-    if (!set) {                                                                                         \
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);               \
-      set = true;                                                                                       \
-    }                                                                                                   \
-    kern<<<grid, (DW + 1) * 32, smem, st>>>(p, sg);                                                     \
-    return 0;                                                                                           \
-  }
   switch (order) {
-    KVR_DEC_CASE(128)
-    KVR_DEC_CASE(64)
-    KVR_DEC_CASE(32)
-    KVR_DEC_CASE(16)
+    case 128: return launch_sel<NT, 128, APP>(grid, smem, st, p, sg);
+    case 64: return launch_sel<NT, 64, APP>(grid, smem, st, p, sg);
+    case 32: return launch_sel<NT, 32, APP>(grid, smem, st, p, sg);
+    case 16: return launch_sel<NT, 16, APP>(grid, smem, st, p, sg);
   }
-#undef KVR_DEC_CASE
   return KVR_ERR_UNSUPPORTED;
 }
 
@@ -883,18 +1277,24 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
                       (reinterpret_cast<uintptr_t>(pool.base) & 15) == 0 && (pool.cell_bytes & 15) == 0;
   if (tma_ok) {
     if (splits <= 0) splits = kvr_pick_splits(batch, pool.H, max_len, pool.P);
-    if (splits > 128) splits = 128;
-    if ((max_len + 15) / 16 > (int64_t)splits * MAX_CTA_TILES) return KVR_ERR_UNSUPPORTED;
+    if (splits > MAX_SPLITS) splits = MAX_SPLITS;
     if (splits > 1 && kvr_decode_ws_bytes(batch, pool.H, nq, 128, splits) > ws_bytes) return KVR_ERR_ARG;
     p.splits = splits;
     const size_t units = (size_t)batch * pool.H * splits * 8;
-    p.ws_o = reinterpret_cast<float*>(ws);
-    p.ws_lse = p.ws_o + units * 128;
-    p.ws_cnt = reinterpret_cast<uint32_t*>(p.ws_lse + units);
+    p.ws_cnt = reinterpret_cast<uint32_t*>(ws);
+    p.ws_lse = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + ws_cnt_bytes(batch, pool.H));
+    p.ws_o = p.ws_lse + units;
     dim3 grid(pool.H, splits, batch);
     const int ord = rotate ? order : 128;
     const size_t smem = decode_smem_bytes();
-    return p.G == 8 ? launch_tma<2>(p, sg, grid, smem, ord, st) : launch_tma<1>(p, sg, grid, smem, ord, st);
+    int cl = 0;
+    while ((16 << cl) < pool.P) ++cl;
+    p.cps_log2 = cl;
+    p.mul24 = 1u << 24;
+    p.use_cluster = splits >= 2 && splits <= 16;
+    if (new_slot)
+      return p.G == 8 ? launch_tma<2, true>(p, sg, grid, smem, ord, st) : launch_tma<1, true>(p, sg, grid, smem, ord, st);
+    return p.G == 8 ? launch_tma<2, false>(p, sg, grid, smem, ord, st) : launch_tma<1, false>(p, sg, grid, smem, ord, st);
   }
   if (new_slot) return KVR_ERR_UNSUPPORTED;  // the fused append lives in the TMA kernel only
   if (pool.d > 256 || (pool.d & 31)) return KVR_ERR_UNSUPPORTED;

@@ -1,4 +1,9 @@
-"""Per-CTA timeline of one C2 decode step (globaltimer stamps) -> gpurun_out/trace.txt."""
+"""Per-CTA timeline of C2 decode launches (globaltimer stamps) -> gpurun_out/trace.txt.
+
+    python tools/trace_decode.py [ctx] [splits ...]
+
+Four independent 32k-token tables (> 126 MB L2 in total) rotate so the traced
+launch reads its KV from HBM, like the bench."""
 import ctypes
 import os
 import sys
@@ -9,48 +14,65 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2604_19157_b200 import DecodePlan, HeadLayout, PageTable, RotationSpec, make_signs, _lib  # noqa: E402
 
-H, G, D, L = 8, 4, 128, int(sys.argv[1]) if len(sys.argv) > 1 else 32768
+H, G, D = 8, 4, 128
+L = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
+split_list = [int(x) for x in sys.argv[2:]] or [0]
 dev = torch.device("cuda")
 layout = HeadLayout(num_q_heads=H * G, num_kv_heads=H, head_dim=D, rot_order=128, page_tokens=16)
 spec = RotationSpec(order=128, signs=make_signs(0, 0, D, 128))
-t = PageTable(layout, num_pages=(L + 15) // 16 + 2, device=dev)
-t.create_sequence(0)
-for c0 in range(0, L, 8192):
-    n = min(8192, L - c0)
-    t.append_batch([0] * n, torch.randn(n, H, D, device=dev).bfloat16(), torch.randn(n, H, D, device=dev).bfloat16(),
-                   spec=spec, check=False)
-plan = DecodePlan(t, [0])
+tables = []
+for _ in range(4):
+    t = PageTable(layout, num_pages=(L + 15) // 16 + 2, device=dev)
+    t.create_sequence(0)
+    for c0 in range(0, L, 8192):
+        n = min(8192, L - c0)
+        t.append_batch([0] * n, torch.randn(n, H, D, device=dev).bfloat16(),
+                       torch.randn(n, H, D, device=dev).bfloat16(), spec=spec, check=False)
+    tables.append(t)
 q = torch.randn(1, H * G, D, device=dev).bfloat16()
-tr = torch.zeros(plan.splits * H * 8, dtype=torch.int64, device=dev)
-for _ in range(3):
-    plan.run(q, spec)
-torch.cuda.synchronize()
-_lib.lib().kvr_debug_decode_trace(ctypes.c_void_p(tr.data_ptr()))
-plan.run(q, spec)
-torch.cuda.synchronize()
-_lib.lib().kvr_debug_decode_trace(None)
-a = tr.view(plan.splits * H, 8).cpu().numpy().astype(np.float64)
-t0 = a[:, 0].min()
-a = (a - t0) / 1000.0
-a[a < 0] = np.nan  # unstamped slots
-names = ["start", "loop start", "loop end", "partial written", "counter back", "merge done", "end"]
-out = [f"splits {plan.splits} ctas {a.shape[0]}"]
-for c, nm in enumerate(names):
-    col = a[:, c]
-    col = col[np.isfinite(col)]
-    if col.size:
-        out.append(f"{nm:16s}: n {col.size:4d} min {col.min():6.2f} med {np.median(col):6.2f} max {col.max():6.2f} us")
-last = np.isfinite(a[:, 5])
-if last.any():
-    out.append("last CTAs: " + "; ".join(
-        " ".join(f"{a[k, c]:.2f}" for c in range(7)) for k in np.nonzero(last)[0][:8]))
-e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-e0.record()
-for _ in range(20):
-    plan.run(q, spec)
-e1.record()
-torch.cuda.synchronize()
-out.append(f"event time per launch (L2-warm): {e0.elapsed_time(e1) / 20 * 1000:.2f} us")
+out_lines = []
+names = {2: "loop start", 3: "loop end", 4: "M published", 5: "warp partials", 6: "partial stored", 7: "counter back",
+         8: "split weights", 9: "merged", 10: "exit"}
+MHZ = float(os.environ.get("SM_MHZ", "1965"))
+for splits in split_list:
+    plans = [DecodePlan(t, [0], num_splits=splits) for t in tables]
+    S = plans[0].splits
+    tr = torch.zeros(S * H * 16, dtype=torch.int64, device=dev)
+    for p in plans:
+        p.run(q, spec)
+    torch.cuda.synchronize()
+    for k in range(3):
+        plans[k].run(q, spec)
+    _lib.lib().kvr_debug_decode_trace(ctypes.c_void_p(tr.data_ptr()))
+    plans[3].run(q, spec)
+    torch.cuda.synchronize()
+    _lib.lib().kvr_debug_decode_trace(None)
+    raw = tr.view(S * H, 16).cpu().numpy().astype(np.float64)
+    g0 = raw[:, 0] - raw[:, 0].min()
+    out_lines.append(f"== ctx {L} splits {S} ctas {raw.shape[0]} (HBM-cold launch; clock64 at {MHZ:.0f} MHz)")
+    out_lines.append(f"{'start':16s}: min {g0.min() / 1e3:6.2f} med {np.median(g0) / 1e3:6.2f} max {g0.max() / 1e3:6.2f} us")
+    for k, nm in names.items():
+        ok = raw[:, k] > 0
+        if ok.any():
+            t = (g0[ok] + (raw[ok, k] - raw[ok, 1]) * 1e3 / MHZ) / 1e3
+            out_lines.append(f"{nm:16s}: n {ok.sum():4d} min {t.min():6.2f} med {np.median(t):6.2f} max {t.max():6.2f} us")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            for k in range(64):
+                plans[k % 4].run(q, spec)
+    torch.cuda.current_stream().wait_stream(s)
+    g.replay()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(4):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    out_lines.append(f"graph time per launch (HBM, back to back): {e0.elapsed_time(e1) / 256 * 1000:.2f} us")
 os.makedirs("gpurun_out", exist_ok=True)
-open("gpurun_out/trace.txt", "w").write("\n".join(out) + "\n")
-print("\n".join(out))
+open("gpurun_out/trace.txt", "w").write("\n".join(out_lines) + "\n")
+print("\n".join(out_lines))
