@@ -41,7 +41,6 @@ struct DecodeParams {
   const int32_t* lens;
   int batch, nq, G, splits, order, rotate, rot_v, has_signs, log2P, max_len;
   int cps_log2;       // log2(cells of one head per page) = log2(P / 16) on the TMA path
-  uint32_t mul24;     // = 2^24 (see shr8)
   int use_cluster;    // 2..16 splits: merge them in a thread-block cluster
   float* out;
   float* ws_o;       // [B][H][S][8][128]
@@ -87,9 +86,6 @@ KVR_DEV void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// x >> 8 on the FMA pipe (IMAD.HI) instead of the ALU pipe, which the nibble
-// masks already keep busy
-// (m = 2^24 arrives as a kernel parameter so ptxas cannot strength-reduce it)
 #ifndef KVR_MERGE_LD
 #define KVR_MERGE_LD 0
 #endif
@@ -110,23 +106,6 @@ KVR_DEV float ld_partial(const float* a) {
   return v;
 #endif
 }
-#ifndef KVR_SHR_IMAD
-#define KVR_SHR_IMAD 0
-#endif
-#ifndef KVR_LATE_V
-#define KVR_LATE_V 1
-#endif
-KVR_DEV uint32_t shr8(uint32_t x, uint32_t m) {
-#if KVR_SHR_IMAD
-  uint32_t r;
-  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(m));
-  return r;
-#else
-  (void)m;
-  return x >> 8;
-#endif
-}
-
 KVR_DEV float ex2f(float x) {
   float r;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -179,7 +158,9 @@ KVR_DEV void cta_fwht_rows(float* s, int rows) {
 // (pairs combined lowest index first, exactly _ref.fwht_rows), * 1/sqrt(ORDER),
 // then _ref.quantize_rows (_ref.py:22-40, 57-80) and the paged store.
 template <int ORDER>
-KVR_DEV void append_row_exact(const DecodeParams& p, const Signs& sg, int b, int h, int side) {
+// returns the stored-space (rotated) dequantised row element of lane l in
+// deq[0..3] (dims 4l..4l+3); false when the row was not finite (not written)
+KVR_DEV bool append_row_exact(const DecodeParams& p, const Signs& sg, int b, int h, int side, float (&deq)[4]) {
   const int lane = threadIdx.x & 31;
   const int64_t slot = p.new_slot[b];
   const int64_t base = ((int64_t)b * p.pool.H + h) * 128 + 4 * lane;
@@ -197,7 +178,8 @@ KVR_DEV void append_row_exact(const DecodeParams& p, const Signs& sg, int b, int
   fin = __all_sync(0xffffffffu, fin);
   if (!fin) {
     if (lane == 0 && p.flags) atomicOr(p.flags, (uint32_t)KVR_FLAG_NONFINITE);
-    return;
+    deq[0] = deq[1] = deq[2] = deq[3] = 0.f;
+    return false;
   }
   const bool rot = side ? (p.rotate && p.rot_v) : p.rotate;
   if (rot) {
@@ -253,6 +235,10 @@ KVR_DEV void append_row_exact(const DecodeParams& p, const Signs& sg, int b, int
     }
     scv = s32;
     zpv = (uint32_t)z;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) deq[u] = (float)((double)s32 * (double)((int)((bytes2 >> (4 * u)) & 15u) - (int)zpv));
+  } else {
+    deq[0] = deq[1] = deq[2] = deq[3] = scv;  // sentinel row: the offset
   }
   *reinterpret_cast<uint16_t*>(cell + (side ? cell_vcode(p.pool, ci) : cell_kcode(p.pool, ci)) + 2 * lane) =
       (uint16_t)bytes2;
@@ -260,6 +246,7 @@ KVR_DEV void append_row_exact(const DecodeParams& p, const Signs& sg, int b, int
     *reinterpret_cast<float*>(cell + (side ? cell_vscale(p.pool, ci) : cell_kscale(p.pool, ci))) = scv;
     cell[side ? cell_vzp(p.pool, ci) : cell_kzp(p.pool, ci)] = (uint8_t)zpv;
   }
+  return true;
 }
 
 KVR_DEV void mbar_arrive(uint64_t* bar) {
@@ -316,7 +303,9 @@ constexpr int MAX_SPLITS = 256;
 constexpr int SM_BARS = NWARPS * RING_CELLS * CELL;
 constexpr int SM_FRAG = SM_BARS + (NWARPS * RING_CELLS + 1) * 8 + 8;  // 16-B aligned
 constexpr int SM_OBUF = SM_FRAG + 4096;
-constexpr int SM_MISC = SM_OBUF + 4096;                               // sumq[8] ksc[8] tot[8] flag lse[8]
+constexpr int SM_QROT = SM_OBUF + 4096;                               // fp32 rotated q [8][128] (APPEND)
+constexpr int SM_VNEW = SM_QROT + 4096;                               // new token's V row [128] (APPEND)
+constexpr int SM_MISC = SM_VNEW + 512;                               // sumq[8] ksc[8] tot[8] flag lse[8]
 constexpr int SM_TOTAL = SM_MISC + 256;
 size_t decode_smem_bytes() { return 1024 + SM_TOTAL; }
 
@@ -362,7 +351,6 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = sm_raw + ((1024u - (smem_u32(sm_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + SM_BARS);
-  uint64_t* app_bar = bars + NWARPS * RING_CELLS;
   uint16_t* sfrag = reinterpret_cast<uint16_t*>(sm + SM_FRAG);  // [NT][8 k-steps][32 lanes][2 regs][2 halves]
   float* obuf = reinterpret_cast<float*>(sm + SM_OBUF);         // [G][128]
   float* s_sumq = reinterpret_cast<float*>(sm + SM_MISC);       // [8]
@@ -371,6 +359,9 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   uint32_t* s_last = reinterpret_cast<uint32_t*>(s_sumq + 24);
   float* s_lse = s_sumq + 25;                                   // [8] (cluster merge)
   float* s_mstar = s_sumq + 40;                                 // [8] CTA reference point per q head
+  float* s_lnew = s_sumq + 48;                                  // [8] new token's logits (APPEND)
+  float* s_qrot = reinterpret_cast<float*>(sm + SM_QROT);
+  float* s_vnew = reinterpret_cast<float*>(sm + SM_VNEW);
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = lane >> 2, i = lane & 3;
@@ -408,14 +399,20 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   int wnext = page_window(1), win_idx = 0;
   const uint8_t* wcur = window_addr(0, page_window(0));
   const int len_raw = __ldg(&p.lens[b]);
-  if (threadIdx.x <= NWARPS * RING_CELLS) mbar_init(&bars[threadIdx.x], 1);  // + app_bar
+  if (threadIdx.x < NWARPS * RING_CELLS) mbar_init(&bars[threadIdx.x], 1);
   fence_mbar_init();
   __syncthreads();
 
   const int len = min(len_raw, p.max_len);
-  const int n_tiles = (len + 15) >> 4;
+  // APPEND: the step's token (position len - 1) is written and scored by the writer
+  // warp straight from registers; the tiles cover the len_kv older tokens, so no
+  // tile load waits for the write
+  const bool app = APPEND && len > 0 && __ldg(&p.new_slot[b]) >= 0;
+  const int len_kv = app ? len - 1 : len;
+  const int t_new = (len - 1) >> 4;
+  const bool app_owner = app && t_new >= lo && t_new < hi_max;  // this CTA writes + scores it
+  const int n_tiles = (len_kv + 15) >> 4;
   const int hi = min(n_tiles, hi_max);
-  const int t_new = APPEND ? ((len - 1) >> 4) : -1;  // tile holding the appended token
   // tiles from `guard` on may hold tokens written by the previous grid (the last
   // step's append): they are requested only after griddepcontrol.wait
   const int guard = max(len - 2, 0) >> 4;
@@ -467,30 +464,8 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
     for (int u = 0; u < 4; ++u)
       qx[u] = load_q(p.q, p.q_dtype, ((int64_t)b * p.nq + (int64_t)h * G + warp) * 128 + 4 * lane + u);
   }
-  // the group holding the new token waits for the writer warp
-  const int k_new = (APPEND && tile_warp && t_new >= lo && t_new < hi && ((t_new - lo) / C) % DW == warp)
-                        ? (t_new - lo) / C / DW
-                        : -1;
-  bool def_pending = false;
 #pragma unroll 1
-  for (int k = k0; k < NSTG && k < my_groups; ++k) {
-    if (k == k_new) {
-      def_pending = true;
-      continue;
-    }
-    issue(k);
-  }
-
-  if (APPEND && warp == DW) {  // the writer warp: append, then release the deferred group
-    if (len > 0 && p.new_slot[b] >= 0) {
-      append_row_exact<ORDER>(p, signs, b, h, 0);
-      append_row_exact<ORDER>(p, signs, b, h, 1);
-      fence_proxy_async_global();
-      __threadfence();
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(app_bar);
-  }
+  for (int k = k0; k < NSTG && k < my_groups; ++k) issue(k);
 
   // ---- query prep: warp j < 4 NT owns q head j of this kv head (sign flip + fp32
   // butterfly, power-of-two normalisation, fp16 hi/lo split in MMA-fragment order);
@@ -522,6 +497,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
 #pragma unroll
       for (int u = 0; u < 4; ++u) x[u] *= inv;
     }
+    if (APPEND) *reinterpret_cast<float4*>(s_qrot + j * 128 + 4 * lane) = make_float4(x[0], x[1], x[2], x[3]);
     float amax = fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])), fmaxf(fabsf(x[2]), fabsf(x[3])));
     amax = warp_max(amax);
     const int e2 = amax > 0.f ? ilogbf(amax) - 13 : 0;  // q' = q 2^-e2, max|q'| in [2^13, 2^14)
@@ -565,6 +541,23 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
     kscale[nt] = s_ksc[4 * nt + i];
   }
 
+  // ---- the writer warp (no tiles of its own, so this overlaps the main loop of the
+  // others) quantizes + stores the new token's K and V rows bit-exactly (f64,
+  // reference arithmetic), keeps their dequantised values and scores the token
+  float knew[4] = {0.f, 0.f, 0.f, 0.f};
+  if (APPEND && warp == DW && app_owner) {
+    float vnew[4];
+    append_row_exact<ORDER>(p, signs, b, h, 0, knew);
+    append_row_exact<ORDER>(p, signs, b, h, 1, vnew);
+    *reinterpret_cast<float4*>(s_vnew + 4 * lane) = make_float4(vnew[0], vnew[1], vnew[2], vnew[3]);
+    for (int j = 0; j < G; ++j) {  // logits (log2 units)
+      const float4 qv = *reinterpret_cast<const float4*>(s_qrot + j * 128 + 4 * lane);
+      const float dot = warp_sum(qv.x * knew[0] + qv.y * knew[1] + qv.z * knew[2] + qv.w * knew[3]);
+      if (lane == 0) s_lnew[j] = dot * (LOG2E * (float)(1.0 / sqrt(128.0)));
+    }
+    __syncwarp();
+  }
+
   float M[NT], lsum[NT], Zs[NT];
   float acc[NT][8][4];
 #pragma unroll
@@ -578,7 +571,6 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
       for (int c = 0; c < 4; ++c) acc[nt][m][c] = 0.f;
   }
   float Mth = -INFINITY;  // min over columns of M + 7: a logit above it forces a rescale
-  const uint32_t m24 = p.mul24;
 
   // ---- main loop over this warp's groups of C tiles ----------------------------------
   KVR_STAMP(2);  // main loop start
@@ -587,22 +579,11 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
 #pragma unroll 1
   for (int k = 0; k < my_groups; ++k) {
     const int tg = tile_of(C * k);  // first tile of the group
-    if (APPEND && def_pending) {
-      if (k == k_new) mbar_wait(app_bar, 0);
-      if (k == k_new || mbar_test(app_bar, 0)) {
-        issue(k_new);
-        def_pending = false;
-      }
-    }
     const uint8_t* st = ring_w + stg * STG;
     mbar_wait(&bar_w[stg], phase);
     CellFrag f[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) load_cell_k(f[c], st + c * CELL, r, i);
-    if (!KVR_LATE_V) {
-#pragma unroll
-      for (int c = 0; c < C; ++c) load_cell_rest(f[c], st + c * CELL, r, i);
-    }
 
     // ---- S = C_k q : 8 k-steps of m16n8k16 per 8-column tile and cell
     // C * NT independent accumulator chains of 8 HMMAs
@@ -618,7 +599,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
 #pragma unroll
       for (int s = 0; s < 8; ++s) {
         const uint32_t wa = kw0[s >> 1], wb = kw1[s >> 1];
-        const uint32_t xa = (s & 1) ? shr8(wa, m24) : wa, xb = (s & 1) ? shr8(wb, m24) : wb;
+        const uint32_t xa = (s & 1) ? (wa >> 8) : wa, xb = (s & 1) ? (wb >> 8) : wb;
         const uint32_t a0 = xa & 0x000F000Fu, a2 = xa & 0x00F000F0u;
         const uint32_t a1 = xb & 0x000F000Fu, a3 = xb & 0x00F000F0u;
 #pragma unroll
@@ -631,15 +612,9 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
 
     // V words and sidecars after the QK MMAs (keeps the register peak down), then
     // refill this stage with group k + NSTG
-    if (KVR_LATE_V) {
 #pragma unroll
-      for (int c = 0; c < C; ++c) load_cell_rest(f[c], st + c * CELL, r, i);
-    }
+    for (int c = 0; c < C; ++c) load_cell_rest(f[c], st + c * CELL, r, i);
     if (k + NSTG < my_groups) {
-      if (k + NSTG == k_new) {
-        mbar_wait(app_bar, 0);
-        def_pending = false;
-      }
       __syncwarp();
       issue(k + NSTG);
     }
@@ -686,8 +661,8 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
         const bool in = tg + c < hi;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          if (!in || t0 >= len) l0[c][nt] = b0[c][nt] = -INFINITY;
-          if (!in || t0 + 8 >= len) l1[c][nt] = b1[c][nt] = -INFINITY;
+          if (!in || t0 >= len_kv) l0[c][nt] = b0[c][nt] = -INFINITY;
+          if (!in || t0 + 8 >= len_kv) l1[c][nt] = b1[c][nt] = -INFINITY;
         }
         if (!in) zv0[c] = zv1[c] = 0.f;
       }
@@ -750,7 +725,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
           const uint32_t wa = q ? f[c].vw[2 * tp].y : f[c].vw[2 * tp].x;
           const uint32_t wb = q ? f[c].vw[2 * tp + 1].y : f[c].vw[2 * tp + 1].x;
           const uint32_t t0w = prmt(wa, wb, 0x5410u), t1w = prmt(wa, wb, 0x7632u);
-          const uint32_t t0s = shr8(t0w, m24), t1s = shr8(t1w, m24);
+          const uint32_t t0s = t0w >> 8, t1s = t1w >> 8;
           xr[tp][q][0] = t0w & 0x000F000Fu;
           xr[tp][q][1] = t0w & 0x00F000F0u;
           xr[tp][q][2] = t0s & 0x000F000Fu;
@@ -790,6 +765,8 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
     }
     if (r == 0) s_m[warp * 8 + 4 * nt + i] = tile_warp ? M[nt] : -INFINITY;
   }
+  if (APPEND && warp == DW && lane < 8)  // the writer warp's partial: the new token alone
+    s_m[DW * 8 + lane] = (app_owner && lane < G) ? s_lnew[lane] : -INFINITY;
   __syncthreads();
   KVR_STAMP(4);  // reference points published
 #pragma unroll
@@ -798,7 +775,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
     if (j < G && tile_warp) {
       float mstar = -INFINITY;
 #pragma unroll
-      for (int w = 0; w < DW; ++w) mstar = fmaxf(mstar, s_m[w * 8 + j]);
+      for (int w = 0; w < NWARPS; ++w) mstar = fmaxf(mstar, s_m[w * 8 + j]);
       if (warp == 0 && r == 0) s_mstar[j] = mstar;
       const float sc = (M[nt] == -INFINITY) ? 0.f : ex2f(M[nt] - mstar);
       float* dst = sred + (warp * 8 + j) * 136 + r;
@@ -811,6 +788,23 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
       if (r == 0) s_lw[warp * 8 + j] = lsum[nt] * sc;
     }
   }
+  if (APPEND && warp == DW) {  // p = 1 at its own reference point, o = its V row
+    const float4 vv = *reinterpret_cast<const float4*>(s_vnew + 4 * lane);
+    const float vr[4] = {vv.x, vv.y, vv.z, vv.w};
+    for (int j = 0; j < G; ++j) {
+      const float mj = s_m[DW * 8 + j];
+      float mstar = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < NWARPS; ++w) mstar = fmaxf(mstar, s_m[w * 8 + j]);
+      const float sc = (mj == -INFINITY) ? 0.f : ex2f(mj - mstar);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int dd = 4 * lane + u;
+        sred[(DW * 8 + j) * 136 + (dd & 15) * 8 + (dd >> 4)] = (sc != 0.f) ? sc * vr[u] : 0.f;
+      }
+      if (lane == 0) s_lw[DW * 8 + j] = sc;
+    }
+  }
   __syncthreads();
   KVR_STAMP(5);  // rescaled warp partials in smem
 
@@ -820,7 +814,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
     const int j = x >> 7, pp = x & 127, dd = (pp & 7) * 16 + (pp >> 3);
     float lt = 0.f, ot = 0.f;
 #pragma unroll
-    for (int w = 0; w < DW; ++w) {
+    for (int w = 0; w < NWARPS; ++w) {  // tile warps (+ the writer warp's new token)
       lt += s_lw[w * 8 + j];
       ot += sred[(w * 8 + j) * 136 + pp];
     }
@@ -1290,7 +1284,6 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
     int cl = 0;
     while ((16 << cl) < pool.P) ++cl;
     p.cps_log2 = cl;
-    p.mul24 = 1u << 24;
     p.use_cluster = splits >= 2 && splits <= 16;
     if (new_slot)
       return p.G == 8 ? launch_tma<2, true>(p, sg, grid, smem, ord, st) : launch_tma<1, true>(p, sg, grid, smem, ord, st);

@@ -16,7 +16,8 @@ from paper_2604_19157_b200 import DecodePlan, HeadLayout, PageTable, RotationSpe
 
 H, G, D = 8, 4, 128
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
-split_list = [int(x) for x in sys.argv[2:]] or [0]
+STEP = "--step" in sys.argv  # fused append + decode (kvr_decode_step)
+split_list = [int(x) for x in sys.argv[2:] if not x.startswith("--")] or [0]
 dev = torch.device("cuda")
 layout = HeadLayout(num_q_heads=H * G, num_kv_heads=H, head_dim=D, rot_order=128, page_tokens=16)
 spec = RotationSpec(order=128, signs=make_signs(0, 0, D, 128))
@@ -30,6 +31,22 @@ for _ in range(4):
                        torch.randn(n, H, D, device=dev).bfloat16(), spec=spec, check=False)
     tables.append(t)
 q = torch.randn(1, H * G, D, device=dev).bfloat16()
+kn = torch.randn(1, H, D, device=dev).bfloat16()
+vn = torch.randn(1, H, D, device=dev).bfloat16()
+slots = []
+if STEP:
+    for t in tables:
+        sl, fresh = t.alloc.plan([0])
+        t._zero_pages(fresh)
+        slots.append(torch.from_numpy(sl).to(dev))
+
+
+def run(plan, k):
+    if STEP:
+        plan.run_step(q, kn, vn, slots[k], spec)
+    else:
+        plan.run(q, spec)
+
 out_lines = []
 names = {2: "loop start", 3: "loop end", 4: "M published", 5: "warp partials", 6: "partial stored", 7: "counter back",
          8: "split weights", 9: "merged", 10: "exit"}
@@ -38,18 +55,18 @@ for splits in split_list:
     plans = [DecodePlan(t, [0], num_splits=splits) for t in tables]
     S = plans[0].splits
     tr = torch.zeros(S * H * 16, dtype=torch.int64, device=dev)
-    for p in plans:
-        p.run(q, spec)
+    for k, p in enumerate(plans):
+        run(p, k)
     torch.cuda.synchronize()
     for k in range(3):
-        plans[k].run(q, spec)
+        run(plans[k], k)
     _lib.lib().kvr_debug_decode_trace(ctypes.c_void_p(tr.data_ptr()))
-    plans[3].run(q, spec)
+    run(plans[3], 3)
     torch.cuda.synchronize()
     _lib.lib().kvr_debug_decode_trace(None)
     raw = tr.view(S * H, 16).cpu().numpy().astype(np.float64)
     g0 = raw[:, 0] - raw[:, 0].min()
-    out_lines.append(f"== ctx {L} splits {S} ctas {raw.shape[0]} (HBM-cold launch; clock64 at {MHZ:.0f} MHz)")
+    out_lines.append(f"== ctx {L} splits {S} ctas {raw.shape[0]} {'fused step' if STEP else 'decode'} (HBM-cold launch; clock64 at {MHZ:.0f} MHz)")
     out_lines.append(f"{'start':16s}: min {g0.min() / 1e3:6.2f} med {np.median(g0) / 1e3:6.2f} max {g0.max() / 1e3:6.2f} us")
     for k, nm in names.items():
         ok = raw[:, k] > 0
@@ -63,7 +80,7 @@ for splits in split_list:
     with torch.cuda.stream(s):
         with torch.cuda.graph(g, stream=s):
             for k in range(64):
-                plans[k % 4].run(q, spec)
+                run(plans[k % 4], k % 4)
     torch.cuda.current_stream().wait_stream(s)
     g.replay()
     torch.cuda.synchronize()
