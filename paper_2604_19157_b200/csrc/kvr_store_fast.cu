@@ -6,12 +6,13 @@
 // -> _kernels.fwht_rows + quantize_rows (_ref.py:22-40, 57-80).
 //
 // Design (B200, sm_100a):
-//  * persistent CTAs of 4 warps; each warp streams 32-row tiles (8 KB) through a
-//    private double buffer filled by TMA (cp.async.bulk.tensor.2d, SWIZZLE_128B:
-//    conflict-free row-per-thread shared-memory reads);
-//  * one thread owns one 128-element row in registers: sign flip + bf16 unpack
-//    fused with the first butterfly stage, the remaining stages as f32x2 (FADD2),
-//    NaN-propagating 3-input min/max (FMNMX3.NAN);
+//  * persistent CTAs of 4 warps, 4 CTAs per SM; each warp streams 16-row tiles
+//    (4 KB) through a private double buffer filled by TMA (cp.async.bulk.tensor.2d,
+//    SWIZZLE_128B: conflict-free half-row-per-thread shared-memory reads);
+//  * a lane pair owns one 128-element row, 64 elements each in registers: sign
+//    flip + bf16 unpack fused with the first butterfly stage, stages up to half 32
+//    as f32x2 (FADD2), the half-64 stage across the pair (64 shuffles), NaN-
+//    propagating 3-input min/max (FMNMX3.NAN) combined across the pair;
 //  * the row scale / zero point are formed in f64 exactly as the reference does,
 //    from the fp32 butterfly's extreme values;
 //  * codes: one FFMA2.RM per element pair evaluates floor((t + z + 1/2) * 2^16)
@@ -19,7 +20,9 @@
 //    the integer part the nibble is the reference's round-half-away code for this
 //    y; a row with an element within delta of a half step is recomputed in f64
 //    from the bf16 inputs with the reference's butterfly order, warp-cooperatively
-//    (warp_exact_row), and its flagged 8-code groups are replaced;
+//    (warp_exact_row), and its flagged 8-code groups are replaced.  Unrotated
+//    (plain) rows hold y exactly, so their flagged groups are fixed in-thread by
+//    exact FMA sign tests against the rounding boundaries instead;
 //  * 8 nibbles are packed with 3 PRMT + 1 IMAD.HI per 4 codes.
 #include "kvr_common.cuh"
 #include "kvr_internal.h"
@@ -28,13 +31,17 @@ namespace kvr {
 
 constexpr int FS_WARPS = 4;
 #ifndef KVR_FS_MINB
-#define KVR_FS_MINB 2
+#define KVR_FS_MINB 4
 #endif
-constexpr int FS_TILE_ROWS = 32;
+constexpr int FS_TILE_ROWS = 16;
+constexpr int FS_SUB_BYTES = FS_TILE_ROWS * 128;    // one 64-element half of the tile's rows
 constexpr int FS_TILE_BYTES = FS_TILE_ROWS * 256;  // 128 x 16-bit per row
 constexpr float FS_MAGIC = 8388608.0f;            // 2^23
 constexpr float FS_FIX = 65536.0f;                // 16 fraction bits
-constexpr float FS_D = 1.0f;                      // +-delta in units of 2^-16 (delta ~ 1.5e-5)
+// +-delta of the boundary test in units of 2^-16 of u = y c + z + 1/2: the
+// magic-number floor works at 2^23 <= U < 2^24, where one unit is the f32 ulp.
+constexpr float FS_D = 1.0f;
+constexpr float FS_D_CLAMP = 1.0f;
 
 struct FastStoreParams {
   Pool pool;
@@ -66,7 +73,7 @@ template <bool F16>
 KVR_DEV void tile_quad(const uint8_t* buf, int src, int l, double (&x)[4]) {
   const int e = 4 * l;
   const int h = e >> 6, c = (e >> 3) & 7, within = e & 7;
-  const uint2 q = *reinterpret_cast<const uint2*>(buf + h * 4096 + src * 128 + ((c ^ (src & 7)) << 4) + within * 2);
+  const uint2 q = *reinterpret_cast<const uint2*>(buf + h * FS_SUB_BYTES + src * 128 + ((c ^ (src & 7)) << 4) + within * 2);
   const uint32_t w[2] = {q.x, q.y};
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
@@ -124,32 +131,44 @@ KVR_DEV uint32_t pack4(uint32_t m0, uint32_t m1, uint32_t m2, uint32_t m3) {
   return __umulhi(c, 1u << 28) + c;  // c | c >> 4: bytes 0 and 2 hold k0|k1<<4, k2|k3<<4
 }
 
-// Quantize this lane's staged row: packed codes, scale, zero point; returns write flag.
+// Exact reference code of a plain (unrotated) element: y is x itself (exact in
+// f32) and s = f32 scale, so round_half_away(x / s64) is decided by the signs of
+// x - (m -+ 1/2) s, each evaluated with one rounding (FMA) and hence exact.
+KVR_DEV uint32_t plain_code_exact(float x, float s, float inv, float z) {
+  const float ax = fabsf(x);
+  float m = floorf(fmaf(ax, inv, 0.5f));
+  if (fmaf(-(m - 0.5f), s, ax) < 0.f) m -= 1.f;
+  else if (fmaf(-(m + 0.5f), s, ax) >= 0.f) m += 1.f;
+  const float q = fminf(fmaxf(copysignf(m, x) + z, 0.f), 15.f);
+  return (uint32_t)q;
+}
+
+// Quantize the half row (64 elements, half `hf`) this lane shares with lane ^ 1:
+// its 32 packed code bytes, the row scale and zero point; returns the write flag.
 template <int ORDER, bool F16, bool ROT>
-KVR_DEV bool row_codes(const uint8_t* buf, int lane, const FastStoreParams& p, const Signs& signs, bool valid,
-                       uint32_t (&packed)[16], float& scale_out, uint32_t& zp_out) {
-  // ---- stage the row: 16 x 16 B swizzled reads; unpack fused with stage half = 1
-  unsigned long long v[64];  // v[j] = (y_{2j}, y_{2j+1})
+KVR_DEV bool half_row_codes(const uint8_t* buf, int row, int hf, const FastStoreParams& p, const Signs& signs,
+                            bool valid, uint32_t (&packed)[8], float& scale_out, uint32_t& zp_out) {
+  const int lane = threadIdx.x & 31;
+  // ---- stage the half row: 8 x 16 B swizzled reads; unpack fused with stage half = 1
+  unsigned long long v[32];  // v[j] = (y_{2j}, y_{2j+1}) of this half
 #pragma unroll
-  for (int h = 0; h < 2; ++h)
+  for (int c = 0; c < 8; ++c) {
+    const uint4 q = *reinterpret_cast<const uint4*>(buf + hf * FS_SUB_BYTES + row * 128 + ((c ^ (row & 7)) << 4));
+    const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const uint4 q = *reinterpret_cast<const uint4*>(buf + h * 4096 + lane * 128 + ((c ^ (lane & 7)) << 4));
-      const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = h * 32 + c * 4 + u;
-        float e, o;
-        unpack_pair<F16, ROT>(w4[u], p.sgn_hi[j], p.sgn_lo[j], e, o);
-        v[j] = ROT ? pk(e + o, e - o) : pk(e, o);
-      }
+    for (int u = 0; u < 4; ++u) {
+      const int j = c * 4 + u;
+      float e, o;
+      unpack_pair<F16, ROT>(w4[u], p.sgn_hi[32 * hf + j], p.sgn_lo[32 * hf + j], e, o);
+      v[j] = ROT ? pk(e + o, e - o) : pk(e, o);
     }
+  }
   if constexpr (ROT) {
-    // stages half = 2 .. ORDER/2: pairs (j, j + hh) of (y_{2j}, y_{2j+1}) vectors
+    // stages half = 2 .. min(ORDER/2, 32) inside the half: pairs (j, j + hh) of (y_{2j}, y_{2j+1})
 #pragma unroll
-    for (int hh = 1; hh < ORDER / 2; hh <<= 1) {
+    for (int hh = 1; hh < ORDER / 2 && hh < 32; hh <<= 1) {
 #pragma unroll
-      for (int j = 0; j < 64; ++j) {
+      for (int j = 0; j < 32; ++j) {
         if ((j & hh) == 0) {
           const unsigned long long a = v[j], c = v[j + hh];
           v[j] = add2(a, c);
@@ -157,11 +176,21 @@ KVR_DEV bool row_codes(const uint8_t* buf, int lane, const FastStoreParams& p, c
         }
       }
     }
+    if constexpr (ORDER == 128) {
+      // stage half = 64 across the lane pair: y_j = a_j + b_j (half 0), a_j - b_j (half 1)
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        float x0, x1;
+        upk(v[j], x0, x1);
+        const float o0 = __shfl_xor_sync(0xffffffffu, x0, 1), o1 = __shfl_xor_sync(0xffffffffu, x1, 1);
+        v[j] = hf ? sub2(pk(o0, o1), v[j]) : add2(v[j], pk(o0, o1));
+      }
+    }
   }
-  // ---- row extremes (NaN-propagating)
-  float mx0, mn0, mx1, mn1;
+  // ---- row extremes (NaN-propagating), combined across the pair
+  float mxf, mnf;
   {
-    float a0, a1, b0, b1;
+    float mx0, mn0, mx1, mn1, a0, a1, b0, b1;
     upk(v[0], a0, a1);
     upk(v[1], b0, b1);
     mx0 = max3_nan(a0, a1, a1);
@@ -169,7 +198,7 @@ KVR_DEV bool row_codes(const uint8_t* buf, int lane, const FastStoreParams& p, c
     mx1 = max3_nan(b0, b1, b1);
     mn1 = min3_nan(b0, b1, b1);
 #pragma unroll
-    for (int j = 2; j < 64; j += 2) {
+    for (int j = 2; j < 32; j += 2) {
       float x0, x1, y0, y1;
       upk(v[j], x0, x1);
       upk(v[j + 1], y0, y1);
@@ -178,26 +207,29 @@ KVR_DEV bool row_codes(const uint8_t* buf, int lane, const FastStoreParams& p, c
       mx1 = max3_nan(mx1, y0, y1);
       mn1 = min3_nan(mn1, y0, y1);
     }
+    const float mxh = max3_nan(mx0, mx1, mx1), mnh = min3_nan(mn0, mn1, mn1);
+    mxf = max3_nan(mxh, __shfl_xor_sync(0xffffffffu, mxh, 1), mxh);
+    mnf = min3_nan(mnh, __shfl_xor_sync(0xffffffffu, mnh, 1), mnh);
   }
-  const float mxf = max3_nan(mx0, mx1, mx1), mnf = min3_nan(mn0, mn1, mn1);
 
 #pragma unroll
-  for (int i = 0; i < 16; ++i) packed[i] = 0u;
+  for (int i = 0; i < 8; ++i) packed[i] = 0u;
   scale_out = 0.f;
   zp_out = 0u;
   bool write = valid;
   if (valid && !(isfinite(mxf) && isfinite(mnf))) {
-    if (p.flags) atomicOr(p.flags, (uint32_t)KVR_FLAG_NONFINITE);
+    if (p.flags && hf == 0) atomicOr(p.flags, (uint32_t)KVR_FLAG_NONFINITE);
     write = false;
   }
   // ---- row scale / zero point in f64, exactly as _ref.quantize_rows
   const double inv64 = 1.0 / sqrt((double)ORDER);
   bool do_codes = false, clamp_row = false;
   double s64 = 1.0, z = 0.0, cst = 0.0;
+  float s32 = 0.f;
   if (write) {
     const double scl = ROT ? inv64 : 1.0;
     const double mx = (double)mxf * scl, mn = (double)mnf * scl;  // == fl64(S * inv) of the reference
-    const float s32 = (float)((mx - mn) / 15.0);
+    s32 = (float)((mx - mn) / 15.0);
     if (s32 == 0.0f) {
       scale_out = (float)mn;  // sentinel row: offset in the scale slot, zp 0xFF, codes 0
       zp_out = 0xFFu;
@@ -216,7 +248,7 @@ KVR_DEV bool row_codes(const uint8_t* buf, int lane, const FastStoreParams& p, c
     }
   }
   const bool clamp = __any_sync(0xffffffffu, do_codes && clamp_row);
-  uint32_t gflags = 0u;  // bit q: an element of 8q..8q+7 is within delta of a rounding boundary
+  uint32_t gflags = 0u;  // bit q: an element of 8q..8q+7 (of this half) is within delta of a boundary
   if (do_codes) {
     if (!clamp) {
       // U = floor((y*c + z + 1/2 (+-delta)) * 2^16) + 2^23, one FFMA2.RM per pair and sign
@@ -225,7 +257,7 @@ KVR_DEV bool row_codes(const uint8_t* buf, int lane, const FastStoreParams& p, c
       const unsigned long long c2 = pk(cf, cf);
       const unsigned long long bp = pk(bias + FS_D, bias + FS_D), bm = pk(bias - FS_D, bias - FS_D);
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
+      for (int q = 0; q < 8; ++q) {
         uint32_t mp[8], dq = 0u;
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
@@ -243,9 +275,10 @@ KVR_DEV bool row_codes(const uint8_t* buf, int lane, const FastStoreParams& p, c
       // clamped variant: u in f32 (error <= 2^-20), clamped to [2^-13, 15.99], then the magic floor
       const float zb = (float)(z + 0.5), cu = (float)cst;
       const unsigned long long fix2 = pk(FS_FIX, FS_FIX);
-      const unsigned long long mgp = pk(FS_MAGIC + FS_D, FS_MAGIC + FS_D), mgm = pk(FS_MAGIC - FS_D, FS_MAGIC - FS_D);
+      const unsigned long long mgp = pk(FS_MAGIC + FS_D_CLAMP, FS_MAGIC + FS_D_CLAMP),
+                               mgm = pk(FS_MAGIC - FS_D_CLAMP, FS_MAGIC - FS_D_CLAMP);
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
+      for (int q = 0; q < 8; ++q) {
         uint32_t mp[8], dq = 0u;
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
@@ -265,19 +298,43 @@ KVR_DEV bool row_codes(const uint8_t* buf, int lane, const FastStoreParams& p, c
       }
     }
   }
-  // ---- rare: reference-exact recomputation of flagged rows, warp-cooperative
-  uint32_t todo = __ballot_sync(0xffffffffu, gflags != 0u);
-  while (todo) {
-    const int src = __ffs(todo) - 1;
-    todo &= todo - 1;
-    const uint32_t gf = __shfl_sync(0xffffffffu, gflags, src);
-    const double sb = __shfl_sync(0xffffffffu, s64, src), zb = __shfl_sync(0xffffffffu, z, src);
-    const uint32_t g16 = warp_exact_row<ORDER, F16, ROT>(buf, src, signs, sb, zb);
+  if constexpr (!ROT) {
+    // plain rows: exact in-thread fix of the flagged groups
+    if (gflags) {
+      const float inv = 1.0f / s32, zf = (float)z;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      if ((gf >> q) & 1u) {  // warp-uniform
-        const uint32_t lo = __shfl_sync(0xffffffffu, g16, 2 * q), hi = __shfl_sync(0xffffffffu, g16, 2 * q + 1);
-        if (lane == src) packed[q] = lo | (hi << 16);
+      for (int q = 0; q < 8; ++q) {
+        if ((gflags >> q) & 1u) {
+          uint32_t w = 0u;
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            float a0, a1;
+            upk(v[q * 4 + r], a0, a1);
+            w |= plain_code_exact(a0, s32, inv, zf) << (8 * r);
+            w |= plain_code_exact(a1, s32, inv, zf) << (8 * r + 4);
+          }
+          packed[q] = w;
+        }
+      }
+    }
+  } else {
+    // ---- rare: reference-exact recomputation of flagged rows, warp-cooperative
+    uint32_t todo = __ballot_sync(0xffffffffu, gflags != 0u);
+    while (todo) {
+      const int src = __ffs(todo) - 1;  // lane src: half (src & 1) of tile row 16 pass + src / 2
+      todo &= todo - 1;
+      const uint32_t gf = __shfl_sync(0xffffffffu, gflags, src);
+      const double sb = __shfl_sync(0xffffffffu, s64, src), zb = __shfl_sync(0xffffffffu, z, src);
+      const int srow = __shfl_sync(0xffffffffu, row, src);
+      const uint32_t g16 = warp_exact_row<ORDER, F16, ROT>(buf, srow, signs, sb, zb);
+      const int hb = (src & 1) * 8;  // the half's groups are row groups hb .. hb + 7
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if ((gf >> q) & 1u) {  // warp-uniform
+          const uint32_t lo = __shfl_sync(0xffffffffu, g16, 2 * (hb + q)),
+                         hi = __shfl_sync(0xffffffffu, g16, 2 * (hb + q) + 1);
+          if (lane == src) packed[q] = lo | (hi << 16);
+        }
       }
     }
   }
@@ -297,6 +354,7 @@ __global__ void __launch_bounds__(FS_WARPS * 32, KVR_FS_MINB)
   const int total_tiles = 2 * p.tiles_per_side;
   const int warp_stride = gridDim.x * FS_WARPS;
   const int H = p.pool.H;
+  const int trow = lane >> 1, hf = lane & 1;  // this lane: half hf of tile row trow
 
   if (lane == 0) {
     prefetch_tensormap(&map_k);
@@ -315,11 +373,11 @@ __global__ void __launch_bounds__(FS_WARPS * 32, KVR_FS_MINB)
     fence_proxy_async();
     mbar_expect_tx(&bars[b], FS_TILE_BYTES);
     tma_load_2d(dst, m, &bars[b], 0, row0);
-    tma_load_2d(dst + 4096, m, &bars[b], 64, row0);
+    tma_load_2d(dst + FS_SUB_BYTES, m, &bars[b], 64, row0);
   };
   auto row_of = [&](int tile) -> int64_t {
     const int side = tile >= p.tiles_per_side;
-    return (int64_t)(side ? tile - p.tiles_per_side : tile) * FS_TILE_ROWS + lane;
+    return (int64_t)(side ? tile - p.tiles_per_side : tile) * FS_TILE_ROWS + trow;
   };
   auto slot_of = [&](int tile) -> int64_t {  // slot id of this lane's row (or -1)
     if (tile >= total_tiles) return -1;
@@ -345,14 +403,14 @@ __global__ void __launch_bounds__(FS_WARPS * 32, KVR_FS_MINB)
     const int64_t row = row_of(tile);
     const bool valid = row < p.n_rows;  // codes are computed whatever the slot; the store is predicated
 
-    uint32_t packed[16];
+    uint32_t packed[8];
     float scale_out;
     uint32_t zp_out;
     bool write;
     if (side ? p.rot_v : p.rot_k)  // warp-uniform
-      write = row_codes<ORDER, F16, true>(buf, lane, p, signs, valid, packed, scale_out, zp_out);
+      write = half_row_codes<ORDER, F16, true>(buf, trow, hf, p, signs, valid, packed, scale_out, zp_out);
     else
-      write = row_codes<128, F16, false>(buf, lane, p, signs, valid, packed, scale_out, zp_out);
+      write = half_row_codes<128, F16, false>(buf, trow, hf, p, signs, valid, packed, scale_out, zp_out);
     __syncwarp();  // every lane done with the staged tile -> buffer may be refilled
 
     if (write && slot >= 0) {
@@ -360,12 +418,13 @@ __global__ void __launch_bounds__(FS_WARPS * 32, KVR_FS_MINB)
       const int head = (int)(row % H);
       int ci;
       uint8_t* cell = cell_of(pl, slot / pl.P, head, (int)(slot % pl.P), ci);
-      uint4* dst = reinterpret_cast<uint4*>(cell + (side ? cell_vcode(pl, ci) : cell_kcode(pl, ci)));
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
-      *reinterpret_cast<float*>(cell + (side ? cell_vscale(pl, ci) : cell_kscale(pl, ci))) = scale_out;
-      cell[side ? cell_vzp(pl, ci) : cell_kzp(pl, ci)] = (uint8_t)zp_out;
+      uint4* dst = reinterpret_cast<uint4*>(cell + (side ? cell_vcode(pl, ci) : cell_kcode(pl, ci)) + 32 * hf);
+      dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+      dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+      if (hf == 0) {
+        *reinterpret_cast<float*>(cell + (side ? cell_vscale(pl, ci) : cell_kscale(pl, ci))) = scale_out;
+        cell[side ? cell_vzp(pl, ci) : cell_kzp(pl, ci)] = (uint8_t)zp_out;
+      }
     }
   }
 }
