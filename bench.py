@@ -246,9 +246,6 @@ def run_ours(args, rank, world, local_rank):
     except Exception:
         pass
 
-    # ---- C1: quantize-store of 4096 tokens x 8 heads (rotated vs plain), rotating inputs
-    c1 = c1_quantize_store(torch, layout, spec, dev, gen, timed)
-
     # ---- e2e through the public API with host buffers
     e2e = e2e_api(torch, layout, spec, dev, sets[0]["table"], args, world)
 
@@ -256,6 +253,20 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         outs = [torch.empty_like(sets[0]["out"]) for _ in range(world)]
         torch.distributed.all_gather(outs, sets[0]["out"])
+    splits = sets[0]["plan"].splits
+
+    # ---- the other BASELINE configs (parity-test cases, reported in `detail`)
+    c1 = c1_quantize_store(torch, layout, spec, dev, gen, timed)
+    c3 = c4 = c5 = None
+    if not args.quick:
+        sets.clear()  # free the headline's buffers first
+        torch.cuda.empty_cache()
+        c3 = c3_sweep(torch, dev, gen, timed)
+        print(f"[bench] C3 {[(r['batch'], r['us'], r['frac']) for r in c3]}", file=sys.stderr, flush=True)
+        c5 = c5_long(torch, dev, gen, timed)
+        print(f"[bench] C5 {[(r['ctx'], r['rot_order'], r['us'], r['frac']) for r in c5]}", file=sys.stderr, flush=True)
+        c4 = c4_llama70b_shard(torch, dev, gen, timed, world)
+        print(f"[bench] C4 step {c4['step_us']} us, {c4['tok_per_s_per_gpu']} tok/s/GPU", file=sys.stderr, flush=True)
 
     cpu = None
     if rank == 0 and not args.no_cpu:
@@ -280,7 +291,7 @@ def run_ours(args, rank, world, local_rank):
             "workload": "BASELINE configs[1] / C2: Llama-3-8B-shaped decode step, batch 1 per GPU, 32768 cached "
                         "tokens (+1 written), GQA 32q/8kv, head_dim 128, Hadamard order 128, page 16, K&V rotated",
             "per_gpu_batch": 1, "ctx": L, "num_q_heads": NQ, "num_kv_heads": H, "head_dim": D,
-            "rot_order": ORDER, "page_tokens": P, "decode_splits": sets[0]["plan"].splits,
+            "rot_order": ORDER, "page_tokens": P, "decode_splits": splits,
             "l2": f"{R} rotating buffer sets of {step_bytes(Lstep) / 1e6:.1f} MB (> 2x 126 MB L2), CUDA-graph replay",
             "parallelism": f"dp{world} (independent sequences per GPU, no data-path collective)",
             "algorithmic_bytes_per_step": per_rank_bytes,
@@ -300,9 +311,154 @@ def run_ours(args, rank, world, local_rank):
             "fused_step_us": round(t_fused * 1e3, 3), "fused_step_plain_us": round(t_fp * 1e3, 3),
             "fused_step_overhead_vs_plain": round(t_fused / t_fp - 1.0, 4),
             "c1_quantize_store": c1,
+            "c3_concurrency_sweep": c3,
+            "c4_llama70b_8gpu_shard": c4,
+            "c5_long_context_1kv_per_gpu": c5,
         },
     }
     print(json.dumps(line), flush=True)
+
+
+def build_table(torch, layout, spec, dev, gen, B, L, extra_tokens=1, chunk=16384):
+    """B sequences of L cached tokens (random bf16 K/V written through K1), with
+    page room for `extra_tokens` more per sequence."""
+    from paper_2604_19157_b200 import PageTable
+
+    P, Hh, Dd = layout.page_tokens, layout.num_kv_heads, layout.head_dim
+    t = PageTable(layout, num_pages=B * -(-(L + extra_tokens) // P), device=dev)
+    for b in range(B):
+        t.create_sequence(b)
+        slots = torch.from_numpy(t.alloc.reserve(b, L)).to(dev)
+        for c0 in range(0, L, chunk):
+            n = min(chunk, L - c0)
+            k = torch.randn((n, Hh, Dd), generator=gen, device=dev).to(torch.bfloat16)
+            v = torch.randn((n, Hh, Dd), generator=gen, device=dev).to(torch.bfloat16)
+            t.store_slots(k, v, slots[c0:c0 + n], spec)
+    return t
+
+
+def clone_table(torch, t):
+    """Same allocator state and page contents in a fresh pool (another layer's cache)."""
+    from paper_2604_19157_b200 import PageTable
+
+    c = PageTable(t.layout, num_pages=t.num_pages, device=t.device)
+    c.pool.copy_(t.pool)
+    c.alloc.seq_pages = {s: list(p) for s, p in t.alloc.seq_pages.items()}
+    c.alloc.seq_len = dict(t.alloc.seq_len)
+    c.alloc.free = list(t.alloc.free)
+    return c
+
+
+def decode_case(torch, dev, tables, spec, timed, fused=False, n=256, gen=None):
+    """Device time of one decode (or fused append + decode) launch per table, with
+    the tables replayed round robin (rotated and plain twin); returns a dict."""
+    from paper_2604_19157_b200 import DecodePlan
+
+    lay = tables[0].layout
+    seqs = sorted(tables[0].alloc.seq_pages)
+    B = len(seqs)
+    cases = []
+    for t in tables:
+        c = {"table": t}
+        if fused:
+            sl, fresh = t.alloc.plan(seqs)
+            t._zero_pages(fresh)
+            c["slot"] = torch.from_numpy(sl).to(dev)
+            c["k"] = torch.randn((B, lay.num_kv_heads, lay.head_dim), generator=gen, device=dev).to(torch.bfloat16)
+            c["v"] = torch.randn((B, lay.num_kv_heads, lay.head_dim), generator=gen, device=dev).to(torch.bfloat16)
+        c["plan"] = DecodePlan(t, seqs)
+        c["q"] = torch.randn((B, lay.num_q_heads, lay.head_dim), generator=gen, device=dev).to(torch.bfloat16)
+        c["out"] = torch.empty((B, lay.num_q_heads, lay.head_dim), dtype=torch.float32, device=dev)
+        cases.append(c)
+    R = len(cases)
+
+    def one(i, sp):
+        c = cases[i % R]
+        if fused:
+            c["plan"].run_step(c["q"], c["k"], c["v"], c["slot"], sp, out=c["out"])
+        else:
+            c["plan"].run(c["q"], sp, out=c["out"])
+
+    t_rot = timed(lambda i: one(i, spec), n) / n
+    t_pl = timed(lambda i: one(i, None), n) / n
+    if fused:  # restore the rotated new token the plain twin overwrote
+        for i in range(R):
+            one(i, spec)
+        torch.cuda.synchronize()
+    L = max(tables[0].alloc.seq_len.values())
+    Hh, G = lay.num_kv_heads, lay.num_q_heads // lay.num_kv_heads
+    tokb = Hh * (lay.head_dim + 10)
+    byts = B * (L * tokb + -(-L // lay.page_tokens) * 4 + lay.num_q_heads * lay.head_dim * (2 + 4))
+    if fused:
+        byts += B * (2 * Hh * lay.head_dim * 2 + tokb + 8)
+    peak, _ = hbm_peak()
+    return {"batch": B, "ctx": L, "num_kv_heads": Hh, "q_per_kv": G, "rot_order": lay.rot_order,
+            "splits": cases[0]["plan"].splits, "algorithmic_bytes": byts,
+            "us": round(t_rot * 1e3, 3), "plain_us": round(t_pl * 1e3, 3),
+            "GBps": round(byts / (t_rot * 1e-3) / 1e9, 1), "frac": round(byts / (t_rot * 1e-3) / 1e9 / peak, 4),
+            "overhead_vs_plain": round(t_rot / t_pl - 1.0, 4), "tok_per_s": round(B / (t_rot * 1e-3), 1),
+            "l2": f"{R} rotating table(s) of {byts / 1e6:.0f} MB"}
+
+
+def c3_sweep(torch, dev, gen, timed):
+    """BASELINE configs[2]: batch 1/16/64/256 x 8k context decode, Hadamard vs plain INT4."""
+    from paper_2604_19157_b200 import HeadLayout, RotationSpec, make_signs
+
+    layout = HeadLayout(num_q_heads=NQ, num_kv_heads=H, head_dim=D, rot_order=ORDER, page_tokens=P)
+    spec = RotationSpec(order=ORDER, signs=make_signs(0, 0, D, ORDER))
+    out = []
+    for B in (1, 16, 64, 256):
+        reps = max(1, -(-300_000_000 // (B * 8192 * TOK_BYTES)))  # > 2x L2 across the rotation
+        base = build_table(torch, layout, spec, dev, gen, B, 8192)
+        tables = [base] + [clone_table(torch, base) for _ in range(reps - 1)]
+        out.append(decode_case(torch, dev, tables, spec, timed, gen=gen))
+        del tables, base
+        torch.cuda.empty_cache()
+    return out
+
+
+def c4_llama70b_shard(torch, dev, gen, timed, world):
+    """BASELINE configs[3] at its 8-GPU shard size on this GPU: Llama-3-70B KV geometry
+    (8 kv heads, 64 q heads, d 128), 128 sequences / 8 GPUs = 16 sequences x 16k
+    context, 80 layers; one step = the fused append + decode of every layer."""
+    from paper_2604_19157_b200 import HeadLayout, RotationSpec, make_signs
+
+    layers, B, L = 80, 128 // 8, 16384
+    layout = HeadLayout(num_q_heads=64, num_kv_heads=8, head_dim=D, rot_order=ORDER, page_tokens=P)
+    spec = RotationSpec(order=ORDER, signs=make_signs(0, 0, D, ORDER))
+    base = build_table(torch, layout, spec, dev, gen, B, L)
+    tables = [base] + [clone_table(torch, base) for _ in range(layers - 1)]
+    r = decode_case(torch, dev, tables, spec, timed, fused=True, n=layers * 4, gen=gen)
+    step_us = r["us"] * layers
+    res = {"layers": layers, "sequences_per_gpu": B, "ctx": L, "q_heads": 64, "kv_heads": 8,
+           "layer_step_us": r["us"], "layer_plain_us": r["plain_us"], "step_us": round(step_us, 1),
+           "tok_per_s_per_gpu": round(B / (step_us * 1e-6), 1), "GBps": r["GBps"], "frac": r["frac"],
+           "overhead_vs_plain": r["overhead_vs_plain"], "splits": r["splits"],
+           "bytes_per_step": r["algorithmic_bytes"] * layers,
+           "note": "per-GPU shard of the 8-GPU configuration (128 x 16k x 80 layers = 186 GB does not fit "
+                   "one 180 GB GPU); 80 layer caches, each step runs all 80 fused append+decode launches"}
+    del tables, base
+    torch.cuda.empty_cache()
+    return res
+
+
+def c5_long(torch, dev, gen, timed):
+    """BASELINE configs[4]: one request at 128k / 1M tokens, KV heads sharded 8 ways
+    (this GPU: 1 kv head + its 4 q heads), split-K decode, Hadamard order 64 / 128."""
+    from paper_2604_19157_b200 import HeadLayout, RotationSpec, make_signs
+
+    out = []
+    for L in (131072, 1048576):
+        for order in (128, 64):
+            layout = HeadLayout(num_q_heads=4, num_kv_heads=1, head_dim=D, rot_order=order, page_tokens=P)
+            spec = RotationSpec(order=order, signs=make_signs(0, 0, D, order))
+            reps = max(2, -(-300_000_000 // (L * (D + 10))))
+            base = build_table(torch, layout, spec, dev, gen, 1, L)
+            tables = [base] + [clone_table(torch, base) for _ in range(reps - 1)]
+            out.append(decode_case(torch, dev, tables, spec, timed, gen=gen, n=128))
+            del tables, base
+            torch.cuda.empty_cache()
+    return out
 
 
 def c1_quantize_store(torch, layout, spec, dev, gen, timed):
@@ -324,7 +480,26 @@ def c1_quantize_store(torch, layout, spec, dev, gen, timed):
     t_pl = timed(lambda i: sets[i % R][0].store_slots(sets[i % R][1], sets[i % R][2], sets[i % R][3], None), n) / n
     byts = n_tok * WRITE_BYTES_PER_TOKEN
     peak, _ = hbm_peak()
+    # K4 flatten-dequant of the same 4096 tokens back to bf16 (stored space)
+    import ctypes
+
+    from paper_2604_19157_b200 import _kernels, _lib
+    outs = []
+    for t, _, _, _ in sets:
+        bt, lens, ml = t.block_table([0])
+        outs.append((t, bt, lens, ml, torch.empty((1, n_tok, H, D), dtype=torch.bfloat16, device=dev),
+                     torch.empty((1, n_tok, H, D), dtype=torch.bfloat16, device=dev)))
+
+    def deq(i):
+        t, bt, lens, ml, ko, vo = outs[i % R]
+        _lib.check(_lib.lib().kvr_dequantize_pages(ctypes.byref(t.desc), _kernels.ptr(bt), bt.shape[1],
+                                                   _kernels.ptr(lens), 1, ml, _kernels.ptr(ko), _kernels.ptr(vo),
+                                                   _lib.KVR_BF16, _kernels.stream_ptr()))
+    t_dq = timed(deq, n) / n
+    dq_bytes = n_tok * (TOK_BYTES + 2 * H * D * 2) + (n_tok // P) * 4
     return {"tokens": n_tok, "algorithmic_bytes": byts, "rot_us": round(t_rot * 1e3, 3),
+            "dequant_us": round(t_dq * 1e3, 3), "dequant_GBps": round(dq_bytes / (t_dq * 1e-3) / 1e9, 1),
+            "dequant_frac": round(dq_bytes / (t_dq * 1e-3) / 1e9 / peak, 4),
             "plain_us": round(t_pl * 1e3, 3), "rot_GBps": round(byts / (t_rot * 1e-3) / 1e9, 1),
             "plain_GBps": round(byts / (t_pl * 1e-3) / 1e9, 1), "rot_frac": round(byts / (t_rot * 1e-3) / 1e9 / peak, 4),
             "overhead_vs_plain": round(t_rot / t_pl - 1.0, 4)}
@@ -494,6 +669,7 @@ def main():
     ap.add_argument("--sets", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--quick", action="store_true", help="headline + C1 only (skip the C3/C4/C5 detail configs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", 0))

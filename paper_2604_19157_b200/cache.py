@@ -176,6 +176,22 @@ class PageAllocator:
         self.seq_pages[seq] = []
         self.seq_len[seq] = 0
 
+    def reserve(self, seq: int, n: int) -> np.ndarray:
+        """Bulk form of plan([seq] * n): slot ids of the next n tokens of `seq`,
+        taking new pages lowest id first (O(pages), for prefill-sized appends)."""
+        self.require(seq)
+        P = self.page_tokens
+        t0 = self.seq_len[seq]
+        owned = self.seq_pages[seq]
+        need = max(0, -(-(t0 + n) // P) - len(owned))
+        if need > len(self.free):
+            raise CapacityExceededError(f"page pool exhausted ({self.num_pages} pages)")
+        owned.extend(heapq.heappop(self.free) for _ in range(need))
+        pos = np.arange(t0, t0 + n, dtype=np.int64)
+        slots = np.asarray(owned, dtype=np.int64)[pos // P] * P + pos % P
+        self.seq_len[seq] = t0 + n
+        return slots
+
     def release(self, seq: int) -> int:
         self.require(seq)
         pages = self.seq_pages.pop(seq)
