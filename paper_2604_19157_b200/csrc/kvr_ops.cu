@@ -202,6 +202,60 @@ __global__ void dequant_pages_kernel(Pool pool, const int32_t* bt, int bt_stride
   }
 }
 
+// Fast flatten-dequant for the serving geometry (d = 128, 16-token cells): one warp
+// per cell (16 tokens of one head); lane pair (2r, 2r+1) owns token r, 64 dims each,
+// reads 32 code bytes as two 16-B loads and writes 64 outputs as full 16-B stores
+// (a token's 128 outputs are one contiguous 256-B (bf16) / 512-B (f32) run).
+// Arithmetic: f32 s * (q - z) (q - z exact, one rounding), then the output cast.
+template <typename TOut>
+__global__ void __launch_bounds__(256) dequant_cells_kernel(Pool pool, const int32_t* bt, int bt_stride,
+                                                            const int32_t* lens, int batch, int max_len, int cps_log2,
+                                                            TOut* k_out, TOut* v_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t cell_id = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int H = pool.H, ntiles = (max_len + 15) >> 4;
+  if (cell_id >= (int64_t)batch * ntiles * H) return;
+  const int head = (int)(cell_id % H);
+  const int64_t bt_ = cell_id / H;
+  const int tile = (int)(bt_ % ntiles), b = (int)(bt_ / ntiles);
+  const int r = lane >> 1, hf = lane & 1, t = tile * 16 + r;
+  if (t >= __ldg(&lens[b]) || t >= max_len) return;
+  const int page = __ldg(&bt[(int64_t)b * bt_stride + (t >> (4 + cps_log2))]);
+  const uint8_t* cell = pool.base + (int64_t)page * pool.page_bytes +
+                        (int64_t)((head << cps_log2) + (tile & ((1 << cps_log2) - 1))) * pool.cell_bytes;
+#pragma unroll
+  for (int side = 0; side < 2; ++side) {
+    const uint4* src = reinterpret_cast<const uint4*>(cell + (side ? 1152 : 128) + r * 64 + hf * 32);
+    const uint4 c0 = __ldg(src), c1 = __ldg(src + 1);
+    const float sc = __ldg(reinterpret_cast<const float*>(cell + side * 64 + r * 4));
+    const uint32_t zp = __ldg(cell + 2176 + side * 16 + r);
+    const uint32_t w[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    float f[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+      const float q = (float)((w[i >> 3] >> (4 * (i & 7))) & 15u);
+      f[i] = zp == 0xFFu ? sc : sc * (q - (float)zp);
+    }
+    TOut* dst = (side ? v_out : k_out) + (((int64_t)b * max_len + t) * H + head) * 128 + hf * 64;
+    if constexpr (sizeof(TOut) == 2) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        uint32_t u[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const __nv_bfloat162 h2 = __floats2bfloat162_rn(f[8 * i + 2 * k], f[8 * i + 2 * k + 1]);
+          u[k] = *reinterpret_cast<const uint32_t*>(&h2);
+        }
+        reinterpret_cast<uint4*>(dst)[i] = make_uint4(u[0], u[1], u[2], u[3]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        reinterpret_cast<float4*>(dst)[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
+    }
+  }
+}
+
 }  // namespace kvr
 
 // ============================ host launchers ================================
@@ -305,6 +359,21 @@ int kvr_launch_store_exact(const void* k, const void* v, int in_dtype, int64_t n
 
 int kvr_launch_dequant_pages(const Pool& pool, const int32_t* bt, int bt_stride, const int32_t* lens, int batch,
                              int max_len, void* k_out, void* v_out, int out_dtype, cudaStream_t st) {
+  int cl = 0;
+  while ((16 << cl) < pool.P) ++cl;
+  const bool fast = pool.d == 128 && pool.T == 16 && (16 << cl) == pool.P && (pool.cell_bytes & 15) == 0 &&
+                    ((reinterpret_cast<uintptr_t>(k_out) | reinterpret_cast<uintptr_t>(v_out)) & 15) == 0;
+  if (fast && (out_dtype == KVR_BF16 || out_dtype == KVR_F32)) {
+    const int64_t cells = (int64_t)batch * ((max_len + 15) / 16) * pool.H;
+    const int g = (int)((cells + 7) / 8);
+    if (out_dtype == KVR_BF16)
+      dequant_cells_kernel<__nv_bfloat16><<<g, 256, 0, st>>>(pool, bt, bt_stride, lens, batch, max_len, cl,
+                                                              (__nv_bfloat16*)k_out, (__nv_bfloat16*)v_out);
+    else
+      dequant_cells_kernel<float><<<g, 256, 0, st>>>(pool, bt, bt_stride, lens, batch, max_len, cl, (float*)k_out,
+                                                      (float*)v_out);
+    return 0;
+  }
   const int64_t work = 2LL * batch * max_len * pool.H * (pool.d / 2);
   const int g = grid_for(work, 256);
   switch (out_dtype) {

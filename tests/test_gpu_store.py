@@ -250,3 +250,30 @@ def test_read_sequence_matches_oracle(golden):
         kf, vf = t.read_sequence(0)
         np.testing.assert_array_equal(np.array([kf.sum(), vf.sum(), np.abs(kf).sum(), np.abs(vf).sum()]),
                                       golden[f"dec_{tag}_kread_sum"])
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("page_tokens", [16, 32])
+def test_fast_dequant_pages_vs_f64(rng, dtype, page_tokens):
+    """K4 serving path (d 128, 16-token cells): bf16 / f32 flatten-dequant of ragged
+    sequences == the exact f64 dequant rounded to the output type (<= 1 ulp)."""
+    layout = HeadLayout(num_q_heads=32, num_kv_heads=8, head_dim=128, rot_order=128, page_tokens=page_tokens)
+    spec = RotationSpec(order=128, signs=make_signs(0, 0, 128, 128))
+    t = PageTable(layout, precision=INT4, num_pages=64)
+    lens = [37, 1, 100, 5]
+    for s, n in enumerate(lens):
+        t.create_sequence(s)
+        k = torch.tensor(rng.standard_normal((n, 8, 128)), dtype=torch.bfloat16)
+        v = torch.tensor(rng.standard_normal((n, 8, 128)), dtype=torch.bfloat16)
+        k[0, 0] = 3.0  # constant row: a sentinel (zp 0xFF) row when stored unrotated (sequence 3)
+        t.append_batch([s] * n, k.cuda(), v.cuda(), spec=spec if s < 3 else None)
+    seqs = list(range(len(lens)))
+    k64, v64 = t.read_sequence_device(seqs, torch.float64)
+    kx, vx = t.read_sequence_device(seqs, dtype)
+    for s, n in enumerate(lens):
+        for ref, got in ((k64, kx), (v64, vx)):
+            want = ref[s, :n].to(dtype).double()
+            have = got[s, :n].double()
+            tol = (want.abs() * (2.0 ** -7 if dtype == torch.bfloat16 else 2.0 ** -23)).clamp_min(1e-30)
+            assert bool(((have - want).abs() <= tol).all())
+    assert float(kx[3, 0, 0, 0]) == 3.0 and float(kx[3, 0, 0, 127]) == 3.0
