@@ -86,26 +86,6 @@ KVR_DEV void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-#ifndef KVR_MERGE_LD
-#define KVR_MERGE_LD 0
-#endif
-#ifndef KVR_ATOM
-#define KVR_ATOM 0
-#endif
-// loads of other CTAs' split partials (after the acquiring counter atomic)
-KVR_DEV float ld_partial(const float* a) {
-#if KVR_MERGE_LD == 0
-  return __ldcg(a);
-#elif KVR_MERGE_LD == 1
-  return *a;
-#elif KVR_MERGE_LD == 2
-  return __ldg(a);
-#else
-  float v;
-  asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(a));
-  return v;
-#endif
-}
 KVR_DEV float ex2f(float x) {
   float r;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -293,10 +273,6 @@ KVR_DEV const float* dsmem_ptr(const float* local, uint32_t rank) {
 constexpr int NWARPS = 16;       // one CTA per SM, 4 warps per SM sub-partition (128-register budget)
 constexpr int CELL = 2208;       // one cell: T = 16 tokens of one head, d = 128
 constexpr int RING_CELLS = 4;    // cells in flight per warp (NSTG stages of C cells)
-#ifndef KVR_PRE
-#define KVR_PRE 32
-#endif
-constexpr int MERGE_PRELOAD = KVR_PRE;  // split partials whose o-values are loaded before the lse pass
 constexpr int MAX_SPLITS = 256;
 
 // smem: ring [NWARPS][RING_CELLS][CELL] | bars [NWARPS*RING_CELLS + 1] | q fragments 4 KB | out 4 KB | misc
@@ -355,8 +331,6 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   float* obuf = reinterpret_cast<float*>(sm + SM_OBUF);         // [G][128]
   float* s_sumq = reinterpret_cast<float*>(sm + SM_MISC);       // [8]
   float* s_ksc = s_sumq + 8;                                    // [8]
-  float* s_tot = s_sumq + 16;                                   // [8]
-  uint32_t* s_last = reinterpret_cast<uint32_t*>(s_sumq + 24);
   float* s_lse = s_sumq + 25;                                   // [8] (cluster merge)
   float* s_mstar = s_sumq + 40;                                 // [8] CTA reference point per q head
   float* s_lnew = s_sumq + 48;                                  // [8] new token's logits (APPEND)
@@ -896,89 +870,9 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
     KVR_STAMP(10);
     return;
   }
-  if (p.splits > 1) {
-    // release the partial: CTA barrier, then one gpu-scope acq_rel atomic by thread 0
-    // (cumulative over the CTA's writes ordered before it by the barrier)
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      if (p.trace) p.trace[cta_id * 16 + 6] = clk64();  // partial stored
-      uint32_t prev;
-#if KVR_ATOM == 0
-      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
-                   : "=r"(prev)
-                   : "l"(&p.ws_cnt[(int64_t)b * H + h])
-                   : "memory");
-#else
-      __threadfence();
-      prev = atomicAdd(&p.ws_cnt[(int64_t)b * H + h], 1u);
-      __threadfence();
-#endif
-      *s_last = (prev == (uint32_t)p.splits - 1) ? 1u : 0u;
-      if (p.trace) p.trace[cta_id * 16 + 7] = clk64();  // counter back
-    }
-    __syncthreads();
-    if (!*s_last) {
-      KVR_STAMP(10);
-      return;
-    }
-    // last CTA of (b, h): LSE-merge all splits.  The o-values of the first
-    // MERGE_PRELOAD splits are requested together with the lse values, so short
-    // merges take one L2 round trip; warp j < G turns the lse column of q head j
-    // into split weights in shared memory.
-    float* s_w = sred + NWARPS * 8 * 136;  // [8][MAX_SPLITS] (past sred)
-    const int x0 = threadIdx.x;  // G * 128 <= 1024 outputs; blockDim = 512
-    constexpr int PRE = NT == 1 ? MERGE_PRELOAD : (MERGE_PRELOAD / 4 > 0 ? MERGE_PRELOAD / 4 : 1);
-    constexpr int REPS = NT == 1 ? 1 : 2;  // G * 128 outputs over 512 threads
-    float ov[REPS][PRE];
-#pragma unroll
-    for (int rep = 0; rep < REPS; ++rep) {
-      const int x = x0 + rep * 512;
-      const int j = x >> 7, dd = x & 127;
-#pragma unroll
-      for (int u = 0; u < PRE; ++u)
-        ov[rep][u] = (j < G && u < p.splits) ? ld_partial(p.ws_o + (hbase + (int64_t)u * 8 + j) * 128 + dd) : 0.f;
-    }
-    if (warp < G) {
-      const int j = warp;
-      float mx = -INFINITY;
-      for (int s0 = 0; s0 < p.splits; s0 += 32) {
-        const float l = (s0 + lane < p.splits) ? ld_partial(p.ws_lse + hbase + (int64_t)(s0 + lane) * 8 + j) : -INFINITY;
-        s_w[j * MAX_SPLITS + s0 + lane] = l;
-        mx = fmaxf(mx, l);
-      }
-      mx = warp_max(mx);
-      float tot = 0.f;
-      for (int s0 = lane; s0 < p.splits; s0 += 32) {
-        const float l = s_w[j * MAX_SPLITS + s0];
-        const float w = (l == -INFINITY) ? 0.f : ex2f(l - mx);
-        s_w[j * MAX_SPLITS + s0] = w;
-        tot += w;
-      }
-      tot = warp_sum(tot);
-      if (lane == 0) s_tot[j] = tot;
-    }
-    __syncthreads();
-    KVR_STAMP(8);  // split weights ready
-#pragma unroll
-    for (int rep = 0; rep < REPS; ++rep) {
-      const int x = x0 + rep * 512;
-      const int j = x >> 7, dd = x & 127;
-      if (j < G) {
-        const float* wj = s_w + j * MAX_SPLITS;
-        float ot = 0.f;
-#pragma unroll
-        for (int u = 0; u < PRE; ++u) ot += (u < p.splits) ? wj[u] * ov[rep][u] : 0.f;
-#pragma unroll 8
-        for (int s = PRE; s < p.splits; ++s)
-          ot += wj[s] * ld_partial(p.ws_o + (hbase + (int64_t)s * 8 + j) * 128 + dd);
-        const float tot = s_tot[j];
-        obuf[x] = tot > 0.f ? ot / tot : 0.f;
-      }
-    }
-    if (threadIdx.x == 0) {
-      p.ws_cnt[(int64_t)b * H + h] = 0u;  // re-arm for the next launch
-      if (p.trace) p.trace[cta_id * 16 + 9] = clk64();  // merged
-    }
+  if (p.splits > 1) {  // the partial is final: decode_merge_kernel (next in the stream) merges
+    KVR_STAMP(6);
+    return;
   }
   __syncthreads();
   // ---- output: inverse rotation of the value branch (o @ H_blk @ diag(signs)),
@@ -1013,6 +907,93 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
     *dst = make_float4(x[0], x[1], x[2], x[3]);
   }
   KVR_STAMP(10);
+}
+
+// Split merge (K3), launched right after a split decode with programmatic
+// dependent launch: one CTA per (q head j, kv head, sequence), 512 threads =
+// 128 dims x 4 split slices.  LSE-weighted sum of the splits' (o, lse)
+// partials, then the inverse rotation of the value branch.
+constexpr int MERGE_THREADS = 512;
+template <int ORDER>
+__global__ void __launch_bounds__(MERGE_THREADS)
+    decode_merge_kernel(const __grid_constant__ DecodeParams p, const __grid_constant__ Signs signs) {
+  __shared__ float s_w[MAX_SPLITS];
+  __shared__ float s_red[16];
+  __shared__ float s_o[4][128];
+  const int j = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int S = p.splits, H = p.pool.H;
+  const int dd = tid & 127, sl = tid >> 7;
+  const int64_t hbase = (((int64_t)b * H + h) * S) * 8;
+  pdl_wait();
+  pdl_launch_dependents();
+  // o-values of this thread's splits s = sl, sl + 4, ... (first 16 preloaded with the lse)
+  float ov[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int s = sl + 4 * u;
+    ov[u] = s < S ? __ldcg(p.ws_o + (hbase + (int64_t)s * 8 + j) * 128 + dd) : 0.f;
+  }
+  float l = -INFINITY;
+  if (tid < S) l = __ldcg(p.ws_lse + hbase + (int64_t)tid * 8 + j);
+  float m = warp_max(l);
+  if (lane == 0) s_red[warp] = m;
+  __syncthreads();
+  m = s_red[lane & 15];
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const float w = (tid < S && l != -INFINITY) ? ex2f(l - m) : 0.f;
+  if (tid < S) s_w[tid] = w;
+  float tw = warp_sum(w);
+  __syncthreads();  // s_red reads done before reuse
+  if (lane == 0) s_red[warp] = tw;
+  __syncthreads();
+  tw = 0.f;
+#pragma unroll
+  for (int q = 0; q < MERGE_THREADS / 32; ++q) tw += s_red[q];
+  float acc = 0.f;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int s = sl + 4 * u;
+    if (s < S) acc += s_w[s] * ov[u];
+  }
+#pragma unroll 8
+  for (int s = sl + 64; s < S; s += 4) acc += s_w[s] * __ldcg(p.ws_o + (hbase + (int64_t)s * 8 + j) * 128 + dd);
+  s_o[sl][dd] = acc;
+  __syncthreads();
+  if (warp == 0) {
+    float x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int d = 4 * lane + u;
+      const float v = s_o[0][d] + s_o[1][d] + s_o[2][d] + s_o[3][d];
+      x[u] = tw > 0.f ? v / tw : 0.f;
+    }
+    if (p.rotate && p.rot_v) {
+      const float a0 = x[0] + x[1], a1 = x[0] - x[1], a2 = x[2] + x[3], a3 = x[2] - x[3];
+      x[0] = a0 + a2;
+      x[1] = a1 + a3;
+      x[2] = a0 - a2;
+      x[3] = a1 - a3;
+#pragma unroll
+      for (int k = 0; (4 << k) < ORDER; ++k) {
+        const bool upper = (lane >> k) & 1;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float o = __shfl_xor_sync(0xffffffffu, x[u], 1 << k);
+          x[u] = upper ? o - x[u] : x[u] + o;
+        }
+      }
+      const float inv = (float)(1.0 / sqrt((double)ORDER));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        x[u] *= inv;
+        if (p.has_signs && sign_bit(signs, 4 * lane + u)) x[u] = -x[u];
+      }
+    }
+    float4* dst = reinterpret_cast<float4*>(p.out + ((int64_t)b * p.nq + (int64_t)h * p.G + j) * 128) + lane;
+    *dst = make_float4(x[0], x[1], x[2], x[3]);
+  }
 }
 
 // Generic (any head_dim <= 256, any group) CUDA-core decode: one CTA per
@@ -1139,18 +1120,31 @@ size_t kvr_decode_ws_bytes(int batch, int H, int nq, int d, int splits) {
   return (bytes + 255) & ~size_t(255);
 }
 
+// Split count: minimise (waves of one-CTA-per-SM) x (tiles per CTA) + a merge cost,
+// keeping >= 2 tiles per warp; ties go to fewer splits.
 int kvr_pick_splits(int batch, int H, int max_len, int P) {
   (void)P;
   const int sms = kvr_num_sms() > 0 ? kvr_num_sms() : 148;
   const int tiles = (max_len + 15) / 16;
-  const int units = batch * H;
-  int s = sms / units;  // one CTA per SM, a single wave
-  const int min_tiles_per_cta = 2 * NWARPS;
-  const int max_s = tiles / min_tiles_per_cta;
-  if (s > max_s) s = max_s;
-  if (s > MAX_SPLITS) s = MAX_SPLITS;
-  if (s < 1) s = 1;
-  return s;
+  const long units = (long)batch * H;
+  if (units <= 0 || tiles <= 0) return 1;
+  int best = 1;
+  double best_cost = 1e300;
+  for (int s = 1; s <= MAX_SPLITS; ++s) {
+    const int per = (tiles + s - 1) / s;
+    if (s > 1 && per < 2 * NWARPS) break;
+    const long ctas = units * s;
+    const long waves = (ctas + sms - 1) / sms;
+    // in tile-times (one tile ~ 1/15 of a warp's 0.9 us per cell): a CTA's fixed
+    // prologue + epilogue ~ 80, its partial write (+ read in the merge) ~ 2, and the
+    // latency of the last CTA's merge chain once
+    const double cost = (double)waves * (80.0 + per + (s > 1 ? 2.0 : 0.0)) + (s > 1 ? 24.0 + 0.25 * s : 0.0);
+    if (cost < best_cost * 0.999) {
+      best_cost = cost;
+      best = s;
+    }
+  }
+  return best;
 }
 
 // One launch of decode_tma_kernel with programmatic stream serialization (PDL: the
@@ -1212,11 +1206,27 @@ static bool cluster_ok(int splits, size_t smem) {
   return cache[splits] == 1;
 }
 
+template <int ORDER>
+static int launch_merge(const DecodeParams& p, const Signs& sg, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.G, p.pool.H, p.batch);
+  cfg.blockDim = dim3(MERGE_THREADS);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, decode_merge_kernel<ORDER>, p, sg) == cudaSuccess ? 0 : KVR_ERR_CUDA;
+}
+
 template <int NT, int ORDER, bool APP>
 static int launch_sel(dim3 grid, size_t smem, cudaStream_t st, const DecodeParams& p, const Signs& sg) {
   if (p.use_cluster && cluster_ok<NT, ORDER, APP>((int)grid.y, smem))
     return launch_one<NT, ORDER, APP, true>(grid, smem, st, p, sg);
-  return launch_one<NT, ORDER, APP, false>(grid, smem, st, p, sg);
+  if (int rc = launch_one<NT, ORDER, APP, false>(grid, smem, st, p, sg)) return rc;
+  return p.splits > 1 ? launch_merge<ORDER>(p, sg, st) : 0;
 }
 
 template <int NT, bool APP>
@@ -1284,7 +1294,13 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
     int cl = 0;
     while ((16 << cl) < pool.P) ++cl;
     p.cps_log2 = cl;
-    p.use_cluster = splits >= 2 && splits <= 16;
+#ifndef KVR_NO_CLUSTER
+    // portable cluster sizes only: 16-CTA clusters of one-CTA-per-SM kernels do not
+    // all co-schedule on B200 (a second wave appears), measured slower
+    p.use_cluster = splits >= 2 && splits <= 8;
+#else
+    p.use_cluster = 0;
+#endif
     if (new_slot)
       return p.G == 8 ? launch_tma<2, true>(p, sg, grid, smem, ord, st) : launch_tma<1, true>(p, sg, grid, smem, ord, st);
     return p.G == 8 ? launch_tma<2, false>(p, sg, grid, smem, ord, st) : launch_tma<1, false>(p, sg, grid, smem, ord, st);

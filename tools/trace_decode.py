@@ -14,7 +14,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2604_19157_b200 import DecodePlan, HeadLayout, PageTable, RotationSpec, make_signs, _lib  # noqa: E402
 
-H, G, D = 8, 4, 128
+H, G, D = int(os.environ.get("TR_H", "8")), int(os.environ.get("TR_G", "4")), 128
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 STEP = "--step" in sys.argv  # fused append + decode (kvr_decode_step)
 split_list = [int(x) for x in sys.argv[2:] if not x.startswith("--")] or [0]
