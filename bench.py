@@ -522,7 +522,9 @@ def e2e_api(torch, layout, spec, dev, table, args, world):
     plan = DecodePlan(table, [0], extra_tokens=steps + 8)
 
     def one():
-        plan.step(qh, kh, vh, spec, out=od)        # one pinned H2D of q/k/v + slot/len metadata
+        # one pinned H2D of q/k/v + slot/len metadata and the decode kernels, replayed
+        # from a CUDA graph; host bookkeeping (slot allocation, page table) per step
+        plan.step(qh, kh, vh, spec, out=od, graph=True)
         oh.copy_(od, non_blocking=True)
 
     for _ in range(3):
@@ -547,7 +549,7 @@ def e2e_api(torch, layout, spec, dev, table, args, world):
     byts = step_bytes(L)
     return {"value": round(world * byts / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "ms_per_step": round(ms, 4),
             "h2d_bytes_per_step": kh.numel() * 2 + vh.numel() * 2 + qh.numel() * 2 + 12,  # + slot id, length
-            "d2h_bytes_per_step": oh.numel() * 4, "api": "DecodePlan.step (fused append + decode) with host buffers",
+            "d2h_bytes_per_step": oh.numel() * 4, "api": "DecodePlan.step(graph=True) (fused append + decode) with host buffers",
             "steps": steps}
 
 

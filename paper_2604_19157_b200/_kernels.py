@@ -39,7 +39,8 @@ def device() -> torch.device:
 
 
 def stream_ptr() -> ctypes.c_void_p:
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    # the raw current stream of the current device (torch.cuda.current_stream() costs ~15 us)
+    return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice()))
 
 
 def ptr(t: torch.Tensor) -> ctypes.c_void_p:

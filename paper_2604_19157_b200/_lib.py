@@ -9,6 +9,8 @@ from __future__ import annotations
 import ctypes
 import os
 
+import numpy as np
+
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -107,8 +109,8 @@ def sign_words(signs, head_dim: int):
     """(d,) +-1 vector -> ctypes uint32 array, bit i set <=> signs[i] == -1."""
     if signs is None:
         return None
-    words = (ctypes.c_uint32 * ((head_dim + 31) // 32))()
-    for i, s in enumerate(signs):
-        if s < 0:
-            words[i >> 5] |= 1 << (i & 31)
-    return words
+    bits = np.zeros(((head_dim + 31) // 32) * 32, dtype=np.uint8)
+    neg = np.asarray(signs) < 0
+    bits[:neg.size] = neg
+    w = np.packbits(bits.reshape(-1, 32), axis=1, bitorder="little").view("<u4").reshape(-1)
+    return (ctypes.c_uint32 * w.size)(*w.tolist())

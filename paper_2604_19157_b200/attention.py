@@ -24,6 +24,7 @@ from .layout import HeadLayout
 from .rotation import RotationSpec, Targets
 
 _Q_CODE = {torch.float32: _lib.KVR_F32, torch.bfloat16: _lib.KVR_BF16, torch.float16: _lib.KVR_F16}
+_KV_CODE = {torch.float64: _lib.KVR_F64, **_Q_CODE}
 
 
 @dataclass(frozen=True)
@@ -70,8 +71,7 @@ class DecodePlan:
         self.slots = self._dev[:8 * B].view(torch.int64)
         self.lens = self._dev[8 * B:12 * B].view(torch.int32)
         self.lens.copy_(lens)
-        self._host = []
-        self._host_i = 0
+        self._layouts = {}
         if num_splits <= 0:
             num_splits = _lib.lib().kvr_decode_pick_splits(B, lay.num_kv_heads, self.max_len, P)
         self.splits = num_splits
@@ -97,15 +97,6 @@ class DecodePlan:
         lens = [self.table.sequence_length(s) for s in self.seqs]
         self.lens.copy_(torch.tensor(lens, dtype=torch.int32))
         self.max_len = max(self.max_len, max(lens))
-
-    def _staging(self, nbytes: int) -> tuple[torch.Tensor, torch.cuda.Event]:
-        if not self._host or self._host[0][0].numel() < nbytes:
-            self._host = [(torch.empty(nbytes, dtype=torch.uint8).pin_memory(), torch.cuda.Event())
-                          for _ in range(self._RING)]
-        buf, ev = self._host[self._host_i]
-        self._host_i = (self._host_i + 1) % self._RING
-        ev.synchronize()  # the copy that last read this buffer has run
-        return buf, ev
 
     def run(self, q: torch.Tensor, spec: Optional[RotationSpec], out: Optional[torch.Tensor] = None) -> torch.Tensor:
         table, lay = self.table, self.table.layout
@@ -138,57 +129,126 @@ class DecodePlan:
         K/V rows (B, H, d) into slot slots[b] (rotated + INT4-quantized bit-exactly
         in f64) and decode over the plan's lengths, which must already include it."""
         table, lay = self.table, self.table.layout
-        q = q.contiguous()
+        if not q.is_contiguous():
+            q = q.contiguous()
+        if not (k_new.is_contiguous() and v_new.is_contiguous()):
+            k_new, v_new = k_new.contiguous(), v_new.contiguous()
         if out is None:
             out = torch.empty(q.shape, dtype=torch.float32, device=table.device)
         rotate = spec is not None
         if rotate and spec.learned is not None:
             raise UnsupportedConfigError("learned rotations are not fused into the decode kernel (row f3)")
-        targets = _lib.KVR_KEYS_ONLY if (rotate and spec.targets is Targets.KEYS_ONLY) else _lib.KVR_KEYS_AND_VALUES
-        from .cache import _TORCH_DTYPE_CODE
-        _lib.check(_lib.lib().kvr_decode_step(
-            _kernels.ptr(q), _Q_CODE[q.dtype], _kernels.ptr(k_new), _kernels.ptr(v_new), _TORCH_DTYPE_CODE[k_new.dtype],
-            _kernels.ptr(slots), ctypes.byref(table.desc), _kernels.ptr(self.bt), self.bt.shape[1],
-            _kernels.ptr(self.lens), len(self.seqs), lay.num_q_heads, self.max_len, spec.order if rotate else 1,
-            1 if rotate else 0, targets, spec.sign_words(lay.head_dim) if rotate else None, _kernels.ptr(out),
-            _kernels.ptr(self.ws), self.ws.numel(), self.splits, _kernels.ptr(table.flags), _kernels.stream_ptr()))
+        # the argument list is rebuilt only when a buffer, the spec or the stream changes
+        stream = torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
+        key = (q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(), slots.data_ptr(), out.data_ptr(), q.dtype,
+               k_new.dtype, id(spec), stream, self.bt.data_ptr(), self.lens.data_ptr(), self.ws.data_ptr())
+        cached = getattr(self, "_step_args", None)
+        if cached is None or cached[0] != key:
+            targets = _lib.KVR_KEYS_ONLY if (rotate and spec.targets is Targets.KEYS_ONLY) else _lib.KVR_KEYS_AND_VALUES
+            head = (_kernels.ptr(q), _Q_CODE[q.dtype], _kernels.ptr(k_new), _kernels.ptr(v_new), _KV_CODE[k_new.dtype],
+                    _kernels.ptr(slots), ctypes.byref(table.desc), _kernels.ptr(self.bt), self.bt.shape[1],
+                    _kernels.ptr(self.lens), len(self.seqs), lay.num_q_heads)
+            tail = (spec.order if rotate else 1, 1 if rotate else 0, targets,
+                    spec.sign_words(lay.head_dim) if rotate else None, _kernels.ptr(out), _kernels.ptr(self.ws),
+                    self.ws.numel(), self.splits, _kernels.ptr(table.flags), ctypes.c_void_p(stream))
+            cached = self._step_args = (key, head, tail)
+        _lib.check(_lib.lib().kvr_decode_step(*cached[1], self.max_len, *cached[2]))
         return out
 
-    def step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, spec: Optional[RotationSpec],
-             out: Optional[torch.Tensor] = None) -> torch.Tensor:
-        """One serving decode step for every sequence of the plan: allocate the new
-        token's slot (reference page order), then one fused append + decode launch.
-        q (B, nq, d) and k_new/v_new (B, H, d) may be host tensors: they travel
-        with the step metadata in one pinned host->device copy."""
-        table = self.table
+
+    def _step_layout(self, host_in) -> dict:
+        """Staging layout for a given set of host inputs (cached per shapes/dtypes):
+        pinned ring buffers, byte offsets and the device views the kernel reads."""
+        key = tuple((tuple(t.shape), t.dtype) for t in host_in)
+        lay = self._layouts.get(key)
+        if lay is not None:
+            return lay
         B = len(self.seqs)
-        slots, fresh = table.alloc.plan(self.seqs)
-        table._zero_pages(fresh)
-        self._patch_pages()
-        lens = np.fromiter((table._seq_len[s] for s in self.seqs), dtype=np.int32, count=B)
-        self.max_len = max(self.max_len, int(lens.max()))
-        host_in = [t for t in (q, k_new, v_new) if not t.is_cuda]
         sizes = [t.numel() * t.element_size() for t in host_in]
         offs, o = [], self._meta_bytes
         for n in sizes:
             offs.append(o)
             o += (n + 255) // 256 * 256
-        buf, ev = self._staging(o)
-        buf[:8 * B].view(torch.int64).numpy()[:] = slots
-        buf[8 * B:12 * B].view(torch.int32).numpy()[:] = lens
-        for t, off, n in zip(host_in, offs, sizes):
-            buf[off:off + n].view(t.dtype).view(t.shape).copy_(t)
         if o > self._dev.numel():
-            dev = torch.zeros(o, dtype=torch.uint8, device=table.device)
+            dev = torch.zeros(o, dtype=torch.uint8, device=self.table.device)
             dev[:self._meta_bytes].copy_(self._dev[:self._meta_bytes])
             self._dev = dev
             self.slots = dev[:8 * B].view(torch.int64)
             self.lens = dev[8 * B:12 * B].view(torch.int32)
-        self._dev[:o].copy_(buf[:o], non_blocking=True)
-        ev.record()
-        dev_in = iter(self._dev[off:off + n].view(t.dtype).view(t.shape) for t, off, n in zip(host_in, offs, sizes))
+            self._layouts.clear()
+        ring = []
+        for _ in range(self._RING):
+            buf = torch.empty(o, dtype=torch.uint8).pin_memory()
+            ring.append((buf, buf.numpy(), buf.data_ptr(), torch.cuda.Event()))
+        views = [self._dev[off:off + n].view(t.dtype).view(t.shape) for t, off, n in zip(host_in, offs, sizes)]
+        lay = {"bytes": o, "offs": offs, "sizes": sizes, "ring": ring, "views": views, "i": 0,
+               "dev_head": self._dev[:o]}
+        self._layouts[key] = lay
+        return lay
+
+    def step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, spec: Optional[RotationSpec],
+             out: Optional[torch.Tensor] = None, graph: bool = False) -> torch.Tensor:
+        """One serving decode step for every sequence of the plan: allocate the new
+        token's slot (reference page order), then one fused append + decode launch.
+        q (B, nq, d) and k_new/v_new (B, H, d) may be host tensors: they travel
+        with the step metadata in one pinned host->device copy.
+
+        graph=True replays the device part (that copy + the decode kernels) from a
+        CUDA graph captured on first use per pinned staging buffer; the block table
+        and lengths keep their addresses and the plan's max_len (its capacity) is
+        fixed, so only the host bookkeeping runs per step."""
+        table = self.table
+        B = len(self.seqs)
+        slots, fresh = table.alloc.plan(self.seqs)
+        if fresh:
+            table._zero_pages(fresh)
+            self._patch_pages()
+        lens = np.fromiter((table._seq_len[s] for s in self.seqs), dtype=np.int32, count=B)
+        mx = int(lens.max())
+        if mx > self.max_len:
+            if graph:
+                raise ShapeError(f"sequence length {mx} passed the plan's capacity {self.max_len}; "
+                                 f"build a new DecodePlan (extra_tokens)")
+            self.max_len = mx
+        host_in = [t for t in (q, k_new, v_new) if not t.is_cuda]
+        lay = self._step_layout(host_in)
+        slot_i = lay["i"]
+        buf, buf_np, buf_ptr, ev = lay["ring"][slot_i]
+        lay["i"] = (slot_i + 1) % self._RING
+        ev.synchronize()  # the copy that last read this pinned buffer has run
+        buf_np[:8 * B] = slots.view(np.uint8)
+        buf_np[8 * B:12 * B] = lens.view(np.uint8)
+        for t, off, n in zip(host_in, lay["offs"], lay["sizes"]):
+            t = t if t.is_contiguous() else t.contiguous()
+            ctypes.memmove(buf_ptr + off, t.data_ptr(), n)
+        dev_in = iter(lay["views"])
         q, k_new, v_new = (t if t.is_cuda else next(dev_in) for t in (q, k_new, v_new))
-        return self.run_step(q, k_new.contiguous(), v_new.contiguous(), self.slots, spec, out)
+        if out is None:
+            out = torch.empty(q.shape, dtype=torch.float32, device=table.device)
+
+        def device_part():
+            lay["dev_head"].copy_(buf[:lay["bytes"]], non_blocking=True)
+            self.run_step(q, k_new, v_new, self.slots, spec, out)
+
+        if not graph:
+            device_part()
+        else:
+            graphs = lay.setdefault("graphs", {})
+            gkey = (slot_i, out.data_ptr(), id(spec), q.data_ptr(), k_new.data_ptr(), v_new.data_ptr())
+            g = graphs.get(gkey)
+            if g is None:
+                device_part()  # eager first run (also warms the launch path)
+                g = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream()
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(side), torch.cuda.graph(g, stream=side):
+                    device_part()
+                torch.cuda.current_stream().wait_stream(side)
+                graphs[gkey] = g
+            else:
+                g.replay()
+        ev.record()
+        return out
 
 
 def decode_batch(q: torch.Tensor, table: PageTable, seqs: Sequence[int], spec: Optional[RotationSpec] = None,

@@ -59,7 +59,11 @@ class RotationSpec:
             object.__setattr__(self, "learned", r)
 
     def sign_words(self, head_dim: int):
-        return _lib.sign_words(self.signs, head_dim)
+        """The signs as the C ABI's bitmask words (memoised: the spec is immutable)."""
+        cache = self.__dict__.setdefault("_words", {})
+        if head_dim not in cache:
+            cache[head_dim] = _lib.sign_words(self.signs, head_dim)
+        return cache[head_dim]
 
 
 def make_signs(seed: int, layer: int, head_dim: int, order: int) -> np.ndarray:

@@ -228,3 +228,30 @@ def test_fused_decode_step(targets, G):
     err = rel_err(out.double().cpu().numpy(), refo)
     print("fused step", G, targets, err)
     assert err <= TOL
+
+
+def test_step_graph_replay_matches_eager():
+    """DecodePlan.step(graph=True) (CUDA-graph replay of the H2D + decode kernels)
+    gives the same outputs and page bytes as the eager path, across page
+    boundaries (fresh pages every 16 steps) and pinned-ring wraparound."""
+    H, G, d = 2, 4, 128
+    lens = [30, 77]
+    outs = {}
+    dumps = {}
+    for mode in (False, True):
+        t, spec, layout = _build(len(lens), lens, H, G, d, 128, 16, "gaussian", Targets.KEYS_AND_VALUES, True,
+                                 seed=5, extra_pages=8)
+        plan = DecodePlan(t, [0, 1], extra_tokens=40)
+        rng = np.random.default_rng(123)
+        res = []
+        od = torch.empty((2, G * H, d), dtype=torch.float32, device="cuda")
+        for _ in range(37):
+            q = torch.tensor(rng.standard_normal((2, G * H, d)), dtype=torch.bfloat16).pin_memory()
+            k = torch.tensor(rng.standard_normal((2, H, d)), dtype=torch.bfloat16).pin_memory()
+            v = torch.tensor(rng.standard_normal((2, H, d)), dtype=torch.bfloat16).pin_memory()
+            res.append(plan.step(q, k, v, spec, out=od, graph=mode).cpu().clone())
+        torch.cuda.synchronize()
+        outs[mode] = torch.stack(res)
+        dumps[mode] = t.dump_bytes()
+    assert torch.equal(outs[False], outs[True])
+    assert dumps[False] == dumps[True]
