@@ -86,6 +86,13 @@ KVR_DEV void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+KVR_DEV void imma16832(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
 KVR_DEV float ex2f(float x) {
   float r;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -323,6 +330,9 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
     decode_tma_kernel(const __grid_constant__ DecodeParams p, const __grid_constant__ Signs signs) {
   constexpr int DW = APPEND ? NWARPS - 1 : NWARPS;
   constexpr int NSTG = RING_CELLS / C;
+  // QK on the int8 tensor path (u8 codes x s8 query digits) for one column tile of
+  // q heads; two (G = 8) keep the fp16 hi/lo HMMA path, which needs fewer B registers
+  constexpr bool QK_INT8 = NT == 1;
   constexpr int STG = C * CELL;
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = sm_raw + ((1024u - (smem_u32(sm_raw) & 1023u)) & 1023u);
@@ -374,6 +384,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   const uint8_t* wcur = window_addr(0, page_window(0));
   const int len_raw = __ldg(&p.lens[b]);
   if (threadIdx.x < NWARPS * RING_CELLS) mbar_init(&bars[threadIdx.x], 1);
+  reinterpret_cast<uint2*>(sfrag)[threadIdx.x] = make_uint2(0u, 0u);  // 4 KB of query digits (padding = 0)
   fence_mbar_init();
   __syncthreads();
 
@@ -472,42 +483,88 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
       for (int u = 0; u < 4; ++u) x[u] *= inv;
     }
     if (APPEND) *reinterpret_cast<float4*>(s_qrot + j * 128 + 4 * lane) = make_float4(x[0], x[1], x[2], x[3]);
-    float amax = fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])), fmaxf(fabsf(x[2]), fabsf(x[3])));
-    amax = warp_max(amax);
-    const int e2 = amax > 0.f ? ilogbf(amax) - 13 : 0;  // q' = q 2^-e2, max|q'| in [2^13, 2^14)
-    const float qs = ldexpf(1.0f, -e2);
-    float hs = 0.f;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int d = 4 * lane + u, rem = d & 31;
-      const int ii = d >> 5, s = 2 * (rem >> 3) + ((rem & 3) >> 1), slot2 = rem & 1, e = (rem >> 2) & 1;
-      const float v = x[u] * qs;
-      const float hi_ = __half2float(__float2half_rn(v));
-      const float lo_ = __half2float(__float2half_rn(v - hi_));
-      hs += hi_ + lo_;
-      const float f = slot2 ? (1.0f / 16.0f) : 1.0f;  // x16 nibble slots
-      const int nt = j >> 2, col = 2 * (j & 3);
-      // sfrag[nt][s][lane'][slot2][e]: lane' = col * 4 + ii owns B-fragment word slot2
-      const int base = (nt * 8 + s) * 128 + slot2 * 2 + e;
-      sfrag[base + ((col + 0) * 4 + ii) * 4] = __half_as_ushort(__float2half_rn(hi_ * f));
-      sfrag[base + ((col + 1) * 4 + ii) * 4] = __half_as_ushort(__float2half_rn(lo_ * f));
-    }
-    hs = warp_sum(hs);
-    if (lane == 0) {
-      s_sumq[j] = hs * 5.9604644775390625e-08f;  // x 2^-24 (MMA units)
-      s_ksc[j] = ldexpf(1.0f, e2 + 24) * LOG2E * (float)(1.0 / sqrt(128.0));
+    if constexpr (QK_INT8) {
+      float amax = fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])), fmaxf(fabsf(x[2]), fabsf(x[3])));
+      amax = warp_max(amax);
+      // q' = rint(q 2^(19 - e2)), |q'| < 2^20, as three balanced base-128 digits
+      // q' = p0 + 128 p1 + 16384 p2 (p0, p1 in [-64, 63], |p2| <= 64): the int8 IMMA
+      // columns.  Lane l owns dims 4l..4l+3; dim d sits in IMMA m = ((d >> 4) & 1) +
+      // 2 (d & 1) (odd dims are the high nibbles), B register (d >> 3) & 1, byte
+      // (d >> 1) & 3 of lane (column * 4 + d / 32).
+      const int e2 = amax > 0.f ? ilogbf(amax) : 0;
+      const float qs = ldexpf(1.0f, 19 - e2);
+      int qsum = 0;
+      uint8_t* s8 = reinterpret_cast<uint8_t*>(sfrag);  // [tile][m][lane][2 regs][4 bytes]
+  #pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int d = 4 * lane + u, rem = d & 31;
+        const int qi = __float2int_rn(x[u] * qs);
+        qsum += qi;
+        const int p0 = ((qi + 64) & 127) - 64;
+        const int t1 = (qi - p0) >> 7;
+        const int p1 = ((t1 + 64) & 127) - 64;
+        const int p2 = (t1 - p1) >> 7;
+        const int m = ((rem >> 4) & 1) + 2 * (rem & 1), reg = (rem >> 3) & 1, e = (rem >> 1) & 3, ii = d >> 5;
+        const int pl[3] = {p0, p1, p2};
+  #pragma unroll
+        for (int pp = 0; pp < 3; ++pp) {
+          int t, c;
+          if (NT == 1) {  // tile 0: (head, plane 0|1) pairs; tile 1: (head, plane 2) on even columns
+            t = pp < 2 ? 0 : 1;
+            c = pp < 2 ? 2 * j + pp : 2 * j;
+          } else {  // tiles 0/1: heads 0-3 / 4-7 planes 0|1; tile 2: plane 2 of heads (c/2, 4 + c/2)
+            t = pp < 2 ? (j >> 2) : 2;
+            c = pp < 2 ? 2 * (j & 3) + pp : 2 * (j & 3) + (j >> 2);
+          }
+          s8[(((t * 4 + m) * 32 + c * 4 + ii) * 2 + reg) * 4 + e] = (uint8_t)(int8_t)pl[pp];
+        }
+      }
+      qsum = __reduce_add_sync(0xffffffffu, qsum);
+      if (lane == 0) {
+        s_sumq[j] = (float)qsum;
+        s_ksc[j] = ldexpf(1.0f, e2 - 19) * LOG2E * (float)(1.0 / sqrt(128.0));
+      }
+  
+    } else {
+      float amax = fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])), fmaxf(fabsf(x[2]), fabsf(x[3])));
+      amax = warp_max(amax);
+      const int e2 = amax > 0.f ? ilogbf(amax) - 13 : 0;  // q' = q 2^-e2, max|q'| in [2^13, 2^14)
+      const float qs = ldexpf(1.0f, -e2);
+      float hs = 0.f;
+  #pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int d = 4 * lane + u, rem = d & 31;
+        const int ii = d >> 5, s = 2 * (rem >> 3) + ((rem & 3) >> 1), slot2 = rem & 1, e = (rem >> 2) & 1;
+        const float v = x[u] * qs;
+        const float hi_ = __half2float(__float2half_rn(v));
+        const float lo_ = __half2float(__float2half_rn(v - hi_));
+        hs += hi_ + lo_;
+        const float f = slot2 ? (1.0f / 16.0f) : 1.0f;  // x16 nibble slots
+        const int nt = j >> 2, col = 2 * (j & 3);
+        // sfrag[nt][s][lane'][slot2][e]: lane' = col * 4 + ii owns B-fragment word slot2
+        const int base = (nt * 8 + s) * 128 + slot2 * 2 + e;
+        sfrag[base + ((col + 0) * 4 + ii) * 4] = __half_as_ushort(__float2half_rn(hi_ * f));
+        sfrag[base + ((col + 1) * 4 + ii) * 4] = __half_as_ushort(__float2half_rn(lo_ * f));
+      }
+      hs = warp_sum(hs);
+      if (lane == 0) {
+        s_sumq[j] = hs * 5.9604644775390625e-08f;  // x 2^-24 (MMA units)
+        s_ksc[j] = ldexpf(1.0f, e2 + 24) * LOG2E * (float)(1.0 / sqrt(128.0));
+      }
+  
     }
   }
   __syncthreads();
   // query B fragments: registers for one 8-column tile; with two (G = 8) they stay
   // in shared memory (one LDS.64 per k-step) to keep the loop inside 128 registers
   constexpr bool BQ_REG = NT == 1;
+  constexpr int NTL = NT + 1;  // int8 column tiles: 3 digit planes x 4 NT heads (+ padding)
   const uint2* sfrag2 = reinterpret_cast<const uint2*>(sfrag);
-  uint2 bq[BQ_REG ? 8 : 1];
+  uint2 bq[BQ_REG ? (QK_INT8 ? NTL * 4 : 8 * NT) : 1];
   float sumq[NT], kscale[NT];
   if (BQ_REG) {
 #pragma unroll
-    for (int s = 0; s < 8; ++s) bq[BQ_REG ? s : 0] = sfrag2[s * 32 + lane];
+    for (int s = 0; s < (QK_INT8 ? NTL * 4 : 8 * NT); ++s) bq[BQ_REG ? s : 0] = sfrag2[s * 32 + lane];
   }
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
@@ -560,26 +617,65 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
     for (int c = 0; c < C; ++c) load_cell_k(f[c], st + c * CELL, r, i);
 
     // ---- S = C_k q : 8 k-steps of m16n8k16 per 8-column tile and cell
-    // C * NT independent accumulator chains of 8 HMMAs
-    float scv[C][NT][4];
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) scv[c][nt][q] = 0.f;
-      const uint32_t kw0[4] = {f[c].ka.x, f[c].ka.y, f[c].ka.z, f[c].ka.w};
-      const uint32_t kw1[4] = {f[c].kb.x, f[c].kb.y, f[c].kb.z, f[c].kb.w};
-#pragma unroll
-      for (int s = 0; s < 8; ++s) {
-        const uint32_t wa = kw0[s >> 1], wb = kw1[s >> 1];
-        const uint32_t xa = (s & 1) ? (wa >> 8) : wa, xb = (s & 1) ? (wb >> 8) : wb;
-        const uint32_t a0 = xa & 0x000F000Fu, a2 = xa & 0x00F000F0u;
-        const uint32_t a1 = xb & 0x000F000Fu, a3 = xb & 0x00F000F0u;
-#pragma unroll
+    float scv[C][NT][4];  // S per (token r -> [0] | r + 8 -> [2]) and head of this lane
+    if constexpr (QK_INT8) {
+      // ---- S = C_k q' on the int8 tensor path: per cell and column tile, two IMMA
+      // m16n8k32 on the low nibbles (mask 0x0F0F0F0F) into D_lo and two on the high
+      // nibbles kept in place (mask 0xF0F0F0F0, = 16 c) into D_hi; S = D_lo + D_hi / 16
+      // is exact.  Column tiles hold the query's three digit planes.
+  #pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const uint32_t kw0[4] = {f[c].ka.x, f[c].ka.y, f[c].ka.z, f[c].ka.w};
+        const uint32_t kw1[4] = {f[c].kb.x, f[c].kb.y, f[c].kb.z, f[c].kb.w};
+        float sp[NTL][4];
+  #pragma unroll
+        for (int t = 0; t < NTL; ++t) {
+          int dlo[4] = {0, 0, 0, 0}, dhi[4] = {0, 0, 0, 0};
+  #pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            const uint32_t mask = m < 2 ? 0x0F0F0F0Fu : 0xF0F0F0F0u;
+            const int w = 2 * (m & 1);
+            const uint2 b0 = BQ_REG ? bq[BQ_REG ? t * 4 + m : 0] : sfrag2[(t * 4 + m) * 32 + lane];
+            imma16832(m < 2 ? dlo : dhi, kw0[w] & mask, kw1[w] & mask, kw0[w + 1] & mask, kw1[w + 1] & mask, b0.x, b0.y);
+          }
+  #pragma unroll
+          for (int q = 0; q < 4; ++q) sp[t][q] = (float)dlo[q] + 0.0625f * (float)dhi[q];
+        }
+  #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          const uint2 bb = BQ_REG ? bq[BQ_REG ? s : 0] : sfrag2[(nt * 8 + s) * 32 + lane];
-          mma16816(scv[c][nt], a0, a1, a2, a3, bb.x, bb.y);
+          // planes of this lane's head(s): tile nt holds (p0, p1) in (c0, c1) / (c2, c3);
+          // the plane-2 tile holds p2 in c0 / c2 (NT == 1) or c(nt) / c(2 + nt) (NT == 2)
+          const int t2 = NTL - 1, q0 = NT == 1 ? 0 : nt, q1 = NT == 1 ? 2 : 2 + nt;
+          scv[c][nt][0] = fmaf(16384.0f, sp[t2][q0], fmaf(128.0f, sp[nt][1], sp[nt][0]));
+          scv[c][nt][2] = fmaf(16384.0f, sp[t2][q1], fmaf(128.0f, sp[nt][3], sp[nt][2]));
+        }
+      }
+    } else {
+      // C * NT independent accumulator chains of 8 HMMAs
+  #pragma unroll
+      for (int c = 0; c < C; ++c) {
+  #pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+  #pragma unroll
+          for (int q = 0; q < 4; ++q) scv[c][nt][q] = 0.f;
+        const uint32_t kw0[4] = {f[c].ka.x, f[c].ka.y, f[c].ka.z, f[c].ka.w};
+        const uint32_t kw1[4] = {f[c].kb.x, f[c].kb.y, f[c].kb.z, f[c].kb.w};
+  #pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          const uint32_t wa = kw0[s >> 1], wb = kw1[s >> 1];
+          const uint32_t xa = (s & 1) ? (wa >> 8) : wa, xb = (s & 1) ? (wb >> 8) : wb;
+          const uint32_t a0 = xa & 0x000F000Fu, a2 = xa & 0x00F000F0u;
+          const uint32_t a1 = xb & 0x000F000Fu, a3 = xb & 0x00F000F0u;
+  #pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const uint2 bb = BQ_REG ? bq[BQ_REG ? s : 0] : sfrag2[(nt * 8 + s) * 32 + lane];
+            mma16816(scv[c][nt], a0, a1, a2, a3, bb.x, bb.y);
+          }
+        }
+  #pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {  // hi + lo query halves
+          scv[c][nt][0] += scv[c][nt][1];
+          scv[c][nt][2] += scv[c][nt][3];
         }
       }
     }
@@ -616,8 +712,8 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
       lgv1[c] = __log2f(sv1);
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        l0[c][nt] = (scv[c][nt][0] + scv[c][nt][1] - zk0 * sumq[nt]) * (sk0 * kscale[nt]);
-        l1[c][nt] = (scv[c][nt][2] + scv[c][nt][3] - zk1 * sumq[nt]) * (sk1 * kscale[nt]);
+        l0[c][nt] = (scv[c][nt][0] - zk0 * sumq[nt]) * (sk0 * kscale[nt]);
+        l1[c][nt] = (scv[c][nt][2] - zk1 * sumq[nt]) * (sk1 * kscale[nt]);
       }
     }
     float b0[C][NT], b1[C][NT];

@@ -72,6 +72,50 @@ __global__ void hmma_tput(float* x, int iters) {
   float s = 0; for (int j = 0; j < 8; j++) s += d[j][0] + d[j][3];
   if (s == 12345) x[0] = 1;
 }
+__global__ void imma_tput(float* x, int iters) {
+  uint32_t a0 = __float_as_uint(x[threadIdx.x]);
+  int d[8][4] = {};
+  for (int i = 0; i < iters; i++) {
+#pragma unroll
+    for (int j = 0; j < 8; j++)
+      asm volatile("mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%4,%4,%4}, {%4,%4}, {%0,%1,%2,%3};"
+        : "+r"(d[j][0]), "+r"(d[j][1]), "+r"(d[j][2]), "+r"(d[j][3]) : "r"(a0));
+  }
+  int s = 0; for (int j = 0; j < 8; j++) s += d[j][0] + d[j][3];
+  if (s == 12345) x[0] = 1;
+}
+__global__ void shf_tput(uint32_t* x, int iters) {
+  uint32_t a[8];
+  for (int j = 0; j < 8; j++) a[j] = x[threadIdx.x] + j;
+  uint32_t sh = x[1] & 7;
+  for (int i = 0; i < iters; i++) {
+#pragma unroll
+    for (int j = 0; j < 8; j++) a[j] = (a[j] >> sh) ^ (a[j] << 3);
+  }
+  uint32_t s = 0; for (int j = 0; j < 8; j++) s += a[j];
+  if (s == 12345) x[0] = 1;
+}
+__global__ void prmt_tput(uint32_t* x, int iters) {
+  uint32_t a[8];
+  for (int j = 0; j < 8; j++) a[j] = x[threadIdx.x] + j;
+  uint32_t b = x[2];
+  for (int i = 0; i < iters; i++) {
+#pragma unroll
+    for (int j = 0; j < 8; j++) asm volatile("prmt.b32 %0, %0, %1, 0x5410;" : "+r"(a[j]) : "r"(b));
+  }
+  uint32_t s = 0; for (int j = 0; j < 8; j++) s += a[j];
+  if (s == 12345) x[0] = 1;
+}
+__global__ void i2f_tput(float* x, int iters) {
+  int a[8]; float f[8];
+  for (int j = 0; j < 8; j++) { a[j] = (int)(x[threadIdx.x] * 100.f) + j; f[j] = 0.f; }
+  for (int i = 0; i < iters; i++) {
+#pragma unroll
+    for (int j = 0; j < 8; j++) { float t; asm volatile("cvt.rn.f32.s32 %0, %1;" : "=f"(t) : "r"(a[j])); f[j] += t; }
+  }
+  float s = 0; for (int j = 0; j < 8; j++) s += f[j];
+  if (s == 12345) x[0] = 1;
+}
 __global__ void mufu_tput(float* x, int iters) {
   float a[8];
   for (int j = 0; j < 8; j++) a[j] = x[threadIdx.x] * 0.001f + j * 0.0001f;
@@ -115,5 +159,13 @@ int main() {
   ms = timeit([&]{ hmma_tput<<<blocks, threads>>>(dx, iters / 4); });
   double mmas = (double)blocks * (threads / 32) * (iters / 4) * 8;
   printf("HMMA m16n8k16: %.3f G warp-mma/s -> %.3f mma/clk/SM ; %.1f TFLOPS\n", mmas / ms / 1e6, mmas / ms / 1e6 / p.multiProcessorCount / 1.9, mmas * 4096 / ms / 1e9);
+  ms = timeit([&]{ imma_tput<<<blocks, threads>>>(dx, iters / 4); });
+  printf("IMMA m16n8k32 u8.s8: %.3f G warp-mma/s -> %.3f mma/clk/SM ; %.1f TOPS\n", mmas / ms / 1e6, mmas / ms / 1e6 / p.multiProcessorCount / 1.9, mmas * 8192 / ms / 1e9);
+  ms = timeit([&]{ shf_tput<<<blocks, threads>>>((uint32_t*)dx, iters); });
+  printf("SHF+LOP pair: %.1f G pair-lanes/s -> %.2f pairs/clk/SM\n", lanes / ms / 1e6, lanes / ms / 1e6 / p.multiProcessorCount / 1.9);
+  ms = timeit([&]{ prmt_tput<<<blocks, threads>>>((uint32_t*)dx, iters); });
+  printf("PRMT: %.1f G lanes/s -> %.2f lanes/clk/SM\n", lanes / ms / 1e6, lanes / ms / 1e6 / p.multiProcessorCount / 1.9);
+  ms = timeit([&]{ i2f_tput<<<blocks, threads>>>(dx, iters); });
+  printf("I2F+FADD: %.1f G lanes/s -> %.2f lanes/clk/SM\n", lanes / ms / 1e6, lanes / ms / 1e6 / p.multiProcessorCount / 1.9);
   return 0;
 }
