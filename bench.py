@@ -120,6 +120,7 @@ def run_ours(args, rank, world, local_rank):
     import torch
 
     from paper_2604_19157_b200 import DecodePlan, HeadLayout, PageTable, RotationSpec, make_signs
+    from paper_2604_19157_b200.shard import gather_rows, max_over_ranks
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -197,12 +198,7 @@ def run_ours(args, rank, world, local_rank):
             gr.replay()
         e1.record()
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
-        if world > 1:
-            tt = torch.tensor([ms], device=dev)
-            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-            ms = float(tt.item())
-        return ms
+        return max_over_ranks(e0.elapsed_time(e1), dev)
 
     # ---- warmup (eager) then the timed K steps
     for i in range(args.warmup):
@@ -250,9 +246,9 @@ def run_ours(args, rank, world, local_rank):
     e2e = e2e_api(torch, layout, spec, dev, sets[0]["table"], args, world)
 
     # ---- verification gather (after timing; NCCL only here)
-    if world > 1:
-        outs = [torch.empty_like(sets[0]["out"]) for _ in range(world)]
-        torch.distributed.all_gather(outs, sets[0]["out"])
+    if world > 1:  # every rank's sequence (batch shard) gathered on all ranks
+        gathered = gather_rows(sets[0]["out"], [1] * world)
+        assert gathered.shape[0] == world
     splits = sets[0]["plan"].splits
 
     # ---- the other BASELINE configs (parity-test cases, reported in `detail`)
