@@ -507,8 +507,9 @@ KVR_DEV RowQ row_quant(float mxf, float mnf, double scl, bool valid) {
 
 // One 16-row tile (rows row0 .. row0 + 15 of one side) through the tensor-core K1.
 template <int ORDER, bool F16, bool ROT>
-KVR_DEV void mma_tile(const uint8_t* buf, uint8_t* stage, const FastStoreParams& p, const Signs& signs,
-                      const uint32_t (&bh)[2][2], int64_t row0, int side, const int64_t (&slot)[2]) {
+KVR_DEV void mma_tile(const uint8_t* buf, uint8_t* stage, const uint2* smask, const FastStoreParams& p,
+                      const Signs& signs, const uint32_t (&bh)[2][2], int64_t row0, int side,
+                      const int64_t (&slot)[2]) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int lrow = (lane & 7) + 8 * ((lane >> 3) & 1), lcol = lane >> 4;
   const uint32_t abase = smem_u32(buf) + lrow * 128;
@@ -521,14 +522,11 @@ KVR_DEV void mma_tile(const uint8_t* buf, uint8_t* stage, const FastStoreParams&
     ldsm_x4(abase + (b >> 2) * FS_SUB_BYTES + (c << 4), a);
     if constexpr (ROT) {
       // sign flips of this lane's elements (cols 16 b + 2 t (+1), and + 8): one XOR each
-      const int c0 = 16 * b + 2 * t;
-      const uint32_t w = signs.w[b >> 1] >> ((c0 & 31));
-      const uint32_t m0 = ((w & 1u) ? 0x8000u : 0u) | ((w & 2u) ? 0x80000000u : 0u);
-      const uint32_t m1 = ((w & 0x100u) ? 0x8000u : 0u) | ((w & 0x200u) ? 0x80000000u : 0u);
-      a[0] ^= m0;
-      a[1] ^= m0;
-      a[2] ^= m1;
-      a[3] ^= m1;
+      const uint2 m = smask[b * 4 + t];
+      a[0] ^= m.x;
+      a[1] ^= m.x;
+      a[2] ^= m.y;
+      a[3] ^= m.y;
       float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
       mma_h16<F16>(d0, a, bh[0][0], bh[0][1]);
       mma_h16<F16>(d1, a, bh[1][0], bh[1][1]);
@@ -634,7 +632,11 @@ KVR_DEV void mma_tile(const uint8_t* buf, uint8_t* stage, const FastStoreParams&
         const uint32_t m0 = (uint32_t)upa, m1 = (uint32_t)(upa >> 32), m2 = (uint32_t)upb, m3 = (uint32_t)(upb >> 32);
         const uint32_t da = (m0 ^ (uint32_t)uma) | (m1 ^ (uint32_t)(uma >> 32));
         const uint32_t db = (m2 ^ (uint32_t)umb) | (m3 ^ (uint32_t)(umb >> 32));
-        fl[rh] |= ((da >= 0x10000u ? 1u : 0u) | (db >= 0x10000u ? 2u : 0u)) << k;
+        if constexpr (ROT) {
+          fl[rh] |= da | db;  // row-level: bits >= 16 set <=> a code is within delta of a boundary
+        } else {
+          fl[rh] |= ((da >= 0x10000u ? 1u : 0u) | (db >= 0x10000u ? 2u : 0u)) << k;
+        }
         const uint32_t two = pack4(m0, m1, m2, m3);  // byte 0: code byte k, byte 2: k + 1
         srow[4 * k] = (uint8_t)two;
         srow[4 * k + 4] = (uint8_t)(two >> 16);
@@ -654,7 +656,11 @@ KVR_DEV void mma_tile(const uint8_t* buf, uint8_t* stage, const FastStoreParams&
         const unsigned long long up = fma2_rm(uu, fix2, mgp), um = fma2_rm(uu, fix2, mgm);
         const uint32_t m0 = (uint32_t)up, m1 = (uint32_t)(up >> 32);
         const uint32_t d = (m0 ^ (uint32_t)um) | (m1 ^ (uint32_t)(um >> 32));
-        fl[rh] |= (cd && d >= 0x10000u ? 1u : 0u) << k;
+        if constexpr (ROT) {
+          fl[rh] |= cd ? d : 0u;
+        } else {
+          fl[rh] |= (cd && d >= 0x10000u ? 1u : 0u) << k;
+        }
         srow[4 * k] = (uint8_t)(((m0 >> 16) & 15u) | ((m1 >> 12) & 0xF0u));
       }
     }
@@ -680,6 +686,7 @@ KVR_DEV void mma_tile(const uint8_t* buf, uint8_t* stage, const FastStoreParams&
     // ---- rare (rotated rows): reference-exact recomputation of flagged rows, warp-cooperative
 #pragma unroll
     for (int rh = 0; rh < 2; ++rh) {
+      fl[rh] = fl[rh] >= 0x10000u ? 0xFFFFu : 0u;  // the whole row is rewritten
       fl[rh] |= __shfl_xor_sync(0xffffffffu, fl[rh], 1);
       fl[rh] |= __shfl_xor_sync(0xffffffffu, fl[rh], 2);
     }
@@ -733,10 +740,20 @@ __global__ void __launch_bounds__(FS_WARPS * 32, KVR_FS_MINB)
   uint8_t* bufs = smem + wib * 2 * FS_TILE_BYTES;
   uint8_t* stage = smem + FS_WARPS * 2 * FS_TILE_BYTES + wib * MS_STAGE;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + FS_WARPS * (2 * FS_TILE_BYTES + MS_STAGE)) + wib * 2;
+  uint2* smask = reinterpret_cast<uint2*>(smem + FS_WARPS * (2 * FS_TILE_BYTES + MS_STAGE) + 64);  // [8 blocks][4 t]
 
   const int total_tiles = 2 * p.tiles_per_side;
   const int warp_stride = gridDim.x * FS_WARPS;
   const int H = p.pool.H;
+
+  // sign-flip masks of A-fragment words: block b, lane column group t -> cols 16 b + 2 t (+1) | + 8
+  if (threadIdx.x < 32) {
+    const int b = threadIdx.x >> 2, tt = threadIdx.x & 3, c0 = 16 * b + 2 * tt;
+    const uint32_t w = signs.w[c0 >> 5] >> (c0 & 31);
+    smask[threadIdx.x] = make_uint2(((w & 1u) ? 0x8000u : 0u) | ((w & 2u) ? 0x80000000u : 0u),
+                                    ((w & 0x100u) ? 0x8000u : 0u) | ((w & 0x200u) ? 0x80000000u : 0u));
+  }
+  __syncthreads();
 
   // H_16 as B fragments (k = 2t, 2t + 1 | 8 + 2t, 9 + 2t; column g + 8 nn), +-1 exact
   uint32_t bh[2][2];
@@ -802,9 +819,9 @@ __global__ void __launch_bounds__(FS_WARPS * 32, KVR_FS_MINB)
     const int side = tile >= p.tiles_per_side;
     const int64_t row0 = (int64_t)(side ? tile - p.tiles_per_side : tile) * FS_TILE_ROWS;
     if (side ? p.rot_v : p.rot_k)  // warp-uniform
-      mma_tile<ORDER, F16, true>(buf, stage, p, signs, bh, row0, side, slot);
+      mma_tile<ORDER, F16, true>(buf, stage, smask, p, signs, bh, row0, side, slot);
     else
-      mma_tile<ORDER, F16, false>(buf, stage, p, signs, bh, row0, side, slot);
+      mma_tile<ORDER, F16, false>(buf, stage, smask, p, signs, bh, row0, side, slot);
   }
 }
 
@@ -840,7 +857,7 @@ static int launch_fast_impl(const void* k, const void* v, int64_t n_tok, const i
   if (kvr_encode_tensor_map_2d(&mv, v, 128, (uint64_t)prm.n_rows, 256, 64, FS_TILE_ROWS,
                                CU_TENSOR_MAP_SWIZZLE_128B) != CUDA_SUCCESS)
     return KVR_ERR_CUDA;
-  const size_t smem = FS_WARPS * (2 * FS_TILE_BYTES + MS_STAGE) + FS_WARPS * 2 * sizeof(uint64_t) + 1024;
+  const size_t smem = FS_WARPS * (2 * FS_TILE_BYTES + MS_STAGE) + 64 + 256 + 1024;
   auto kern = store_mma_kernel<ORDER, F16>;
   static bool attr_set = false;
   if (!attr_set) {
