@@ -155,6 +155,13 @@ int kvr_dequantize_pages(const kvr_pool* pool, const int32_t* block_table, int32
  *   least kvr_decode_workspace_bytes(...) bytes and zero-filled once before
  *   first use (the kernels leave the split counters at zero afterwards).
  */
+/*
+ * Both decode entry points launch with programmatic dependent launch: before their
+ * dependency wait they read block_table, seq_lens, new_slot and pool cells older
+ * than the last two tokens of each sequence (a preceding kernel that writes those
+ * must not trigger launch_dependents early).  With more than 8 splits a second,
+ * split-merge kernel follows the decode kernel on the stream.
+ */
 size_t kvr_decode_workspace_bytes(int32_t batch, int32_t num_kv_heads, int32_t num_q_heads,
                                   int32_t head_dim, int32_t num_splits);
 int kvr_decode_pick_splits(int32_t batch, int32_t num_kv_heads, int32_t max_seq_len,

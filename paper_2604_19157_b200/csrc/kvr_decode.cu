@@ -383,6 +383,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   int wnext = page_window(1), win_idx = 0;
   const uint8_t* wcur = window_addr(0, page_window(0));
   const int len_raw = __ldg(&p.lens[b]);
+  const int64_t new_slot = APPEND ? __ldg(&p.new_slot[b]) : -1;  // host-written, like lens: read with it
   if (threadIdx.x < NWARPS * RING_CELLS) mbar_init(&bars[threadIdx.x], 1);
   reinterpret_cast<uint2*>(sfrag)[threadIdx.x] = make_uint2(0u, 0u);  // 4 KB of query digits (padding = 0)
   fence_mbar_init();
@@ -392,7 +393,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   // APPEND: the step's token (position len - 1) is written and scored by the writer
   // warp straight from registers; the tiles cover the len_kv older tokens, so no
   // tile load waits for the write
-  const bool app = APPEND && len > 0 && __ldg(&p.new_slot[b]) >= 0;
+  const bool app = APPEND && len > 0 && new_slot >= 0;
   const int len_kv = app ? len - 1 : len;
   const int t_new = (len - 1) >> 4;
   const bool app_owner = app && t_new >= lo && t_new < hi_max;  // this CTA writes + scores it
