@@ -801,6 +801,10 @@ __global__ void __launch_bounds__(FS_WARPS * 32, KVR_FS_MINB)
     }
   };
 
+  // programmatic dependent launch: the setup above overlaps the previous kernel;
+  // the inputs, slot ids and the pool may come from it
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   int tile = blockIdx.x * FS_WARPS + wib;
   if (tile < total_tiles && lane == 0) issue(tile, 0);
   uint32_t phases = 0u;  // bit b: parity of buffer b
@@ -869,8 +873,17 @@ static int launch_fast_impl(const void* k, const void* v, int64_t n_tok, const i
   const int cap = kvr_num_sms() * KVR_FS_MINB;
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
-  kern<<<grid, FS_WARPS * 32, smem, st>>>(prm, mk, mv, sg);
-  return 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(FS_WARPS * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, prm, mk, mv, sg) == cudaSuccess ? 0 : KVR_ERR_CUDA;
 }
 
 int kvr_launch_store_fast(const void* k, const void* v, int in_dtype, int64_t n_tok, const int64_t* slots,
