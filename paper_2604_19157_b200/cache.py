@@ -1,9 +1,10 @@
 """Paged INT4 KV cache in B200 HBM (mirrors kvrot.cache.PageTable, cache.py:122-450).
 
-Device layout: one uint8 tensor [num_pages, page_bytes]; each row is a page blob
-whose byte layout is the reference `.kvpg` page record
-    k_payload u8[P][H][d/2] | v_payload | k_scale f32[P][H] | k_zp u8[P][H] | v_scale | v_zp
-(cache.py:103-114, 387-397), so `dump` is a header plus a page-ordered copy.
+Device layout: one uint8 tensor [num_pages, page_bytes]; a page holds, per kv
+head, P / 16 "cells" of 16 tokens with everything a decode tile needs contiguous
+(k_scale | v_scale | K codes | V codes | k_zp | v_zp, include/kvrot_b200.h), so a
+(page, head) tile is one bulk copy.  `dump` / `load` convert cells to and from
+the reference `.kvpg` page records (cache.py:387-397) byte for byte.
 
 Host side: the same lowest-id-first page heap and per-sequence page lists as
 the reference (cache.py:150-151, 211-223), so page ids -- and therefore dump

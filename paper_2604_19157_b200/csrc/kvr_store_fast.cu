@@ -5,25 +5,10 @@
 // _rotate_token (cache.py:453-462) -> apply_block_rotation (rotation.py:118-142)
 // -> _kernels.fwht_rows + quantize_rows (_ref.py:22-40, 57-80).
 //
-// Design (B200, sm_100a):
-//  * persistent CTAs of 4 warps, 4 CTAs per SM; each warp streams 16-row tiles
-//    (4 KB) through a private double buffer filled by TMA (cp.async.bulk.tensor.2d,
-//    SWIZZLE_128B: conflict-free half-row-per-thread shared-memory reads);
-//  * a lane pair owns one 128-element row, 64 elements each in registers: sign
-//    flip + bf16 unpack fused with the first butterfly stage, stages up to half 32
-//    as f32x2 (FADD2), the half-64 stage across the pair (64 shuffles), NaN-
-//    propagating 3-input min/max (FMNMX3.NAN) combined across the pair;
-//  * the row scale / zero point are formed in f64 exactly as the reference does,
-//    from the fp32 butterfly's extreme values;
-//  * codes: one FFMA2.RM per element pair evaluates floor((t + z + 1/2) * 2^16)
-//    as a fixed-point integer (magic 2^23), twice (+-delta) -- if both agree on
-//    the integer part the nibble is the reference's round-half-away code for this
-//    y; a row with an element within delta of a half step is recomputed in f64
-//    from the bf16 inputs with the reference's butterfly order, warp-cooperatively
-//    (warp_exact_row), and its flagged 8-code groups are replaced.  Unrotated
-//    (plain) rows hold y exactly, so their flagged groups are fixed in-thread by
-//    exact FMA sign tests against the rounding boundaries instead;
-//  * 8 nibbles are packed with 3 PRMT + 1 IMAD.HI per 4 codes.
+// Design (B200, sm_100a): see store_mma_kernel below -- H_128 = H_8 (x) H_16 with
+// H_16 on the tensor cores (bf16/fp16 HMMA, +-1 weights), H_8 as lane-local FADD2
+// stages, the reference's f64 row scale / zero point, codes by FFMA2.RM with a
+// +-delta boundary test and an exact recomputation of flagged rows.
 #include "kvr_common.cuh"
 #include "kvr_internal.h"
 
@@ -50,24 +35,8 @@ struct FastStoreParams {
   int64_t n_rows;          // n_tok * H
   int32_t tiles_per_side;  // ceil(n_rows / 32)
   int32_t rot_k, rot_v;
-  uint32_t sgn_hi[64];  // word j: bit 31 <=> element 2j+1 negated
-  uint32_t sgn_lo[64];  // word j: 0x80000000 <=> element 2j negated (added to w << 16)
   int32_t log2P;        // page_tokens = 2^log2P (tensor-core path)
 };
-
-template <bool F16, bool ROT>
-KVR_DEV void unpack_pair(uint32_t w, uint32_t s_hi, uint32_t s_lo, float& e, float& o) {
-  if constexpr (!F16) {
-    // bf16 pair -> two f32 (exact); the sign flip is folded into the same ops
-    e = __uint_as_float(ROT ? (w << 16) + s_lo : (w << 16));
-    o = __uint_as_float(ROT ? ((w ^ s_hi) & 0xFFFF0000u) : (w & 0xFFFF0000u));
-  } else {
-    const uint32_t ws = ROT ? (w ^ ((s_lo >> 16) | s_hi)) : w;
-    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&ws));
-    e = f.x;
-    o = f.y;
-  }
-}
 
 // Elements 4l..4l+3 of the row staged for lane `src` in the swizzled tile, as f64.
 template <bool F16>
@@ -142,292 +111,6 @@ KVR_DEV uint32_t plain_code_exact(float x, float s, float inv, float z) {
   else if (fmaf(-(m + 0.5f), s, ax) >= 0.f) m += 1.f;
   const float q = fminf(fmaxf(copysignf(m, x) + z, 0.f), 15.f);
   return (uint32_t)q;
-}
-
-// Quantize the half row (64 elements, half `hf`) this lane shares with lane ^ 1:
-// its 32 packed code bytes, the row scale and zero point; returns the write flag.
-template <int ORDER, bool F16, bool ROT>
-KVR_DEV bool half_row_codes(const uint8_t* buf, int row, int hf, const FastStoreParams& p, const Signs& signs,
-                            bool valid, uint32_t (&packed)[8], float& scale_out, uint32_t& zp_out) {
-  const int lane = threadIdx.x & 31;
-  // ---- stage the half row: 8 x 16 B swizzled reads; unpack fused with stage half = 1
-  unsigned long long v[32];  // v[j] = (y_{2j}, y_{2j+1}) of this half
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const uint4 q = *reinterpret_cast<const uint4*>(buf + hf * FS_SUB_BYTES + row * 128 + ((c ^ (row & 7)) << 4));
-    const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int j = c * 4 + u;
-      float e, o;
-      unpack_pair<F16, ROT>(w4[u], p.sgn_hi[32 * hf + j], p.sgn_lo[32 * hf + j], e, o);
-      v[j] = ROT ? pk(e + o, e - o) : pk(e, o);
-    }
-  }
-  if constexpr (ROT) {
-    // stages half = 2 .. min(ORDER/2, 32) inside the half: pairs (j, j + hh) of (y_{2j}, y_{2j+1})
-#pragma unroll
-    for (int hh = 1; hh < ORDER / 2 && hh < 32; hh <<= 1) {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        if ((j & hh) == 0) {
-          const unsigned long long a = v[j], c = v[j + hh];
-          v[j] = add2(a, c);
-          v[j + hh] = sub2(a, c);
-        }
-      }
-    }
-    if constexpr (ORDER == 128) {
-      // stage half = 64 across the lane pair: y_j = a_j + b_j (half 0), a_j - b_j (half 1)
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        float x0, x1;
-        upk(v[j], x0, x1);
-        const float o0 = __shfl_xor_sync(0xffffffffu, x0, 1), o1 = __shfl_xor_sync(0xffffffffu, x1, 1);
-        v[j] = hf ? sub2(pk(o0, o1), v[j]) : add2(v[j], pk(o0, o1));
-      }
-    }
-  }
-  // ---- row extremes (NaN-propagating), combined across the pair
-  float mxf, mnf;
-  {
-    float mx0, mn0, mx1, mn1, a0, a1, b0, b1;
-    upk(v[0], a0, a1);
-    upk(v[1], b0, b1);
-    mx0 = max3_nan(a0, a1, a1);
-    mn0 = min3_nan(a0, a1, a1);
-    mx1 = max3_nan(b0, b1, b1);
-    mn1 = min3_nan(b0, b1, b1);
-#pragma unroll
-    for (int j = 2; j < 32; j += 2) {
-      float x0, x1, y0, y1;
-      upk(v[j], x0, x1);
-      upk(v[j + 1], y0, y1);
-      mx0 = max3_nan(mx0, x0, x1);
-      mn0 = min3_nan(mn0, x0, x1);
-      mx1 = max3_nan(mx1, y0, y1);
-      mn1 = min3_nan(mn1, y0, y1);
-    }
-    const float mxh = max3_nan(mx0, mx1, mx1), mnh = min3_nan(mn0, mn1, mn1);
-    mxf = max3_nan(mxh, __shfl_xor_sync(0xffffffffu, mxh, 1), mxh);
-    mnf = min3_nan(mnh, __shfl_xor_sync(0xffffffffu, mnh, 1), mnh);
-  }
-
-#pragma unroll
-  for (int i = 0; i < 8; ++i) packed[i] = 0u;
-  scale_out = 0.f;
-  zp_out = 0u;
-  bool write = valid;
-  if (valid && !(isfinite(mxf) && isfinite(mnf))) {
-    if (p.flags && hf == 0) atomicOr(p.flags, (uint32_t)KVR_FLAG_NONFINITE);
-    write = false;
-  }
-  // ---- row scale / zero point in f64, exactly as _ref.quantize_rows
-  const double inv64 = 1.0 / sqrt((double)ORDER);
-  bool do_codes = false, clamp_row = false;
-  double s64 = 1.0, z = 0.0, cst = 0.0;
-  float s32 = 0.f;
-  if (write) {
-    const double scl = ROT ? inv64 : 1.0;
-    const double mx = (double)mxf * scl, mn = (double)mnf * scl;  // == fl64(S * inv) of the reference
-    s32 = (float)((mx - mn) / 15.0);
-    if (s32 == 0.0f) {
-      scale_out = (float)mn;  // sentinel row: offset in the scale slot, zp 0xFF, codes 0
-      zp_out = 0xFFu;
-    } else {
-      s64 = (double)s32;
-      z = round_half_away(-mn / s64);
-      z = z < 0.0 ? 0.0 : (z > 15.0 ? 15.0 : z);
-      scale_out = s32;
-      zp_out = (uint32_t)z;
-      cst = scl / s64;
-      const double ulo = mn * (1.0 / s64) + z + 0.5, uhi = mx * (1.0 / s64) + z + 0.5;
-      // rows whose codes may leave [0, 15] (z clipped / boundary ties) clamp u first;
-      // clamping is exact at both ends because floor-then-clip agrees on either side
-      clamp_row = !((ulo > 1e-3) && (uhi < 16.0 - 1e-3));
-      do_codes = true;
-    }
-  }
-  const bool clamp = __any_sync(0xffffffffu, do_codes && clamp_row);
-  uint32_t gflags = 0u;  // bit q: an element of 8q..8q+7 (of this half) is within delta of a boundary
-  if (do_codes) {
-    if (!clamp) {
-      // U = floor((y*c + z + 1/2 (+-delta)) * 2^16) + 2^23, one FFMA2.RM per pair and sign
-      const float cf = (float)(cst * (double)FS_FIX);
-      const float bias = (float)((z + 0.5) * (double)FS_FIX) + FS_MAGIC;
-      const unsigned long long c2 = pk(cf, cf);
-      const unsigned long long bp = pk(bias + FS_D, bias + FS_D), bm = pk(bias - FS_D, bias - FS_D);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        uint32_t mp[8], dq = 0u;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const unsigned long long up = fma2_rm(v[q * 4 + r], c2, bp);
-          const unsigned long long um = fma2_rm(v[q * 4 + r], c2, bm);
-          const uint32_t p0 = (uint32_t)up, p1 = (uint32_t)(up >> 32);
-          dq |= (p0 ^ (uint32_t)um) | (p1 ^ (uint32_t)(um >> 32));
-          mp[2 * r] = p0;
-          mp[2 * r + 1] = p1;
-        }
-        packed[q] = prmt(pack4(mp[0], mp[1], mp[2], mp[3]), pack4(mp[4], mp[5], mp[6], mp[7]), 0x6420u);
-        gflags |= (dq >= 0x10000u ? 1u : 0u) << q;
-      }
-    } else {
-      // clamped variant: u in f32 (error <= 2^-20), clamped to [2^-13, 15.99], then the magic floor
-      const float zb = (float)(z + 0.5), cu = (float)cst;
-      const unsigned long long fix2 = pk(FS_FIX, FS_FIX);
-      const unsigned long long mgp = pk(FS_MAGIC + FS_D_CLAMP, FS_MAGIC + FS_D_CLAMP),
-                               mgm = pk(FS_MAGIC - FS_D_CLAMP, FS_MAGIC - FS_D_CLAMP);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        uint32_t mp[8], dq = 0u;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          float a0, a1;
-          upk(v[q * 4 + r], a0, a1);
-          const float u0 = fminf(fmaxf(fmaf(a0, cu, zb), 1.0f / 8192.0f), 15.99f);
-          const float u1 = fminf(fmaxf(fmaf(a1, cu, zb), 1.0f / 8192.0f), 15.99f);
-          const unsigned long long uu = pk(u0, u1);
-          const unsigned long long up = fma2_rm(uu, fix2, mgp);
-          const unsigned long long um = fma2_rm(uu, fix2, mgm);
-          mp[2 * r] = (uint32_t)up;
-          mp[2 * r + 1] = (uint32_t)(up >> 32);
-          dq |= ((uint32_t)up ^ (uint32_t)um) | ((uint32_t)(up >> 32) ^ (uint32_t)(um >> 32));
-        }
-        packed[q] = prmt(pack4(mp[0], mp[1], mp[2], mp[3]), pack4(mp[4], mp[5], mp[6], mp[7]), 0x6420u);
-        gflags |= (dq >= 0x10000u ? 1u : 0u) << q;
-      }
-    }
-  }
-  if constexpr (!ROT) {
-    // plain rows: exact in-thread fix of the flagged groups
-    if (gflags) {
-      const float inv = 1.0f / s32, zf = (float)z;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        if ((gflags >> q) & 1u) {
-          uint32_t w = 0u;
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            float a0, a1;
-            upk(v[q * 4 + r], a0, a1);
-            w |= plain_code_exact(a0, s32, inv, zf) << (8 * r);
-            w |= plain_code_exact(a1, s32, inv, zf) << (8 * r + 4);
-          }
-          packed[q] = w;
-        }
-      }
-    }
-  } else {
-    // ---- rare: reference-exact recomputation of flagged rows, warp-cooperative
-    uint32_t todo = __ballot_sync(0xffffffffu, gflags != 0u);
-    while (todo) {
-      const int src = __ffs(todo) - 1;  // lane src: half (src & 1) of tile row 16 pass + src / 2
-      todo &= todo - 1;
-      const uint32_t gf = __shfl_sync(0xffffffffu, gflags, src);
-      const double sb = __shfl_sync(0xffffffffu, s64, src), zb = __shfl_sync(0xffffffffu, z, src);
-      const int srow = __shfl_sync(0xffffffffu, row, src);
-      const uint32_t g16 = warp_exact_row<ORDER, F16, ROT>(buf, srow, signs, sb, zb);
-      const int hb = (src & 1) * 8;  // the half's groups are row groups hb .. hb + 7
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        if ((gf >> q) & 1u) {  // warp-uniform
-          const uint32_t lo = __shfl_sync(0xffffffffu, g16, 2 * (hb + q)),
-                         hi = __shfl_sync(0xffffffffu, g16, 2 * (hb + q) + 1);
-          if (lane == src) packed[q] = lo | (hi << 16);
-        }
-      }
-    }
-  }
-  return write;
-}
-
-template <int ORDER, bool F16>
-__global__ void __launch_bounds__(FS_WARPS * 32, KVR_FS_MINB)
-    store_fast_kernel(const __grid_constant__ FastStoreParams p, const __grid_constant__ CUtensorMap map_k,
-                      const __grid_constant__ CUtensorMap map_v, const __grid_constant__ Signs signs) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  uint8_t* bufs = smem + wib * 2 * FS_TILE_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + FS_WARPS * 2 * FS_TILE_BYTES) + wib * 2;
-
-  const int total_tiles = 2 * p.tiles_per_side;
-  const int warp_stride = gridDim.x * FS_WARPS;
-  const int H = p.pool.H;
-  const int trow = lane >> 1, hf = lane & 1;  // this lane: half hf of tile row trow
-
-  if (lane == 0) {
-    prefetch_tensormap(&map_k);
-    prefetch_tensormap(&map_v);
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    fence_mbar_init();
-  }
-  __syncwarp();
-
-  auto issue = [&](int tile, int b) {
-    const int side = tile >= p.tiles_per_side;
-    const int row0 = (side ? tile - p.tiles_per_side : tile) * FS_TILE_ROWS;
-    const CUtensorMap* m = side ? &map_v : &map_k;
-    uint8_t* dst = bufs + b * FS_TILE_BYTES;
-    fence_proxy_async();
-    mbar_expect_tx(&bars[b], FS_TILE_BYTES);
-    tma_load_2d(dst, m, &bars[b], 0, row0);
-    tma_load_2d(dst + FS_SUB_BYTES, m, &bars[b], 64, row0);
-  };
-  auto row_of = [&](int tile) -> int64_t {
-    const int side = tile >= p.tiles_per_side;
-    return (int64_t)(side ? tile - p.tiles_per_side : tile) * FS_TILE_ROWS + trow;
-  };
-  auto slot_of = [&](int tile) -> int64_t {  // slot id of this lane's row (or -1)
-    if (tile >= total_tiles) return -1;
-    const int64_t row = row_of(tile);
-    return row < p.n_rows ? __ldg(&p.slots[row / H]) : -1;
-  };
-
-  int tile = blockIdx.x * FS_WARPS + wib;
-  if (tile < total_tiles && lane == 0) issue(tile, 0);
-  uint32_t phase[2] = {0u, 0u};
-  int64_t slot_cur = slot_of(tile);
-
-  for (int it = 0; tile < total_tiles; ++it, tile += warp_stride) {
-    const int b = it & 1;
-    const int next = tile + warp_stride;
-    if (next < total_tiles && lane == 0) issue(next, b ^ 1);
-    const int64_t slot = slot_cur;
-    slot_cur = slot_of(next);  // prefetch: consumed one tile later
-    mbar_wait(&bars[b], phase[b]);
-    phase[b] ^= 1u;
-    const uint8_t* buf = bufs + b * FS_TILE_BYTES;
-    const int side = tile >= p.tiles_per_side;
-    const int64_t row = row_of(tile);
-    const bool valid = row < p.n_rows;  // codes are computed whatever the slot; the store is predicated
-
-    uint32_t packed[8];
-    float scale_out;
-    uint32_t zp_out;
-    bool write;
-    if (side ? p.rot_v : p.rot_k)  // warp-uniform
-      write = half_row_codes<ORDER, F16, true>(buf, trow, hf, p, signs, valid, packed, scale_out, zp_out);
-    else
-      write = half_row_codes<128, F16, false>(buf, trow, hf, p, signs, valid, packed, scale_out, zp_out);
-    __syncwarp();  // every lane done with the staged tile -> buffer may be refilled
-
-    if (write && slot >= 0) {
-      const Pool& pl = p.pool;
-      const int head = (int)(row % H);
-      int ci;
-      uint8_t* cell = cell_of(pl, slot / pl.P, head, (int)(slot % pl.P), ci);
-      uint4* dst = reinterpret_cast<uint4*>(cell + (side ? cell_vcode(pl, ci) : cell_kcode(pl, ci)) + 32 * hf);
-      dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-      dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
-      if (hf == 0) {
-        *reinterpret_cast<float*>(cell + (side ? cell_vscale(pl, ci) : cell_kscale(pl, ci))) = scale_out;
-        cell[side ? cell_vzp(pl, ci) : cell_kzp(pl, ci)] = (uint8_t)zp_out;
-      }
-    }
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -846,12 +529,6 @@ static int launch_fast_impl(const void* k, const void* v, int64_t n_tok, const i
   prm.rot_v = rot_v;
   prm.log2P = 0;
   while ((1 << prm.log2P) < pool.P) ++prm.log2P;
-  for (int j = 0; j < 64; ++j) {
-    const bool ne = has && ((s.w[(2 * j) >> 5] >> ((2 * j) & 31)) & 1u);
-    const bool no = has && ((s.w[(2 * j + 1) >> 5] >> ((2 * j + 1) & 31)) & 1u);
-    prm.sgn_lo[j] = ne ? 0x80000000u : 0u;
-    prm.sgn_hi[j] = no ? 0x80000000u : 0u;
-  }
   Signs sg = s;
   if (!has) for (auto& x : sg.w) x = 0u;
   CUtensorMap mk, mv;
