@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define KVR_ABI_VERSION 1
+#define KVR_ABI_VERSION 2
 #define KVR_MAX_HEAD_DIM 256
 
 typedef enum {
@@ -78,13 +78,24 @@ typedef struct {
   int32_t head_dim;     /* d  */
   int32_t page_bytes;   /* H * (P / T) * cell_bytes                        */
   int32_t cell_tokens;  /* T                                                */
-  int32_t cell_bytes;   /* roundup16(T * (d + 10))                          */
+  int32_t cell_bytes;   /* INT4: roundup16(T * (d + 10)); BF16: 4 * T * d   */
+  int32_t precision;    /* KVR_PREC_INT4 | KVR_PREC_BF16                    */
 } kvr_pool;
+
+/* Page precision (cache.py:36-37).  A BF16 pool (cache.py:115-118) stores the raw
+ * K / V vectors as bf16 bits, rounded f32 -> bf16 to nearest even (cache.py:43-47);
+ * its cell is  k_bits u16[T][d] | v_bits u16[T][d]  and it ignores rotations
+ * (append_token, cache.py:243-246; decode_step uses the query as-is, attention.py:67-71). */
+#define KVR_PREC_INT4 0
+#define KVR_PREC_BF16 1
 
 /* Fill a kvr_pool for (P, H, d); the page size is returned in pool->page_bytes. */
 int kvr_pool_init(kvr_pool* pool, void* base, int64_t num_pages, int32_t page_tokens,
                   int32_t num_kv_heads, int32_t head_dim);
 
+/* Same for a BF16 pool (precision KVR_PREC_BF16). */
+int kvr_pool_init_bf16(kvr_pool* pool, void* base, int64_t num_pages, int32_t page_tokens,
+                       int32_t num_kv_heads, int32_t head_dim);
 const char* kvr_last_error(void);
 /* Profiling aid: when non-NULL, decode launches record a per-CTA timeline into
  * `trace` (device buffer of batch * splits * num_kv_heads * 16 u64): [0] the

@@ -19,10 +19,11 @@ LIB_PATH = os.environ.get("KVR_LIB_PATH") or os.path.join(_HERE, "_lib", "libkvr
 KVR_F64, KVR_F32, KVR_BF16, KVR_F16 = 0, 1, 2, 3
 KVR_KEYS_ONLY, KVR_KEYS_AND_VALUES = 0, 1
 KVR_FLAG_NONFINITE = 1
+KVR_PREC_INT4, KVR_PREC_BF16 = 0, 1
 
 # every symbol include/kvrot_b200.h declares
 EXPORTED = (
-    "kvr_pool_init", "kvr_last_error", "kvr_abi_version", "kvr_device_sms",
+    "kvr_pool_init", "kvr_pool_init_bf16", "kvr_last_error", "kvr_abi_version", "kvr_device_sms",
     "kvr_fwht_rows_f64", "kvr_pack_rows", "kvr_unpack_rows", "kvr_quantize_rows_f64",
     "kvr_dequantize_rows_f64", "kvr_block_rotate", "kvr_rotate_quantize_store",
     "kvr_dequantize_pages", "kvr_decode_workspace_bytes", "kvr_decode_pick_splits",
@@ -40,6 +41,7 @@ class KvrPool(ctypes.Structure):
         ("page_bytes", ctypes.c_int32),
         ("cell_tokens", ctypes.c_int32),
         ("cell_bytes", ctypes.c_int32),
+        ("precision", ctypes.c_int32),
     ]
 
 
@@ -51,6 +53,7 @@ _P, _I32, _I64, _SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_
 def _declare(lib):
     sig = {
         "kvr_pool_init": (_I32, [ctypes.POINTER(KvrPool), _P, _I64, _I32, _I32, _I32]),
+        "kvr_pool_init_bf16": (_I32, [ctypes.POINTER(KvrPool), _P, _I64, _I32, _I32, _I32]),
         "kvr_last_error": (ctypes.c_char_p, []),
         "kvr_debug_decode_trace": (None, [_P]),
         "kvr_abi_version": (_I32, []),

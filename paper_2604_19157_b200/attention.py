@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 from . import _kernels, _lib
-from .cache import PageTable
+from .cache import INT4, PageTable
 from .errors import EmptySequenceError, NonFiniteInputError, ShapeError, UnsupportedConfigError
 from .layout import HeadLayout
 from .rotation import RotationSpec, Targets
@@ -108,6 +108,8 @@ class DecodePlan:
                              f"got {tuple(q.shape)}")
         if out is None:
             out = torch.empty(q.shape, dtype=torch.float32, device=table.device)
+        if table.precision != INT4:
+            spec = None  # BF16 pools hold raw vectors: the query is used as-is (attention.py:67-71)
         rotate = spec is not None
         if rotate:
             if spec.order != lay.rot_order:
@@ -135,6 +137,8 @@ class DecodePlan:
             k_new, v_new = k_new.contiguous(), v_new.contiguous()
         if out is None:
             out = torch.empty(q.shape, dtype=torch.float32, device=table.device)
+        if table.precision != INT4:
+            spec = None
         rotate = spec is not None
         if rotate and spec.learned is not None:
             raise UnsupportedConfigError("learned rotations are not fused into the decode kernel (row f3)")

@@ -77,23 +77,50 @@ def cell_tokens(layout: HeadLayout) -> int:
     return 16 if layout.page_tokens % 16 == 0 else layout.page_tokens
 
 
-def cell_bytes(layout: HeadLayout) -> int:
+def cell_bytes(layout: HeadLayout, precision: str = INT4) -> int:
+    if precision == BF16:  # k_bits u16[T][d] | v_bits u16[T][d]
+        return 4 * cell_tokens(layout) * layout.head_dim
     return (cell_tokens(layout) * (layout.head_dim + 10) + 15) & ~15
 
 
-def page_bytes(layout: HeadLayout) -> int:
+def page_bytes(layout: HeadLayout, precision: str = INT4) -> int:
     """Size of one device page blob: H x (P / T) cells."""
-    return layout.num_kv_heads * (layout.page_tokens // cell_tokens(layout)) * cell_bytes(layout)
+    return layout.num_kv_heads * (layout.page_tokens // cell_tokens(layout)) * cell_bytes(layout, precision)
 
 
-def record_bytes(layout: HeadLayout) -> int:
+def record_bytes(layout: HeadLayout, precision: str = INT4) -> int:
     """Size of one reference `.kvpg` page record (cache.py:387-397)."""
+    if precision == BF16:  # k_payload u16[P][H][d] | v_payload
+        return 4 * layout.page_tokens * layout.num_kv_heads * layout.head_dim
     return layout.page_tokens * layout.num_kv_heads * (layout.head_dim + 10)
 
 
-def cells_to_records(blobs: np.ndarray, layout: HeadLayout) -> np.ndarray:
+def _bf16_cells_to_records(blobs: np.ndarray, layout: HeadLayout) -> np.ndarray:
+    P, H, d = layout.page_tokens, layout.num_kv_heads, layout.head_dim
+    T = cell_tokens(layout)
+    n = blobs.shape[0]
+    c = np.ascontiguousarray(blobs, dtype=np.uint8).reshape(n, H, P // T, 2, T, 2 * d)  # [.., side, t, row bytes]
+    kv = np.ascontiguousarray(c.transpose(3, 0, 2, 4, 1, 5)).reshape(2, n, P * H * 2 * d)  # (side, n, P, H, row)
+    return np.concatenate([kv[0], kv[1]], axis=1)
+
+
+def _bf16_records_to_cells(records: np.ndarray, layout: HeadLayout) -> np.ndarray:
+    P, H, d = layout.page_tokens, layout.num_kv_heads, layout.head_dim
+    T = cell_tokens(layout)
+    n = records.shape[0]
+    r = np.ascontiguousarray(records, dtype=np.uint8).reshape(n, 2, P, H, 2 * d)
+    r = np.moveaxis(r, 3, 2)  # (n, 2, H, P, 2d)
+    r = r.reshape(n, 2, H, P // T, T, 2 * d)
+    r = np.ascontiguousarray(np.moveaxis(r, 1, 3))  # (n, H, P/T, 2, T, 2d)
+    return r.reshape(n, -1)
+
+
+def cells_to_records(blobs: np.ndarray, layout: HeadLayout, precision: str = INT4) -> np.ndarray:
     """Device page blobs [n, page_bytes] -> reference page records [n, record_bytes]
-    (k_payload [P][H][d/2] | v_payload | k_scale f32[P][H] | k_zp [P][H] | v_scale | v_zp)."""
+    (INT4: k_payload [P][H][d/2] | v_payload | k_scale f32[P][H] | k_zp [P][H] | v_scale | v_zp;
+    BF16: k_payload u16[P][H][d] | v_payload)."""
+    if precision == BF16:
+        return _bf16_cells_to_records(blobs, layout)
     P, H, d = layout.page_tokens, layout.num_kv_heads, layout.head_dim
     T, cb = cell_tokens(layout), cell_bytes(layout)
     n = blobs.shape[0]
@@ -121,8 +148,10 @@ def cells_to_records(blobs: np.ndarray, layout: HeadLayout) -> np.ndarray:
     return np.concatenate([p.reshape(n, -1).view(np.uint8) for p in parts], axis=1)
 
 
-def records_to_cells(records: np.ndarray, layout: HeadLayout) -> np.ndarray:
+def records_to_cells(records: np.ndarray, layout: HeadLayout, precision: str = INT4) -> np.ndarray:
     """Inverse of cells_to_records (used by PageTable.load)."""
+    if precision == BF16:
+        return _bf16_records_to_cells(records, layout)
     P, H, d = layout.page_tokens, layout.num_kv_heads, layout.head_dim
     T, cb = cell_tokens(layout), cell_bytes(layout)
     n = records.shape[0]
@@ -243,8 +272,6 @@ class PageTable:
             raise ConfigError(f"unknown precision {precision!r}")
         if (budget_bytes is None) == (num_pages is None):
             raise ConfigError("specify exactly one of budget_bytes or num_pages")
-        if precision == BF16:
-            raise UnsupportedConfigError("BF16 pages are not built in this round (SURVEY row f2); use INT4")
         self.layout = layout
         self.precision = precision
         self.budget_bytes = budget_bytes
@@ -254,11 +281,12 @@ class PageTable:
             raise ConfigError(f"num_pages={num_pages} must be >= 0")
         self.num_pages = num_pages
         self.device = torch.device(device) if device is not None else _kernels.device()
-        self.page_bytes = page_bytes(layout)
+        self.page_bytes = page_bytes(layout, precision)
         self.pool = torch.zeros((max(num_pages, 1), self.page_bytes), dtype=torch.uint8, device=self.device)
         self.desc = _lib.KvrPool()
-        _lib.check(_lib.lib().kvr_pool_init(ctypes.byref(self.desc), ctypes.c_void_p(self.pool.data_ptr()),
-                                            num_pages, layout.page_tokens, layout.num_kv_heads, layout.head_dim))
+        init = _lib.lib().kvr_pool_init_bf16 if precision == BF16 else _lib.lib().kvr_pool_init
+        _lib.check(init(ctypes.byref(self.desc), ctypes.c_void_p(self.pool.data_ptr()), num_pages,
+                        layout.page_tokens, layout.num_kv_heads, layout.head_dim))
         assert self.desc.page_bytes == self.page_bytes
         self.flags = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.alloc = PageAllocator(num_pages, layout.page_tokens)
@@ -333,6 +361,8 @@ class PageTable:
     # -- writes -----------------------------------------------------------------
     def _store(self, k: torch.Tensor, v: torch.Tensor, slots: np.ndarray, spec: Optional[RotationSpec],
                exact: bool) -> None:
+        if self.precision == BF16:
+            spec = None  # BF16 pools store the raw vectors and ignore the spec (cache.py:243-246)
         n = k.shape[0]
         slot_t = torch.from_numpy(slots).to(self.device, non_blocking=True)
         rotate = spec is not None
@@ -386,7 +416,7 @@ class PageTable:
         h, d = self.layout.num_kv_heads, self.layout.head_dim
         kt = torch.from_numpy(ks).to(self.device)
         vt = torch.from_numpy(vs).to(self.device)
-        if spec is not None:
+        if spec is not None and self.precision == INT4:
             from .rotation import apply_block_rotation, value_branch_spec
 
             kt = apply_block_rotation(kt.reshape(t * h, d), self.layout, spec).reshape(t, h, d)
@@ -427,6 +457,8 @@ class PageTable:
         slot_mapping.  The caller owns the slot assignment."""
         if slots.dtype != torch.int64 or not slots.is_cuda:
             raise ShapeError("slots must be an int64 CUDA tensor")
+        if self.precision == BF16:
+            spec = None
         rotate = spec is not None
         targets = _lib.KVR_KEYS_ONLY if (rotate and spec.targets is Targets.KEYS_ONLY) else _lib.KVR_KEYS_AND_VALUES
         _lib.check(_lib.lib().kvr_rotate_quantize_store(
@@ -499,9 +531,9 @@ class PageTable:
     def page_records(self, pids) -> np.ndarray:
         """Reference `.kvpg` page records [len(pids), record_bytes] of device pages."""
         if len(pids) == 0:
-            return np.zeros((0, record_bytes(self.layout)), dtype=np.uint8)
+            return np.zeros((0, record_bytes(self.layout, self.precision)), dtype=np.uint8)
         idx = torch.tensor(list(pids), dtype=torch.long, device=self.device)
-        return cells_to_records(self.pool.index_select(0, idx).cpu().numpy(), self.layout)
+        return cells_to_records(self.pool.index_select(0, idx).cpu().numpy(), self.layout, self.precision)
 
     def dump_bytes(self) -> bytes:
         blob = self._header()
@@ -530,11 +562,11 @@ class PageTable:
         table.budget_bytes = header["budget_bytes"]
         allocated = sorted(p for s in header["sequences"].values() for p in s["pages"])
         body = np.frombuffer(raw, dtype=np.uint8, offset=12 + hlen)
-        rb = record_bytes(layout)
+        rb = record_bytes(layout, header["precision"])
         if body.size != len(allocated) * rb:
             raise ConfigError(f"{path}: page payload size mismatch")
         if allocated:
-            cells = records_to_cells(body.reshape(len(allocated), rb), layout)
+            cells = records_to_cells(body.reshape(len(allocated), rb), layout, header["precision"])
             blobs = torch.from_numpy(cells).to(table.device)
             table.pool.index_copy_(0, torch.tensor(allocated, dtype=torch.long, device=table.device), blobs)
         taken = set(allocated)

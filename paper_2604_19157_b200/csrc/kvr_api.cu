@@ -53,7 +53,10 @@ static int to_pool(const kvr_pool* in, Pool& p) {
   p.page_bytes = in->page_bytes;
   p.T = in->cell_tokens;
   p.cell_bytes = in->cell_bytes;
-  if (p.T < 1 || p.P % p.T != 0 || p.cell_bytes < p.T * (p.d + 10))
+  p.prec = in->precision;
+  if (p.prec != KVR_PREC_INT4 && p.prec != KVR_PREC_BF16) return fail(KVR_ERR_ARG, "bad pool precision %d", p.prec);
+  const int64_t need = p.prec == KVR_PREC_BF16 ? 4LL * p.T * p.d : (int64_t)p.T * (p.d + 10);
+  if (p.T < 1 || p.P % p.T != 0 || p.cell_bytes < need)
     return fail(KVR_ERR_SHAPE, "inconsistent pool geometry (P=%d, T=%d, cell=%d)", p.P, p.T, p.cell_bytes);
   return KVR_OK;
 }
@@ -115,7 +118,19 @@ int kvr_pool_init(kvr_pool* pool, void* base, int64_t num_pages, int32_t page_to
   pool->head_dim = head_dim;
   pool->cell_tokens = T;
   pool->cell_bytes = (T * (head_dim + 10) + 15) & ~15;
+  pool->precision = KVR_PREC_INT4;
   const int64_t pb = (int64_t)num_kv_heads * (page_tokens / T) * pool->cell_bytes;
+  if (pb > 0x7fffffff) return fail(KVR_ERR_SHAPE, "page too large");
+  pool->page_bytes = (int32_t)pb;
+  return KVR_OK;
+}
+
+int kvr_pool_init_bf16(kvr_pool* pool, void* base, int64_t num_pages, int32_t page_tokens, int32_t num_kv_heads,
+                       int32_t head_dim) {
+  if (int rc = kvr_pool_init(pool, base, num_pages, page_tokens, num_kv_heads, head_dim)) return rc;
+  pool->precision = KVR_PREC_BF16;
+  pool->cell_bytes = 4 * pool->cell_tokens * head_dim;  // head_dim even -> 16-B multiple when T * d % 4 == 0
+  const int64_t pb = (int64_t)num_kv_heads * (page_tokens / pool->cell_tokens) * pool->cell_bytes;
   if (pb > 0x7fffffff) return fail(KVR_ERR_SHAPE, "page too large");
   pool->page_bytes = (int32_t)pb;
   return KVR_OK;
@@ -198,6 +213,11 @@ int kvr_rotate_quantize_store(const void* k, const void* v, int32_t in_dtype, in
   const int rot_k = rotate ? 1 : 0;
   const int rot_v = (rotate && targets == KVR_KEYS_AND_VALUES) ? 1 : 0;
   cudaStream_t st = (cudaStream_t)stream;
+  if (pl.prec == KVR_PREC_BF16) {  // raw vectors, rotation ignored (cache.py:264-266)
+    if (int rc = kvr_launch_store_bf16(k, v, in_dtype, n_tok, slot_mapping, pl, flags, st))
+      return fail(rc, "rotate_quantize_store (bf16 pool): launch failed (%d)", rc);
+    return check_launch("rotate_quantize_store");
+  }
   int rc = KVR_ERR_UNSUPPORTED;
   if (!exact) rc = kvr_launch_store_fast(k, v, in_dtype, n_tok, slot_mapping, pl, rot_order, rot_k, rot_v, s, has,
                                          flags, st);
@@ -245,6 +265,7 @@ int kvr_paged_decode(const void* q, int32_t q_dtype, const kvr_pool* pool, const
     return fail(KVR_ERR_SHAPE, "max_seq_len=%d exceeds bt_stride=%d pages of %d tokens", max_seq_len, bt_stride, pl.P);
   if (q_dtype != KVR_F32 && q_dtype != KVR_BF16 && q_dtype != KVR_F16)
     return fail(KVR_ERR_ARG, "q dtype %d unsupported (F32/BF16/F16)", q_dtype);
+  if (pl.prec == KVR_PREC_BF16) rotate = 0;  // raw vectors: the query is used as-is (attention.py:67-71)
   if (rotate) {
     if (int rc = check_order(pl.d, rot_order)) return rc;
   } else {
@@ -278,6 +299,19 @@ int kvr_decode_step(const void* q, int32_t q_dtype, const void* new_k, const voi
   if (kv_dtype < KVR_F64 || kv_dtype > KVR_F16) return fail(KVR_ERR_ARG, "bad kv dtype %d", kv_dtype);
   if (q_dtype != KVR_F32 && q_dtype != KVR_BF16 && q_dtype != KVR_F16)
     return fail(KVR_ERR_ARG, "q dtype %d unsupported (F32/BF16/F16)", q_dtype);
+  if (pl.prec == KVR_PREC_BF16) {
+    // BF16 pool: write the raw new rows, then a plain decode with the query as-is
+    if (int rc = kvr_launch_store_bf16(new_k, new_v, kv_dtype, batch, new_slot, pl, flags, (cudaStream_t)stream))
+      return fail(rc, "decode_step (bf16 pool): store failed (%d)", rc);
+    Signs s0;
+    int has0;
+    make_signs(nullptr, pl.d, s0, has0);
+    int rc = kvr_launch_decode(q, q_dtype, pl, block_table, bt_stride, seq_lens, batch, num_q_heads, max_seq_len, 1,
+                               0, 0, s0, has0, out, workspace, workspace_bytes, num_splits, (cudaStream_t)stream);
+    if (rc == KVR_ERR_ARG) return fail(rc, "decode workspace too small");
+    if (rc) return fail(rc, "decode_step (bf16 pool): unsupported geometry (d=%d)", pl.d);
+    return check_launch("decode_step");
+  }
   if (rotate) {
     if (int rc = check_order(pl.d, rot_order)) return rc;
   } else {

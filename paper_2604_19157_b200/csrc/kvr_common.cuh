@@ -24,6 +24,7 @@ struct Pool {
   uint8_t* base;
   int64_t num_pages;
   int32_t P, H, d, page_bytes, T, cell_bytes;
+  int32_t prec;  // KVR_PREC_INT4 | KVR_PREC_BF16
 };
 
 // Address of the cell holding (page, head, slot) and the slot's index in it.
@@ -39,6 +40,9 @@ KVR_DEV int cell_kcode(const Pool& p, int i) { return 8 * p.T + i * (p.d >> 1); 
 KVR_DEV int cell_vcode(const Pool& p, int i) { return 8 * p.T + p.T * (p.d >> 1) + i * (p.d >> 1); }
 KVR_DEV int cell_kzp(const Pool& p, int i) { return 8 * p.T + p.T * p.d + i; }
 KVR_DEV int cell_vzp(const Pool& p, int i) { return 9 * p.T + p.T * p.d + i; }
+
+// BF16 cells: k_bits u16[T][d] | v_bits u16[T][d]
+KVR_DEV int cell_bf16(const Pool& p, int side, int i) { return 2 * p.d * (side * p.T + i); }
 
 KVR_DEV bool sign_bit(const Signs& s, int i) { return (s.w[i >> 5] >> (i & 31)) & 1u; }
 

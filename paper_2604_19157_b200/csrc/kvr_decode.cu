@@ -1134,17 +1134,25 @@ __global__ void decode_generic_kernel(const __grid_constant__ DecodeParams p, co
   for (int t = warp; t < len; t += nw) {
     int ci;
     const uint8_t* cell = token_cell(p, b, t, h, ci);
-    const float ks = *reinterpret_cast<const float*>(cell + cell_kscale(p.pool, ci));
-    const uint8_t kz = cell[cell_kzp(p.pool, ci)];
-    const float vs = *reinterpret_cast<const float*>(cell + cell_vscale(p.pool, ci));
-    const uint8_t vz = cell[cell_vzp(p.pool, ci)];
+    const bool bf = p.pool.prec == KVR_PREC_BF16;  // raw bf16 rows (cache.py:115-118)
+    const uint16_t* kb = reinterpret_cast<const uint16_t*>(cell + cell_bf16(p.pool, 0, ci));
+    const uint16_t* vb = reinterpret_cast<const uint16_t*>(cell + cell_bf16(p.pool, 1, ci));
+    const float ks = bf ? 0.f : *reinterpret_cast<const float*>(cell + cell_kscale(p.pool, ci));
+    const uint8_t kz = bf ? 0 : cell[cell_kzp(p.pool, ci)];
+    const float vs = bf ? 0.f : *reinterpret_cast<const float*>(cell + cell_vscale(p.pool, ci));
+    const uint8_t vz = bf ? 0 : cell[cell_vzp(p.pool, ci)];
     const uint8_t* kc = cell + cell_kcode(p.pool, ci);
     const uint8_t* vc = cell + cell_vcode(p.pool, ci);
     float dot = 0.f;
     for (int k = 0, x = lane; x < d; x += 32, ++k) {
-      const uint8_t byte = kc[x >> 1];
-      const float c = (float)((x & 1) ? (byte >> 4) : (byte & 15));
-      const float kh = (kz == 0xFF) ? ks : ks * (c - (float)kz);
+      float kh;
+      if (bf) {
+        kh = __uint_as_float((uint32_t)kb[x] << 16);
+      } else {
+        const uint8_t byte = kc[x >> 1];
+        const float c = (float)((x & 1) ? (byte >> 4) : (byte & 15));
+        kh = (kz == 0xFF) ? ks : ks * (c - (float)kz);
+      }
       dot += kh * sq[x];
     }
     dot = warp_sum(dot) * scale;
@@ -1152,9 +1160,14 @@ __global__ void decode_generic_kernel(const __grid_constant__ DecodeParams p, co
     const float a = exp2f((m - mn) * LOG2E), pw = exp2f((dot - mn) * LOG2E);
     l = l * a + pw;
     for (int k = 0, x = lane; x < d; x += 32, ++k) {
-      const uint8_t byte = vc[x >> 1];
-      const float c = (float)((x & 1) ? (byte >> 4) : (byte & 15));
-      const float vh = (vz == 0xFF) ? vs : vs * (c - (float)vz);
+      float vh;
+      if (bf) {
+        vh = __uint_as_float((uint32_t)vb[x] << 16);
+      } else {
+        const uint8_t byte = vc[x >> 1];
+        const float c = (float)((x & 1) ? (byte >> 4) : (byte & 15));
+        vh = (vz == 0xFF) ? vs : vs * (c - (float)vz);
+      }
       o[k] = o[k] * a + pw * vh;
     }
     m = mn;
@@ -1374,7 +1387,8 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
   Signs sg = s;
   if (!has) for (auto& x : sg.w) x = 0u;
   if (!pow2) return KVR_ERR_UNSUPPORTED;
-  const bool tma_ok = pool.d == 128 && pool.T == 16 && (p.G == 1 || p.G == 2 || p.G == 4 || p.G == 8) &&
+  const bool tma_ok = pool.prec == KVR_PREC_INT4 && pool.d == 128 && pool.T == 16 &&
+                      (p.G == 1 || p.G == 2 || p.G == 4 || p.G == 8) &&
                       (reinterpret_cast<uintptr_t>(pool.base) & 15) == 0 && (pool.cell_bytes & 15) == 0;
   if (tma_ok) {
     if (splits <= 0) splits = kvr_pick_splits(batch, pool.H, max_len, pool.P);

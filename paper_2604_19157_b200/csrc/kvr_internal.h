@@ -22,6 +22,8 @@ int kvr_launch_block_rotate(const void* x, int in_dtype, void* out, int out_dtyp
 int kvr_launch_store_exact(const void* k, const void* v, int in_dtype, int64_t n_tok, const int64_t* slots,
                            const kvr::Pool& pool, int order, int rot_k, int rot_v, const kvr::Signs& s, int has,
                            uint32_t* flags, cudaStream_t st);
+int kvr_launch_store_bf16(const void* k, const void* v, int in_dtype, int64_t n_tok, const int64_t* slots,
+                          const kvr::Pool& pool, uint32_t* flags, cudaStream_t st);
 int kvr_launch_dequant_pages(const kvr::Pool& pool, const int32_t* bt, int bt_stride, const int32_t* lens, int batch,
                              int max_len, void* k_out, void* v_out, int out_dtype, cudaStream_t st);
 

@@ -256,6 +256,75 @@ __global__ void __launch_bounds__(256) dequant_cells_kernel(Pool pool, const int
   }
 }
 
+// BF16 pool write (cache.py:264-266): one warp per (token, head, side) row; raw
+// values rounded f64 -> f32 (RN) -> bf16 (RNE, cache.py:43-47).  A non-finite row
+// is not written and raises the flag (the reference rejects it, cache.py:453-462).
+KVR_DEV uint16_t f32_to_bf16_rne(float x) {
+  const uint32_t u = __float_as_uint(x);
+  return (uint16_t)((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
+}
+template <typename T>
+__global__ void store_bf16_kernel(const T* k, const T* v, int64_t n_tok, const int64_t* slots, Pool pool,
+                                  uint32_t* flags) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // (token, head, side)
+  const int H = pool.H, d = pool.d;
+  if (row >= 2 * n_tok * H) return;
+  const int side = (int)(row & 1);
+  const int64_t th = row >> 1, tok = th / H;
+  const int head = (int)(th % H);
+  const int64_t slot = slots[tok];
+  const T* src = (side ? v : k) + th * d;
+  float x[8];
+  bool fin = true;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int i = lane + 32 * e;
+    x[e] = i < d ? (float)load_as_f64<T>(src, i) : 0.f;
+    fin &= (bool)isfinite(x[e]);
+  }
+  fin = __all_sync(0xffffffffu, fin);
+  if (!fin) {
+    if (lane == 0 && flags) atomicOr(flags, (uint32_t)KVR_FLAG_NONFINITE);
+    return;
+  }
+  if (slot < 0) return;
+  int ci;
+  uint8_t* cell = cell_of(pool, slot / pool.P, head, (int)(slot % pool.P), ci);
+  uint16_t* dst = reinterpret_cast<uint16_t*>(cell + cell_bf16(pool, side, ci));
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int i = lane + 32 * e;
+    if (i < d) dst[i] = f32_to_bf16_rne(x[e]);
+  }
+}
+
+// BF16 pool flatten-read (cache.py:355-361): bf16 bits -> out dtype, exact.
+template <typename TOut>
+__global__ void dequant_bf16_kernel(Pool pool, const int32_t* bt, int bt_stride, const int32_t* lens, int batch,
+                                    int max_len, TOut* k_out, TOut* v_out) {
+  const int d = pool.d, H = pool.H;
+  const int64_t per_side = (int64_t)batch * max_len * H * d;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < 2 * per_side;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int side = idx >= per_side;
+    int64_t r = side ? idx - per_side : idx;
+    const int e = (int)(r % d);
+    r /= d;
+    const int head = (int)(r % H);
+    r /= H;
+    const int t = (int)(r % max_len);
+    const int b = (int)(r / max_len);
+    if (t >= lens[b]) continue;
+    const int page = bt[(int64_t)b * bt_stride + t / pool.P];
+    int ci;
+    const uint8_t* cell = cell_of(pool, page, head, t % pool.P, ci);
+    const uint16_t bits = reinterpret_cast<const uint16_t*>(cell + cell_bf16(pool, side, ci))[e];
+    const float f = __uint_as_float((uint32_t)bits << 16);
+    (side ? v_out : k_out)[(((int64_t)b * max_len + t) * H + head) * d + e] = (TOut)f;
+  }
+}
+
 }  // namespace kvr
 
 // ============================ host launchers ================================
@@ -357,8 +426,41 @@ int kvr_launch_store_exact(const void* k, const void* v, int in_dtype, int64_t n
   return 0;
 }
 
+int kvr_launch_store_bf16(const void* k, const void* v, int in_dtype, int64_t n_tok, const int64_t* slots,
+                          const Pool& pool, uint32_t* flags, cudaStream_t st) {
+  if (pool.d > 256) return KVR_ERR_UNSUPPORTED;
+  const int64_t rows = 2 * n_tok * pool.H;
+  const int g = (int)((rows * 32 + 255) / 256);
+  switch (in_dtype) {
+    case KVR_F64: store_bf16_kernel<double><<<g, 256, 0, st>>>((const double*)k, (const double*)v, n_tok, slots, pool, flags); break;
+    case KVR_F32: store_bf16_kernel<float><<<g, 256, 0, st>>>((const float*)k, (const float*)v, n_tok, slots, pool, flags); break;
+    case KVR_BF16:
+      store_bf16_kernel<__nv_bfloat16><<<g, 256, 0, st>>>((const __nv_bfloat16*)k, (const __nv_bfloat16*)v, n_tok, slots,
+                                                          pool, flags);
+      break;
+    case KVR_F16:
+      store_bf16_kernel<__half><<<g, 256, 0, st>>>((const __half*)k, (const __half*)v, n_tok, slots, pool, flags);
+      break;
+    default: return KVR_ERR_ARG;
+  }
+  return 0;
+}
+
 int kvr_launch_dequant_pages(const Pool& pool, const int32_t* bt, int bt_stride, const int32_t* lens, int batch,
                              int max_len, void* k_out, void* v_out, int out_dtype, cudaStream_t st) {
+  if (pool.prec == KVR_PREC_BF16) {
+    const int g = grid_for(2LL * batch * max_len * pool.H * pool.d, 256);
+    switch (out_dtype) {
+      case KVR_F64: dequant_bf16_kernel<double><<<g, 256, 0, st>>>(pool, bt, bt_stride, lens, batch, max_len, (double*)k_out, (double*)v_out); break;
+      case KVR_F32: dequant_bf16_kernel<float><<<g, 256, 0, st>>>(pool, bt, bt_stride, lens, batch, max_len, (float*)k_out, (float*)v_out); break;
+      case KVR_BF16:
+        dequant_bf16_kernel<__nv_bfloat16><<<g, 256, 0, st>>>(pool, bt, bt_stride, lens, batch, max_len,
+                                                               (__nv_bfloat16*)k_out, (__nv_bfloat16*)v_out);
+        break;
+      default: return KVR_ERR_ARG;
+    }
+    return 0;
+  }
   int cl = 0;
   while ((16 << cl) < pool.P) ++cl;
   const bool fast = pool.d == 128 && pool.T == 16 && (16 << cl) == pool.P && (pool.cell_bytes & 15) == 0 &&

@@ -25,3 +25,9 @@ def golden():
 def rng():
     return np.random.default_rng(1234)
 
+
+
+@pytest.fixture(scope="session")
+def golden_bf16():
+    with np.load(os.path.join(GOLDEN_DIR, "golden_bf16.npz")) as z:
+        return {k: z[k] for k in z.files}

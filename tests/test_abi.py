@@ -55,7 +55,7 @@ def test_pool_init_layout(libpath):
     assert (pool.cell_tokens, pool.cell_bytes) == (16, 2208)
     assert lib.kvr_pool_init(ctypes.byref(pool), None, 10, 4, 2, 32) == 0
     assert (pool.cell_tokens, pool.cell_bytes, pool.page_bytes) == (4, 176, 2 * 176)
-    assert lib.kvr_abi_version() == 1
+    assert lib.kvr_abi_version() == 2
     assert lib.kvr_decode_workspace_bytes(1, 8, 32, 128, 4) > 0
 
 
