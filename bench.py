@@ -603,8 +603,29 @@ class CpuOracleSequence:
         return time.perf_counter() - t0
 
 
+def _cpu_kernels():
+    """Use the reference's compiled kernels (oracle/_ref) when they were built;
+    returns the cpu_baseline kind."""
+    from oracle import build_ref
+    from oracle import kvrot_oracle as O
+
+    mod = build_ref.load()
+    if mod is None:
+        return "port"
+    O.use_reference_kernels(mod)
+    return "reference"
+
+
+_KIND_NOTE = {"reference": "the reference's compiled kernels (oracle/_ref: _core.pyx built from the reference "
+                           "sources) for rotate / quantize / dequantize + the numpy restatement of "
+                           "attention.decode_step's contraction",
+              "port": "the numpy oracle port of the reference"}
+
+
 def cpu_baseline_c2(seconds: float):
     from oracle import kvrot_oracle as O
+
+    kind = _cpu_kernels()
 
     rng = np.random.default_rng(0)
     signs = O.make_signs(0, 0, D, ORDER)
@@ -616,8 +637,8 @@ def cpu_baseline_c2(seconds: float):
         times.append(seq.step())
     t = float(np.median(times))
     return {"value": round(step_bytes(L + 1) / t / 1e9, 4), "unit": "GB/s", "cores": _cpu_threads(),
-            "kind": "port", "sample": f"{len(times)} full C2 steps (1-token write + decode over {L + 1} tokens) with "
-                                      f"the numpy oracle (numpy/OpenBLAS threads), median {t * 1e3:.1f} ms/step"}
+            "kind": kind, "sample": f"{len(times)} full C2 steps (1-token write + decode over {L + 1} tokens) with "
+                                    f"{_KIND_NOTE[kind]} (numpy/OpenBLAS threads), median {t * 1e3:.1f} ms/step"}
 
 
 def run_reference(args, rank, world):
@@ -627,6 +648,7 @@ def run_reference(args, rank, world):
         return
     from oracle import kvrot_oracle as O
 
+    kind = _cpu_kernels()
     rng = np.random.default_rng(0)
     signs = O.make_signs(0, 0, D, ORDER)
     # bound the run to a few minutes: each step is a full C2 step when affordable,
@@ -651,8 +673,9 @@ def run_reference(args, rank, world):
         "config": {"workload": "BASELINE configs[1] / C2 decode step on the host CPU (reference algorithm)",
                    "ctx": L, "num_q_heads": NQ, "num_kv_heads": H, "head_dim": D, "rot_order": ORDER,
                    "page_tokens": P},
-        "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": _cpu_threads(), "kind": "port",
-                         "sample": f"{args.steps} steps, each a 1-token write + decode over {L + 1} tokens"
+        "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": _cpu_threads(), "kind": kind,
+                         "sample": f"{args.steps} steps, each a 1-token write + decode over {L + 1} tokens, "
+                                   f"{_KIND_NOTE[kind]}"
                                    + ("" if L == CTX else f" (context bounded from {CTX} to fit the time budget)")},
         "e2e": {"value": round(val, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

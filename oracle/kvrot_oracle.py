@@ -125,6 +125,15 @@ def dequantize_rows(packed, scale, zp, logical_len: int) -> np.ndarray:
 
 # --------------------------------------------------------- L1 / L2 method ----
 
+def use_reference_kernels(mod) -> None:
+    """Route this module's L0 kernels through the reference's own compiled ones
+    (oracle/_ref, built by oracle/build_ref.py from _core.pyx, bit-identical to
+    _ref.py per _core.pyx:1-8); used by the CPU-baseline legs of bench.py."""
+    g = globals()
+    for name in ("fwht_rows", "pack_rows", "unpack_rows", "quantize_rows", "dequantize_rows"):
+        g[name] = getattr(mod, name)
+
+
 def make_hadamard(order: int) -> np.ndarray:
     """Orthonormal Sylvester matrix (hadamard.py:33-52): kron-doubling then * 1/sqrt(order)."""
     h = np.ones((1, 1))
