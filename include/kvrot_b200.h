@@ -98,10 +98,12 @@ int kvr_pool_init_bf16(kvr_pool* pool, void* base, int64_t num_pages, int32_t pa
                        int32_t num_kv_heads, int32_t head_dim);
 const char* kvr_last_error(void);
 /* Profiling aid: when non-NULL, decode launches record a per-CTA timeline into
- * `trace` (device buffer of batch * splits * num_kv_heads * 16 u64): [0] the
- * globaltimer (ns) and [1] clock64 at CTA entry, [k >= 2] clock64 at stamp k
- * (2 loop start, 3 loop end, 4/5 CTA merge, 6 partial stored, 7 split counter
- * back, 8 split weights, 9 merged, 10 exit; 0 = not reached).  NULL disables. */
+ * `trace` (device buffer of (batch * splits * num_kv_heads + batch * num_q_heads)
+ * * 16 u64): decode CTA rows first, [0] the globaltimer (ns) and [1] clock64 at
+ * CTA entry, [k >= 2] clock64 at stamp k (2 loop start, 3 loop end, 4/5 CTA
+ * merge, 6 partial stored / cluster barrier, 9 merged, 10 exit; 0 = not
+ * reached); then one row per split-merge CTA (splits > 8): globaltimer at [0]
+ * entry, [1] past the grid-dependency wait, [2] exit.  NULL disables. */
 void kvr_debug_decode_trace(void* trace);
 int kvr_abi_version(void);
 /* Number of SMs of the current device (0 if no device). */

@@ -125,6 +125,20 @@ KVR_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// same with an L2 cache policy (createpolicy): streamed KV cells go in as
+// evict-first so they do not push code, queries and tables out of L2
+KVR_DEV void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+KVR_DEV uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 KVR_DEV void prefetch_tensormap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }

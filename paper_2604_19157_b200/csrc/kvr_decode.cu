@@ -25,6 +25,8 @@
 //    operand with movmatrix.trans (no shared memory round trip);
 //  * per-split (lse, o) partials go to a workspace; the last CTA of a
 //    (sequence, kv head) merges them and applies the inverse rotation.
+#include <cstdlib>
+
 #include "kvr_common.cuh"
 #include "kvr_internal.h"
 
@@ -53,6 +55,10 @@ struct DecodeParams {
   const int64_t* new_slot;  // [B] slot id of the appended token (it is the last of seq_lens[b])
   uint32_t* flags;
   unsigned long long* trace;  // optional: per CTA 8 globaltimer stamps (ns), see kvr_debug_decode_trace
+  int pre_groups;   // ring groups requested before griddepcontrol.wait (<= NSTG)
+  int merge_late;   // decode_merge_kernel releases its dependents after its loads
+  int evict_first;  // KV cells are streamed with an L2 evict-first policy
+  int merge_inline;   // splits > 1 without a cluster: the last CTA merges (ws_cnt counters)
 };
 
 KVR_DEV unsigned long long clk64() {
@@ -281,6 +287,7 @@ constexpr int NWARPS = 16;       // one CTA per SM, 4 warps per SM sub-partition
 constexpr int CELL = 2208;       // one cell: T = 16 tokens of one head, d = 128
 constexpr int RING_CELLS = 4;    // cells in flight per warp (NSTG stages of C cells)
 constexpr int MAX_SPLITS = 256;
+constexpr int MERGE_INLINE_MAX = 32;  // up to this many splits the last CTA merges them inline
 
 // smem: ring [NWARPS][RING_CELLS][CELL] | bars [NWARPS*RING_CELLS + 1] | q fragments 4 KB | out 4 KB | misc
 constexpr int SM_BARS = NWARPS * RING_CELLS * CELL;
@@ -321,6 +328,40 @@ KVR_DEV void load_cell_rest(CellFrag& f, const uint8_t* st, int r, int i) {
   f.vz1 = st[2192 + r + 8];
 }
 
+// One q head's final output (warp-wide, lane owns dims 4l..4l+3): the inverse
+// rotation of the value branch (o @ H_blk @ diag(signs)) as an fp32 butterfly in
+// registers / shuffles, then a 16-B store per lane.  `row` is o in natural order.
+template <int ORDER>
+KVR_DEV void emit_head(const DecodeParams& p, const Signs& signs, int b, int h, int j, const float* row, int lane) {
+  float x[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) x[u] = row[4 * lane + u];
+  if (p.rotate && p.rot_v) {
+    const float a0 = x[0] + x[1], a1 = x[0] - x[1], a2 = x[2] + x[3], a3 = x[2] - x[3];
+    x[0] = a0 + a2;
+    x[1] = a1 + a3;
+    x[2] = a0 - a2;
+    x[3] = a1 - a3;
+#pragma unroll
+    for (int k = 0; (4 << k) < ORDER; ++k) {
+      const bool upper = (lane >> k) & 1;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float o = __shfl_xor_sync(0xffffffffu, x[u], 1 << k);
+        x[u] = upper ? o - x[u] : x[u] + o;
+      }
+    }
+    const float inv = (float)(1.0 / sqrt((double)ORDER));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      x[u] *= inv;
+      if (p.has_signs && sign_bit(signs, 4 * lane + u)) x[u] = -x[u];
+    }
+  }
+  float4* dst = reinterpret_cast<float4*>(p.out + ((int64_t)b * p.nq + (int64_t)h * p.G + j) * 128) + lane;
+  *dst = make_float4(x[0], x[1], x[2], x[3]);
+}
+
 // K2+K3.  grid (kv head, split, sequence); NWARPS warps, one CTA per SM.  With
 // APPEND the last warp writes the step's new K/V token (bit-exact f64) while the
 // other DW warps stream their tiles through private rings of NSTG stages of C
@@ -355,6 +396,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   if (p.trace && threadIdx.x == 0) {
     p.trace[cta_id * 16 + 0] = gtimer();
     p.trace[cta_id * 16 + 1] = clk64();
+    for (int k = 2; k < 16; ++k) p.trace[cta_id * 16 + k] = 0ull;
   }
 
   // ---- prologue (independent of the previous grid): split range from max_len,
@@ -413,6 +455,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
       wnext = page_window(win_idx + 1);
     }
   };
+  const uint64_t pol = policy_evict_first();
   // group k -> stage k % NSTG: one expect_tx, one bulk copy per valid cell
   auto issue = [&](int k) {
     advance_to(C * k);
@@ -429,7 +472,12 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
       mbar_expect_tx(&bar_w[s], (uint32_t)(nc * CELL));
 #pragma unroll
       for (int c = 0; c < C; ++c)
-        if (c < nc) bulk_g2s(ring_w + s * STG + c * CELL, src[c], (uint32_t)CELL, &bar_w[s]);
+        if (c < nc) {
+          if (p.evict_first)
+            bulk_g2s_hint(ring_w + s * STG + c * CELL, src[c], (uint32_t)CELL, &bar_w[s], pol);
+          else
+            bulk_g2s(ring_w + s * STG + c * CELL, src[c], (uint32_t)CELL, &bar_w[s]);
+        }
     }
   };
   auto group_last = [&](int k) { return min(tile_of(C * k) + C, hi) - 1; };
@@ -437,10 +485,11 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   // the previous grid (programmatic dependent launch overlaps them with its tail)
   int k0 = 0;
 #pragma unroll 1
-  for (; k0 < NSTG && k0 < my_groups && group_last(k0) < guard; ++k0) issue(k0);
+  for (; k0 < NSTG && k0 < p.pre_groups && k0 < my_groups && group_last(k0) < guard; ++k0) issue(k0);
 
   pdl_wait();  // q, the new token, the workspace and recent pages may come from the previous grid
   pdl_launch_dependents();
+  KVR_STAMP(11);  // past the grid-dependency wait
   if (threadIdx.x == 0 && len_raw > p.max_len && p.flags && h == 0 && split == 0)
     atomicOr(p.flags, KVR_FLAG_LEN_OVERFLOW);
 
@@ -449,6 +498,10 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       qx[u] = load_q(p.q, p.q_dtype, ((int64_t)b * p.nq + (int64_t)h * G + warp) * 128 + 4 * lane + u);
+  }
+  if (p.trace) {  // q landed
+    asm volatile("" ::"f"(qx[0]), "f"(qx[1]), "f"(qx[2]), "f"(qx[3]));
+    KVR_STAMP(13);
   }
 #pragma unroll 1
   for (int k = k0; k < NSTG && k < my_groups; ++k) issue(k);
@@ -555,6 +608,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   
     }
   }
+  KVR_STAMP(12);  // warp 0's query prep done
   __syncthreads();
   // query B fragments: registers for one 8-column tile; with two (G = 8) they stay
   // in shared memory (one LDS.64 per k-step) to keep the loop inside 128 registers
@@ -933,76 +987,76 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
       }
     }
     __syncthreads();
-    if (warp < G && warp % S == rank) {
-      float x[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) x[u] = omerge[warp * 128 + 4 * lane + u];
-      if (p.rotate && p.rot_v) {
-        const float a0 = x[0] + x[1], a1 = x[0] - x[1], a2 = x[2] + x[3], a3 = x[2] - x[3];
-        x[0] = a0 + a2;
-        x[1] = a1 + a3;
-        x[2] = a0 - a2;
-        x[3] = a1 - a3;
-#pragma unroll
-        for (int k = 0; (4 << k) < ORDER; ++k) {
-          const bool upper = (lane >> k) & 1;
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float o = __shfl_xor_sync(0xffffffffu, x[u], 1 << k);
-            x[u] = upper ? o - x[u] : x[u] + o;
-          }
-        }
-        const float inv = (float)(1.0 / sqrt((double)ORDER));
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          x[u] *= inv;
-          if (p.has_signs && sign_bit(signs, 4 * lane + u)) x[u] = -x[u];
-        }
-      }
-      float4* dst = reinterpret_cast<float4*>(p.out + ((int64_t)b * p.nq + (int64_t)h * G + warp) * 128) + lane;
-      *dst = make_float4(x[0], x[1], x[2], x[3]);
-    }
+    if (warp < G && warp % S == rank) emit_head<ORDER>(p, signs, b, h, warp, omerge + warp * 128, lane);
     KVR_STAMP(9);  // merged + stored
     cluster_sync_relaxed();  // every CTA's partial stays readable until all merges are done
     KVR_STAMP(10);
     return;
   }
-  if (p.splits > 1) {  // the partial is final: decode_merge_kernel (next in the stream) merges
+  if (p.splits > 1 && !p.merge_inline) {  // the partial is final: decode_merge_kernel (next in the stream) merges
     KVR_STAMP(6);
     return;
   }
-  __syncthreads();
-  // ---- output: inverse rotation of the value branch (o @ H_blk @ diag(signs)),
-  // one warp per q head, fp32 butterfly in registers / shuffles
-  if (warp < G) {
-    float x[4];
+  if (p.splits > 1) {
+    // ---- inline split merge: the last CTA of (sequence, kv head) to publish its
+    // partial merges all of them (one L2 round trip: the lse into smem while every
+    // thread loads its dims' partials) and resets the counter for the next launch
+    __syncthreads();  // every thread's partial stores precede thread 0's release
+    int* s_last = reinterpret_cast<int*>(s_sumq + 56);
+    if (threadIdx.x == 0) {
+      // release the CTA's partial (ordered before by the barrier), acquire the others'
+      uint32_t prev;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                   : "=r"(prev)
+                   : "l"(p.ws_cnt + (int64_t)b * H + h)
+                   : "memory");
+      *s_last = prev == (uint32_t)(p.splits - 1);
+    }
+    __syncthreads();
+    KVR_STAMP(6);  // partial stored, counter back
+    if (!*s_last) return;
+    const int S = p.splits;
+    float* s_l = reinterpret_cast<float*>(sm);            // [8][MERGE_INLINE_MAX] split lse
+    float* omerge = s_l + 8 * MERGE_INLINE_MAX;            // [8][128]
+    for (int x = threadIdx.x; x < G * S; x += blockDim.x) {
+      const int j = x / S, sp = x - j * S;
+      s_l[j * MERGE_INLINE_MAX + sp] = __ldcg(p.ws_lse + hbase + (int64_t)sp * 8 + j);
+    }
+    for (int x0 = 0; x0 < G * 128; x0 += blockDim.x) {
+      const int x = x0 + threadIdx.x, j = x >> 7, dd = x & 127;
+      float ov[MERGE_INLINE_MAX];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) x[u] = obuf[warp * 128 + 4 * lane + u];
-    if (p.rotate && p.rot_v) {
-      const float a0 = x[0] + x[1], a1 = x[0] - x[1], a2 = x[2] + x[3], a3 = x[2] - x[3];
-      x[0] = a0 + a2;
-      x[1] = a1 + a3;
-      x[2] = a0 - a2;
-      x[3] = a1 - a3;
+      for (int sp = 0; sp < MERGE_INLINE_MAX; ++sp)
+        ov[sp] = (sp < S && j < G) ? __ldcg(p.ws_o + (hbase + (int64_t)sp * 8 + j) * 128 + dd) : 0.f;
+      __syncthreads();  // s_l visible (and, on a second pass, omerge of the first)
+      if (j < G) {
+        const float* lj = s_l + j * MERGE_INLINE_MAX;
+        float mx = -INFINITY;
 #pragma unroll
-      for (int k = 0; (4 << k) < ORDER; ++k) {
-        const bool upper = (lane >> k) & 1;
+        for (int sp = 0; sp < MERGE_INLINE_MAX; ++sp)
+          if (sp < S) mx = fmaxf(mx, lj[sp]);
+        float tot = 0.f, ot = 0.f;
+        if (mx != -INFINITY) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float o = __shfl_xor_sync(0xffffffffu, x[u], 1 << k);
-          x[u] = upper ? o - x[u] : x[u] + o;
+          for (int sp = 0; sp < MERGE_INLINE_MAX; ++sp)
+            if (sp < S && lj[sp] != -INFINITY) {
+              const float w = ex2f(lj[sp] - mx);
+              tot += w;
+              ot += w * ov[sp];
+            }
         }
-      }
-      const float inv = (float)(1.0 / sqrt((double)ORDER));
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        x[u] *= inv;
-        if (p.has_signs && sign_bit(signs, 4 * lane + u)) x[u] = -x[u];
+        omerge[j * 128 + dd] = tot > 0.f ? ot / tot : 0.f;
       }
     }
-    float4* dst = reinterpret_cast<float4*>(p.out + ((int64_t)b * p.nq + (int64_t)h * G + warp) * 128) + lane;
-    *dst = make_float4(x[0], x[1], x[2], x[3]);
+    __syncthreads();
+    if (warp < G) emit_head<ORDER>(p, signs, b, h, warp, omerge + warp * 128, lane);
+    if (threadIdx.x == 0) p.ws_cnt[(int64_t)b * H + h] = 0u;  // read again only after this grid completes
+    KVR_STAMP(9);
+    return;
   }
+  __syncthreads();
+  // ---- output: one warp per q head
+  if (warp < G) emit_head<ORDER>(p, signs, b, h, warp, obuf + warp * 128, lane);
   KVR_STAMP(10);
 }
 
@@ -1022,8 +1076,14 @@ __global__ void __launch_bounds__(MERGE_THREADS)
   const int S = p.splits, H = p.pool.H;
   const int dd = tid & 127, sl = tid >> 7;
   const int64_t hbase = (((int64_t)b * H + h) * S) * 8;
+  // trace rows after the decode grid's: [0] entry, [1] past the wait, [2] exit (globaltimer)
+  unsigned long long* tr = nullptr;
+  if (p.trace && tid == 0)
+    tr = p.trace + ((int64_t)gridDim.z * S * H + ((int64_t)b * H + h) * gridDim.x + j) * 16;
+  if (tr) tr[0] = gtimer();
   pdl_wait();
-  pdl_launch_dependents();
+  if (!p.merge_late) pdl_launch_dependents();
+  if (tr) tr[1] = gtimer();
   // o-values of this thread's splits s = sl, sl + 4, ... (first 16 preloaded with the lse)
   float ov[16];
 #pragma unroll
@@ -1036,6 +1096,8 @@ __global__ void __launch_bounds__(MERGE_THREADS)
   float m = warp_max(l);
   if (lane == 0) s_red[warp] = m;
   __syncthreads();
+  if (tr) tr[3] = gtimer();
+  if (p.merge_late) pdl_launch_dependents();
   m = s_red[lane & 15];
 #pragma unroll
   for (int o = 8; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -1091,6 +1153,7 @@ __global__ void __launch_bounds__(MERGE_THREADS)
     float4* dst = reinterpret_cast<float4*>(p.out + ((int64_t)b * p.nq + (int64_t)h * p.G + j) * 128) + lane;
     *dst = make_float4(x[0], x[1], x[2], x[3]);
   }
+  if (tr) tr[2] = gtimer();
 }
 
 // Generic (any head_dim <= 256, any group) CUDA-core decode: one CTA per
@@ -1335,8 +1398,11 @@ template <int NT, int ORDER, bool APP>
 static int launch_sel(dim3 grid, size_t smem, cudaStream_t st, const DecodeParams& p, const Signs& sg) {
   if (p.use_cluster && cluster_ok<NT, ORDER, APP>((int)grid.y, smem))
     return launch_one<NT, ORDER, APP, true>(grid, smem, st, p, sg);
-  if (int rc = launch_one<NT, ORDER, APP, false>(grid, smem, st, p, sg)) return rc;
-  return p.splits > 1 ? launch_merge<ORDER>(p, sg, st) : 0;
+  // KVR_DEBUG_PART (profiling only): 1 = decode grid alone, 2 = merge grid alone
+  static const int part = getenv("KVR_DEBUG_PART") ? atoi(getenv("KVR_DEBUG_PART")) : 0;
+  if (part != 2)
+    if (int rc = launch_one<NT, ORDER, APP, false>(grid, smem, st, p, sg)) return rc;
+  return (p.splits > 1 && !p.merge_inline && part != 1) ? launch_merge<ORDER>(p, sg, st) : 0;
 }
 
 template <int NT, bool APP>
@@ -1380,6 +1446,13 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
   p.flags = flags;
   p.trace = g_trace;
   p.max_len = max_len;
+  static const int env_pre = getenv("KVR_PREWAIT") ? atoi(getenv("KVR_PREWAIT")) : 1 << 20;
+  static const int env_ml = getenv("KVR_MERGE_LATE") ? atoi(getenv("KVR_MERGE_LATE")) : 0;
+  p.pre_groups = env_pre;
+  p.merge_late = env_ml;
+  static const int env_ef = getenv("KVR_EVICT_FIRST") ? atoi(getenv("KVR_EVICT_FIRST")) : 1;
+  p.evict_first = env_ef;
+  static const int env_mi = getenv("KVR_MERGE_INLINE") ? atoi(getenv("KVR_MERGE_INLINE")) : 1;
   int l2 = 0;
   while ((1 << l2) < pool.P) ++l2;
   const bool pow2 = (1 << l2) == pool.P;
@@ -1412,6 +1485,7 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
 #else
     p.use_cluster = 0;
 #endif
+    p.merge_inline = env_mi && !p.use_cluster && splits > 1 && splits <= MERGE_INLINE_MAX;
     if (new_slot)
       return p.G == 8 ? launch_tma<2, true>(p, sg, grid, smem, ord, st) : launch_tma<1, true>(p, sg, grid, smem, ord, st);
     return p.G == 8 ? launch_tma<2, false>(p, sg, grid, smem, ord, st) : launch_tma<1, false>(p, sg, grid, smem, ord, st);

@@ -1,9 +1,12 @@
-"""Per-CTA timeline of C2 decode launches (globaltimer stamps) -> gpurun_out/trace.txt.
+"""Per-CTA timeline of C2 decode launches (globaltimer/clock64 stamps) -> gpurun_out/trace.txt.
 
-    python tools/trace_decode.py [ctx] [splits ...]
+    python tools/trace_decode.py [ctx] [splits ...] [--step] [--steady]
 
-Four independent 32k-token tables (> 126 MB L2 in total) rotate so the traced
-launch reads its KV from HBM, like the bench."""
+Four independent tables (> 126 MB L2 in total) rotate so the traced launch reads
+its KV from HBM, like the bench.  Default: the traced launch starts on an idle
+GPU.  --steady: back-to-back launches, the last one traced,
+so its start overlaps the previous launch's tail as in the bench's graph replay
+(traced inside a CUDA graph of 16 steps; the last one's rows are kept)."""
 import ctypes
 import os
 import sys
@@ -17,6 +20,7 @@ from paper_2604_19157_b200 import DecodePlan, HeadLayout, PageTable, RotationSpe
 H, G, D = int(os.environ.get("TR_H", "8")), int(os.environ.get("TR_G", "4")), 128
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 STEP = "--step" in sys.argv  # fused append + decode (kvr_decode_step)
+STEADY = "--steady" in sys.argv
 split_list = [int(x) for x in sys.argv[2:] if not x.startswith("--")] or [0]
 dev = torch.device("cuda")
 layout = HeadLayout(num_q_heads=H * G, num_kv_heads=H, head_dim=D, rot_order=128, page_tokens=16)
@@ -47,32 +51,58 @@ def run(plan, k):
     else:
         plan.run(q, spec)
 
+
 out_lines = []
-names = {2: "loop start", 3: "loop end", 4: "M published", 5: "warp partials", 6: "partial stored", 7: "counter back",
-         8: "split weights", 9: "merged", 10: "exit"}
+names = {11: "past wait", 13: "q landed", 12: "q prep done", 2: "loop start", 3: "loop end", 4: "M published", 5: "warp partials", 6: "partial stored",
+         9: "merged", 10: "exit"}
 MHZ = float(os.environ.get("SM_MHZ", "1965"))
+lib = _lib.lib()
 for splits in split_list:
     plans = [DecodePlan(t, [0], num_splits=splits) for t in tables]
     S = plans[0].splits
-    tr = torch.zeros(S * H * 16, dtype=torch.int64, device=dev)
+    nd = S * H
+    tr = torch.zeros((nd + H * G) * 16, dtype=torch.int64, device=dev)
     for k, p in enumerate(plans):
         run(p, k)
     torch.cuda.synchronize()
-    for k in range(3):
-        run(plans[k], k)
-    _lib.lib().kvr_debug_decode_trace(ctypes.c_void_p(tr.data_ptr()))
-    run(plans[3], 3)
+    if STEADY:  # a CUDA graph of 16 back-to-back steps, traced: the last step's rows survive
+        lib.kvr_debug_decode_trace(ctypes.c_void_p(tr.data_ptr()))
+        gt = torch.cuda.CUDAGraph()
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            with torch.cuda.graph(gt, stream=st):
+                for k in range(16):
+                    run(plans[k % 4], k % 4)
+        torch.cuda.current_stream().wait_stream(st)
+        torch.cuda.synchronize()
+        gt.replay()
+    else:
+        for k in range(3):
+            run(plans[k], k)
+        lib.kvr_debug_decode_trace(ctypes.c_void_p(tr.data_ptr()))
+        run(plans[3], 3)
     torch.cuda.synchronize()
-    _lib.lib().kvr_debug_decode_trace(None)
-    raw = tr.view(S * H, 16).cpu().numpy().astype(np.float64)
-    g0 = raw[:, 0] - raw[:, 0].min()
-    out_lines.append(f"== ctx {L} splits {S} ctas {raw.shape[0]} {'fused step' if STEP else 'decode'} (HBM-cold launch; clock64 at {MHZ:.0f} MHz)")
+    lib.kvr_debug_decode_trace(None)
+    raw_all = tr.view(-1, 16).cpu().numpy().astype(np.float64)
+    raw = raw_all[:nd]
+    t0 = raw[:, 0].min()
+    g0 = raw[:, 0] - t0
+    out_lines.append(f"== ctx {L} splits {S} ctas {nd} {'fused step' if STEP else 'decode'} "
+                     f"({'steady: back-to-back launches' if STEADY else 'launch on an idle GPU'}; HBM-cold KV; "
+                     f"clock64 at {MHZ:.0f} MHz; us from the first CTA's entry)")
     out_lines.append(f"{'start':16s}: min {g0.min() / 1e3:6.2f} med {np.median(g0) / 1e3:6.2f} max {g0.max() / 1e3:6.2f} us")
     for k, nm in names.items():
         ok = raw[:, k] > 0
         if ok.any():
             t = (g0[ok] + (raw[ok, k] - raw[ok, 1]) * 1e3 / MHZ) / 1e3
             out_lines.append(f"{nm:16s}: n {ok.sum():4d} min {t.min():6.2f} med {np.median(t):6.2f} max {t.max():6.2f} us")
+    mg = raw_all[nd:]
+    mg = mg[mg[:, 0] > 0]
+    for k, nm in ((0, "merge entry"), (1, "merge past wait"), (3, "merge lse in"), (2, "merge exit")):
+        if len(mg):
+            t = (mg[:, k] - t0) / 1e3
+            out_lines.append(f"{nm:16s}: n {len(mg):4d} min {t.min():6.2f} med {np.median(t):6.2f} max {t.max():6.2f} us")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     g = torch.cuda.CUDAGraph()
     s = torch.cuda.Stream()
@@ -91,5 +121,5 @@ for splits in split_list:
     torch.cuda.synchronize()
     out_lines.append(f"graph time per launch (HBM, back to back): {e0.elapsed_time(e1) / 256 * 1000:.2f} us")
 os.makedirs("gpurun_out", exist_ok=True)
-open("gpurun_out/trace.txt", "w").write("\n".join(out_lines) + "\n")
+open("gpurun_out/trace.txt", "a").write("\n".join(out_lines) + "\n")
 print("\n".join(out_lines))
