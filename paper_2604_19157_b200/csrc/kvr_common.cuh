@@ -49,6 +49,17 @@ KVR_DEV bool sign_bit(const Signs& s, int i) { return (s.w[i >> 5] >> (i & 31)) 
 // ---- f64 reference arithmetic (_ref.py:16-19) ------------------------------
 KVR_DEV double round_half_away(double t) { return copysign(floor(fabs(t) + 0.5), t); }
 
+// a / b correctly rounded (IEEE double, round to nearest) from rb = RN(1 / b):
+// q0 = RN(a rb) is within an ulp of a / b, the fma residual a - b q0 is exact and
+// RN(q0 + r rb) is RN(a / b) (Markstein) while nothing over/underflows.  b is an
+// f32 value or 15 here, so its significand is never all ones.  Results that
+// leave the safe range (or NaN from an infinite b) take the IEEE division.
+KVR_DEV double div_rn_recip(double a, double b, double rb) {
+  const double q0 = a * rb;
+  const double q = fma(fma(-q0, b, a), rb, q0);
+  return fabs(q) < 0x1p1000 ? q : a / b;
+}
+
 // ---- f32x2 packed arithmetic (FADD2 / FFMA2 on sm_100a) --------------------
 KVR_DEV unsigned long long pk(float a, float b) {
   unsigned long long r;

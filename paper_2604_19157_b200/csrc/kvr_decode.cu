@@ -145,101 +145,143 @@ KVR_DEV void cta_fwht_rows(float* s, int rows) {
   __syncthreads();
 }
 
-// ---- the fused decode-step append: one token's K or V row of head h, computed
-// reference-exactly in f64 by one warp (lane l owns elements 4l..4l+3): sign
+// ---- the fused decode-step append: one token's K and V rows of head h, computed
+// reference-exactly in f64 by one warp (lane l owns elements 4l..4l+3 of both
+// rows; the two rows are interleaved for instruction-level parallelism): sign
 // flip, butterfly stages half = 1, 2 in registers and 4..ORDER/2 via shuffles
 // (pairs combined lowest index first, exactly _ref.fwht_rows), * 1/sqrt(ORDER),
 // then _ref.quantize_rows (_ref.py:22-40, 57-80) and the paged store.
+// Returns the stored-space (rotated) dequantised elements of lane l in deq[side]
+// (dims 4l..4l+3); a non-finite row is flagged, not written, and reads as 0.
 template <int ORDER>
-// returns the stored-space (rotated) dequantised row element of lane l in
-// deq[0..3] (dims 4l..4l+3); false when the row was not finite (not written)
-KVR_DEV bool append_row_exact(const DecodeParams& p, const Signs& sg, int b, int h, int side, float (&deq)[4]) {
+KVR_DEV void append_rows_exact(const DecodeParams& p, const Signs& sg, int b, int h, float (&deq)[2][4],
+                               unsigned long long* tr = nullptr) {
   const int lane = threadIdx.x & 31;
   const int64_t slot = p.new_slot[b];
   const int64_t base = ((int64_t)b * p.pool.H + h) * 128 + 4 * lane;
-  const void* src = side ? p.new_v : p.new_k;
-  double x[4];
-  bool fin = true;
+  double x[2][4];
+  bool fin[2];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    if (p.new_dtype == KVR_BF16) x[u] = (double)__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(src)[base + u]);
-    else if (p.new_dtype == KVR_F16) x[u] = (double)__half2float(reinterpret_cast<const __half*>(src)[base + u]);
-    else if (p.new_dtype == KVR_F32) x[u] = (double)reinterpret_cast<const float*>(src)[base + u];
-    else x[u] = reinterpret_cast<const double*>(src)[base + u];
-    fin &= (bool)isfinite(x[u]);
-  }
-  fin = __all_sync(0xffffffffu, fin);
-  if (!fin) {
-    if (lane == 0 && p.flags) atomicOr(p.flags, (uint32_t)KVR_FLAG_NONFINITE);
-    deq[0] = deq[1] = deq[2] = deq[3] = 0.f;
-    return false;
-  }
-  const bool rot = side ? (p.rotate && p.rot_v) : p.rotate;
-  if (rot) {
-    if (p.has_signs) {
+  for (int sd = 0; sd < 2; ++sd) {
+    const void* src = sd ? p.new_v : p.new_k;
+    fin[sd] = true;
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (sign_bit(sg, 4 * lane + u)) x[u] = x[u] * -1.0;
+    for (int u = 0; u < 4; ++u) {
+      if (p.new_dtype == KVR_BF16) x[sd][u] = (double)__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(src)[base + u]);
+      else if (p.new_dtype == KVR_F16) x[sd][u] = (double)__half2float(reinterpret_cast<const __half*>(src)[base + u]);
+      else if (p.new_dtype == KVR_F32) x[sd][u] = (double)reinterpret_cast<const float*>(src)[base + u];
+      else x[sd][u] = reinterpret_cast<const double*>(src)[base + u];
+      fin[sd] &= (bool)isfinite(x[sd][u]);
     }
-    double a0 = x[0] + x[1], a1 = x[0] - x[1], a2 = x[2] + x[3], a3 = x[2] - x[3];  // half = 1
-    x[0] = a0 + a2;                                                               // half = 2
-    x[1] = a1 + a3;
-    x[2] = a0 - a2;
-    x[3] = a1 - a3;
-#pragma unroll
-    for (int k = 0; (4 << k) < ORDER; ++k) {  // half = 4 << k: partner lane = lane ^ (1 << k)
-      const bool upper = (lane >> k) & 1;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const double o = __shfl_xor_sync(0xffffffffu, x[u], 1 << k);
-        x[u] = upper ? o - x[u] : x[u] + o;
-      }
-    }
-    const double inv = 1.0 / sqrt((double)ORDER);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) x[u] = x[u] * inv;
-  }
-  double mn = x[0], mx = x[0];
-#pragma unroll
-  for (int u = 1; u < 4; ++u) {
-    mn = x[u] < mn ? x[u] : mn;
-    mx = x[u] > mx ? x[u] : mx;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double a = __shfl_xor_sync(0xffffffffu, mn, o), c = __shfl_xor_sync(0xffffffffu, mx, o);
-    mn = a < mn ? a : mn;
-    mx = c > mx ? c : mx;
   }
   int ci;
   uint8_t* cell = cell_of(p.pool, slot >> p.log2P, h, (int)(slot & ((1 << p.log2P) - 1)), ci);
-  const float s32 = (float)((mx - mn) / 15.0);
-  uint32_t bytes2 = 0u, zpv = 0xFFu;
-  float scv = (float)mn;
-  if (s32 != 0.0f) {
-    const double s64 = (double)s32;
-    double z = round_half_away(-mn / s64);
-    z = z < 0.0 ? 0.0 : (z > 15.0 ? 15.0 : z);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      double q = round_half_away(x[u] / s64) + z;
-      q = q < 0.0 ? 0.0 : (q > 15.0 ? 15.0 : q);
-      bytes2 |= (uint32_t)q << (4 * u);
+  for (int sd = 0; sd < 2; ++sd) {
+    fin[sd] = __all_sync(0xffffffffu, fin[sd]);
+    if (tr && sd == 0) tr[14] = clk64();  // rows landed
+    if (!fin[sd] && lane == 0 && p.flags) atomicOr(p.flags, (uint32_t)KVR_FLAG_NONFINITE);
+  }
+  const bool rot[2] = {p.rotate != 0, p.rotate && p.rot_v};
+#pragma unroll
+  for (int sd = 0; sd < 2; ++sd)
+    if (rot[sd] && p.has_signs) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (sign_bit(sg, 4 * lane + u)) x[sd][u] = x[sd][u] * -1.0;
     }
-    scv = s32;
-    zpv = (uint32_t)z;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) deq[u] = (float)((double)s32 * (double)((int)((bytes2 >> (4 * u)) & 15u) - (int)zpv));
-  } else {
-    deq[0] = deq[1] = deq[2] = deq[3] = scv;  // sentinel row: the offset
+  for (int sd = 0; sd < 2; ++sd)
+    if (rot[sd]) {
+      const double a0 = x[sd][0] + x[sd][1], a1 = x[sd][0] - x[sd][1];  // half = 1
+      const double a2 = x[sd][2] + x[sd][3], a3 = x[sd][2] - x[sd][3];
+      x[sd][0] = a0 + a2;                                                  // half = 2
+      x[sd][1] = a1 + a3;
+      x[sd][2] = a0 - a2;
+      x[sd][3] = a1 - a3;
+    }
+#pragma unroll
+  for (int k = 0; (4 << k) < ORDER; ++k) {  // half = 4 << k: partner lane = lane ^ (1 << k)
+    const bool upper = (lane >> k) & 1;
+#pragma unroll
+    for (int sd = 0; sd < 2; ++sd)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double o = __shfl_xor_sync(0xffffffffu, x[sd][u], 1 << k);
+        if (rot[sd]) x[sd][u] = upper ? o - x[sd][u] : x[sd][u] + o;
+      }
   }
-  *reinterpret_cast<uint16_t*>(cell + (side ? cell_vcode(p.pool, ci) : cell_kcode(p.pool, ci)) + 2 * lane) =
-      (uint16_t)bytes2;
-  if (lane == 0) {
-    *reinterpret_cast<float*>(cell + (side ? cell_vscale(p.pool, ci) : cell_kscale(p.pool, ci))) = scv;
-    cell[side ? cell_vzp(p.pool, ci) : cell_kzp(p.pool, ci)] = (uint8_t)zpv;
+  if (tr) tr[15] = clk64();  // rotated
+  const double inv = 1.0 / sqrt((double)ORDER);
+  double mn[2], mx[2];
+#pragma unroll
+  for (int sd = 0; sd < 2; ++sd) {
+    if (rot[sd]) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[sd][u] = x[sd][u] * inv;
+    }
+    mn[sd] = x[sd][0];
+    mx[sd] = x[sd][0];
+#pragma unroll
+    for (int u = 1; u < 4; ++u) {
+      mn[sd] = x[sd][u] < mn[sd] ? x[sd][u] : mn[sd];
+      mx[sd] = x[sd][u] > mx[sd] ? x[sd][u] : mx[sd];
+    }
   }
-  return true;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int sd = 0; sd < 2; ++sd) {
+      const double a = __shfl_xor_sync(0xffffffffu, mn[sd], o), c = __shfl_xor_sync(0xffffffffu, mx[sd], o);
+      mn[sd] = a < mn[sd] ? a : mn[sd];
+      mx[sd] = c > mx[sd] ? c : mx[sd];
+    }
+#pragma unroll
+  for (int sd = 0; sd < 2; ++sd) {
+    // the reference's f64 divisions, each correctly rounded (div_rn_recip): one
+    // reciprocal per row instead of six divisions
+    const float s32 = (float)div_rn_recip(mx[sd] - mn[sd], 15.0, 1.0 / 15.0);
+    uint32_t bytes2 = 0u, zpv = 0xFFu;
+    float scv = (float)mn[sd];
+    if (s32 != 0.0f) {
+      const double s64 = (double)s32;
+      const double rs = 1.0 / s64;
+      double z = round_half_away(div_rn_recip(-mn[sd], s64, rs));
+      z = z < 0.0 ? 0.0 : (z > 15.0 ? 15.0 : z);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        double q = round_half_away(div_rn_recip(x[sd][u], s64, rs)) + z;
+        q = q < 0.0 ? 0.0 : (q > 15.0 ? 15.0 : q);
+        bytes2 |= (uint32_t)q << (4 * u);
+      }
+      scv = s32;
+      zpv = (uint32_t)z;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        deq[sd][u] = (float)((double)s32 * (double)((int)((bytes2 >> (4 * u)) & 15u) - (int)zpv));
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) deq[sd][u] = scv;  // sentinel row: the offset
+    }
+    if (!fin[sd]) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) deq[sd][u] = 0.f;
+      continue;
+    }
+    *reinterpret_cast<uint16_t*>(cell + (sd ? cell_vcode(p.pool, ci) : cell_kcode(p.pool, ci)) + 2 * lane) =
+        (uint16_t)bytes2;
+    if (lane == 0) {
+      *reinterpret_cast<float*>(cell + (sd ? cell_vscale(p.pool, ci) : cell_kscale(p.pool, ci))) = scv;
+      cell[sd ? cell_vzp(p.pool, ci) : cell_kzp(p.pool, ci)] = (uint8_t)zpv;
+    }
+  }
+}
+
+// named barriers (id 0 is __syncthreads): 1 = the tile warps after query prep,
+// 2 = query-prep warps -> writer warp (rotated q in smem for scoring the new token)
+KVR_DEV void named_bar_sync(int id, int threads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory"); }
+KVR_DEV void named_bar_arrive(int id, int threads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 KVR_DEV void mbar_arrive(uint64_t* bar) {
@@ -332,7 +374,7 @@ KVR_DEV void load_cell_rest(CellFrag& f, const uint8_t* st, int r, int i) {
 // rotation of the value branch (o @ H_blk @ diag(signs)) as an fp32 butterfly in
 // registers / shuffles, then a 16-B store per lane.  `row` is o in natural order.
 template <int ORDER>
-KVR_DEV void emit_head(const DecodeParams& p, const Signs& signs, int b, int h, int j, const float* row, int lane) {
+KVR_DEV void emit_head(const DecodeParams& p, uint32_t sgw, int b, int h, int j, const float* row, int lane) {
   float x[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) x[u] = row[4 * lane + u];
@@ -355,7 +397,7 @@ KVR_DEV void emit_head(const DecodeParams& p, const Signs& signs, int b, int h, 
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       x[u] *= inv;
-      if (p.has_signs && sign_bit(signs, 4 * lane + u)) x[u] = -x[u];
+      if ((sgw >> (4 * (lane & 7) + u)) & 1u) x[u] = -x[u];
     }
   }
   float4* dst = reinterpret_cast<float4*>(p.out + ((int64_t)b * p.nq + (int64_t)h * p.G + j) * 128) + lane;
@@ -425,6 +467,9 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   int wnext = page_window(1), win_idx = 0;
   const uint8_t* wcur = window_addr(0, page_window(0));
   const int len_raw = __ldg(&p.lens[b]);
+  // this lane's word of the sign vector (dims 4l..4l+3), read from the parameter
+  // bank before the dependency wait (0 = no flips)
+  const uint32_t sgw = p.has_signs ? signs.w[lane >> 3] : 0u;
   const int64_t new_slot = APPEND ? __ldg(&p.new_slot[b]) : -1;  // host-written, like lens: read with it
   if (threadIdx.x < NWARPS * RING_CELLS) mbar_init(&bars[threadIdx.x], 1);
   reinterpret_cast<uint2*>(sfrag)[threadIdx.x] = make_uint2(0u, 0u);  // 4 KB of query digits (padding = 0)
@@ -490,6 +535,14 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   pdl_wait();  // q, the new token, the workspace and recent pages may come from the previous grid
   pdl_launch_dependents();
   KVR_STAMP(11);  // past the grid-dependency wait
+  // ---- the writer warp (no tiles of its own) quantizes + stores the new token's K
+  // and V rows bit-exactly (f64, reference arithmetic) right away, overlapping the
+  // query prep and the main loop of the others; scored once the rotated q is in smem
+  float newd[2][4];
+  if (APPEND && warp == DW && app_owner) {
+    append_rows_exact<ORDER>(p, signs, b, h, newd, p.trace && lane == 0 ? p.trace + cta_id * 16 : nullptr);
+    *reinterpret_cast<float4*>(s_vnew + 4 * lane) = make_float4(newd[1][0], newd[1][1], newd[1][2], newd[1][3]);
+  }
   if (threadIdx.x == 0 && len_raw > p.max_len && p.flags && h == 0 && split == 0)
     atomicOr(p.flags, KVR_FLAG_LEN_OVERFLOW);
 
@@ -515,7 +568,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       x[u] = qx[u];
-      if (p.rotate && p.has_signs && sign_bit(signs, 4 * lane + u)) x[u] = -x[u];
+      if (p.rotate && ((sgw >> (4 * (lane & 7) + u)) & 1u)) x[u] = -x[u];
     }
     if (p.rotate) {
       const float a0 = x[0] + x[1], a1 = x[0] - x[1], a2 = x[2] + x[3], a3 = x[2] - x[3];
@@ -536,7 +589,10 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
 #pragma unroll
       for (int u = 0; u < 4; ++u) x[u] *= inv;
     }
-    if (APPEND) *reinterpret_cast<float4*>(s_qrot + j * 128 + 4 * lane) = make_float4(x[0], x[1], x[2], x[3]);
+    if (APPEND && app_owner) {  // hand the rotated q to the writer warp
+      *reinterpret_cast<float4*>(s_qrot + j * 128 + 4 * lane) = make_float4(x[0], x[1], x[2], x[3]);
+      named_bar_arrive(2, (4 * NT + 1) * 32);
+    }
     if constexpr (QK_INT8) {
       float amax = fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])), fmaxf(fabsf(x[2]), fabsf(x[3])));
       amax = warp_max(amax);
@@ -609,7 +665,11 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
     }
   }
   KVR_STAMP(12);  // warp 0's query prep done
-  __syncthreads();
+  if (APPEND) {  // the tile warps only: the writer warp joins again after the loop
+    if (tile_warp) named_bar_sync(1, DW * 32);
+  } else {
+    __syncthreads();
+  }
   // query B fragments: registers for one 8-column tile; with two (G = 8) they stay
   // in shared memory (one LDS.64 per k-step) to keep the loop inside 128 registers
   constexpr bool BQ_REG = NT == 1;
@@ -627,18 +687,14 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
     kscale[nt] = s_ksc[4 * nt + i];
   }
 
-  // ---- the writer warp (no tiles of its own, so this overlaps the main loop of the
-  // others) quantizes + stores the new token's K and V rows bit-exactly (f64,
-  // reference arithmetic), keeps their dequantised values and scores the token
-  float knew[4] = {0.f, 0.f, 0.f, 0.f};
+  // ---- the writer warp scores the new token (logits in log2 units)
   if (APPEND && warp == DW && app_owner) {
-    float vnew[4];
-    append_row_exact<ORDER>(p, signs, b, h, 0, knew);
-    append_row_exact<ORDER>(p, signs, b, h, 1, vnew);
-    *reinterpret_cast<float4*>(s_vnew + 4 * lane) = make_float4(vnew[0], vnew[1], vnew[2], vnew[3]);
-    for (int j = 0; j < G; ++j) {  // logits (log2 units)
+    if (p.trace && lane == 0) p.trace[cta_id * 16 + 8] = clk64();  // append done
+    named_bar_sync(2, (4 * NT + 1) * 32);  // rotated q of every head in smem
+    for (int j = 0; j < G; ++j) {
       const float4 qv = *reinterpret_cast<const float4*>(s_qrot + j * 128 + 4 * lane);
-      const float dot = warp_sum(qv.x * knew[0] + qv.y * knew[1] + qv.z * knew[2] + qv.w * knew[3]);
+      const float dot =
+          warp_sum(qv.x * newd[0][0] + qv.y * newd[0][1] + qv.z * newd[0][2] + qv.w * newd[0][3]);
       if (lane == 0) s_lnew[j] = dot * (LOG2E * (float)(1.0 / sqrt(128.0)));
     }
     __syncwarp();
@@ -987,7 +1043,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
       }
     }
     __syncthreads();
-    if (warp < G && warp % S == rank) emit_head<ORDER>(p, signs, b, h, warp, omerge + warp * 128, lane);
+    if (warp < G && warp % S == rank) emit_head<ORDER>(p, sgw, b, h, warp, omerge + warp * 128, lane);
     KVR_STAMP(9);  // merged + stored
     cluster_sync_relaxed();  // every CTA's partial stays readable until all merges are done
     KVR_STAMP(10);
@@ -999,10 +1055,16 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   }
   if (p.splits > 1) {
     // ---- inline split merge: the last CTA of (sequence, kv head) to publish its
-    // partial merges all of them (one L2 round trip: the lse into smem while every
-    // thread loads its dims' partials) and resets the counter for the next launch
+    // partial merges all of them.  Its thread 0 pulls the S contiguous partials
+    // ([S][8][128] o, [S][8] lse) into the free rings with two bulk copies (one
+    // round trip), then every thread merges its (q head, dim) in compact loops --
+    // once-per-launch code is kept short, it runs from a cold instruction cache.
     __syncthreads();  // every thread's partial stores precede thread 0's release
     int* s_last = reinterpret_cast<int*>(s_sumq + 56);
+    const int S = p.splits;
+    float* so = reinterpret_cast<float*>(sm);  // [S][8][128]
+    float* sl = so + S * 1024;                 // [S][8]
+    uint64_t* mbar = bars + NWARPS * RING_CELLS;
     if (threadIdx.x == 0) {
       // release the CTA's partial (ordered before by the barrier), acquire the others'
       uint32_t prev;
@@ -1010,53 +1072,50 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
                    : "=r"(prev)
                    : "l"(p.ws_cnt + (int64_t)b * H + h)
                    : "memory");
-      *s_last = prev == (uint32_t)(p.splits - 1);
+      const int last = prev == (uint32_t)(S - 1);
+      *s_last = last;
+      if (last) {
+        fence_proxy_async_global();  // the others' generic-proxy stores -> the bulk reads
+        fence_proxy_async();         // this CTA's generic smem accesses -> the bulk writes
+        mbar_init(mbar, 1);
+        fence_mbar_init();
+        mbar_expect_tx(mbar, (uint32_t)(S * 4096 + S * 32));
+        bulk_g2s(so, p.ws_o + hbase * 128, (uint32_t)(S * 4096), mbar);
+        bulk_g2s(sl, p.ws_lse + hbase, (uint32_t)(S * 32), mbar);
+      }
     }
     __syncthreads();
     KVR_STAMP(6);  // partial stored, counter back
     if (!*s_last) return;
-    const int S = p.splits;
-    float* s_l = reinterpret_cast<float*>(sm);            // [8][MERGE_INLINE_MAX] split lse
-    float* omerge = s_l + 8 * MERGE_INLINE_MAX;            // [8][128]
-    for (int x = threadIdx.x; x < G * S; x += blockDim.x) {
-      const int j = x / S, sp = x - j * S;
-      s_l[j * MERGE_INLINE_MAX + sp] = __ldcg(p.ws_lse + hbase + (int64_t)sp * 8 + j);
-    }
-    for (int x0 = 0; x0 < G * 128; x0 += blockDim.x) {
-      const int x = x0 + threadIdx.x, j = x >> 7, dd = x & 127;
-      float ov[MERGE_INLINE_MAX];
-#pragma unroll
-      for (int sp = 0; sp < MERGE_INLINE_MAX; ++sp)
-        ov[sp] = (sp < S && j < G) ? __ldcg(p.ws_o + (hbase + (int64_t)sp * 8 + j) * 128 + dd) : 0.f;
-      __syncthreads();  // s_l visible (and, on a second pass, omerge of the first)
-      if (j < G) {
-        const float* lj = s_l + j * MERGE_INLINE_MAX;
-        float mx = -INFINITY;
-#pragma unroll
-        for (int sp = 0; sp < MERGE_INLINE_MAX; ++sp)
-          if (sp < S) mx = fmaxf(mx, lj[sp]);
-        float tot = 0.f, ot = 0.f;
-        if (mx != -INFINITY) {
-#pragma unroll
-          for (int sp = 0; sp < MERGE_INLINE_MAX; ++sp)
-            if (sp < S && lj[sp] != -INFINITY) {
-              const float w = ex2f(lj[sp] - mx);
-              tot += w;
-              ot += w * ov[sp];
-            }
+    mbar_wait(mbar, 0);
+    KVR_STAMP(7);  // merge inputs landed
+#pragma unroll 1
+    for (int x = threadIdx.x; x < G * 128; x += blockDim.x) {
+      const int j = x >> 7, dd = x & 127;
+      float mx = -INFINITY;
+#pragma unroll 4
+      for (int sp = 0; sp < S; ++sp) mx = fmaxf(mx, sl[sp * 8 + j]);
+      float tot = 0.f, ot = 0.f;
+      if (mx != -INFINITY) {
+#pragma unroll 4
+        for (int sp = 0; sp < S; ++sp) {
+          const float l = sl[sp * 8 + j];
+          const float w = (l == -INFINITY) ? 0.f : ex2f(l - mx);
+          tot += w;
+          ot += w * so[(sp * 8 + j) * 128 + dd];
         }
-        omerge[j * 128 + dd] = tot > 0.f ? ot / tot : 0.f;
       }
+      obuf[j * 128 + dd] = tot > 0.f ? ot / tot : 0.f;
     }
     __syncthreads();
-    if (warp < G) emit_head<ORDER>(p, signs, b, h, warp, omerge + warp * 128, lane);
+    if (warp < G) emit_head<ORDER>(p, sgw, b, h, warp, obuf + warp * 128, lane);
     if (threadIdx.x == 0) p.ws_cnt[(int64_t)b * H + h] = 0u;  // read again only after this grid completes
-    KVR_STAMP(9);
+    KVR_STAMP(9);  // merged + stored
     return;
   }
   __syncthreads();
   // ---- output: one warp per q head
-  if (warp < G) emit_head<ORDER>(p, signs, b, h, warp, obuf + warp * 128, lane);
+  if (warp < G) emit_head<ORDER>(p, sgw, b, h, warp, obuf + warp * 128, lane);
   KVR_STAMP(10);
 }
 

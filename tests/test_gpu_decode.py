@@ -255,3 +255,37 @@ def test_step_graph_replay_matches_eager():
         dumps[mode] = t.dump_bytes()
     assert torch.equal(outs[False], outs[True])
     assert dumps[False] == dumps[True]
+
+
+@pytest.mark.parametrize("kind", ["gaussian", "outlier", "correlated", "adversarial"])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.float64])
+def test_fused_append_bit_exact_many_rows(kind, dtype):
+    """The fused step's writer warp (f64 rotate + quantize, reciprocal-based
+    correctly rounded divisions) stores exactly the reference's bytes for 256
+    sequences x 8 heads of each row family, in bf16 / f32 / f64 inputs."""
+    B, H, G, d = 256, 8, 1, 128
+    layout = HeadLayout(num_q_heads=G * H, num_kv_heads=H, head_dim=d, rot_order=128, page_tokens=16)
+    t = PageTable(layout, num_pages=B)
+    spec = RotationSpec(order=128, signs=make_signs(9, 0, d, 128), targets=Targets.KEYS_AND_VALUES)
+    for s in range(B):
+        t.create_sequence(s)
+    rows = gen_rows(kind, 2 * B * H, d, 1234)
+    if dtype is not torch.bfloat16:  # full-mantissa inputs: dense rounding-boundary coverage
+        rng = np.random.default_rng(5)
+        rows = rows * (1.0 + rng.standard_normal(rows.shape) * 1e-3)
+        if dtype is torch.float32:
+            rows = rows.astype(np.float32).astype(np.float64)
+    k_new = rows[: B * H].reshape(B, H, d)
+    v_new = rows[B * H:].reshape(B, H, d)
+    plan = DecodePlan(t, list(range(B)), extra_tokens=1)
+    q = torch.zeros((B, G * H, d), dtype=torch.float32, device="cuda")
+    plan.step(q, torch.tensor(k_new, dtype=dtype).cuda(), torch.tensor(v_new, dtype=dtype).cuda(), spec)
+    torch.cuda.synchronize()
+    from kvtest_util import page_fields
+    for b in range(B):
+        f = page_fields(t.page_records([t.sequence_pages(b)[0]]), 16, H, d)
+        for side, x in (("k", k_new[b]), ("v", v_new[b])):
+            pk, sk, zk = O.quantize_rows(O.rotate_rows(np.array(x, dtype=np.float64), 128, spec.signs))
+            np.testing.assert_array_equal(f[f"{side}_payload"][0, 0], pk)
+            np.testing.assert_array_equal(f[f"{side}_scale"][0, 0], sk)
+            np.testing.assert_array_equal(f[f"{side}_zp"][0, 0], zk)
