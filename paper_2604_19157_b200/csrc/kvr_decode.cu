@@ -55,7 +55,8 @@ struct DecodeParams {
   const int64_t* new_slot;  // [B] slot id of the appended token (it is the last of seq_lens[b])
   uint32_t* flags;
   unsigned long long* trace;  // optional: per CTA 8 globaltimer stamps (ns), see kvr_debug_decode_trace
-  int pre_groups;   // ring groups requested before griddepcontrol.wait (<= NSTG)
+  int pre_groups;   // ring groups per warp requested before griddepcontrol.wait (default 1: a
+                    // deeper pre-wait burst queues the query load behind it; measured)
   int merge_late;   // decode_merge_kernel releases its dependents after its loads
   int evict_first;  // KV cells are streamed with an L2 evict-first policy
   int merge_inline;   // splits > 1 without a cluster: the last CTA merges (ws_cnt counters)
@@ -526,8 +527,8 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
     }
   };
   auto group_last = [&](int k) { return min(tile_of(C * k) + C, hi) - 1; };
-  // first NSTG groups of this warp: the immutable ones go out before the wait on
-  // the previous grid (programmatic dependent launch overlaps them with its tail)
+  // the first pre_groups groups of this warp: immutable ones go out before the wait
+  // on the previous grid (programmatic dependent launch overlaps them with its tail)
   int k0 = 0;
 #pragma unroll 1
   for (; k0 < NSTG && k0 < p.pre_groups && k0 < my_groups && group_last(k0) < guard; ++k0) issue(k0);
@@ -1505,7 +1506,7 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
   p.flags = flags;
   p.trace = g_trace;
   p.max_len = max_len;
-  static const int env_pre = getenv("KVR_PREWAIT") ? atoi(getenv("KVR_PREWAIT")) : 1 << 20;
+  static const int env_pre = getenv("KVR_PREWAIT") ? atoi(getenv("KVR_PREWAIT")) : 1;
   static const int env_ml = getenv("KVR_MERGE_LATE") ? atoi(getenv("KVR_MERGE_LATE")) : 0;
   p.pre_groups = env_pre;
   p.merge_late = env_ml;
