@@ -292,15 +292,17 @@ def run_ours(args, rank, world, local_rank):
             "parallelism": f"dp{world} (independent sequences per GPU, no data-path collective)",
             "algorithmic_bytes_per_step": per_rank_bytes,
         },
-        "roofline": {"bound": "hbm", "kernel": "decode_tma_kernel + decode_merge_kernel (one kvr_decode_step: fused "
-                               "append + split-K decode + split merge)",
+        "roofline": {"bound": "hbm", "kernel": ("decode_tma_kernel (one kvr_decode_step: fused append + split-K "
+                                                "decode + inline split merge by the last CTA)") if splits <= 32 else
+                     "decode_tma_kernel + decode_merge_kernel (fused append + split-K decode, then the split merge)",
                      "achieved": round(ach, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": round(ach / peak, 4), "traffic": traffic, "algorithmic_bytes": dbytes,
                      "avg_launch_us": round(t_fused * 1e3, 3)},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        # per step: the fused decode kernel + the split-merge kernel (more than 8 splits)
-        "gpu_launches": args.steps * (2 if splits > 8 else 1),
+        # per step: the fused decode kernel (+ the split-merge kernel above 32 splits;
+        # 2..8 merge in a cluster, 9..32 inline in the last CTA)
+        "gpu_launches": args.steps * (2 if splits > 32 else 1),
         "clocks": clocks,
         "detail": {
             "k1_write_1tok_us": round(t_k1 * 1e3, 3), "k1_plain_1tok_us": round(t_k1p * 1e3, 3),

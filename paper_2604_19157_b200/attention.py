@@ -19,9 +19,9 @@ import torch
 
 from . import _kernels, _lib
 from .cache import INT4, PageTable
-from .errors import EmptySequenceError, NonFiniteInputError, ShapeError, UnsupportedConfigError
+from .errors import EmptySequenceError, NonFiniteInputError, ShapeError
 from .layout import HeadLayout
-from .rotation import RotationSpec, Targets
+from .rotation import RotationSpec, Targets, apply_block_rotation, apply_inverse_rotation, value_branch_spec
 
 _Q_CODE = {torch.float32: _lib.KVR_F32, torch.bfloat16: _lib.KVR_BF16, torch.float16: _lib.KVR_F16}
 _KV_CODE = {torch.float64: _lib.KVR_F64, **_Q_CODE}
@@ -115,7 +115,7 @@ class DecodePlan:
             if spec.order != lay.rot_order:
                 raise ShapeError(f"spec order {spec.order} != layout rot_order {lay.rot_order}")
             if spec.learned is not None:
-                raise UnsupportedConfigError("learned rotations are not fused into the decode kernel (row f3)")
+                return self._run_learned(q, spec, out)
         targets = _lib.KVR_KEYS_ONLY if (rotate and spec.targets is Targets.KEYS_ONLY) else _lib.KVR_KEYS_AND_VALUES
         _lib.check(_lib.lib().kvr_paged_decode(
             _kernels.ptr(q), _Q_CODE[q.dtype], ctypes.byref(table.desc), _kernels.ptr(self.bt), self.bt.shape[1],
@@ -124,6 +124,19 @@ class DecodePlan:
             _kernels.ptr(self.ws), self.ws.numel(), self.splits, _kernels.stream_ptr()))
         return out
 
+
+    def _run_learned(self, q: torch.Tensor, spec: RotationSpec, out: torch.Tensor) -> torch.Tensor:
+        """Row f3, unfused: q through the full transform (signs, H, learned R) in f64
+        on the device, the INT4 decode kernel on the pre-rotated query, then the
+        value branch's inverse transform on the output (attention.py:63-85)."""
+        lay = self.table.layout
+        d = lay.head_dim
+        qr = apply_block_rotation(q.reshape(-1, d), lay, spec).reshape(q.shape).float()
+        self.run(qr, None, out)
+        vspec = value_branch_spec(spec)
+        if vspec is not None:
+            out.copy_(apply_inverse_rotation(out.reshape(-1, d), lay, vspec).reshape(out.shape))
+        return out
 
     def run_step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, slots: torch.Tensor,
                  spec: Optional[RotationSpec], out: Optional[torch.Tensor] = None) -> torch.Tensor:
@@ -140,8 +153,9 @@ class DecodePlan:
         if table.precision != INT4:
             spec = None
         rotate = spec is not None
-        if rotate and spec.learned is not None:
-            raise UnsupportedConfigError("learned rotations are not fused into the decode kernel (row f3)")
+        if rotate and spec.learned is not None:  # row f3: unfused write, then decode
+            table.store_slots(k_new, v_new, slots, spec, exact=True)
+            return self.run(q, spec, out)
         # the argument list is rebuilt only when a buffer, the spec or the stream changes
         stream = torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
         key = (q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(), slots.data_ptr(), out.data_ptr(), q.dtype,

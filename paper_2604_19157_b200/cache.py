@@ -24,8 +24,7 @@ import numpy as np
 import torch
 
 from . import _kernels, _lib
-from .errors import (CapacityExceededError, ConfigError, NonFiniteInputError, SequenceNotFoundError, ShapeError,
-                     UnsupportedConfigError)
+from .errors import CapacityExceededError, ConfigError, NonFiniteInputError, SequenceNotFoundError, ShapeError
 from .layout import HeadLayout
 from .rotation import RotationSpec, Targets
 
@@ -369,8 +368,11 @@ class PageTable:
         if rotate:
             if spec.order != self.layout.rot_order:
                 raise ShapeError(f"spec order {spec.order} != layout rot_order {self.layout.rot_order}")
-            if spec.learned is not None:
-                raise UnsupportedConfigError("learned rotations are not fused into the write kernel (row f3)")
+            if spec.learned is not None:  # row f3: learned R after H, unfused f64 transform on the device
+                from .rotation import rotate_kv_learned
+
+                k, v = rotate_kv_learned(k, v, self.layout, spec)
+                spec, rotate, exact = None, False, True
         targets = _lib.KVR_KEYS_ONLY if (rotate and spec.targets is Targets.KEYS_ONLY) else _lib.KVR_KEYS_AND_VALUES
         words = spec.sign_words(self.layout.head_dim) if rotate else None
         _lib.check(_lib.lib().kvr_rotate_quantize_store(
@@ -459,6 +461,11 @@ class PageTable:
             raise ShapeError("slots must be an int64 CUDA tensor")
         if self.precision == BF16:
             spec = None
+        if spec is not None and spec.learned is not None:  # row f3, unfused (see _store)
+            from .rotation import rotate_kv_learned
+
+            k, v = rotate_kv_learned(k, v, self.layout, spec)
+            spec, exact = None, True
         rotate = spec is not None
         targets = _lib.KVR_KEYS_ONLY if (rotate and spec.targets is Targets.KEYS_ONLY) else _lib.KVR_KEYS_AND_VALUES
         _lib.check(_lib.lib().kvr_rotate_quantize_store(

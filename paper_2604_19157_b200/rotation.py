@@ -103,7 +103,7 @@ def _rotate(x, layout: HeadLayout, spec: RotationSpec, inverse: bool):
         raise ShapeError(f"expected (n, {layout.head_dim}) rows, got {tuple(t.shape)}")
     _check_spec_layout(spec, layout)
     n, d = t.shape
-    learned = None if spec.learned is None else torch.from_numpy(np.asarray(spec.learned)).to(t.device)
+    learned = learned_on(spec, t.device)
     if inverse and learned is not None:
         t = (t @ learned.T).contiguous()
     out = torch.empty_like(t)
@@ -113,6 +113,29 @@ def _rotate(x, layout: HeadLayout, spec: RotationSpec, inverse: bool):
     if not inverse and learned is not None:
         out = out @ learned
     return out.cpu().numpy() if is_np else out
+
+
+def learned_on(spec: RotationSpec, device) -> Optional[torch.Tensor]:
+    """The learned factor as an f64 device tensor (memoised per device, so graph
+    capture and steady-state steps do no host->device copy)."""
+    if spec.learned is None:
+        return None
+    cache = spec.__dict__.setdefault("_learned_dev", {})
+    key = str(torch.device(device))
+    if key not in cache:
+        cache[key] = torch.from_numpy(np.array(spec.learned, dtype=np.float64)).to(device)
+    return cache[key]
+
+
+def rotate_kv_learned(k: torch.Tensor, v: torch.Tensor, layout: HeadLayout, spec: RotationSpec):
+    """Row f3 (learned R composed after the Hadamard), unfused on the device: the
+    K rows through the full transform, the V rows through value_branch_spec
+    (rotation.py:118-142, 162-168).  Returns f64 tensors shaped like k / v."""
+    d = layout.head_dim
+    kr = apply_block_rotation(k.reshape(-1, d), layout, spec).reshape(k.shape)
+    vspec = value_branch_spec(spec)
+    vr = v.to(torch.float64) if vspec is None else apply_block_rotation(v.reshape(-1, d), layout, vspec).reshape(v.shape)
+    return kr.contiguous(), vr.contiguous()
 
 
 def apply_block_rotation(x, layout: HeadLayout, spec: RotationSpec):

@@ -1,0 +1,118 @@
+"""Row f3: a learned orthogonal R composed after the block Hadamard
+(rotation.py:118-168): writes, decode and the serving step on the device,
+against the oracle with the reference's composition order.
+
+The dense x @ R product goes through a BLAS on both sides (numpy/OpenBLAS in the
+reference, cuBLAS DGEMM here) with unspecified summation order, so stored codes
+may differ by one step where the rotated value sits on a rounding boundary:
+the test bounds that count; decode outputs stay within the 1e-3 tolerance.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from kvtest_util import gen_rows, page_fields  # noqa: E402
+from oracle import kvrot_oracle as O  # noqa: E402
+from paper_2604_19157_b200.attention import DecodePlan, decode_batch  # noqa: E402
+from paper_2604_19157_b200.cache import PageTable  # noqa: E402
+from paper_2604_19157_b200.layout import HeadLayout  # noqa: E402
+from paper_2604_19157_b200.rotation import RotationSpec, Targets, make_signs  # noqa: E402
+
+TOL = 1e-3
+
+
+def _orth(d, seed):
+    q, r = np.linalg.qr(np.random.default_rng(seed).standard_normal((d, d)))
+    return q * np.sign(np.diag(r))
+
+
+def _ref_rotate(x, spec, values):
+    """Reference transform of rows: signs, FWHT, then R (values: R only if learned_values)."""
+    if values and spec.targets is Targets.KEYS_ONLY:
+        return x
+    y = O.rotate_rows(x, spec.order, spec.signs)
+    if not values or spec.learned_values:
+        y = y @ spec.learned
+    return y
+
+
+@pytest.mark.parametrize("targets,learned_values", [(Targets.KEYS_AND_VALUES, False), (Targets.KEYS_AND_VALUES, True),
+                                                    (Targets.KEYS_ONLY, False)])
+def test_learned_write_and_decode(targets, learned_values):
+    H, G, d, P = 2, 4, 128, 16
+    lens = [7, 40, 300]
+    layout = HeadLayout(num_q_heads=G * H, num_kv_heads=H, head_dim=d, rot_order=128, page_tokens=P)
+    t = PageTable(layout, num_pages=sum((L + P - 1) // P for L in lens) + 2)
+    spec = RotationSpec(order=128, signs=make_signs(4, 0, d, 128), learned=_orth(d, 11), targets=targets,
+                        learned_values=learned_values)
+    seqs, ks, vs = [], [], []
+    for s, L in enumerate(lens):
+        t.create_sequence(s)
+        seqs += [s] * L
+        ks.append(gen_rows("gaussian", L * H, d, 100 + s).reshape(L, H, d))
+        vs.append(gen_rows("outlier", L * H, d, 200 + s).reshape(L, H, d))
+    k, v = np.concatenate(ks), np.concatenate(vs)
+    t.append_batch(seqs, torch.tensor(k), torch.tensor(v), spec=spec)
+    # 1) stored bytes vs the reference composition (codes: at most a few boundary steps)
+    kr = _ref_rotate(k.reshape(-1, d), spec, values=False)
+    vr = _ref_rotate(v.reshape(-1, d), spec, values=True)
+    mism = total = 0
+    row = 0
+    for s, L in enumerate(lens):
+        f = page_fields(t.page_records(t.sequence_pages(s)), P, H, d)
+        for side, ref in (("k", kr), ("v", vr)):
+            pk, sk, zk = O.quantize_rows(ref[row * H:(row + L) * H])
+            got = f[f"{side}_payload"].reshape(-1, H, d // 2)[:L].reshape(-1, d // 2)
+            gl, gh = got & 15, got >> 4
+            rl, rh = pk & 15, pk >> 4
+            dl = np.abs(gl.astype(int) - rl) + np.abs(gh.astype(int) - rh)
+            assert dl.max() <= 1
+            mism += int((dl > 0).sum())
+            total += dl.size * 2
+            np.testing.assert_allclose(f[f"{side}_scale"].reshape(-1, H)[:L].reshape(-1), sk, rtol=1e-6)
+        row += L
+    print("learned: nibble mismatches", mism, "of", total)
+    assert mism <= total * 1e-3
+    # 2) decode: q through the full transform, the value branch undone on the output
+    q = np.random.default_rng(9).standard_normal((len(lens), G * H, d))
+    out = decode_batch(torch.tensor(q, dtype=torch.float32).cuda(), t, list(range(len(lens))), spec=spec)
+    kd, vd = t.read_sequence_device(list(range(len(lens))), torch.float64)
+    for b, L in enumerate(lens):
+        qf = _ref_rotate(q[b], spec, values=False)
+        o = O.decode_flat(qf, kd[b, :L].cpu().numpy(), vd[b, :L].cpu().numpy(), G)
+        if targets is Targets.KEYS_AND_VALUES:
+            if learned_values:
+                o = o @ spec.learned.T
+            o = O.unrotate_rows(o, spec.order, spec.signs)
+        err = np.abs(out[b].double().cpu().numpy() - o).max() / np.abs(o).max()
+        print("learned decode", b, err)
+        assert err <= TOL
+
+
+def test_learned_serving_step():
+    """DecodePlan.step with a learned spec: unfused write of the new token, then decode."""
+    H, G, d = 2, 4, 128
+    layout = HeadLayout(num_q_heads=G * H, num_kv_heads=H, head_dim=d, rot_order=128, page_tokens=16)
+    t = PageTable(layout, num_pages=16)
+    spec = RotationSpec(order=128, signs=make_signs(4, 0, d, 128), learned=_orth(d, 12), learned_values=True)
+    for s in range(2):
+        t.create_sequence(s)
+    k0 = gen_rows("gaussian", 2 * 50 * H, d, 5).reshape(100, H, d)
+    v0 = gen_rows("gaussian", 2 * 50 * H, d, 6).reshape(100, H, d)
+    t.append_batch([0] * 50 + [1] * 50, torch.tensor(k0), torch.tensor(v0), spec=spec)
+    plan = DecodePlan(t, [0, 1], extra_tokens=4)
+    rng = np.random.default_rng(3)
+    for _ in range(3):
+        q = rng.standard_normal((2, G * H, d))
+        kn = torch.tensor(rng.standard_normal((2, H, d)), dtype=torch.bfloat16)
+        vn = torch.tensor(rng.standard_normal((2, H, d)), dtype=torch.bfloat16)
+        out = plan.step(torch.tensor(q, dtype=torch.float32), kn, vn, spec).cpu().numpy()
+        kd, vd = t.read_sequence_device([0, 1], torch.float64)
+        for b in range(2):
+            L = t.sequence_length(b)
+            o = O.decode_flat(_ref_rotate(q[b], spec, False), kd[b, :L].cpu().numpy(), vd[b, :L].cpu().numpy(), G)
+            o = O.unrotate_rows(o @ spec.learned.T, spec.order, spec.signs)
+            assert np.abs(out[b] - o).max() / np.abs(o).max() <= TOL

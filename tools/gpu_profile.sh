@@ -9,6 +9,4 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:deco
   -o gpurun_out/prof_decode python bench.py --steps 40 --warmup 3 --no-cpu --sets 2 --quick > gpurun_out/ncu_dec.out 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:store_mma -s 2 -c 1 \
   -o gpurun_out/prof_store python tools/c1_store.py --ncu > gpurun_out/ncu_store.out 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:decode_merge -s 30 -c 1 \
-  -o gpurun_out/prof_merge python bench.py --steps 40 --warmup 3 --no-cpu --sets 2 --quick > gpurun_out/ncu_merge.out 2>&1
 ls -la gpurun_out
