@@ -93,7 +93,9 @@ for splits in split_list:
                      f"clock64 at {MHZ:.0f} MHz; us from the first CTA's entry)")
     out_lines.append(f"{'start':16s}: min {g0.min() / 1e3:6.2f} med {np.median(g0) / 1e3:6.2f} max {g0.max() / 1e3:6.2f} us")
     for k, nm in names.items():
-        ok = raw[:, k] > 0
+        # rows whose stamp belongs to this launch (the last CTA of an older step can
+        # stamp a row after the next step's CTA re-armed it)
+        ok = (raw[:, k] > raw[:, 1]) & (raw[:, k] - raw[:, 1] < 1e6)
         if ok.any():
             t = (g0[ok] + (raw[ok, k] - raw[ok, 1]) * 1e3 / MHZ) / 1e3
             out_lines.append(f"{nm:16s}: n {ok.sum():4d} min {t.min():6.2f} med {np.median(t):6.2f} max {t.max():6.2f} us")
