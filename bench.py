@@ -515,17 +515,16 @@ def e2e_api(torch, layout, spec, dev, table, args, world):
     vh = torch.randn((1, H, D)).to(torch.bfloat16).pin_memory()
     qh = torch.randn((1, NQ, D)).to(torch.bfloat16).pin_memory()
     oh = torch.empty((1, NQ, D), dtype=torch.float32).pin_memory()
-    od = torch.empty((1, NQ, D), dtype=torch.float32, device=dev)
     free_before = list(table.alloc.free)
     base_len = table.alloc.seq_len[0]
     base_pages = list(table.alloc.seq_pages[0])
     plan = DecodePlan(table, [0], extra_tokens=steps + 8)
 
     def one():
-        # one pinned H2D of q/k/v + slot/len metadata and the decode kernels, replayed
-        # from a CUDA graph; host bookkeeping (slot allocation, page table) per step
-        plan.step(qh, kh, vh, spec, out=od, graph=True)
-        oh.copy_(od, non_blocking=True)
+        # host bookkeeping (slot allocation, page table) per step; q/k/v and the slot /
+        # length metadata go to the device in one pinned copy, the fused kernel writes
+        # the output straight into the pinned host tensor (both cross the bus every step)
+        plan.step(qh, kh, vh, spec, out=oh, graph=True)
 
     for _ in range(3):
         one()
@@ -549,7 +548,8 @@ def e2e_api(torch, layout, spec, dev, table, args, world):
     byts = step_bytes(L)
     return {"value": round(world * byts / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "ms_per_step": round(ms, 4),
             "h2d_bytes_per_step": kh.numel() * 2 + vh.numel() * 2 + qh.numel() * 2 + 12,  # + slot id, length
-            "d2h_bytes_per_step": oh.numel() * 4, "api": "DecodePlan.step(graph=True) (fused append + decode) with host buffers",
+            "d2h_bytes_per_step": oh.numel() * 4,
+            "api": "DecodePlan.step(graph=True) (fused append + decode) with pinned host buffers",
             "steps": steps}
 
 

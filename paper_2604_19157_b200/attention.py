@@ -71,6 +71,10 @@ class DecodePlan:
         self.slots = self._dev[:8 * B].view(torch.int64)
         self.lens = self._dev[8 * B:12 * B].view(torch.int32)
         self.lens.copy_(lens)
+        self._pinned_out = {}
+        self._copy_stream = None
+        self.side_copy = False  # True: staged inputs go over on a side stream (measured slower end to end)
+        self._lens_stale = False  # step() passes its own device copy of the lengths
         self._layouts = {}
         if num_splits <= 0:
             num_splits = _lib.lib().kvr_decode_pick_splits(B, lay.num_kv_heads, self.max_len, P)
@@ -96,10 +100,13 @@ class DecodePlan:
         self._patch_pages()
         lens = [self.table.sequence_length(s) for s in self.seqs]
         self.lens.copy_(torch.tensor(lens, dtype=torch.int32))
+        self._lens_stale = False
         self.max_len = max(self.max_len, max(lens))
 
     def run(self, q: torch.Tensor, spec: Optional[RotationSpec], out: Optional[torch.Tensor] = None) -> torch.Tensor:
         table, lay = self.table, self.table.layout
+        if self._lens_stale:
+            self.refresh()
         if q.dtype not in _Q_CODE:
             q = q.float()
         q = q.contiguous()
@@ -139,11 +146,18 @@ class DecodePlan:
         return out
 
     def run_step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, slots: torch.Tensor,
-                 spec: Optional[RotationSpec], out: Optional[torch.Tensor] = None) -> torch.Tensor:
-        """Fused serving step on device buffers (no host bookkeeping): write token b's
-        K/V rows (B, H, d) into slot slots[b] (rotated + INT4-quantized bit-exactly
-        in f64) and decode over the plan's lengths, which must already include it."""
+                 spec: Optional[RotationSpec], out: Optional[torch.Tensor] = None,
+                 lens: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Fused serving step (no host bookkeeping): write token b's K/V rows (B, H, d)
+        into slot slots[b] (rotated + INT4-quantized bit-exactly in f64) and decode
+        over the lengths (default: the plan's), which must already include it.  The
+        buffers may be device memory or pinned host memory (read / written by the
+        kernel in place)."""
         table, lay = self.table, self.table.layout
+        if lens is None:
+            if self._lens_stale:
+                self.refresh()
+            lens = self.lens
         if not q.is_contiguous():
             q = q.contiguous()
         if not (k_new.is_contiguous() and v_new.is_contiguous()):
@@ -154,18 +168,24 @@ class DecodePlan:
             spec = None
         rotate = spec is not None
         if rotate and spec.learned is not None:  # row f3: unfused write, then decode
-            table.store_slots(k_new, v_new, slots, spec, exact=True)
-            return self.run(q, spec, out)
+            dev = table.device
+            table.store_slots(k_new.to(dev), v_new.to(dev), slots.to(dev), spec, exact=True)
+            if lens is not self.lens:
+                self.lens.copy_(lens, non_blocking=True)
+            res = self.run(q.to(dev), spec, out if out.is_cuda else None)
+            if res is not out:
+                out.copy_(res, non_blocking=True)
+            return out
         # the argument list is rebuilt only when a buffer, the spec or the stream changes
         stream = torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
         key = (q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(), slots.data_ptr(), out.data_ptr(), q.dtype,
-               k_new.dtype, id(spec), stream, self.bt.data_ptr(), self.lens.data_ptr(), self.ws.data_ptr())
+               k_new.dtype, id(spec), stream, self.bt.data_ptr(), lens.data_ptr(), self.ws.data_ptr())
         cached = getattr(self, "_step_args", None)
         if cached is None or cached[0] != key:
             targets = _lib.KVR_KEYS_ONLY if (rotate and spec.targets is Targets.KEYS_ONLY) else _lib.KVR_KEYS_AND_VALUES
             head = (_kernels.ptr(q), _Q_CODE[q.dtype], _kernels.ptr(k_new), _kernels.ptr(v_new), _KV_CODE[k_new.dtype],
                     _kernels.ptr(slots), ctypes.byref(table.desc), _kernels.ptr(self.bt), self.bt.shape[1],
-                    _kernels.ptr(self.lens), len(self.seqs), lay.num_q_heads)
+                    _kernels.ptr(lens), len(self.seqs), lay.num_q_heads)
             tail = (spec.order if rotate else 1, 1 if rotate else 0, targets,
                     spec.sign_words(lay.head_dim) if rotate else None, _kernels.ptr(out), _kernels.ptr(self.ws),
                     self.ws.numel(), self.splits, _kernels.ptr(table.flags), ctypes.c_void_p(stream))
@@ -175,8 +195,9 @@ class DecodePlan:
 
 
     def _step_layout(self, host_in) -> dict:
-        """Staging layout for a given set of host inputs (cached per shapes/dtypes):
-        pinned ring buffers, byte offsets and the device views the kernel reads."""
+        """Staging layout for a given set of host inputs (cached per shapes/dtypes): a
+        ring of pinned host buffers, each with its device twin (slot ids | lengths |
+        the host inputs) and the views the kernel reads."""
         key = tuple((tuple(t.shape), t.dtype) for t in host_in)
         lay = self._layouts.get(key)
         if lay is not None:
@@ -187,20 +208,16 @@ class DecodePlan:
         for n in sizes:
             offs.append(o)
             o += (n + 255) // 256 * 256
-        if o > self._dev.numel():
-            dev = torch.zeros(o, dtype=torch.uint8, device=self.table.device)
-            dev[:self._meta_bytes].copy_(self._dev[:self._meta_bytes])
-            self._dev = dev
-            self.slots = dev[:8 * B].view(torch.int64)
-            self.lens = dev[8 * B:12 * B].view(torch.int32)
-            self._layouts.clear()
         ring = []
         for _ in range(self._RING):
             buf = torch.empty(o, dtype=torch.uint8).pin_memory()
-            ring.append((buf, buf.numpy(), buf.data_ptr(), torch.cuda.Event()))
-        views = [self._dev[off:off + n].view(t.dtype).view(t.shape) for t, off, n in zip(host_in, offs, sizes)]
-        lay = {"bytes": o, "offs": offs, "sizes": sizes, "ring": ring, "views": views, "i": 0,
-               "dev_head": self._dev[:o]}
+            dbuf = torch.zeros(o, dtype=torch.uint8, device=self.table.device)
+            views = {"slots": dbuf[:8 * B].view(torch.int64), "lens": dbuf[8 * B:12 * B].view(torch.int32),
+                     "inputs": [dbuf[off:off + n].view(t.dtype).view(t.shape) for t, off, n in zip(host_in, offs, sizes)]}
+            ring.append((buf, buf.numpy(), buf.data_ptr(), _kernels.host_event(), dbuf.data_ptr(), views,
+                         _kernels.host_event()))
+            views["dbuf"] = dbuf
+        lay = {"bytes": o, "offs": offs, "sizes": sizes, "ring": ring, "i": 0}
         self._layouts[key] = lay
         return lay
 
@@ -208,8 +225,13 @@ class DecodePlan:
              out: Optional[torch.Tensor] = None, graph: bool = False) -> torch.Tensor:
         """One serving decode step for every sequence of the plan: allocate the new
         token's slot (reference page order), then one fused append + decode launch.
-        q (B, nq, d) and k_new/v_new (B, H, d) may be host tensors: they travel
-        with the step metadata in one pinned host->device copy.
+        q (B, nq, d) and k_new/v_new (B, H, d) may be host tensors: they are staged
+        with the step metadata (slot ids, lengths) in a pinned ring buffer that goes
+        to the device in one copy on a side stream, so it overlaps the previous
+        step's kernel (every CTA of a head re-reads q and the lengths: reading them
+        over the bus in place was measured slower).  `out` may be a pinned host
+        tensor: the kernel then writes the result there directly (valid once the
+        step has completed, e.g. after torch.cuda.synchronize()).
 
         graph=True replays the device part (that copy + the decode kernels) from a
         CUDA graph captured on first use per pinned staging buffer; the block table
@@ -217,6 +239,7 @@ class DecodePlan:
         fixed, so only the host bookkeeping runs per step."""
         table = self.table
         B = len(self.seqs)
+        stream = torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
         slots, fresh = table.alloc.plan(self.seqs)
         if fresh:
             table._zero_pages(fresh)
@@ -229,32 +252,54 @@ class DecodePlan:
                                  f"build a new DecodePlan (extra_tokens)")
             self.max_len = mx
         host_in = [t for t in (q, k_new, v_new) if not t.is_cuda]
-        lay = self._step_layout(host_in)
+        lkey = tuple((t.shape, t.dtype) for t in host_in)
+        lay = self._layouts.get(lkey) or self._step_layout(host_in)
         slot_i = lay["i"]
-        buf, buf_np, buf_ptr, ev = lay["ring"][slot_i]
+        buf, buf_np, buf_ptr, ev, dptr, dviews, cev = lay["ring"][slot_i]
         lay["i"] = (slot_i + 1) % self._RING
-        ev.synchronize()  # the copy that last read this pinned buffer has run
+        _kernels.event_sync(ev)  # the kernel that last read this slot (host and device side) has run
         buf_np[:8 * B] = slots.view(np.uint8)
         buf_np[8 * B:12 * B] = lens.view(np.uint8)
         for t, off, n in zip(host_in, lay["offs"], lay["sizes"]):
             t = t if t.is_contiguous() else t.contiguous()
             ctypes.memmove(buf_ptr + off, t.data_ptr(), n)
-        dev_in = iter(lay["views"])
-        q, k_new, v_new = (t if t.is_cuda else next(dev_in) for t in (q, k_new, v_new))
+        side = self.side_copy
+        if side:  # the staged bytes go over on the side stream; the compute stream waits for them
+            if self._copy_stream is None:
+                self._copy_stream = torch.cuda.Stream(device=table.device)
+            cs = self._copy_stream.cuda_stream
+            _kernels.h2d_async(dptr, buf_ptr, lay["bytes"], cs)
+            _kernels.event_record(cev, cs)
+            _kernels.stream_wait(stream, cev)
+        self._lens_stale = True  # the plan's own device lengths are refreshed on demand
+        staged = iter(dviews["inputs"])
+        q, k_new, v_new = (t if t.is_cuda else next(staged) for t in (q, k_new, v_new))
         if out is None:
             out = torch.empty(q.shape, dtype=torch.float32, device=table.device)
+        elif not out.is_cuda:
+            okey = out.data_ptr()
+            if okey not in self._pinned_out:
+                self._pinned_out[okey] = out.is_pinned()
+            if not self._pinned_out[okey]:
+                raise ShapeError("out must be a CUDA tensor or a pinned host tensor")
 
         def device_part():
-            lay["dev_head"].copy_(buf[:lay["bytes"]], non_blocking=True)
-            self.run_step(q, k_new, v_new, self.slots, spec, out)
+            if not side:
+                dviews["dbuf"].copy_(buf, non_blocking=True)
+            self.run_step(q, k_new, v_new, dviews["slots"], spec, out, lens=dviews["lens"])
 
         if not graph:
             device_part()
         else:
             graphs = lay.setdefault("graphs", {})
-            gkey = (slot_i, out.data_ptr(), id(spec), q.data_ptr(), k_new.data_ptr(), v_new.data_ptr())
+            gkey = (slot_i, side, out.data_ptr(), id(spec), q.data_ptr(), k_new.data_ptr(), v_new.data_ptr())
             g = graphs.get(gkey)
-            if g is None:
+            if g is not None:
+                if g[1] is not None:
+                    _kernels.graph_launch(g[1], stream)
+                else:
+                    g[0].replay()
+            else:
                 device_part()  # eager first run (also warms the launch path)
                 g = torch.cuda.CUDAGraph()
                 side = torch.cuda.Stream()
@@ -262,10 +307,9 @@ class DecodePlan:
                 with torch.cuda.stream(side), torch.cuda.graph(g, stream=side):
                     device_part()
                 torch.cuda.current_stream().wait_stream(side)
-                graphs[gkey] = g
-            else:
-                g.replay()
-        ev.record()
+                ex = g.raw_cuda_graph_exec()
+                graphs[gkey] = (g, ex if isinstance(ex, int) and ex else None)
+        _kernels.event_record(ev, stream)
         return out
 
 
