@@ -216,7 +216,7 @@ class DecodePlan:
                      "inputs": [dbuf[off:off + n].view(t.dtype).view(t.shape) for t, off, n in zip(host_in, offs, sizes)]}
             ring.append((buf, buf.numpy(), buf.data_ptr(), _kernels.host_event(), dbuf.data_ptr(), views,
                          _kernels.host_event()))
-            views["dbuf"] = dbuf
+            views["dbuf"] = dbuf  # keeps the device twin alive
         lay = {"bytes": o, "offs": offs, "sizes": sizes, "ring": ring, "i": 0}
         self._layouts[key] = lay
         return lay
@@ -283,9 +283,10 @@ class DecodePlan:
             if not self._pinned_out[okey]:
                 raise ShapeError("out must be a CUDA tensor or a pinned host tensor")
 
+        if not side:  # the staged bytes go over on the compute stream, ahead of the kernel
+            _kernels.h2d_async(dptr, buf_ptr, lay["bytes"], stream)
+
         def device_part():
-            if not side:
-                dviews["dbuf"].copy_(buf, non_blocking=True)
             self.run_step(q, k_new, v_new, dviews["slots"], spec, out, lens=dviews["lens"])
 
         if not graph:

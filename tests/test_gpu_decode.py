@@ -289,3 +289,32 @@ def test_fused_append_bit_exact_many_rows(kind, dtype):
             np.testing.assert_array_equal(f[f"{side}_payload"][0, 0], pk)
             np.testing.assert_array_equal(f[f"{side}_scale"][0, 0], sk)
             np.testing.assert_array_equal(f[f"{side}_zp"][0, 0], zk)
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_step_pinned_host_out_matches_device_out(graph):
+    """DecodePlan.step with a pinned host `out` (the kernel writes the result over the
+    bus) gives the same bytes as with a device `out`, step after step."""
+    H, G, d = 2, 4, 128
+    lens = [33, 70]
+    res = {}
+    for host_out in (False, True):
+        t, spec, layout = _build(len(lens), lens, H, G, d, 128, 16, "gaussian", Targets.KEYS_AND_VALUES, True,
+                                 seed=8, extra_pages=4)
+        plan = DecodePlan(t, [0, 1], extra_tokens=12)
+        rng = np.random.default_rng(99)
+        od = (torch.empty((2, G * H, d), dtype=torch.float32).pin_memory() if host_out
+              else torch.empty((2, G * H, d), dtype=torch.float32, device="cuda"))
+        outs = []
+        for _ in range(9):
+            q = torch.tensor(rng.standard_normal((2, G * H, d)), dtype=torch.bfloat16).pin_memory()
+            k = torch.tensor(rng.standard_normal((2, H, d)), dtype=torch.bfloat16).pin_memory()
+            v = torch.tensor(rng.standard_normal((2, H, d)), dtype=torch.bfloat16).pin_memory()
+            o = plan.step(q, k, v, spec, out=od, graph=graph)
+            torch.cuda.synchronize()
+            outs.append(o.cpu().clone())
+        res[host_out] = torch.stack(outs)
+        # the plan's own lengths follow the steps (refreshed on demand)
+        assert plan.run(torch.zeros((2, G * H, d), device="cuda"), spec).shape == (2, G * H, d)
+        assert [int(x) for x in plan.lens.cpu()] == [lens[0] + 9, lens[1] + 9]
+    assert torch.equal(res[False], res[True])
