@@ -226,17 +226,16 @@ class DecodePlan:
         """One serving decode step for every sequence of the plan: allocate the new
         token's slot (reference page order), then one fused append + decode launch.
         q (B, nq, d) and k_new/v_new (B, H, d) may be host tensors: they are staged
-        with the step metadata (slot ids, lengths) in a pinned ring buffer that goes
-        to the device in one copy on a side stream, so it overlaps the previous
-        step's kernel (every CTA of a head re-reads q and the lengths: reading them
-        over the bus in place was measured slower).  `out` may be a pinned host
-        tensor: the kernel then writes the result there directly (valid once the
-        step has completed, e.g. after torch.cuda.synchronize()).
+        with the step metadata (slot ids, lengths) in a ring of pinned buffers, each
+        going to its device twin in one copy ahead of the kernel (every CTA of a head
+        re-reads q and the lengths, so reading them over the bus in place was
+        measured slower; `side_copy` moves the copy to a side stream).  `out` may be
+        a pinned host tensor: the kernel then writes the result there directly
+        (valid once the step has completed, e.g. after torch.cuda.synchronize()).
 
-        graph=True replays the device part (that copy + the decode kernels) from a
-        CUDA graph captured on first use per pinned staging buffer; the block table
-        and lengths keep their addresses and the plan's max_len (its capacity) is
-        fixed, so only the host bookkeeping runs per step."""
+        graph=True launches the kernel from a CUDA graph captured on first use per
+        ring slot; the block table keeps its address and the plan's max_len (its
+        capacity) is fixed, so only the host bookkeeping runs per step."""
         table = self.table
         B = len(self.seqs)
         stream = torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
@@ -303,11 +302,11 @@ class DecodePlan:
             else:
                 device_part()  # eager first run (also warms the launch path)
                 g = torch.cuda.CUDAGraph()
-                side = torch.cuda.Stream()
-                side.wait_stream(torch.cuda.current_stream())
-                with torch.cuda.stream(side), torch.cuda.graph(g, stream=side):
+                cap = torch.cuda.Stream()
+                cap.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(cap), torch.cuda.graph(g, stream=cap):
                     device_part()
-                torch.cuda.current_stream().wait_stream(side)
+                torch.cuda.current_stream().wait_stream(cap)
                 ex = g.raw_cuda_graph_exec()
                 graphs[gkey] = (g, ex if isinstance(ex, int) and ex else None)
         _kernels.event_record(ev, stream)
