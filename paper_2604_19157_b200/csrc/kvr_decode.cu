@@ -25,8 +25,6 @@
 //    operand with movmatrix.trans (no shared memory round trip);
 //  * per-split (lse, o) partials go to a workspace; the last CTA of a
 //    (sequence, kv head) merges them and applies the inverse rotation.
-#include <cstdlib>
-
 #include "kvr_common.cuh"
 #include "kvr_internal.h"
 
@@ -55,11 +53,9 @@ struct DecodeParams {
   const int64_t* new_slot;  // [B] slot id of the appended token (it is the last of seq_lens[b])
   uint32_t* flags;
   unsigned long long* trace;  // optional: per CTA 8 globaltimer stamps (ns), see kvr_debug_decode_trace
-  int pre_groups;   // ring groups per warp requested before griddepcontrol.wait (default 1: a
-                    // deeper pre-wait burst queues the query load behind it; measured)
-  int merge_late;   // decode_merge_kernel releases its dependents after its loads
-  int evict_first;  // KV cells are streamed with an L2 evict-first policy
-  int merge_inline;   // splits > 1 without a cluster: the last CTA merges (ws_cnt counters)
+  int pre_groups;    // ring groups per warp requested before griddepcontrol.wait
+  int evict_first;   // KV cells are streamed with an L2 evict-first policy
+  int merge_inline;  // splits > 1 without a cluster: the last CTA merges (ws_cnt counters)
 };
 
 KVR_DEV unsigned long long clk64() {
@@ -329,6 +325,15 @@ KVR_DEV const float* dsmem_ptr(const float* local, uint32_t rank) {
 constexpr int NWARPS = 16;       // one CTA per SM, 4 warps per SM sub-partition (128-register budget)
 constexpr int CELL = 2208;       // one cell: T = 16 tokens of one head, d = 128
 constexpr int RING_CELLS = 4;    // cells in flight per warp (NSTG stages of C cells)
+#ifndef KVR_PREWAIT_GROUPS
+#define KVR_PREWAIT_GROUPS 1
+#endif
+#ifndef KVR_EVICT_FIRST
+#define KVR_EVICT_FIRST 1
+#endif
+#ifndef KVR_MERGE_INLINE
+#define KVR_MERGE_INLINE 1
+#endif
 constexpr int MAX_SPLITS = 256;
 constexpr int MERGE_INLINE_MAX = 32;  // up to this many splits the last CTA merges them inline
 
@@ -1142,7 +1147,7 @@ __global__ void __launch_bounds__(MERGE_THREADS)
     tr = p.trace + ((int64_t)gridDim.z * S * H + ((int64_t)b * H + h) * gridDim.x + j) * 16;
   if (tr) tr[0] = gtimer();
   pdl_wait();
-  if (!p.merge_late) pdl_launch_dependents();
+  pdl_launch_dependents();
   if (tr) tr[1] = gtimer();
   // o-values of this thread's splits s = sl, sl + 4, ... (first 16 preloaded with the lse)
   float ov[16];
@@ -1157,7 +1162,6 @@ __global__ void __launch_bounds__(MERGE_THREADS)
   if (lane == 0) s_red[warp] = m;
   __syncthreads();
   if (tr) tr[3] = gtimer();
-  if (p.merge_late) pdl_launch_dependents();
   m = s_red[lane & 15];
 #pragma unroll
   for (int o = 8; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -1458,11 +1462,8 @@ template <int NT, int ORDER, bool APP>
 static int launch_sel(dim3 grid, size_t smem, cudaStream_t st, const DecodeParams& p, const Signs& sg) {
   if (p.use_cluster && cluster_ok<NT, ORDER, APP>((int)grid.y, smem))
     return launch_one<NT, ORDER, APP, true>(grid, smem, st, p, sg);
-  // KVR_DEBUG_PART (profiling only): 1 = decode grid alone, 2 = merge grid alone
-  static const int part = getenv("KVR_DEBUG_PART") ? atoi(getenv("KVR_DEBUG_PART")) : 0;
-  if (part != 2)
-    if (int rc = launch_one<NT, ORDER, APP, false>(grid, smem, st, p, sg)) return rc;
-  return (p.splits > 1 && !p.merge_inline && part != 1) ? launch_merge<ORDER>(p, sg, st) : 0;
+  if (int rc = launch_one<NT, ORDER, APP, false>(grid, smem, st, p, sg)) return rc;
+  return (p.splits > 1 && !p.merge_inline) ? launch_merge<ORDER>(p, sg, st) : 0;
 }
 
 template <int NT, bool APP>
@@ -1506,13 +1507,12 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
   p.flags = flags;
   p.trace = g_trace;
   p.max_len = max_len;
-  static const int env_pre = getenv("KVR_PREWAIT") ? atoi(getenv("KVR_PREWAIT")) : 1;
-  static const int env_ml = getenv("KVR_MERGE_LATE") ? atoi(getenv("KVR_MERGE_LATE")) : 0;
-  p.pre_groups = env_pre;
-  p.merge_late = env_ml;
-  static const int env_ef = getenv("KVR_EVICT_FIRST") ? atoi(getenv("KVR_EVICT_FIRST")) : 1;
-  p.evict_first = env_ef;
-  static const int env_mi = getenv("KVR_MERGE_INLINE") ? atoi(getenv("KVR_MERGE_INLINE")) : 1;
+  // tuning switches (compile-time, for A/B builds with tools/build_variants.py; the
+  // defaults are the measured best): one ring group per warp before the wait (a
+  // full-ring burst queues the query load behind it), evict-first KV streaming,
+  // inline split merge for 9..32 splits
+  p.pre_groups = KVR_PREWAIT_GROUPS;
+  p.evict_first = KVR_EVICT_FIRST;
   int l2 = 0;
   while ((1 << l2) < pool.P) ++l2;
   const bool pow2 = (1 << l2) == pool.P;
@@ -1545,7 +1545,7 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
 #else
     p.use_cluster = 0;
 #endif
-    p.merge_inline = env_mi && !p.use_cluster && splits > 1 && splits <= MERGE_INLINE_MAX;
+    p.merge_inline = KVR_MERGE_INLINE && !p.use_cluster && splits > 1 && splits <= MERGE_INLINE_MAX;
     if (new_slot)
       return p.G == 8 ? launch_tma<2, true>(p, sg, grid, smem, ord, st) : launch_tma<1, true>(p, sg, grid, smem, ord, st);
     return p.G == 8 ? launch_tma<2, false>(p, sg, grid, smem, ord, st) : launch_tma<1, false>(p, sg, grid, smem, ord, st);
