@@ -65,6 +65,21 @@ if os.path.exists(lc):
         lines.append(f"  {k:70s} n={len(d):4d} mean={sum(d) / len(d) / 1e3:8.2f} us share={sum(d) / tot:6.1%} "
                      f"dram_rd/launch={sum(m['dram__bytes_read.sum']) / len(d) / 1e6:8.2f} MB")
 os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+if os.path.exists(lc):  # the per-launch list itself, one row per launch
+    launches = {}
+    for r in rows[hi + 1:]:
+        if len(r) > vi:
+            d = launches.setdefault(r[h.index("ID")], {"kernel": r[ki].split("(")[0], "grid": r[h.index("Grid Size")],
+                                                       "block": r[h.index("Block Size")]})
+            d[r[mi]] = r[vi]
+    cols = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum"]
+    with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_launches.csv"), "w", newline="") as f:
+        f.write("# ncu --metrics " + ",".join(cols) + " --clock-control none\n")
+        f.write("# command: python bench.py --steps 40 --warmup 3 --no-cpu --sets 2 --quick (tools/gpu_profile.sh)\n")
+        w = csv.writer(f)
+        w.writerow(["ID", "kernel", "grid", "block"] + cols)
+        for i, d in launches.items():
+            w.writerow([i, d["kernel"], d["grid"], d["block"]] + [d.get(c, "") for c in cols])
 with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.txt"), "w") as f:
     f.write("\n".join(lines) + "\n")
 if traffic:
