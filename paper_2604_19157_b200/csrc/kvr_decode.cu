@@ -1367,15 +1367,21 @@ int kvr_pick_splits(int batch, int H, int max_len, int P) {
   if (units <= 0 || tiles <= 0) return 1;
   int best = 1;
   double best_cost = 1e300;
+  const long fill = sms / units;  // splits that fill the SMs in one wave
   for (int s = 1; s <= MAX_SPLITS; ++s) {
     const int per = (tiles + s - 1) / s;
     if (s > 1 && per < 2 * NWARPS) break;
+    // above the inline-merge range only multiples of 16 and the one-wave fill are
+    // tried (measured on C5 128k: other counts run 5-15 % slower)
+    if (s > MERGE_INLINE_MAX && (s % 16) && s != fill) continue;
     const long ctas = units * s;
     const long waves = (ctas + sms - 1) / sms;
     // in tile-times (one tile ~ 1/15 of a warp's 0.9 us per cell): a CTA's fixed
     // prologue + epilogue ~ 80, its partial write (+ read in the merge) ~ 2, and the
-    // latency of the last CTA's merge chain once
-    const double cost = (double)waves * (80.0 + per + (s > 1 ? 2.0 : 0.0)) + (s > 1 ? 24.0 + 0.25 * s : 0.0);
+    // latency of the split merge once (inline up to 32 splits; the merge kernel's
+    // grows faster with the split count)
+    const double merge = s <= MERGE_INLINE_MAX ? 24.0 + 0.25 * s : 32.0 + 0.5 * (s - MERGE_INLINE_MAX);
+    const double cost = (double)waves * (80.0 + per + (s > 1 ? 2.0 : 0.0)) + (s > 1 ? merge : 0.0);
     if (cost < best_cost * 0.999) {
       best_cost = cost;
       best = s;
