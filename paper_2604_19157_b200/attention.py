@@ -71,7 +71,6 @@ class DecodePlan:
         self.slots = self._dev[:8 * B].view(torch.int64)
         self.lens = self._dev[8 * B:12 * B].view(torch.int32)
         self.lens.copy_(lens)
-        self._pinned_out = {}
         self._copy_stream = None
         self.side_copy = False  # True: staged inputs go over on a side stream (measured slower end to end)
         self._lens_stale = False  # step() passes its own device copy of the lengths
@@ -275,12 +274,8 @@ class DecodePlan:
         q, k_new, v_new = (t if t.is_cuda else next(staged) for t in (q, k_new, v_new))
         if out is None:
             out = torch.empty(q.shape, dtype=torch.float32, device=table.device)
-        elif not out.is_cuda:
-            okey = out.data_ptr()
-            if okey not in self._pinned_out:
-                self._pinned_out[okey] = out.is_pinned()
-            if not self._pinned_out[okey]:
-                raise ShapeError("out must be a CUDA tensor or a pinned host tensor")
+        elif not out.is_cuda and not out.is_pinned():
+            raise ShapeError("out must be a CUDA tensor or a pinned host tensor")
 
         if not side:  # the staged bytes go over on the compute stream, ahead of the kernel
             _kernels.h2d_async(dptr, buf_ptr, lay["bytes"], stream)
