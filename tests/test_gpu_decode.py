@@ -318,3 +318,44 @@ def test_step_pinned_host_out_matches_device_out(graph):
         assert plan.run(torch.zeros((2, G * H, d), device="cuda"), spec).shape == (2, G * H, d)
         assert [int(x) for x in plan.lens.cpu()] == [lens[0] + 9, lens[1] + 9]
     assert torch.equal(res[False], res[True])
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_decode_full_size_c5_uniform_keys(fused):
+    """C5 at full size (1 kv head, 4 q heads, 1,048,576 cached tokens: 148 splits and
+    the split-merge kernel) through a size-independent property: with every key row
+    identical the softmax is uniform, so the output is the mean of the stored
+    values, undone by the inverse rotation -- computed exactly from the dequantized
+    pool in f64."""
+    H, G, d, L = 1, 4, 128, 1 << 20
+    layout = HeadLayout(num_q_heads=G * H, num_kv_heads=H, head_dim=d, rot_order=128, page_tokens=16)
+    t = PageTable(layout, num_pages=L // 16 + 2)
+    spec = RotationSpec(order=128, signs=make_signs(2, 0, d, 128), targets=Targets.KEYS_AND_VALUES)
+    t.create_sequence(0)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    krow = torch.randn((1, H, d), generator=gen, device="cuda").bfloat16()
+    n0 = L - 1 if fused else L
+    slots = torch.from_numpy(t.alloc.reserve(0, n0)).cuda()
+    for c0 in range(0, n0, 1 << 16):
+        n = min(1 << 16, n0 - c0)
+        v = torch.randn((n, H, d), generator=gen, device="cuda").bfloat16()
+        t.store_slots(krow.expand(n, H, d).contiguous(), v, slots[c0:c0 + n], spec)
+    q = torch.randn((1, G * H, d), generator=gen, device="cuda").bfloat16()
+    if fused:  # the step's token is written (same key row) and attended in one launch
+        plan = DecodePlan(t, [0], extra_tokens=1)
+        vnew = torch.randn((1, H, d), generator=gen, device="cuda").bfloat16()
+        out = plan.step(q, krow, vnew, spec)
+    else:
+        plan = DecodePlan(t, [0])
+        out = plan.run(q, spec)
+    torch.cuda.synchronize()
+    assert plan.splits > 32  # the split-merge kernel path
+    kd, vd = t.read_sequence_device([0], torch.float64)
+    assert t.sequence_length(0) == L
+    assert torch.equal(kd[0, 0], kd[0, L - 1])  # identical stored keys
+    mean_v = vd[0, :L, 0].mean(dim=0, keepdim=True).cpu().numpy()
+    ref = O.unrotate_rows(mean_v, 128, spec.signs)[0]
+    got = out[0].double().cpu().numpy()
+    err = np.abs(got - ref[None, :]).max() / np.abs(ref).max()
+    print("C5 full size uniform-key rel err", err)
+    assert err <= TOL
