@@ -1095,23 +1095,25 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
     if (!*s_last) return;
     mbar_wait(mbar, 0);
     KVR_STAMP(7);  // merge inputs landed
+    // split weights once per q head (warp j, lane = split): w_s = 2^(lse_s - max),
+    // normalised by their sum; then every (head, dim) thread is S FMAs
+    float* sw = s_qrot;  // [8][32] normalised split weights (the query copy is dead)
+    if (warp < G) {
+      const float l = lane < S ? sl[lane * 8 + warp] : -INFINITY;
+      const float mx = warp_max(l);
+      const float w = (l == -INFINITY) ? 0.f : ex2f(l - mx);
+      const float tot = warp_sum(w);
+      sw[warp * 32 + lane] = tot > 0.f ? w / tot : 0.f;
+    }
+    __syncthreads();
 #pragma unroll 1
     for (int x = threadIdx.x; x < G * 128; x += blockDim.x) {
       const int j = x >> 7, dd = x & 127;
-      float mx = -INFINITY;
+      const float* wj = sw + j * 32;
+      float ot = 0.f;
 #pragma unroll 4
-      for (int sp = 0; sp < S; ++sp) mx = fmaxf(mx, sl[sp * 8 + j]);
-      float tot = 0.f, ot = 0.f;
-      if (mx != -INFINITY) {
-#pragma unroll 4
-        for (int sp = 0; sp < S; ++sp) {
-          const float l = sl[sp * 8 + j];
-          const float w = (l == -INFINITY) ? 0.f : ex2f(l - mx);
-          tot += w;
-          ot += w * so[(sp * 8 + j) * 128 + dd];
-        }
-      }
-      obuf[j * 128 + dd] = tot > 0.f ? ot / tot : 0.f;
+      for (int sp = 0; sp < S; ++sp) ot += wj[sp] * so[(sp * 8 + j) * 128 + dd];
+      obuf[j * 128 + dd] = ot;
     }
     __syncthreads();
     if (warp < G) emit_head<ORDER>(p, sgw, b, h, warp, obuf + warp * 128, lane);
