@@ -227,8 +227,8 @@ class DecodePlan:
         q (B, nq, d) and k_new/v_new (B, H, d) may be host tensors: they are staged
         with the step metadata (slot ids, lengths) in a ring of pinned buffers, each
         going to its device twin in one copy ahead of the kernel (every CTA of a head
-        re-reads q and the lengths, so reading them over the bus in place was
-        measured slower; `side_copy` moves the copy to a side stream).  `out` may be
+        re-reads q, so reading the staged bytes over the bus in place was measured
+        slower (tools/e2e_probe.py); `side_copy` moves the copy to a side stream).  `out` may be
         a pinned host tensor: the kernel then writes the result there directly
         (valid once the step has completed, e.g. after torch.cuda.synchronize()).
 

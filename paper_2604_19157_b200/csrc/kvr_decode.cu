@@ -114,6 +114,23 @@ KVR_DEV float load_q(const void* q, int dtype, int64_t i) {
   return reinterpret_cast<const float*>(q)[i];
 }
 
+// Elements i..i+3 (i % 4 == 0) of the query as one 8-B (bf16/f16) or 16-B (f32) load.
+KVR_DEV void load_q4(const void* q, int dtype, int64_t i, float (&x)[4]) {
+  if (dtype == KVR_F32) {
+    const float4 v = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(q) + i);
+    x[0] = v.x;
+    x[1] = v.y;
+    x[2] = v.z;
+    x[3] = v.w;
+    return;
+  }
+  const uint2 w = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(q) + i);
+  const uint32_t h[4] = {w.x & 0xFFFFu, w.x >> 16, w.y & 0xFFFFu, w.y >> 16};
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    x[u] = dtype == KVR_BF16 ? __uint_as_float(h[u] << 16) : __half2float(__ushort_as_half((unsigned short)h[u]));
+}
+
 // Cell of (sequence b, token t, head h) and the token's index inside it.
 KVR_DEV const uint8_t* token_cell(const DecodeParams& p, int b, int t, int h, int& ci) {
   const int page = p.bt[(int64_t)b * p.bt_stride + (t >> p.log2P)];
@@ -472,15 +489,23 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   };
   int wnext = page_window(1), win_idx = 0;
   const uint8_t* wcur = window_addr(0, page_window(0));
-  const int len_raw = __ldg(&p.lens[b]);
+  // the length and the new token's slot (host-written, read before the wait): one
+  // load per CTA, broadcast through shared memory (they may live in mapped host memory)
+  int* s_len = reinterpret_cast<int*>(s_sumq + 58);
+  long long* s_slot = reinterpret_cast<long long*>(s_sumq + 60);
+  if (threadIdx.x == 0) {
+    *s_len = __ldg(&p.lens[b]);
+    if (APPEND) *s_slot = __ldg(&p.new_slot[b]);
+  }
   // this lane's word of the sign vector (dims 4l..4l+3), read from the parameter
   // bank before the dependency wait (0 = no flips)
   const uint32_t sgw = p.has_signs ? signs.w[lane >> 3] : 0u;
-  const int64_t new_slot = APPEND ? __ldg(&p.new_slot[b]) : -1;  // host-written, like lens: read with it
   if (threadIdx.x < NWARPS * RING_CELLS) mbar_init(&bars[threadIdx.x], 1);
   reinterpret_cast<uint2*>(sfrag)[threadIdx.x] = make_uint2(0u, 0u);  // 4 KB of query digits (padding = 0)
   fence_mbar_init();
   __syncthreads();
+  const int len_raw = *s_len;
+  const int64_t new_slot = APPEND ? *s_slot : -1;
 
   const int len = min(len_raw, p.max_len);
   // APPEND: the step's token (position len - 1) is written and scored by the writer
@@ -553,11 +578,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
     atomicOr(p.flags, KVR_FLAG_LEN_OVERFLOW);
 
   float qx[4] = {0.f, 0.f, 0.f, 0.f};
-  if (warp < G) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      qx[u] = load_q(p.q, p.q_dtype, ((int64_t)b * p.nq + (int64_t)h * G + warp) * 128 + 4 * lane + u);
-  }
+  if (warp < G) load_q4(p.q, p.q_dtype, ((int64_t)b * p.nq + (int64_t)h * G + warp) * 128 + 4 * lane, qx);
   if (p.trace) {  // q landed
     asm volatile("" ::"f"(qx[0]), "f"(qx[1]), "f"(qx[2]), "f"(qx[3]));
     KVR_STAMP(13);
@@ -1530,7 +1551,8 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
   if (!pow2) return KVR_ERR_UNSUPPORTED;
   const bool tma_ok = pool.prec == KVR_PREC_INT4 && pool.d == 128 && pool.T == 16 &&
                       (p.G == 1 || p.G == 2 || p.G == 4 || p.G == 8) &&
-                      (reinterpret_cast<uintptr_t>(pool.base) & 15) == 0 && (pool.cell_bytes & 15) == 0;
+                      (reinterpret_cast<uintptr_t>(pool.base) & 15) == 0 && (pool.cell_bytes & 15) == 0 &&
+                      (reinterpret_cast<uintptr_t>(q) & 15) == 0;  // vector query loads
   if (tma_ok) {
     if (splits <= 0) splits = kvr_pick_splits(batch, pool.H, max_len, pool.P);
     if (splits > MAX_SPLITS) splits = MAX_SPLITS;
