@@ -114,8 +114,14 @@ KVR_DEV float load_q(const void* q, int dtype, int64_t i) {
   return reinterpret_cast<const float*>(q)[i];
 }
 
-// Elements i..i+3 (i % 4 == 0) of the query as one 8-B (bf16/f16) or 16-B (f32) load.
+// Elements i..i+3 (i % 4 == 0) of the query as one 8-B (bf16/f16) or 16-B (f32) load
+// (element loads when the query is not aligned for that).
 KVR_DEV void load_q4(const void* q, int dtype, int64_t i, float (&x)[4]) {
+  if (reinterpret_cast<uintptr_t>(q) & (dtype == KVR_F32 ? 15 : 7)) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = load_q(q, dtype, i + u);
+    return;
+  }
   if (dtype == KVR_F32) {
     const float4 v = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(q) + i);
     x[0] = v.x;
@@ -1551,8 +1557,7 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
   if (!pow2) return KVR_ERR_UNSUPPORTED;
   const bool tma_ok = pool.prec == KVR_PREC_INT4 && pool.d == 128 && pool.T == 16 &&
                       (p.G == 1 || p.G == 2 || p.G == 4 || p.G == 8) &&
-                      (reinterpret_cast<uintptr_t>(pool.base) & 15) == 0 && (pool.cell_bytes & 15) == 0 &&
-                      (reinterpret_cast<uintptr_t>(q) & 15) == 0;  // vector query loads
+                      (reinterpret_cast<uintptr_t>(pool.base) & 15) == 0 && (pool.cell_bytes & 15) == 0;
   if (tma_ok) {
     if (splits <= 0) splits = kvr_pick_splits(batch, pool.H, max_len, pool.P);
     if (splits > MAX_SPLITS) splits = MAX_SPLITS;

@@ -359,3 +359,17 @@ def test_decode_full_size_c5_uniform_keys(fused):
     err = np.abs(got - ref[None, :]).max() / np.abs(ref).max()
     print("C5 full size uniform-key rel err", err)
     assert err <= TOL
+
+
+def test_decode_unaligned_query_view():
+    """A query that is a contiguous view at a 2-byte offset (not 8-B aligned) decodes
+    the same as an aligned copy (the kernel falls back to element loads)."""
+    H, G, d = 2, 4, 128
+    lens = [40, 90]
+    t, spec, layout = _build(len(lens), lens, H, G, d, 128, 16, "gaussian", Targets.KEYS_AND_VALUES, True, seed=6)
+    base = torch.randn(2 * G * H * d + 1, device="cuda").bfloat16()
+    q_view = base[1:].view(2, G * H, d)  # storage offset of one element
+    assert q_view.data_ptr() % 8 != 0 and q_view.is_contiguous()
+    a = decode_batch(q_view, t, [0, 1], spec=spec)
+    b = decode_batch(q_view.clone(), t, [0, 1], spec=spec)
+    assert torch.equal(a, b)
