@@ -222,13 +222,13 @@ KVR_DEV void append_rows_exact(const DecodeParams& p, const Signs& sg, int b, in
     }
 #pragma unroll
   for (int k = 0; (4 << k) < ORDER; ++k) {  // half = 4 << k: partner lane = lane ^ (1 << k)
-    const bool upper = (lane >> k) & 1;
+    const double sgn = ((lane >> k) & 1) ? -1.0 : 1.0;  // upper half of the pair: o - x
 #pragma unroll
     for (int sd = 0; sd < 2; ++sd)
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const double o = __shfl_xor_sync(0xffffffffu, x[sd][u], 1 << k);
-        if (rot[sd]) x[sd][u] = upper ? o - x[sd][u] : x[sd][u] + o;
+        if (rot[sd]) x[sd][u] = fma(sgn, x[sd][u], o);  // o -+ x, one rounding
       }
   }
   if (tr) tr[15] = clk64();  // rotated
@@ -415,11 +415,11 @@ KVR_DEV void emit_head(const DecodeParams& p, uint32_t sgw, int b, int h, int j,
     x[3] = a1 - a3;
 #pragma unroll
     for (int k = 0; (4 << k) < ORDER; ++k) {
-      const bool upper = (lane >> k) & 1;
+      const float sgn = ((lane >> k) & 1) ? -1.f : 1.f;  // upper half of the pair: o - x
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const float o = __shfl_xor_sync(0xffffffffu, x[u], 1 << k);
-        x[u] = upper ? o - x[u] : x[u] + o;
+        x[u] = fmaf(sgn, x[u], o);  // o -+ x, one rounding
       }
     }
     const float inv = (float)(1.0 / sqrt((double)ORDER));
@@ -611,11 +611,11 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
       x[3] = a1 - a3;
 #pragma unroll
       for (int k = 0; (4 << k) < ORDER; ++k) {
-        const bool upper = (lane >> k) & 1;
+        const float sgn = ((lane >> k) & 1) ? -1.f : 1.f;  // upper half of the pair: o - x
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const float o = __shfl_xor_sync(0xffffffffu, x[u], 1 << k);
-          x[u] = upper ? o - x[u] : x[u] + o;
+          x[u] = fmaf(sgn, x[u], o);  // o -+ x, one rounding
         }
       }
       const float inv = (float)(1.0 / sqrt((double)ORDER));
@@ -1229,11 +1229,11 @@ __global__ void __launch_bounds__(MERGE_THREADS)
       x[3] = a1 - a3;
 #pragma unroll
       for (int k = 0; (4 << k) < ORDER; ++k) {
-        const bool upper = (lane >> k) & 1;
+        const float sgn = ((lane >> k) & 1) ? -1.f : 1.f;  // upper half of the pair: o - x
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const float o = __shfl_xor_sync(0xffffffffu, x[u], 1 << k);
-          x[u] = upper ? o - x[u] : x[u] + o;
+          x[u] = fmaf(sgn, x[u], o);  // o -+ x, one rounding
         }
       }
       const float inv = (float)(1.0 / sqrt((double)ORDER));

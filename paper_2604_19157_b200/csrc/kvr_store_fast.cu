@@ -74,11 +74,11 @@ __device__ __noinline__ uint32_t warp_exact_row(const uint8_t* buf, int src, con
     x[3] = a1 - a3;
 #pragma unroll
     for (int k = 0; (4 << k) < ORDER; ++k) {
-      const bool upper = (lane >> k) & 1;
+      const double sgn = ((lane >> k) & 1) ? -1.0 : 1.0;  // upper half of the pair: o - x
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const double o = __shfl_xor_sync(0xffffffffu, x[u], 1 << k);
-        x[u] = upper ? o - x[u] : x[u] + o;
+        x[u] = fma(sgn, x[u], o);  // o -+ x, one rounding
       }
     }
     const double inv = 1.0 / sqrt((double)ORDER);
