@@ -318,6 +318,18 @@ KVR_DEV bool mbar_test(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0u;
 }
+// One lane of the (converged) warp, chosen by the hardware: elect.sync keeps the
+// issuing region warp-uniform for the compiler, so the bulk-copy operands move to
+// uniform registers without a per-lane loop.
+KVR_DEV bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(pred));
+  return pred != 0;
+}
 KVR_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 // Programmatic dependent launch: wait for the previous grid in the stream / let
 // the next one start its prologue (griddepcontrol, sm_90+).
@@ -546,7 +558,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
     for (int c = 0; c < C; ++c)
       src[c] = reinterpret_cast<const uint8_t*>(
           __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(wcur), (C * k + c) & 31));
-    if (lane == 0) {
+    if (elect_one()) {
       const int t0 = tile_of(C * k);
       const int nc = min(C, hi - t0);
       const int s = k % NSTG;
