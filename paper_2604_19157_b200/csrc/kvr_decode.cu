@@ -318,18 +318,6 @@ KVR_DEV bool mbar_test(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0u;
 }
-// One lane of the (converged) warp, chosen by the hardware: elect.sync keeps the
-// issuing region warp-uniform for the compiler, so the bulk-copy operands move to
-// uniform registers without a per-lane loop.
-KVR_DEV bool elect_one() {
-  uint32_t pred = 0;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "elect.sync _|p, 0xffffffff;\n\t"
-      "selp.u32 %0, 1, 0, p;\n}"
-      : "=r"(pred));
-  return pred != 0;
-}
 KVR_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 // Programmatic dependent launch: wait for the previous grid in the stream / let
 // the next one start its prologue (griddepcontrol, sm_90+).

@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(FS_WARPS * 32, KVR_FS_MINB)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   int tile = blockIdx.x * FS_WARPS + wib;
-  if (tile < total_tiles && lane == 0) issue(tile, 0);
+  if (tile < total_tiles && elect_one()) issue(tile, 0);
   uint32_t phases = 0u;  // bit b: parity of buffer b
   int64_t slot_cur[2];
   slot_pair(tile, slot_cur);
@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(FS_WARPS * 32, KVR_FS_MINB)
   for (int it = 0; tile < total_tiles; ++it, tile += warp_stride) {
     const int bsel = it & 1;
     const int next = tile + warp_stride;
-    if (next < total_tiles && lane == 0) issue(next, bsel ^ 1);
+    if (next < total_tiles && elect_one()) issue(next, bsel ^ 1);
     const int64_t slot[2] = {slot_cur[0], slot_cur[1]};
     slot_pair(next, slot_cur);  // prefetch: consumed one tile later
     mbar_wait(&bars[bsel], (phases >> bsel) & 1u);
