@@ -716,8 +716,10 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   }
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
-    sumq[nt] = s_sumq[4 * nt + i];
-    kscale[nt] = s_ksc[4 * nt + i];
+    // the int8 QK yields 16 S (integer combination of the nibble planes): fold the
+    // 1/16 into the query sum and the scale (powers of two: the same roundings)
+    sumq[nt] = s_sumq[4 * nt + i] * (QK_INT8 ? 16.0f : 1.0f);
+    kscale[nt] = s_ksc[4 * nt + i] * (QK_INT8 ? 0.0625f : 1.0f);
   }
 
   // ---- the writer warp scores the new token (logits in log2 units)
@@ -783,7 +785,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
             imma16832(m < 2 ? dlo : dhi, kw0[w] & mask, kw1[w] & mask, kw0[w + 1] & mask, kw1[w + 1] & mask, b0.x, b0.y);
           }
   #pragma unroll
-          for (int q = 0; q < 4; ++q) sp[t][q] = (float)dlo[q] + 0.0625f * (float)dhi[q];
+          for (int q = 0; q < 4; ++q) sp[t][q] = (float)(dlo[q] * 16 + dhi[q]);  // 16 S, exact (< 2^24)
         }
   #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
