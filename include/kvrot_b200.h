@@ -172,8 +172,10 @@ int kvr_dequantize_pages(const kvr_pool* pool, const int32_t* block_table, int32
  * Both decode entry points launch with programmatic dependent launch: before their
  * dependency wait they read block_table, seq_lens, new_slot and pool cells older
  * than the last two tokens of each sequence (a preceding kernel that writes those
- * must not trigger launch_dependents early).  With more than 8 splits a second,
- * split-merge kernel follows the decode kernel on the stream.
+ * must not trigger launch_dependents early).  Splits merge inside the decode
+ * kernel up to 32 splits (a thread-block cluster up to 8, the last CTA of each
+ * (sequence, kv head) above that); with more, a second split-merge kernel follows
+ * the decode kernel on the stream.
  */
 size_t kvr_decode_workspace_bytes(int32_t batch, int32_t num_kv_heads, int32_t num_q_heads,
                                   int32_t head_dim, int32_t num_splits);
