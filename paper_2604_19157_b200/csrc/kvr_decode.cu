@@ -747,7 +747,6 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[nt][m][c] = 0.f;
   }
-  float Mth = -INFINITY;  // min over columns of M + 7: a logit above it forces a rescale
 
   // ---- main loop over this warp's groups of C tiles ----------------------------------
   KVR_STAMP(2);  // main loop start
@@ -837,7 +836,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
 
     // ---- logits from the sidecars (sentinel rows: the scale slot holds the
     // offset and the codes are 0)
-    float l0[C][NT], l1[C][NT], lgv0[C], lgv1[C], zv0[C], zv1[C];
+    float l0[C][NT], l1[C][NT], svc0[C], svc1[C], zv0[C], zv1[C];
     bool sentinel = false;
 #pragma unroll
     for (int c = 0; c < C; ++c) sentinel |= (f[c].kz0 | f[c].kz1 | f[c].vz0 | f[c].vz1) > 15u;
@@ -854,22 +853,14 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
         if (f[c].vz0 == 0xFFu) { zv0[c] = -sv0; sv0 = 1.f; }
         if (f[c].vz1 == 0xFFu) { zv1[c] = -sv1; sv1 = 1.f; }
       }
-      lgv0[c] = __log2f(sv0);
-      lgv1[c] = __log2f(sv1);
+      svc0[c] = sv0;
+      svc1[c] = sv1;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         l0[c][nt] = (scv[c][nt][0] - zk0 * sumq[nt]) * (sk0 * kscale[nt]);
         l1[c][nt] = (scv[c][nt][2] - zk1 * sumq[nt]) * (sk1 * kscale[nt]);
       }
     }
-    float b0[C][NT], b1[C][NT];
-#pragma unroll
-    for (int c = 0; c < C; ++c)
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        b0[c][nt] = l0[c][nt] + lgv0[c];  // log2(p * s_v)
-        b1[c][nt] = l1[c][nt] + lgv1[c];
-      }
     if (tg + C > hi || tg + C >= n_tiles) {  // a missing or partial tile in this group
 #pragma unroll
       for (int c = 0; c < C; ++c) {
@@ -877,26 +868,37 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
         const bool in = tg + c < hi;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          if (!in || t0 >= len_kv) l0[c][nt] = b0[c][nt] = -INFINITY;
-          if (!in || t0 + 8 >= len_kv) l1[c][nt] = b1[c][nt] = -INFINITY;
+          if (!in || t0 >= len_kv) l0[c][nt] = -INFINITY;
+          if (!in || t0 + 8 >= len_kv) l1[c][nt] = -INFINITY;
         }
         if (!in) zv0[c] = zv1[c] = 0.f;
       }
     }
+    // probabilities at the current reference point, p = 2^(l - M), and the PV
+    // weights w = p s_v.  Lazy rescaling: M only moves when a weight exceeds 2^7
+    // (log2(p s_v) > M + 7, so w * 2^8 stays inside fp16 range) or on the first logits
+    float pr0[C][NT], pr1[C][NT];
     bool over = false;
 #pragma unroll
-    for (int c = 0; c < C; ++c)
+    for (int nt = 0; nt < NT; ++nt) {
+      const float ms = (M[nt] == -INFINITY) ? 0.f : M[nt];
+      float lmax = -INFINITY;
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) over |= fmaxf(b0[c][nt], b1[c][nt]) > Mth;
-    // lazy rescaling: the reference point M only moves when a logit exceeds it by
-    // > 2^7, so w = 2^(b - M) <= 128 and w * 2^8 stays inside fp16 range
+      for (int c = 0; c < C; ++c) {
+        pr0[c][nt] = ex2f(l0[c][nt] - ms);
+        pr1[c][nt] = ex2f(l1[c][nt] - ms);
+        over |= fmaxf(pr0[c][nt] * svc0[c], pr1[c][nt] * svc1[c]) > 128.0f;
+        lmax = fmaxf(lmax, fmaxf(l0[c][nt], l1[c][nt]));
+      }
+      over |= M[nt] == -INFINITY && lmax > -INFINITY;
+    }
     if (__any_sync(0xffffffffu, over)) {
-      Mth = INFINITY;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        float tm = -INFINITY;
+        float tm = -INFINITY;  // max of log2(p s_v) over the group
 #pragma unroll
-        for (int c = 0; c < C; ++c) tm = fmaxf(tm, fmaxf(b0[c][nt], b1[c][nt]));
+        for (int c = 0; c < C; ++c)
+          tm = fmaxf(tm, fmaxf(l0[c][nt] + __log2f(svc0[c]), l1[c][nt] + __log2f(svc1[c])));
         tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 4));
         tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 8));
         tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 16));
@@ -909,8 +911,12 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
 #pragma unroll
             for (int q = 0; q < 4; ++q) acc[nt][m][q] *= alpha;
           M[nt] = tm;
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            pr0[c][nt] = ex2f(l0[c][nt] - tm);
+            pr1[c][nt] = ex2f(l1[c][nt] - tm);
+          }
         }
-        Mth = fminf(Mth, M[nt] + 7.0f);
       }
     }
 
@@ -919,9 +925,8 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
       uint32_t wlo[NT], whi[NT];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        const float ms = (M[nt] == -INFINITY) ? 0.f : M[nt];
-        const float w0 = ex2f(b0[c][nt] - ms), w1 = ex2f(b1[c][nt] - ms);  // = p_t * s_v * 2^(.)
-        const float p0 = ex2f(l0[c][nt] - ms), p1 = ex2f(l1[c][nt] - ms);  // = p_t * 2^(.)
+        const float p0 = pr0[c][nt], p1 = pr1[c][nt];  // = p_t * 2^(.)
+        const float w0 = p0 * svc0[c], w1 = p1 * svc1[c];  // = p_t * s_v * 2^(.)
         lsum[nt] += p0 + p1;
         Zs[nt] += w0 * zv0[c] + w1 * zv1[c];
         // fp16 hi/lo of w * 2^8 (w <= 2^7): 22-bit weights, the lo half out of fp16
