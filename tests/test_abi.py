@@ -67,3 +67,21 @@ def test_errors_without_device(libpath):
     assert lib.kvr_fwht_rows_f64(None, 4, 24, 16, None) == 2  # InvalidOrder: 16 does not divide 24
     assert b"does not divide" in lib.kvr_last_error()
     assert lib.kvr_quantize_rows_f64(None, 4, 7, None, None, None, None) == 1
+
+
+def test_split_count_model(libpath):
+    """kvr_decode_pick_splits on the BASELINE configs (148-SM fallback without a GPU):
+    one wave of CTAs, inline merge for C2 / C3 B = 1, the merge kernel's 16-multiples
+    and the one-wave fill for C5, no split for the batched configs."""
+    from paper_2604_19157_b200 import _lib
+
+    pick = _lib.lib().kvr_decode_pick_splits
+    assert pick(1, 8, 32768 + 1, 16) == 18       # C2: 8 x 18 = 144 CTAs, inline merge
+    assert pick(1, 8, 8192 + 1, 16) == 16        # C3 B = 1
+    assert pick(16, 8, 8192 + 1, 16) == 1        # C3 B = 16: 128 units already
+    assert pick(16, 8, 16384 + 1, 16) == 1       # C4 per-GPU shard
+    assert pick(1, 1, 131072 + 1, 16) == 128     # C5 128k: a multiple of 16 above 32
+    assert pick(1, 1, 1048576 + 1, 16) == 148    # C5 1M: the one-wave fill
+    for b, h, L in ((1, 8, 32769), (2, 8, 32768), (1, 1, 1 << 20), (4, 8, 4096)):
+        s = pick(b, h, L, 16)
+        assert 1 <= s <= 256 and (b * h * s <= 148 or s == 1)
