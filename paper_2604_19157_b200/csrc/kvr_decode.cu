@@ -348,6 +348,9 @@ KVR_DEV const float* dsmem_ptr(const float* local, uint32_t rank) {
 constexpr int NWARPS = 16;       // one CTA per SM, 4 warps per SM sub-partition (128-register budget)
 constexpr int CELL = 2208;       // one cell: T = 16 tokens of one head, d = 128
 constexpr int RING_CELLS = 4;    // cells in flight per warp (NSTG stages of C cells)
+#ifndef KVR_NT2_CELLS
+#define KVR_NT2_CELLS 2  // cells per ring group of the G = 8 kernel (2: -2 % on C4 despite a small spill)
+#endif
 #ifndef KVR_PREWAIT_GROUPS
 #define KVR_PREWAIT_GROUPS 1
 #endif
@@ -1431,7 +1434,7 @@ int kvr_pick_splits(int batch, int H, int max_len, int P) {
 // cluster spanning the splits of one (sequence, kv head) so they merge in DSMEM.
 template <int NT, int ORDER, bool APP, bool CL>
 static int launch_one(dim3 grid, size_t smem, cudaStream_t st, const DecodeParams& p, const Signs& sg) {
-  auto kern = decode_tma_kernel<NT, ORDER, APP, NT == 1 ? 2 : 1, CL>;
+  auto kern = decode_tma_kernel<NT, ORDER, APP, NT == 1 ? 2 : KVR_NT2_CELLS, CL>;
   static bool set = false;  // one flag per instantiation
   if (!set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -1463,7 +1466,7 @@ static bool cluster_ok(int splits, size_t smem) {
   static int cache[17] = {0};  // 0 unknown, 1 yes, 2 no
   if (splits < 2 || splits > 16) return false;
   if (!cache[splits]) {
-    auto kern = decode_tma_kernel<NT, ORDER, APP, NT == 1 ? 2 : 1, true>;
+    auto kern = decode_tma_kernel<NT, ORDER, APP, NT == 1 ? 2 : KVR_NT2_CELLS, true>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
