@@ -874,7 +874,10 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
           if (!in || t0 >= len_kv) l0[c][nt] = -INFINITY;
           if (!in || t0 + 8 >= len_kv) l1[c][nt] = -INFINITY;
         }
-        if (!in) zv0[c] = zv1[c] = 0.f;
+        // a masked token's weight p * s_v and offset term must be 0 whatever its slot
+        // holds (a stale or never-written scale / sentinel may be Inf/NaN: 0 * NaN)
+        if (!in || t0 >= len_kv) svc0[c] = zv0[c] = 0.f;
+        if (!in || t0 + 8 >= len_kv) svc1[c] = zv1[c] = 0.f;
       }
     }
     // probabilities at the current reference point, p = 2^(l - M), and the PV

@@ -373,3 +373,33 @@ def test_decode_unaligned_query_view():
     a = decode_batch(q_view, t, [0, 1], spec=spec)
     b = decode_batch(q_view.clone(), t, [0, 1], spec=spec)
     assert torch.equal(a, b)
+
+
+def test_decode_ignores_nan_in_unwritten_slots():
+    """Slots past a sequence's length (the rest of its last page, whole pages a split
+    range covers but the sequence does not) may hold anything -- here NaN scale and
+    code bytes -- and must not reach the output (the reference never reads them)."""
+    H, G, d, P = 2, 4, 128, 16
+    lens = [21, 70]  # partial last pages
+    layout = HeadLayout(num_q_heads=G * H, num_kv_heads=H, head_dim=d, rot_order=128, page_tokens=P)
+    spec = RotationSpec(order=128, signs=make_signs(3, 0, d, 128), targets=Targets.KEYS_AND_VALUES)
+    ref = {}
+    for poison in (False, True):
+        t = PageTable(layout, num_pages=16)
+        if poison:  # every byte 0xFF: NaN scales, 0xFF zero points
+            t.pool.fill_(0xFF)
+        slots = []
+        for s, L in enumerate(lens):
+            t.create_sequence(s)
+            slots.append(torch.from_numpy(t.alloc.reserve(s, L)).cuda())
+        gen = torch.Generator(device="cuda").manual_seed(5)
+        for s, L in enumerate(lens):
+            t.store_slots(torch.randn(L, H, d, generator=gen, device="cuda").bfloat16(),
+                          torch.randn(L, H, d, generator=gen, device="cuda").bfloat16(), slots[s], spec)
+        q = torch.randn((2, G * H, d), generator=gen, device="cuda").bfloat16()
+        outs = [decode_batch(q, t, [0, 1], spec=spec, num_splits=n) for n in (1, 3, 12, 40)]
+        for o in outs:
+            assert torch.isfinite(o).all()
+        ref[poison] = outs
+    for a, b in zip(ref[False], ref[True]):
+        assert torch.equal(a, b)
