@@ -192,7 +192,11 @@ int kvr_paged_decode(const void* q, int32_t q_dtype, const kvr_pool* pool,
  * new token's K/V rows (new_k/new_v: (batch, H, d) of kv_dtype) are rotated and
  * INT4-quantized reference-exactly (f64) into slot new_slot[b], and the decode
  * attends over seq_lens[b] tokens -- which must already count that token (the
- * host allocator's slot).  Same output/workspace contract as kvr_paged_decode.
+ * host allocator's slot).  new_slot[b] < 0 skips the write for sequence b (its
+ * decode then covers seq_lens[b] stored tokens).  A row with NaN/Inf is not
+ * written and sets KVR_FLAG_NONFINITE in *flags.  Slots past a sequence's length
+ * are never read (their bytes may be anything).  Same output/workspace contract
+ * as kvr_paged_decode.
  */
 int kvr_decode_step(const void* q, int32_t q_dtype, const void* new_k, const void* new_v, int32_t kv_dtype,
                     const int64_t* new_slot, const kvr_pool* pool, const int32_t* block_table, int32_t bt_stride,
