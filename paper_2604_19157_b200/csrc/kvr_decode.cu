@@ -114,6 +114,14 @@ KVR_DEV float load_q(const void* q, int dtype, int64_t i) {
   return reinterpret_cast<const float*>(q)[i];
 }
 
+// floor(log2 a) of a finite a > 0 (ilogbf) from the exponent bits; 2^e (ldexpf(1, e))
+// as bits -- the library forms only for subnormals / out-of-range exponents
+KVR_DEV int ilog2_pos(float a) {
+  const int ex = (__float_as_int(a) >> 23) & 0xFF;
+  return ex ? ex - 127 : ilogbf(a);
+}
+KVR_DEV float exp2i(int e) { return (e >= -126 && e <= 127) ? __int_as_float((e + 127) << 23) : ldexpf(1.0f, e); }
+
 // Elements i..i+3 (i % 4 == 0) of the query as one 8-B (bf16/f16) or 16-B (f32) load
 // (element loads when the query is not aligned for that).
 KVR_DEV void load_q4(const void* q, int dtype, int64_t i, float (&x)[4]) {
@@ -637,8 +645,8 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
       // columns.  Lane l owns dims 4l..4l+3; dim d sits in IMMA m = ((d >> 4) & 1) +
       // 2 (d & 1) (odd dims are the high nibbles), B register (d >> 3) & 1, byte
       // (d >> 1) & 3 of lane (column * 4 + d / 32).
-      const int e2 = amax > 0.f ? ilogbf(amax) : 0;
-      const float qs = ldexpf(1.0f, 19 - e2);
+      const int e2 = amax > 0.f ? ilog2_pos(amax) : 0;
+      const float qs = exp2i(19 - e2);
       int qsum = 0;
       uint8_t* s8 = reinterpret_cast<uint8_t*>(sfrag);  // [tile][m][lane][2 regs][4 bytes]
   #pragma unroll
@@ -668,14 +676,14 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
       qsum = __reduce_add_sync(0xffffffffu, qsum);
       if (lane == 0) {
         s_sumq[j] = (float)qsum;
-        s_ksc[j] = ldexpf(1.0f, e2 - 19) * LOG2E * (float)(1.0 / sqrt(128.0));
+        s_ksc[j] = exp2i(e2 - 19) * LOG2E * (float)(1.0 / sqrt(128.0));
       }
   
     } else {
       float amax = fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])), fmaxf(fabsf(x[2]), fabsf(x[3])));
       amax = warp_max(amax);
-      const int e2 = amax > 0.f ? ilogbf(amax) - 13 : 0;  // q' = q 2^-e2, max|q'| in [2^13, 2^14)
-      const float qs = ldexpf(1.0f, -e2);
+      const int e2 = amax > 0.f ? ilog2_pos(amax) - 13 : 0;  // q' = q 2^-e2, max|q'| in [2^13, 2^14)
+      const float qs = exp2i(-e2);
       float hs = 0.f;
   #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -695,7 +703,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
       hs = warp_sum(hs);
       if (lane == 0) {
         s_sumq[j] = hs * 5.9604644775390625e-08f;  // x 2^-24 (MMA units)
-        s_ksc[j] = ldexpf(1.0f, e2 + 24) * LOG2E * (float)(1.0 / sqrt(128.0));
+        s_ksc[j] = exp2i(e2 + 24) * LOG2E * (float)(1.0 / sqrt(128.0));
       }
   
     }
