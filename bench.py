@@ -265,7 +265,7 @@ def run_ours(args, rank, world, local_rank):
         print(f"[bench] C4 step {c4['step_us']} us, {c4['tok_per_s_per_gpu']} tok/s/GPU", file=sys.stderr, flush=True)
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:  # the CPU baseline: rank 0 at N = 1 only
         cpu = cpu_baseline_c2(args.cpu_seconds)
     if rank != 0:
         return
