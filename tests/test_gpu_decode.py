@@ -375,11 +375,13 @@ def test_decode_unaligned_query_view():
     assert torch.equal(a, b)
 
 
-def test_decode_ignores_nan_in_unwritten_slots():
+@pytest.mark.parametrize("G", [4, 8])
+def test_decode_ignores_nan_in_unwritten_slots(G):
     """Slots past a sequence's length (the rest of its last page, whole pages a split
     range covers but the sequence does not) may hold anything -- here NaN scale and
-    code bytes -- and must not reach the output (the reference never reads them)."""
-    H, G, d, P = 2, 4, 128, 16
+    code bytes -- and must not reach the output (the reference never reads them);
+    plain decode over several split paths and the fused serving step."""
+    H, d, P = 2, 128, 16
     lens = [21, 70]  # partial last pages
     layout = HeadLayout(num_q_heads=G * H, num_kv_heads=H, head_dim=d, rot_order=128, page_tokens=P)
     spec = RotationSpec(order=128, signs=make_signs(3, 0, d, 128), targets=Targets.KEYS_AND_VALUES)
@@ -398,6 +400,11 @@ def test_decode_ignores_nan_in_unwritten_slots():
                           torch.randn(L, H, d, generator=gen, device="cuda").bfloat16(), slots[s], spec)
         q = torch.randn((2, G * H, d), generator=gen, device="cuda").bfloat16()
         outs = [decode_batch(q, t, [0, 1], spec=spec, num_splits=n) for n in (1, 3, 12, 40)]
+        plan = DecodePlan(t, [0, 1], extra_tokens=2)
+        kn = torch.randn((2, H, d), generator=gen, device="cuda").bfloat16()
+        vn = torch.randn((2, H, d), generator=gen, device="cuda").bfloat16()
+        outs.append(plan.step(q, kn, vn, spec).clone())
+        torch.cuda.synchronize()
         for o in outs:
             assert torch.isfinite(o).all()
         ref[poison] = outs
