@@ -106,6 +106,8 @@ def to_device(a, dtype: torch.dtype) -> torch.Tensor:
     if isinstance(a, torch.Tensor):
         return a.to(device=dev, dtype=dtype).contiguous()
     arr = np.ascontiguousarray(a, dtype=torch.empty((), dtype=dtype).numpy().dtype)
+    if not arr.flags.writeable:  # read-only inputs (e.g. frozen arrays): torch wants writable memory
+        arr = arr.copy()
     return torch.from_numpy(arr).to(dev)
 
 
