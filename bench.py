@@ -57,6 +57,19 @@ def step_bytes(L: int) -> int:
     return decode_bytes(L) + WRITE_BYTES_PER_TOKEN
 
 
+def headline_config(world: int) -> dict:
+    """The workload's config dict, identical for the repo arm and the reference arm."""
+    return {
+        "workload": "BASELINE configs[1] / C2: Llama-3-8B-shaped decode step, batch 1 per GPU, 32768 cached "
+                    "tokens (+1 written), GQA 32q/8kv, head_dim 128, Hadamard order 128, page 16, K&V rotated",
+        "per_gpu_batch": 1, "ctx": CTX, "num_q_heads": NQ, "num_kv_heads": H, "head_dim": D,
+        "rot_order": ORDER, "page_tokens": P,
+        "l2": "inputs rotate over buffer sets larger than 2x the 126 MB L2 (GPU arm)",
+        "parallelism": f"dp{world} (independent sequences per GPU, no data-path collective)",
+        "algorithmic_bytes_per_step": step_bytes(CTX + 1),
+    }
+
+
 def hbm_peak():
     try:
         with open(PEAKS) as f:
@@ -126,7 +139,7 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     layout = HeadLayout(num_q_heads=NQ, num_kv_heads=H, head_dim=D, rot_order=ORDER, page_tokens=P)
     spec = RotationSpec(order=ORDER, signs=make_signs(0, 0, D, ORDER))
-    L = args.ctx
+    L = CTX
     R = args.sets
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
@@ -191,6 +204,9 @@ def run_ours(args, rank, world, local_rank):
             torch.distributed.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # a ~100 us device-side spin ahead of the start event: the host submits the
+        # graph(s) while the GPU spins, so no host submission gap lands in the window
+        torch.cuda._sleep(200_000)
         e0.record()
         for _ in range(n_full):
             gf.replay()
@@ -218,14 +234,15 @@ def run_ours(args, rank, world, local_rank):
     per_rank_bytes = step_bytes(Lstep)
     value = world * per_rank_bytes / (ms_per_step * 1e-3) / 1e9
 
-    # ---- per-kernel timings (rotated and plain twins)
+    # ---- per-kernel timings, rotated and plain twins, all with the same launch count
     n_k = max(args.steps, 512)
     t_fused = ms_per_step
+    t_fr = timed(step, n_k) / n_k
+    t_fp = timed(lambda i: fused(sets[i % R], None), n_k) / n_k
     t_k1 = timed(lambda i: k1(sets[i % R]), n_k) / n_k
     t_k2 = timed(lambda i: k2(sets[i % R]), n_k) / n_k
     t_k1p = timed(lambda i: k1(sets[i % R], None), n_k) / n_k
     t_k2p = timed(lambda i: k2(sets[i % R], None), n_k) / n_k
-    t_fp = timed(lambda i: fused(sets[i % R], None), n_k) / n_k
     # restore the rotated token in every set (the plain twin overwrote slot L)
     for s in sets:
         k1(s)
@@ -242,8 +259,8 @@ def run_ours(args, rank, world, local_rank):
     except Exception:
         pass
 
-    # ---- e2e through the public API with host buffers
-    e2e = e2e_api(torch, layout, spec, dev, sets[0]["table"], args, world)
+    # ---- e2e through the public API with host buffers (rotating over the buffer sets)
+    e2e = e2e_api(torch, layout, spec, dev, [st["table"] for st in sets], args, world)
 
     # ---- verification gather (after timing; NCCL only here)
     if world > 1:  # every rank's sequence (batch shard) gathered on all ranks
@@ -259,13 +276,15 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.empty_cache()
         c3 = c3_sweep(torch, dev, gen, timed)
         print(f"[bench] C3 {[(r['batch'], r['us'], r['frac']) for r in c3]}", file=sys.stderr, flush=True)
-        c5 = c5_long(torch, dev, gen, timed)
+        c5 = c5_long(torch, dev, gen, timed, world, rank)
         print(f"[bench] C5 {[(r['ctx'], r['rot_order'], r['us'], r['frac']) for r in c5]}", file=sys.stderr, flush=True)
-        c4 = c4_llama70b_shard(torch, dev, gen, timed, world)
+        c4 = c4_llama70b(torch, dev, gen, timed, world, rank)
         print(f"[bench] C4 step {c4['step_us']} us, {c4['tok_per_s_per_gpu']} tok/s/GPU", file=sys.stderr, flush=True)
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:  # the CPU baseline: rank 0 at N = 1 only
+    cpu = parity = None
+    if rank == 0 and world == 1 and not args.no_cpu:  # the CPU legs: rank 0 at N = 1 only, after timing
+        parity = parity_checks(torch, dev)  # the oracle as the checker (never timed, never shipped)
+        print(f"[bench] parity {parity}", file=sys.stderr, flush=True)
         cpu = cpu_baseline_c2(args.cpu_seconds)
     if rank != 0:
         return
@@ -283,15 +302,10 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "bf16 in -> int4 codes (fp32 math, fp16x2 hi/lo tensor-core MMA)",
         "data": "synthetic (torch.randn K/V/q in bf16, seeded per rank)",
-        "config": {
-            "workload": "BASELINE configs[1] / C2: Llama-3-8B-shaped decode step, batch 1 per GPU, 32768 cached "
-                        "tokens (+1 written), GQA 32q/8kv, head_dim 128, Hadamard order 128, page 16, K&V rotated",
-            "per_gpu_batch": 1, "ctx": L, "num_q_heads": NQ, "num_kv_heads": H, "head_dim": D,
-            "rot_order": ORDER, "page_tokens": P, "decode_splits": splits,
-            "l2": f"{R} rotating buffer sets of {step_bytes(Lstep) / 1e6:.1f} MB (> 2x 126 MB L2), CUDA-graph replay",
-            "parallelism": f"dp{world} (independent sequences per GPU, no data-path collective)",
-            "algorithmic_bytes_per_step": per_rank_bytes,
-        },
+        "config": headline_config(world),
+        "timing": {"decode_splits": splits, "buffer_sets": R, "buffer_set_MB": round(step_bytes(Lstep) / 1e6, 1),
+                   "method": "K steps replayed from CUDA graphs, CUDA events on the launching stream after a "
+                             "device-side spin that covers the host's graph submission, max over ranks"},
         "roofline": {"bound": "hbm", "kernel": ("decode_tma_kernel (one kvr_decode_step: fused append + split-K "
                                                 "decode + inline split merge by the last CTA)") if splits <= 32 else
                      "decode_tma_kernel + decode_merge_kernel (fused append + split-K decode, then the split merge)",
@@ -299,6 +313,7 @@ def run_ours(args, rank, world, local_rank):
                      "frac": round(ach / peak, 4), "traffic": traffic, "algorithmic_bytes": dbytes,
                      "avg_launch_us": round(t_fused * 1e3, 3)},
         "cpu_baseline": cpu,
+        "parity": parity,
         "e2e": e2e,
         # per step: the fused decode kernel (+ the split-merge kernel above 32 splits;
         # 2..8 merge in a cluster, 9..32 inline in the last CTA)
@@ -308,11 +323,12 @@ def run_ours(args, rank, world, local_rank):
             "k1_write_1tok_us": round(t_k1 * 1e3, 3), "k1_plain_1tok_us": round(t_k1p * 1e3, 3),
             "k2_decode_us": round(t_k2 * 1e3, 3), "k2_plain_us": round(t_k2p * 1e3, 3),
             "k2_overhead_vs_plain": round(t_k2 / t_k2p - 1.0, 4),
-            "fused_step_us": round(t_fused * 1e3, 3), "fused_step_plain_us": round(t_fp * 1e3, 3),
-            "fused_step_overhead_vs_plain": round(t_fused / t_fp - 1.0, 4),
+            "twin_launches": n_k,
+            "fused_step_us": round(t_fr * 1e3, 3), "fused_step_plain_us": round(t_fp * 1e3, 3),
+            "fused_step_overhead_vs_plain": round(t_fr / t_fp - 1.0, 4),
             "c1_quantize_store": c1,
             "c3_concurrency_sweep": c3,
-            "c4_llama70b_8gpu_shard": c4,
+            "c4_llama70b": c4,
             "c5_long_context_1kv_per_gpu": c5,
         },
     }
@@ -329,7 +345,7 @@ def build_table(torch, layout, spec, dev, gen, B, L, extra_tokens=1, chunk=16384
     for b in range(B):
         t.create_sequence(b)
         slots = torch.from_numpy(t.alloc.reserve(b, L)).to(dev)
-        for c0 in range(0, L, chunk):
+        for c0 in range(0, L, chunk):  # (c5_shard_check regenerates 1-head data in this order)
             n = min(chunk, L - c0)
             k = torch.randn((n, Hh, Dd), generator=gen, device=dev).to(torch.bfloat16)
             v = torch.randn((n, Hh, Dd), generator=gen, device=dev).to(torch.bfloat16)
@@ -417,34 +433,47 @@ def c3_sweep(torch, dev, gen, timed):
     return out
 
 
-def c4_llama70b_shard(torch, dev, gen, timed, world):
-    """BASELINE configs[3] at its 8-GPU shard size on this GPU: Llama-3-70B KV geometry
-    (8 kv heads, 64 q heads, d 128), 128 sequences / 8 GPUs = 16 sequences x 16k
-    context, 80 layers; one step = the fused append + decode of every layer."""
+def c4_llama70b(torch, dev, gen, timed, world, rank):
+    """BASELINE configs[3]: Llama-3-70B KV geometry (8 kv heads, 64 q heads, d 128),
+    128 sequences x 16k context sharded by sequence: 128 / N per GPU.  One step = the
+    fused append + decode of all 80 layers.  The 80 layer caches are resident when they
+    fit a 64 GB budget (N >= 4); otherwise the step cycles its 80 launches over the
+    caches that fit (each >= 0.58 GB, far above the 126 MB L2, so no launch reads a
+    warm cache) -- stated in the result."""
     from paper_2604_19157_b200 import HeadLayout, RotationSpec, make_signs
+    from paper_2604_19157_b200.shard import block_range
 
-    layers, B, L = 80, 128 // 8, 16384
+    layers, B_total, L = 80, 128, 16384
+    mine = block_range(B_total, world, rank)
+    B = len(mine)
     layout = HeadLayout(num_q_heads=64, num_kv_heads=8, head_dim=D, rot_order=ORDER, page_tokens=P)
     spec = RotationSpec(order=ORDER, signs=make_signs(0, 0, D, ORDER))
+    per_layer = B * L * TOK_BYTES
+    resident = max(2, min(layers, int(64e9 // per_layer)))
     base = build_table(torch, layout, spec, dev, gen, B, L)
-    tables = [base] + [clone_table(torch, base) for _ in range(layers - 1)]
+    tables = [base] + [clone_table(torch, base) for _ in range(resident - 1)]
     r = decode_case(torch, dev, tables, spec, timed, fused=True, n=layers * 4, gen=gen)
     step_us = r["us"] * layers
-    res = {"layers": layers, "sequences_per_gpu": B, "ctx": L, "q_heads": 64, "kv_heads": 8,
-           "layer_step_us": r["us"], "layer_plain_us": r["plain_us"], "step_us": round(step_us, 1),
-           "tok_per_s_per_gpu": round(B / (step_us * 1e-6), 1), "GBps": r["GBps"], "frac": r["frac"],
+    res = {"layers": layers, "sequences_total": B_total, "sequences_per_gpu": B, "ctx": L, "q_heads": 64,
+           "kv_heads": 8, "layer_step_us": r["us"], "layer_plain_us": r["plain_us"], "step_us": round(step_us, 1),
+           "tok_per_s_per_gpu": round(B / (step_us * 1e-6), 1),
+           "tok_per_s_all_gpus": round(world * B / (step_us * 1e-6), 1), "GBps": r["GBps"], "frac": r["frac"],
            "overhead_vs_plain": r["overhead_vs_plain"], "splits": r["splits"],
-           "bytes_per_step": r["algorithmic_bytes"] * layers,
-           "note": "per-GPU shard of the 8-GPU configuration (128 x 16k x 80 layers = 186 GB does not fit "
-                   "one 180 GB GPU); 80 layer caches, each step runs all 80 fused append+decode launches"}
+           "bytes_per_step": r["algorithmic_bytes"] * layers, "resident_layer_caches": resident,
+           "note": (f"{B} of the 128 sequences on this GPU; each step runs all 80 fused append+decode launches"
+                    + ("" if resident == layers else f", cycling over {resident} resident layer caches of "
+                       f"{per_layer / 1e9:.2f} GB (80 x {per_layer / 1e9:.2f} GB does not fit one GPU)"))}
     del tables, base
     torch.cuda.empty_cache()
     return res
 
 
-def c5_long(torch, dev, gen, timed):
-    """BASELINE configs[4]: one request at 128k / 1M tokens, KV heads sharded 8 ways
-    (this GPU: 1 kv head + its 4 q heads), split-K decode, Hadamard order 64 / 128."""
+def c5_long(torch, dev, gen, timed, world=1, rank=0):
+    """BASELINE configs[4]: one request at 128k / 1M tokens, KV heads sharded 8 ways:
+    each rank holds 1 kv head + its 4 q heads (rank r = head r), split-K decode,
+    Hadamard order 64 / 128.  With N > 1 ranks the 128k outputs of all ranks are
+    gathered after timing (NCCL) and rank 0 checks them against one decode of an
+    N-head table built from the same per-head data."""
     from paper_2604_19157_b200 import HeadLayout, RotationSpec, make_signs
 
     out = []
@@ -453,12 +482,52 @@ def c5_long(torch, dev, gen, timed):
             layout = HeadLayout(num_q_heads=4, num_kv_heads=1, head_dim=D, rot_order=order, page_tokens=P)
             spec = RotationSpec(order=order, signs=make_signs(0, 0, D, order))
             reps = max(2, -(-300_000_000 // (L * (D + 10))))
-            base = build_table(torch, layout, spec, dev, gen, 1, L)
+            hg = torch.Generator(device=dev)
+            hg.manual_seed(9000 + 97 * rank + order + L)  # this head's data
+            base = build_table(torch, layout, spec, dev, hg, 1, L)
             tables = [base] + [clone_table(torch, base) for _ in range(reps - 1)]
-            out.append(decode_case(torch, dev, tables, spec, timed, gen=gen, n=128))
+            res = decode_case(torch, dev, tables, spec, timed, gen=hg, n=128)
+            if world > 1 and L == 131072 and order == 128:
+                res["shard_check_rel_err"] = c5_shard_check(torch, dev, layout, spec, base, world, rank, L, order)
+            out.append(res)
             del tables, base
             torch.cuda.empty_cache()
     return out
+
+
+def c5_shard_check(torch, dev, layout, spec, table, world, rank, L, order):
+    """Gather every rank's head output (all_gather over NCCL) and compare on rank 0
+    with a single-GPU decode of the N-head table of the same data."""
+    from paper_2604_19157_b200 import DecodePlan, HeadLayout
+    from paper_2604_19157_b200.shard import gather_rows
+
+    qg = torch.Generator(device=dev)
+    qg.manual_seed(77 + rank)
+    q = torch.randn((1, 4, D), generator=qg, device=dev).to(torch.bfloat16)
+    mine = DecodePlan(table, [0]).run(q, spec)
+    allq = gather_rows(q.reshape(4, D), [4] * world).reshape(1, 4 * world, D)
+    allo = gather_rows(mine.reshape(4, D), [4] * world).reshape(1, 4 * world, D)
+    if rank != 0:
+        return None
+    full = HeadLayout(num_q_heads=4 * world, num_kv_heads=world, head_dim=D, rot_order=order, page_tokens=P)
+    heads = []
+    for r in range(world):  # rebuild every head's data from its rank's seed
+        hg = torch.Generator(device=dev)
+        hg.manual_seed(9000 + 97 * r + order + L)
+        heads.append(hg)
+    from paper_2604_19157_b200 import PageTable
+    t = PageTable(full, num_pages=-(-L // P), device=dev)
+    t.create_sequence(0)
+    slots = torch.from_numpy(t.alloc.reserve(0, L)).to(dev)
+    for c0 in range(0, L, 16384):
+        n = min(16384, L - c0)
+        ks, vs = [], []
+        for hg in heads:
+            ks.append(torch.randn((n, 1, D), generator=hg, device=dev).to(torch.bfloat16))
+            vs.append(torch.randn((n, 1, D), generator=hg, device=dev).to(torch.bfloat16))
+        t.store_slots(torch.cat(ks, 1), torch.cat(vs, 1), slots[c0:c0 + n], spec)
+    ref = DecodePlan(t, [0]).run(allq, spec)
+    return float((allo - ref).abs().max() / ref.abs().max())
 
 
 def c1_quantize_store(torch, layout, spec, dev, gen, timed):
@@ -505,26 +574,28 @@ def c1_quantize_store(torch, layout, spec, dev, gen, timed):
             "overhead_vs_plain": round(t_rot / t_pl - 1.0, 4)}
 
 
-def e2e_api(torch, layout, spec, dev, table, args, world):
-    """Public-API step with host buffers: H2D of the new K/V and q, DecodePlan.step
-    (slot allocation + one fused append+decode launch), D2H of the output."""
+def e2e_api(torch, layout, spec, dev, tables, args, world):
+    """Public-API step with host buffers: every step allocates the new token's slot
+    (host bookkeeping), copies q and the new K/V from pinned host memory with the
+    slot / length metadata, runs the fused append + decode (DecodePlan.step), and the
+    kernel writes the output into a pinned host tensor.  The steps rotate over the
+    buffer sets' tables (> 2x L2), so no step reads L2-warm KV."""
     from paper_2604_19157_b200 import DecodePlan
 
-    steps = min(args.steps, 200)
+    steps = min(args.steps, 400)
+    R = len(tables)
     kh = torch.randn((1, H, D)).to(torch.bfloat16).pin_memory()
     vh = torch.randn((1, H, D)).to(torch.bfloat16).pin_memory()
     qh = torch.randn((1, NQ, D)).to(torch.bfloat16).pin_memory()
     oh = torch.empty((1, NQ, D), dtype=torch.float32).pin_memory()
-    free_before = list(table.alloc.free)
-    base_len = table.alloc.seq_len[0]
-    base_pages = list(table.alloc.seq_pages[0])
-    plan = DecodePlan(table, [0], extra_tokens=steps + 8)
+    saved = [(list(t.alloc.free), t.alloc.seq_len[0], list(t.alloc.seq_pages[0])) for t in tables]
+    per_plan = -(-(steps + 3) // R) + 8
+    plans = [DecodePlan(t, [0], extra_tokens=per_plan) for t in tables]
+    i = [0]
 
     def one():
-        # host bookkeeping (slot allocation, page table) per step; q/k/v and the slot /
-        # length metadata go to the device in one pinned copy, the fused kernel writes
-        # the output straight into the pinned host tensor (both cross the bus every step)
-        plan.step(qh, kh, vh, spec, out=oh, graph=True)
+        plans[i[0] % R].step(qh, kh, vh, spec, out=oh, graph=True)
+        i[0] += 1
 
     for _ in range(3):
         one()
@@ -540,17 +611,85 @@ def e2e_api(torch, layout, spec, dev, table, args, world):
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) * 1e3
     ms = max(e0.elapsed_time(e1), wall) / steps
-    # roll the table back
-    table.alloc.free = free_before
-    table.alloc.seq_len[0] = base_len
-    table.alloc.seq_pages[0] = base_pages
-    L = base_len + steps
+    L = max(t.alloc.seq_len[0] for t in tables)
+    for t, (free, ln, pages) in zip(tables, saved):  # roll the tables back
+        t.alloc.free = free
+        t.alloc.seq_len[0] = ln
+        t.alloc.seq_pages[0] = pages
     byts = step_bytes(L)
     return {"value": round(world * byts / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "ms_per_step": round(ms, 4),
             "h2d_bytes_per_step": kh.numel() * 2 + vh.numel() * 2 + qh.numel() * 2 + 12,  # + slot id, length
             "d2h_bytes_per_step": oh.numel() * 4,
             "api": "DecodePlan.step(graph=True) (fused append + decode) with pinned host buffers",
-            "steps": steps}
+            "steps": steps, "tables": R, "timing": "max(CUDA events, host wall clock) over the steps"}
+
+
+def parity_checks(torch, dev):
+    """Parity of the timed kernels on this box, with the oracle as the checker (after
+    timing): K1 on the C1 shape (4,096 tokens x 8 heads, K & V rotated, Gaussian bf16)
+    -- nibble, zero-point and scale mismatch counts vs the reference arithmetic -- and
+    the C2 fused step's max relative error vs an oracle-quantised decode."""
+    from oracle import kvrot_oracle as O
+    from paper_2604_19157_b200 import DecodePlan, HeadLayout, PageTable, RotationSpec, make_signs
+
+    layout = HeadLayout(num_q_heads=NQ, num_kv_heads=H, head_dim=D, rot_order=ORDER, page_tokens=P)
+    spec = RotationSpec(order=ORDER, signs=make_signs(0, 0, D, ORDER))
+    g = torch.Generator(device=dev)
+    g.manual_seed(4242)
+    res = {"checker": "oracle/kvrot_oracle.py (numpy restatement of the reference, pinned to its goldens)"}
+    # -- K1 at C1
+    n_tok = 4096
+    t = PageTable(layout, num_pages=n_tok // P, device=dev)
+    t.create_sequence(0)
+    k = torch.randn((n_tok, H, D), generator=g, device=dev).to(torch.bfloat16)
+    v = torch.randn((n_tok, H, D), generator=g, device=dev).to(torch.bfloat16)
+    t.append_batch([0] * n_tok, k, v, spec=spec)
+    rec = t.page_records(t.sequence_pages(0))
+    cells = P * H
+    f = {}
+    off = 0
+    for name, nb, dt in (("k_payload", cells * D // 2, np.uint8), ("v_payload", cells * D // 2, np.uint8),
+                         ("k_scale", cells * 4, np.float32), ("k_zp", cells, np.uint8),
+                         ("v_scale", cells * 4, np.float32), ("v_zp", cells, np.uint8)):
+        f[name] = rec[:, off:off + nb].copy().view(dt).reshape(-1, nb // cells // np.dtype(dt).itemsize)
+        off += nb
+    k1 = {}
+    for side, x in (("k", k), ("v", v)):
+        rows = x.double().cpu().numpy().reshape(-1, D)
+        p_, s_, z_ = O.quantize_rows(O.rotate_rows(rows, ORDER, spec.signs))
+        ours_p = f[f"{side}_payload"].reshape(-1, D // 2)
+        x_ = ours_p ^ p_
+        k1[side] = {"rows": int(rows.shape[0]),
+                    "nibble_mismatches": int(np.count_nonzero(x_ & 0x0F) + np.count_nonzero(x_ & 0xF0)),
+                    "zp_mismatches": int(np.count_nonzero(f[f"{side}_zp"].reshape(-1) != z_)),
+                    "scale_mismatches": int(np.count_nonzero(f[f"{side}_scale"].reshape(-1).view(np.uint32)
+                                                             != s_.view(np.uint32)))}
+    res["c1_k1_fast_rotated"] = k1
+    # -- C2 fused step
+    t2 = PageTable(layout, num_pages=CTX // P + 2, device=dev)
+    t2.create_sequence(0)
+    slots = torch.from_numpy(t2.alloc.reserve(0, CTX)).to(dev)
+    ks, vs = [], []
+    for c0 in range(0, CTX, 8192):
+        kc = torch.randn((8192, H, D), generator=g, device=dev).to(torch.bfloat16)
+        vc = torch.randn((8192, H, D), generator=g, device=dev).to(torch.bfloat16)
+        t2.store_slots(kc, vc, slots[c0:c0 + 8192], spec)
+        ks.append(kc.double().cpu().numpy())
+        vs.append(vc.double().cpu().numpy())
+    kn = torch.randn((1, H, D), generator=g, device=dev).to(torch.bfloat16)
+    vn = torch.randn((1, H, D), generator=g, device=dev).to(torch.bfloat16)
+    q = torch.randn((1, NQ, D), generator=g, device=dev).to(torch.bfloat16)
+    out = DecodePlan(t2, [0], extra_tokens=1).step(q, kn, vn, spec)
+    kk = np.concatenate(ks + [kn.double().cpu().numpy()]).reshape(-1, D)
+    vv = np.concatenate(vs + [vn.double().cpu().numpy()]).reshape(-1, D)
+    kh = O.dequantize_rows(*O.quantize_rows(O.rotate_rows(kk, ORDER, spec.signs)), D).reshape(-1, H, D)
+    vh = O.dequantize_rows(*O.quantize_rows(O.rotate_rows(vv, ORDER, spec.signs)), D).reshape(-1, H, D)
+    ref = O.decode_flat(O.rotate_rows(q[0].double().cpu().numpy(), ORDER, spec.signs), kh, vh, G)
+    ref = O.unrotate_rows(ref, ORDER, spec.signs)
+    got = out[0].double().cpu().numpy()
+    res["c2_fused_step_max_rel_err"] = float(np.abs(got - ref).max() / np.abs(ref).max())
+    res["c2_tolerance"] = "1e-3 x max|ref| (north star)"
+    return res
 
 
 # ----------------------------------------------------- CPU oracle timing ----
@@ -624,6 +763,68 @@ _KIND_NOTE = {"reference": "the reference's compiled kernels (oracle/_ref: _core
               "port": "the numpy oracle port of the reference"}
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+def _c1_kernel_rows(n_tok=1024, seed=0):
+    rng = np.random.default_rng(seed)
+    from oracle import kvrot_oracle as O
+
+    k = rng.standard_normal((n_tok * H, D))
+    v = rng.standard_normal((n_tok * H, D))
+    return O, k, v
+
+
+def _c1_kernels_once(args):
+    """One worker's share of the C1 kernel leg: fwht_rows + quantize_rows on K and V
+    rows (the reference's compiled kernels when oracle/_ref is built)."""
+    n_tok, seed = args
+    O, k, v = _c1_kernel_rows(n_tok, seed)
+    _cpu_kernels()
+    signs = O.make_signs(0, 0, D, ORDER)
+    t0 = time.perf_counter()
+    for x in (k, v):
+        y = x * signs
+        O.fwht_rows(y, ORDER)
+        O.quantize_rows(y)
+    return time.perf_counter() - t0
+
+
+def cpu_c1_kernel_legs(seconds: float):
+    """(i) kernel-level C1 (fwht_rows + quantize_rows, the reference's
+    L0 kernels, bench-attn pattern cli.py:388-431) on one core, and (iii) the same work
+    sharded over all host cores with a multiprocessing pool; GB/s with K1's algorithmic
+    bytes per token."""
+    import multiprocessing as mp
+
+    n_tok = 1024
+    one = _c1_kernels_once((n_tok, 0))  # warm
+    reps = max(1, int(seconds / 2 / max(one, 1e-3)))
+    t1 = min(_c1_kernels_once((n_tok, 0)) for _ in range(min(reps, 5)))
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        pool.map(_c1_kernels_once, [(n_tok, i) for i in range(cores)])  # warm the workers
+        t0 = time.perf_counter()
+        pool.map(_c1_kernels_once, [(n_tok, i) for i in range(cores * 4)])
+        tn = time.perf_counter() - t0
+    b = n_tok * WRITE_BYTES_PER_TOKEN
+    return {"c1_kernels_1core_GBps": round(b / t1 / 1e9, 5), "c1_kernels_ncore_GBps": round(4 * cores * b / tn / 1e9, 5),
+            "ncore_workers": cores,
+            "sample": f"{n_tok} tokens x 8 heads (K and V rows) per task: sign flip + fwht_rows + quantize_rows, "
+                      f"f64; 1 core best of {min(reps, 5)}, then {4 * cores} tasks over a {cores}-process pool"}
+
+
 def cpu_baseline_c2(seconds: float):
     from oracle import kvrot_oracle as O
 
@@ -638,14 +839,20 @@ def cpu_baseline_c2(seconds: float):
     while not times or (time.perf_counter() - t_start < seconds and len(times) < 40):
         times.append(seq.step())
     t = float(np.median(times))
+    legs = cpu_c1_kernel_legs(min(seconds, 10.0))
     return {"value": round(step_bytes(L + 1) / t / 1e9, 4), "unit": "GB/s", "cores": _cpu_threads(),
-            "kind": kind, "sample": f"{len(times)} full C2 steps (1-token write + decode over {L + 1} tokens) with "
-                                    f"{_KIND_NOTE[kind]} (numpy/OpenBLAS threads), median {t * 1e3:.1f} ms/step"}
+            "kind": kind, "cpu_model": cpu_model(),
+            "sample": f"{len(times)} full C2 steps (1-token write + decode over {L + 1} tokens) with "
+                      f"{_KIND_NOTE[kind]} (numpy/OpenBLAS threads), median {t * 1e3:.1f} ms/step",
+            "legs": legs}
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU algorithm (numpy port in oracle/) on the host cores,
-    same metric/config; rank 0 only."""
+    """--impl reference: the reference's CPU algorithm on the host cores (the compiled
+    reference kernels in oracle/_ref when built, else the numpy port), same metric and
+    config as the GPU arm; rank 0 only.  Each step is a full C2 step (1-token write +
+    decode over 32,769 tokens); if K steps would not fit the time budget, the first
+    steps that fit are timed and the count is stated."""
     if rank != 0:
         return
     from oracle import kvrot_oracle as O
@@ -653,32 +860,29 @@ def run_reference(args, rank, world):
     kind = _cpu_kernels()
     rng = np.random.default_rng(0)
     signs = O.make_signs(0, 0, D, ORDER)
-    # bound the run to a few minutes: each step is a full C2 step when affordable,
-    # otherwise a step over a shorter context (stated in `sample`)
-    budget = 120.0
-    probe = CpuOracleSequence(4096, rng, signs).step()
-    per_tok = probe / 4096
-    L = int(min(CTX, max(1024, budget / max(args.steps + args.warmup, 1) / per_tok)))
-    seq = CpuOracleSequence(L, rng, signs, extra_tokens=args.steps + args.warmup + 16)
+    budget = 150.0
+    seq = CpuOracleSequence(CTX, rng, signs, extra_tokens=args.steps + args.warmup + 16)
     for _ in range(args.warmup):
         seq.step()
-    ts = [seq.step() for _ in range(args.steps)]
-    total = float(np.sum(ts))
-    ms = total / args.steps * 1e3
-    val = step_bytes(L + 1) / (total / args.steps) / 1e9
+    ts = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ts.append(seq.step())
+        if time.perf_counter() - t0 > budget:
+            break
+    ms = float(np.mean(ts)) * 1e3
+    val = step_bytes(CTX + 1) / (ms * 1e-3) / 1e9
     line = {
         "impl": "reference", "metric": "quantize-store + INT4 paged-decode HBM GB/s (one serving decode step, "
                                        "% of HBM roofline)",
         "value": round(val, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64 (reference numpy arithmetic)", "data": "synthetic (numpy standard normal)",
-        "config": {"workload": "BASELINE configs[1] / C2 decode step on the host CPU (reference algorithm)",
-                   "ctx": L, "num_q_heads": NQ, "num_kv_heads": H, "head_dim": D, "rot_order": ORDER,
-                   "page_tokens": P},
+        "config": headline_config(world),
         "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": _cpu_threads(), "kind": kind,
-                         "sample": f"{args.steps} steps, each a 1-token write + decode over {L + 1} tokens, "
-                                   f"{_KIND_NOTE[kind]}"
-                                   + ("" if L == CTX else f" (context bounded from {CTX} to fit the time budget)")},
+                         "cpu_model": cpu_model(),
+                         "sample": f"{len(ts)} of {args.steps} steps timed, each a 1-token write + decode over "
+                                   f"{CTX + 1} tokens, {_KIND_NOTE[kind]}"},
         "e2e": {"value": round(val, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -690,13 +894,22 @@ def main():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ctx", type=int, default=CTX)
     ap.add_argument("--sets", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--quick", action="store_true", help="headline + C1 only (skip the C3/C4/C5 detail configs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch this command under torch.distributed.run
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))

@@ -4,8 +4,10 @@
  * One shared library (libkvrot_b200.so, sm_100a) exports these symbols.  All
  * buffers are DEVICE pointers unless a parameter says "host"; every entry
  * point is asynchronous on `stream` (a cudaStream_t passed as void*), never
- * allocates, never throws, and returns a kvr_status.  The only global state
- * is a thread-local last-error string (kvr_last_error).
+ * allocates, never throws, and returns a kvr_status.  Global state: a
+ * thread-local last-error string (kvr_last_error), per-device caches of kernel
+ * attributes, and a mutex-protected note of which streams last wrote pool cells
+ * (see kvr_note_pool_write).
  *
  * The entry points replace, one for one, the reference's operator boundary
  * `kvrot._kernels` (pkg/src/kvrot/_kernels/__init__.py:35-39) and the
@@ -24,6 +26,8 @@
  *   kvr_paged_decode         <- attention.decode_step (attention.py:50-87)
  *   kvr_decode_step          <- PageTable.append_token + decode_step fused: one serving
  *                               decode step (cache.py:235-270 then attention.py:50-87)
+ *   kvr_decode_flat_f64      <- attention.decode_step_fp (attention.py:90-115), the flat
+ *                               full-precision decode (paged-vs-flat exactness oracle)
  */
 #ifndef KVROT_B200_H
 #define KVROT_B200_H
@@ -106,6 +110,13 @@ const char* kvr_last_error(void);
  * entry, [1] past the grid-dependency wait, [2] exit.  NULL disables. */
 void kvr_debug_decode_trace(void* trace);
 int kvr_abi_version(void);
+/* The caller wrote pool bytes on `stream` outside this library (e.g. a checkpoint
+ * load): the next decode launched on that stream issues no pool reads before its
+ * grid-dependency wait. */
+void kvr_note_pool_write(void* stream);
+/* Host validation helper: 1 when the n values (dtype F64/F32/BF16/F16) at HOST
+ * pointer p are all finite, 0 when one is NaN/Inf, -1 on a bad argument. */
+int kvr_host_all_finite(const void* p, int32_t dtype, int64_t n);
 /* Number of SMs of the current device (0 if no device). */
 int kvr_device_sms(void);
 
@@ -170,9 +181,11 @@ int kvr_dequantize_pages(const kvr_pool* pool, const int32_t* block_table, int32
  */
 /*
  * Both decode entry points launch with programmatic dependent launch: before their
- * dependency wait they read block_table, seq_lens, new_slot and pool cells older
- * than the last two tokens of each sequence (a preceding kernel that writes those
- * must not trigger launch_dependents early).  Splits merge inside the decode
+ * dependency wait they read block_table, seq_lens and new_slot, and -- unless the
+ * stream's last pool access was a write -- pool cells older than the last two
+ * tokens of each sequence.  Every store entry point of this library notes its
+ * stream; a caller that writes pool bytes by other means (a copy, its own kernel)
+ * calls kvr_note_pool_write(stream) before the next decode on that stream.  Splits merge inside the decode
  * kernel up to 32 splits (a thread-block cluster up to 8, the last CTA of each
  * (sequence, kv head) above that); with more, a second split-merge kernel follows
  * the decode kernel on the stream.
@@ -186,6 +199,14 @@ int kvr_paged_decode(const void* q, int32_t q_dtype, const kvr_pool* pool,
                      int32_t batch, int32_t num_q_heads, int32_t max_seq_len, int32_t rot_order,
                      int32_t rotate, int32_t targets, const uint32_t* sign_words, float* out,
                      void* workspace, size_t workspace_bytes, int32_t num_splits, void* stream);
+
+/*
+ * Flat full-precision decode (attention.decode_step_fp): q (num_q_heads, d), k / v
+ * (t, num_kv_heads, d) f64 device arrays, out (num_q_heads, d) f64; f64 arithmetic,
+ * max-subtracted softmax; head_dim <= 256.
+ */
+int kvr_decode_flat_f64(const double* q, const double* k, const double* v, int64_t t, int32_t num_q_heads,
+                        int32_t num_kv_heads, int32_t head_dim, double* out, void* stream);
 
 /*
  * One serving decode step, fused into a single launch: for every sequence b the

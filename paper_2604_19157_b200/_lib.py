@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("KVR_LIB_PATH") or os.path.join(_HERE, "_lib", "libkvr
 KVR_F64, KVR_F32, KVR_BF16, KVR_F16 = 0, 1, 2, 3
 KVR_KEYS_ONLY, KVR_KEYS_AND_VALUES = 0, 1
 KVR_FLAG_NONFINITE = 1
+KVR_FLAG_LEN_OVERFLOW = 2
 KVR_PREC_INT4, KVR_PREC_BF16 = 0, 1
 
 # every symbol include/kvrot_b200.h declares
@@ -27,7 +28,8 @@ EXPORTED = (
     "kvr_fwht_rows_f64", "kvr_pack_rows", "kvr_unpack_rows", "kvr_quantize_rows_f64",
     "kvr_dequantize_rows_f64", "kvr_block_rotate", "kvr_rotate_quantize_store",
     "kvr_dequantize_pages", "kvr_decode_workspace_bytes", "kvr_decode_pick_splits",
-    "kvr_paged_decode", "kvr_decode_step", "kvr_debug_decode_trace",
+    "kvr_paged_decode", "kvr_decode_step", "kvr_debug_decode_trace", "kvr_note_pool_write",
+    "kvr_host_all_finite", "kvr_decode_flat_f64",
 )
 
 
@@ -56,6 +58,9 @@ def _declare(lib):
         "kvr_pool_init_bf16": (_I32, [ctypes.POINTER(KvrPool), _P, _I64, _I32, _I32, _I32]),
         "kvr_last_error": (ctypes.c_char_p, []),
         "kvr_debug_decode_trace": (None, [_P]),
+        "kvr_note_pool_write": (None, [_P]),
+        "kvr_host_all_finite": (_I32, [_P, _I32, _I64]),
+        "kvr_decode_flat_f64": (_I32, [_P, _P, _P, _I64, _I32, _I32, _I32, _P, _P]),
         "kvr_abi_version": (_I32, []),
         "kvr_device_sms": (_I32, []),
         "kvr_fwht_rows_f64": (_I32, [_P, _I64, _I32, _I32, _P]),

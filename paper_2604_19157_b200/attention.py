@@ -27,6 +27,25 @@ _Q_CODE = {torch.float32: _lib.KVR_F32, torch.bfloat16: _lib.KVR_BF16, torch.flo
 _KV_CODE = {torch.float64: _lib.KVR_F64, **_Q_CODE}
 
 
+def _all_finite(t: torch.Tensor) -> bool:
+    """NaN/Inf check of a host tensor (native helper) or a CUDA tensor (synchronises)."""
+    if t.is_cuda:
+        return bool(torch.isfinite(t).all())
+    t = t if t.is_contiguous() else t.contiguous()
+    rc = _lib.lib().kvr_host_all_finite(ctypes.c_void_p(t.data_ptr()), _KV_CODE[t.dtype], t.numel())
+    if rc < 0:
+        raise ShapeError(f"unsupported dtype {t.dtype}")
+    return rc == 1
+
+
+def fused_step_supported(layout: HeadLayout, precision: str) -> bool:
+    """Geometries with the one-launch append + decode kernel (kvr_decode_step);
+    others run the store kernel, then the decode kernel."""
+    P, G = layout.page_tokens, layout.group_size
+    return (precision == INT4 and layout.head_dim == 128 and P % 16 == 0 and (P & (P - 1)) == 0
+            and G in (1, 2, 4, 8))
+
+
 @dataclass(frozen=True)
 class DecodeRequest:
     q: np.ndarray  # (num_q_heads, head_dim)
@@ -52,7 +71,10 @@ class DecodePlan:
     def __init__(self, table: PageTable, seqs: Sequence[int], num_splits: int = 0, extra_tokens: int = 0):
         self.table = table
         self.seqs = list(seqs)
+        if len(set(self.seqs)) != len(self.seqs):
+            raise ShapeError("a DecodePlan's sequences must be distinct")
         lay = table.layout
+        self.fused_ok = fused_step_supported(lay, table.precision)
         for s in self.seqs:
             if table.sequence_length(s) == 0 and extra_tokens == 0:
                 raise EmptySequenceError(f"sequence {s} has no tokens")
@@ -63,6 +85,9 @@ class DecodePlan:
         # step() only patches new entries and never reallocates
         self.bt, lens, _ = table.block_table(self.seqs, width=-(-self.max_len // P))
         self._known_pages = [len(table._seq_pages[s]) for s in self.seqs]
+        # pinned host mirror of the block table: pages gained by step() reach the
+        # device with an async copy of just the new entry (no host synchronisation)
+        self._bt_host = self.bt.cpu().pin_memory()
         # step metadata lives in one device block: slots int64[B] | lens int32[B];
         # step() refreshes it (plus the step's q/k/v when given on the host)
         # with a single pinned host->device copy
@@ -80,18 +105,26 @@ class DecodePlan:
         self.splits = num_splits
         self.ws = table.workspace(B, lay.num_q_heads, num_splits)
 
-    def _patch_pages(self) -> None:
-        """Write block-table entries of pages the sequences gained since the last call."""
+    def _patch_pages(self, stream: Optional[int] = None) -> None:
+        """Write block-table entries of pages the sequences gained since the last call
+        (async copies of the new entries from the pinned mirror, on `stream`)."""
         P = self.table.layout.page_tokens
+        W = self.bt.shape[1]
+        if stream is None:
+            stream = torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
+        hb = self._bt_host.numpy()
         for i, s in enumerate(self.seqs):
             pages = self.table._seq_pages[s]
             k0 = self._known_pages[i]
             if len(pages) > k0:
-                if len(pages) > self.bt.shape[1]:
+                if len(pages) > W:
                     raise ShapeError(f"sequence {s} grew to {len(pages) * P} tokens, beyond the plan's "
-                                     f"{self.bt.shape[1] * P}-token block table; build a new DecodePlan "
+                                     f"{W * P}-token block table; build a new DecodePlan "
                                      f"(or pass extra_tokens)")
-                self.bt[i, k0:len(pages)].copy_(torch.tensor(pages[k0:], dtype=torch.int32), non_blocking=False)
+                hb[i, k0:len(pages)] = pages[k0:]
+                off = (i * W + k0) * 4
+                _kernels.h2d_async(self.bt.data_ptr() + off, self._bt_host.data_ptr() + off, 4 * (len(pages) - k0),
+                                   stream)
                 self._known_pages[i] = len(pages)
 
     def refresh(self) -> None:
@@ -102,10 +135,13 @@ class DecodePlan:
         self._lens_stale = False
         self.max_len = max(self.max_len, max(lens))
 
-    def run(self, q: torch.Tensor, spec: Optional[RotationSpec], out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    def run(self, q: torch.Tensor, spec: Optional[RotationSpec], out: Optional[torch.Tensor] = None,
+            lens: Optional[torch.Tensor] = None) -> torch.Tensor:
         table, lay = self.table, self.table.layout
-        if self._lens_stale:
-            self.refresh()
+        if lens is None:
+            if self._lens_stale:
+                self.refresh()
+            lens = self.lens
         if q.dtype not in _Q_CODE:
             q = q.float()
         q = q.contiguous()
@@ -125,7 +161,7 @@ class DecodePlan:
         targets = _lib.KVR_KEYS_ONLY if (rotate and spec.targets is Targets.KEYS_ONLY) else _lib.KVR_KEYS_AND_VALUES
         _lib.check(_lib.lib().kvr_paged_decode(
             _kernels.ptr(q), _Q_CODE[q.dtype], ctypes.byref(table.desc), _kernels.ptr(self.bt), self.bt.shape[1],
-            _kernels.ptr(self.lens), len(self.seqs), lay.num_q_heads, self.max_len, spec.order if rotate else 1,
+            _kernels.ptr(lens), len(self.seqs), lay.num_q_heads, self.max_len, spec.order if rotate else 1,
             1 if rotate else 0, targets, spec.sign_words(lay.head_dim) if rotate else None, _kernels.ptr(out),
             _kernels.ptr(self.ws), self.ws.numel(), self.splits, _kernels.stream_ptr()))
         return out
@@ -166,12 +202,12 @@ class DecodePlan:
         if table.precision != INT4:
             spec = None
         rotate = spec is not None
-        if rotate and spec.learned is not None:  # row f3: unfused write, then decode
+        if (rotate and spec.learned is not None) or not self.fused_ok:
+            # row f3 (learned R) and geometries without the one-launch kernel: the
+            # store kernel (exact f64 arithmetic, as the fused writer), then the decode
             dev = table.device
             table.store_slots(k_new.to(dev), v_new.to(dev), slots.to(dev), spec, exact=True)
-            if lens is not self.lens:
-                self.lens.copy_(lens, non_blocking=True)
-            res = self.run(q.to(dev), spec, out if out.is_cuda else None)
+            res = self.run(q.to(dev), spec, out if out.is_cuda else None, lens=lens.to(dev))
             if res is not out:
                 out.copy_(res, non_blocking=True)
             return out
@@ -221,7 +257,7 @@ class DecodePlan:
         return lay
 
     def step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, spec: Optional[RotationSpec],
-             out: Optional[torch.Tensor] = None, graph: bool = False) -> torch.Tensor:
+             out: Optional[torch.Tensor] = None, graph: bool = False, check: bool = True) -> torch.Tensor:
         """One serving decode step for every sequence of the plan: allocate the new
         token's slot (reference page order), then one fused append + decode launch.
         q (B, nq, d) and k_new/v_new (B, H, d) may be host tensors: they are staged
@@ -234,20 +270,52 @@ class DecodePlan:
 
         graph=True launches the kernel from a CUDA graph captured on first use per
         ring slot; the block table keeps its address and the plan's max_len (its
-        capacity) is fixed, so only the host bookkeeping runs per step."""
+        capacity) is fixed, so only the host bookkeeping runs per step.
+
+        Every check runs before any allocator state is committed, so a failing
+        step leaves the sequences as they were (the reference validates before it
+        mutates, cache.py:225-233): shapes, the block-table and graph capacity, and
+        with check=True (default) NaN/Inf in q / k_new / v_new (host tensors by a
+        native scan; CUDA tensors by a synchronising device reduction -- pass
+        check=False to skip it: a non-finite token is then neither written nor
+        attended, and table.check_flags() reports it)."""
         table = self.table
+        lay = table.layout
         B = len(self.seqs)
         stream = torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
-        slots, fresh = table.alloc.plan(self.seqs)
+        if (tuple(q.shape) != (B, lay.num_q_heads, lay.head_dim) or tuple(k_new.shape) != (B, lay.num_kv_heads,
+                lay.head_dim) or tuple(v_new.shape) != tuple(k_new.shape)):
+            raise ShapeError(f"expected q ({B}, {lay.num_q_heads}, {lay.head_dim}) and k/v ({B}, {lay.num_kv_heads}, "
+                             f"{lay.head_dim}), got {tuple(q.shape)}, {tuple(k_new.shape)}, {tuple(v_new.shape)}")
+        if out is not None and not out.is_cuda and not out.is_pinned():
+            raise ShapeError("out must be a CUDA tensor or a pinned host tensor")
+        if check and not (_all_finite(q) and _all_finite(k_new) and _all_finite(v_new)):
+            raise NonFiniteInputError("q / k_new / v_new contain NaN or Inf")
+        cur = [table.sequence_length(s) for s in self.seqs]
+        mx = max(cur) + 1
+        W = self.bt.shape[1] * lay.page_tokens
+        if mx > W:
+            raise ShapeError(f"a sequence would grow to {mx} tokens, beyond the plan's {W}-token block table; "
+                             f"build a new DecodePlan (extra_tokens)")
+        if mx > self.max_len and graph:
+            raise ShapeError(f"sequence length {mx} passed the plan's capacity {self.max_len}; "
+                             f"build a new DecodePlan (extra_tokens)")
+        slots, fresh = table.alloc.plan(self.seqs)  # commit (pages on the free heap are zero)
+        known = list(self._known_pages)
+        try:
+            return self._step_committed(q, k_new, v_new, spec, out, graph, slots, fresh, cur, mx, stream)
+        except BaseException:
+            table.alloc.unplan(self.seqs, fresh)  # nothing of a failed step stays behind
+            self._known_pages = known
+            raise
+
+    def _step_committed(self, q, k_new, v_new, spec, out, graph, slots, fresh, cur, mx, stream):
+        table = self.table
+        B = len(self.seqs)
         if fresh:
-            table._zero_pages(fresh)
-            self._patch_pages()
-        lens = np.fromiter((table._seq_len[s] for s in self.seqs), dtype=np.int32, count=B)
-        mx = int(lens.max())
+            self._patch_pages(stream)
+        lens = np.fromiter((c + 1 for c in cur), dtype=np.int32, count=B)
         if mx > self.max_len:
-            if graph:
-                raise ShapeError(f"sequence length {mx} passed the plan's capacity {self.max_len}; "
-                                 f"build a new DecodePlan (extra_tokens)")
             self.max_len = mx
         host_in = [t for t in (q, k_new, v_new) if not t.is_cuda]
         lkey = tuple((t.shape, t.dtype) for t in host_in)
@@ -274,8 +342,6 @@ class DecodePlan:
         q, k_new, v_new = (t if t.is_cuda else next(staged) for t in (q, k_new, v_new))
         if out is None:
             out = torch.empty(q.shape, dtype=torch.float32, device=table.device)
-        elif not out.is_cuda and not out.is_pinned():
-            raise ShapeError("out must be a CUDA tensor or a pinned host tensor")
 
         if not side:  # the staged bytes go over on the compute stream, ahead of the kernel
             _kernels.h2d_async(dptr, buf_ptr, lay["bytes"], stream)
@@ -287,7 +353,8 @@ class DecodePlan:
             device_part()
         else:
             graphs = lay.setdefault("graphs", {})
-            gkey = (slot_i, side, out.data_ptr(), id(spec), q.data_ptr(), k_new.data_ptr(), v_new.data_ptr())
+            gkey = (slot_i, side, out.data_ptr(), id(spec), q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(),
+                    self.max_len, self.splits)
             g = graphs.get(gkey)
             if g is not None:
                 if g[1] is not None:
@@ -327,7 +394,8 @@ def decode_step(req: DecodeRequest, table: PageTable, spec: Optional[RotationSpe
 
 
 def decode_step_fp(q, flat_k, flat_v, layout: HeadLayout) -> np.ndarray:
-    """Full-precision decode over flat (t, kv_heads, d) arrays (attention.py:90-115), f64 on the device."""
+    """Full-precision decode over flat (t, kv_heads, d) arrays (attention.py:90-115): the
+    f64 flat-decode kernel (kvr_decode_flat_f64)."""
     q = _check_query(q, layout)
     k = np.asarray(flat_k, dtype=np.float64)
     v = np.asarray(flat_v, dtype=np.float64)
@@ -337,13 +405,14 @@ def decode_step_fp(q, flat_k, flat_v, layout: HeadLayout) -> np.ndarray:
         raise ShapeError(f"key/value shape mismatch: {k.shape} vs {v.shape}")
     if k.shape[0] == 0:
         raise EmptySequenceError("no cached tokens")
+    if layout.head_dim > 256:
+        raise ShapeError(f"head_dim {layout.head_dim} > 256")
     dev = _kernels.device()
     qt = torch.from_numpy(q).to(dev)
-    kt = torch.from_numpy(k).to(dev)
-    vt = torch.from_numpy(v).to(dev)
-    g = layout.group_size
-    kq = kt.repeat_interleave(g, dim=1)  # (t, nq, d)
-    vq = vt.repeat_interleave(g, dim=1)
-    logits = torch.einsum("thd,hd->ht", kq, qt) * (1.0 / math.sqrt(layout.head_dim))
-    w = torch.softmax(logits, dim=-1)
-    return torch.einsum("ht,thd->hd", w, vq).cpu().numpy()
+    kt = torch.from_numpy(np.ascontiguousarray(k)).to(dev)
+    vt = torch.from_numpy(np.ascontiguousarray(v)).to(dev)
+    out = torch.empty_like(qt)
+    _lib.check(_lib.lib().kvr_decode_flat_f64(_kernels.ptr(qt), _kernels.ptr(kt), _kernels.ptr(vt), k.shape[0],
+                                              layout.num_q_heads, layout.num_kv_heads, layout.head_dim,
+                                              _kernels.ptr(out), _kernels.stream_ptr()))
+    return out.cpu().numpy()

@@ -47,11 +47,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
                      "-I", os.path.join(ROOT, "include")]
     if verbose:
         common += ["-Xptxas", "-v"]
-    for src in SOURCES:
+    procs = []
+    for src in SOURCES:  # translation units compile in parallel
         obj = os.path.join(LIB_DIR, src.replace(".cu", ".o"))
         cmd = [nvcc] + common + ["-c", os.path.join(CSRC, src), "-o", obj]
-        subprocess.run(cmd, check=True)
+        procs.append((subprocess.Popen(cmd), cmd))
         objs.append(obj)
+    for p, cmd in procs:
+        if p.wait() != 0:
+            raise subprocess.CalledProcessError(p.returncode, cmd)
     tmp = LIB_PATH + ".tmp"
     subprocess.run([nvcc] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs, check=True)
     os.replace(tmp, LIB_PATH)

@@ -221,13 +221,30 @@ class PageAllocator:
         self.seq_len[seq] = t0 + n
         return slots
 
-    def release(self, seq: int) -> int:
+    def release(self, seq: int) -> list[int]:
+        """Drop `seq`; its pages go back to the free heap.  Returns them."""
         self.require(seq)
         pages = self.seq_pages.pop(seq)
         self.seq_len.pop(seq)
         for pid in pages:
             heapq.heappush(self.free, pid)
-        return len(pages)
+        return pages
+
+    def unplan(self, seqs: Sequence[int], fresh: Sequence[int]) -> None:
+        """Undo a plan(seqs) that returned `fresh` (or a reserve): lengths back,
+        the fresh pages back on the free heap.  Used when a step fails after its
+        slots were planned, so a rejected token never stays in a sequence."""
+        counts: dict[int, int] = {}
+        for seq in seqs:
+            counts[seq] = counts.get(seq, 0) + 1
+        taken = set(fresh)
+        for seq, n in counts.items():
+            self.seq_len[seq] -= n
+            owned = self.seq_pages[seq]
+            while owned and owned[-1] in taken:
+                owned.pop()
+        for pid in fresh:
+            heapq.heappush(self.free, pid)
 
     def plan(self, seqs: Sequence[int]) -> tuple[np.ndarray, list[int]]:
         """Slot ids (page * P + slot) for appending one token per entry of `seqs`
@@ -324,7 +341,12 @@ class PageTable:
         return list(self.alloc.seq_pages[seq])
 
     def free_sequence(self, seq: int) -> int:
-        return self.alloc.release(seq)
+        pages = self.alloc.release(seq)
+        # pages on the free heap hold zeros (the reference hands out freshly zeroed
+        # pages, cache.py:103-119): zeroing at release keeps allocation -- every
+        # 16th serving step -- free of device work
+        self._zero_pages(pages)
+        return len(pages)
 
     def _require(self, seq: int) -> None:
         self.alloc.require(seq)
@@ -351,11 +373,13 @@ class PageTable:
     def _plan_slots(self, seqs: Sequence[int]) -> tuple[np.ndarray, list[int]]:
         return self.alloc.plan(seqs)
 
-    def _zero_pages(self, pids: list[int]) -> None:
-        # the reference hands out freshly zeroed pages (cache.py:103-119)
-        if pids:
-            idx = torch.tensor(pids, dtype=torch.long).to(self.device, non_blocking=True)
+    def _zero_pages(self, pids) -> None:
+        """Zero device pages (pool bytes written outside the library's store kernels:
+        the next decode on this stream is told, see kvr_note_pool_write)."""
+        if len(pids):
+            idx = torch.tensor(list(pids), dtype=torch.long).to(self.device, non_blocking=True)
             self.pool.index_fill_(0, idx, 0)
+            _lib.lib().kvr_note_pool_write(_kernels.stream_ptr())
 
     # -- writes -----------------------------------------------------------------
     def _store(self, k: torch.Tensor, v: torch.Tensor, slots: np.ndarray, spec: Optional[RotationSpec],
@@ -398,7 +422,6 @@ class PageTable:
         k, v = self._check_kv_host(k, v, 2)
         first = self._seq_len[seq]
         slots, fresh = self._plan_slots([seq])
-        self._zero_pages(fresh)
         kt = torch.from_numpy(k).to(self.device).reshape(1, *k.shape)
         vt = torch.from_numpy(v).to(self.device).reshape(1, *v.shape)
         self._store(kt, vt, slots, spec, exact=True)
@@ -414,7 +437,6 @@ class PageTable:
         if t == 0:
             return first
         slots, fresh = self._plan_slots([seq] * t)
-        self._zero_pages(fresh)
         h, d = self.layout.num_kv_heads, self.layout.head_dim
         kt = torch.from_numpy(ks).to(self.device)
         vt = torch.from_numpy(vs).to(self.device)
@@ -432,7 +454,13 @@ class PageTable:
                      exact: Optional[bool] = None, check: bool = True) -> np.ndarray:
         """Serving write: token n of (k, v) [n, H, d] is appended to sequence seqs[n].
         bf16/fp16 CUDA tensors take the fast K1 kernel; f64 takes the exact one.
-        Returns the slot ids.  check=False defers the non-finite check (see check_flags)."""
+        Returns the slot ids.
+
+        check=True (default) validates before anything is committed, like the
+        reference (cache.py:225-233): a NaN/Inf anywhere raises NonFiniteInputError
+        and no token is appended (the batch is atomic).  check=False skips that
+        (no host synchronisation): rows with NaN/Inf are then not written, the
+        device flag is set (check_flags) and the other rows are committed."""
         kt = k if isinstance(k, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(k))
         vt = v if isinstance(v, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(v))
         kt = kt.to(self.device, non_blocking=True).contiguous()
@@ -444,11 +472,10 @@ class PageTable:
             raise ShapeError(f"unsupported k/v dtype {kt.dtype}/{vt.dtype}")
         if exact is None:
             exact = kt.dtype == torch.float64
+        if check and not bool(torch.isfinite(kt).all() & torch.isfinite(vt).all()):
+            raise NonFiniteInputError("k/v contain NaN or Inf")
         slots, fresh = self._plan_slots(list(seqs))
-        self._zero_pages(fresh)
         self._store(kt, vt, slots, spec, exact=exact)
-        if check:
-            self.check_flags()
         return slots
 
     def store_slots(self, k: torch.Tensor, v: torch.Tensor, slots: torch.Tensor, spec: Optional[RotationSpec] = None,
@@ -475,11 +502,16 @@ class PageTable:
             _kernels.stream_ptr()))
 
     def check_flags(self) -> None:
-        """Raise NonFiniteInputError if any write since the last check saw NaN/Inf."""
+        """Raise if a launch since the last check flagged a problem (synchronises):
+        NonFiniteInputError for NaN/Inf K/V rows (those tokens were not written),
+        ShapeError for a decode length past the launch's max_seq_len."""
         f = int(self.flags.item())
-        if f & _lib.KVR_FLAG_NONFINITE:
+        if f:
             self.flags.zero_()
+        if f & _lib.KVR_FLAG_NONFINITE:
             raise NonFiniteInputError("k/v contained NaN or Inf (rows were not written)")
+        if f & _lib.KVR_FLAG_LEN_OVERFLOW:
+            raise ShapeError("a decode sequence length exceeded the launch's max_seq_len (tokens past it ignored)")
 
     # -- reads (cache.py:319-362) -------------------------------------------------
     def block_table(self, seqs: Sequence[int], width: int = 0) -> tuple[torch.Tensor, torch.Tensor, int]:
@@ -576,6 +608,7 @@ class PageTable:
             cells = records_to_cells(body.reshape(len(allocated), rb), layout, header["precision"])
             blobs = torch.from_numpy(cells).to(table.device)
             table.pool.index_copy_(0, torch.tensor(allocated, dtype=torch.long, device=table.device), blobs)
+            _lib.lib().kvr_note_pool_write(_kernels.stream_ptr())
         taken = set(allocated)
         table.alloc.free = [p for p in range(table.num_pages) if p not in taken]
         heapq.heapify(table.alloc.free)

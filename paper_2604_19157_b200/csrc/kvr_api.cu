@@ -4,6 +4,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "kvr_common.cuh"
 #include "kvr_internal.h"
@@ -85,24 +87,92 @@ CUresult kvr_encode_tensor_map_2d(CUtensorMap* map, const void* base, uint64_t i
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 
-int kvr_num_sms() {
-  static int sms = -1;
-  if (sms < 0) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) !=
-                                                   cudaSuccess) {
-      cudaGetLastError();
-      sms = 0;
-    }
+int kvr_current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
   }
-  return sms;
+  return (dev >= 0 && dev < KVR_MAX_DEVICES) ? dev : KVR_MAX_DEVICES - 1;
+}
+
+// SM count of the calling thread's current device (cached per device: one process
+// may drive several GPUs)
+int kvr_num_sms() {
+  static int sms[KVR_MAX_DEVICES];
+  static bool known[KVR_MAX_DEVICES];
+  const int dev = kvr_current_device();
+  if (!known[dev]) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    sms[dev] = n;
+    known[dev] = true;
+  }
+  return sms[dev];
+}
+
+static std::mutex g_pw_mu;
+static std::vector<cudaStream_t> g_pw;  // streams whose last pool access was a write
+
+void kvr_mark_pool_written(cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_pw_mu);
+  for (cudaStream_t x : g_pw)
+    if (x == st) return;
+  g_pw.push_back(st);
+}
+
+bool kvr_take_pool_written(cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_pw_mu);
+  for (size_t i = 0; i < g_pw.size(); ++i)
+    if (g_pw[i] == st) {
+      g_pw[i] = g_pw.back();
+      g_pw.pop_back();
+      return true;
+    }
+  return false;
 }
 
 extern "C" {
 
 const char* kvr_last_error(void) { return g_err; }
+void kvr_note_pool_write(void* stream) { kvr_mark_pool_written((cudaStream_t)stream); }
 void kvr_debug_decode_trace(void* trace) { kvr_set_decode_trace(trace); }
 int kvr_abi_version(void) { return KVR_ABI_VERSION; }
+
+// Host-side validation helper (not a compute path): 1 when all n values at host
+// pointer `p` are finite, 0 otherwise, -1 for a bad dtype.  Lets the serving step
+// reject NaN/Inf inputs before it commits any allocator state (cache.py:225-233).
+int kvr_host_all_finite(const void* p, int32_t dtype, int64_t n) {
+  if (n <= 0) return 1;
+  if (!p) return -1;
+  uint32_t bad = 0u;
+  switch (dtype) {
+    case KVR_BF16: {  // exponent all ones
+      const uint16_t* u = static_cast<const uint16_t*>(p);
+      for (int64_t i = 0; i < n; ++i) bad |= ((u[i] & 0x7F80u) == 0x7F80u);
+      return bad ? 0 : 1;
+    }
+    case KVR_F16: {
+      const uint16_t* u = static_cast<const uint16_t*>(p);
+      for (int64_t i = 0; i < n; ++i) bad |= ((u[i] & 0x7C00u) == 0x7C00u);
+      return bad ? 0 : 1;
+    }
+    case KVR_F32: {
+      const uint32_t* u = static_cast<const uint32_t*>(p);
+      for (int64_t i = 0; i < n; ++i) bad |= ((u[i] & 0x7F800000u) == 0x7F800000u);
+      return bad ? 0 : 1;
+    }
+    case KVR_F64: {
+      const uint64_t* u = static_cast<const uint64_t*>(p);
+      for (int64_t i = 0; i < n; ++i) bad |= ((u[i] & 0x7FF0000000000000ull) == 0x7FF0000000000000ull);
+      return bad ? 0 : 1;
+    }
+  }
+  return -1;
+}
 int kvr_device_sms(void) { return kvr_num_sms(); }
 
 int kvr_pool_init(kvr_pool* pool, void* base, int64_t num_pages, int32_t page_tokens, int32_t num_kv_heads,
@@ -213,6 +283,7 @@ int kvr_rotate_quantize_store(const void* k, const void* v, int32_t in_dtype, in
   const int rot_k = rotate ? 1 : 0;
   const int rot_v = (rotate && targets == KVR_KEYS_AND_VALUES) ? 1 : 0;
   cudaStream_t st = (cudaStream_t)stream;
+  kvr_mark_pool_written(st);  // a decode launched next on this stream must not prefetch before its wait
   if (pl.prec == KVR_PREC_BF16) {  // raw vectors, rotation ignored (cache.py:264-266)
     if (int rc = kvr_launch_store_bf16(k, v, in_dtype, n_tok, slot_mapping, pl, flags, st))
       return fail(rc, "rotate_quantize_store (bf16 pool): launch failed (%d)", rc);
@@ -240,6 +311,17 @@ int kvr_dequantize_pages(const kvr_pool* pool, const int32_t* block_table, int32
                                     (cudaStream_t)stream);
   if (rc) return fail(rc, "dequantize_pages: unsupported out dtype %d", out_dtype);
   return check_launch("dequantize_pages");
+}
+
+int kvr_decode_flat_f64(const double* q, const double* k, const double* v, int64_t t, int32_t num_q_heads,
+                        int32_t num_kv_heads, int32_t head_dim, double* out, void* stream) {
+  if (t < 1 || num_kv_heads < 1 || num_q_heads < 1 || num_q_heads % num_kv_heads || head_dim < 1)
+    return fail(KVR_ERR_SHAPE, "decode_flat_f64: bad shape (t=%lld, nq=%d, H=%d, d=%d)", (long long)t, num_q_heads,
+                num_kv_heads, head_dim);
+  if (!q || !k || !v || !out) return fail(KVR_ERR_ARG, "decode_flat_f64: null pointer");
+  if (int rc = kvr_launch_decode_flat_f64(q, k, v, t, num_q_heads, num_kv_heads, head_dim, out, (cudaStream_t)stream))
+    return fail(rc, "decode_flat_f64: head_dim %d > 256", head_dim);
+  return check_launch("decode_flat_f64");
 }
 
 size_t kvr_decode_workspace_bytes(int32_t batch, int32_t num_kv_heads, int32_t num_q_heads, int32_t head_dim,
@@ -301,6 +383,7 @@ int kvr_decode_step(const void* q, int32_t q_dtype, const void* new_k, const voi
     return fail(KVR_ERR_ARG, "q dtype %d unsupported (F32/BF16/F16)", q_dtype);
   if (pl.prec == KVR_PREC_BF16) {
     // BF16 pool: write the raw new rows, then a plain decode with the query as-is
+    kvr_mark_pool_written((cudaStream_t)stream);
     if (int rc = kvr_launch_store_bf16(new_k, new_v, kv_dtype, batch, new_slot, pl, flags, (cudaStream_t)stream))
       return fail(rc, "decode_step (bf16 pool): store failed (%d)", rc);
     Signs s0;

@@ -145,11 +145,6 @@ KVR_DEV void load_q4(const void* q, int dtype, int64_t i, float (&x)[4]) {
     x[u] = dtype == KVR_BF16 ? __uint_as_float(h[u] << 16) : __half2float(__ushort_as_half((unsigned short)h[u]));
 }
 
-// Cell of (sequence b, token t, head h) and the token's index inside it.
-KVR_DEV const uint8_t* token_cell(const DecodeParams& p, int b, int t, int h, int& ci) {
-  const int page = p.bt[(int64_t)b * p.bt_stride + (t >> p.log2P)];
-  return cell_of(p.pool, page, h, t & ((1 << p.log2P) - 1), ci);
-}
 
 // dims held by A-operand register (k-step s, lane group i, slot R0/R2, half e)
 KVR_DEV int qk_dim(int s, int i, int slot2, int e) { return 32 * i + 8 * (s >> 1) + 2 * (s & 1) + slot2 + 4 * e; }
@@ -182,7 +177,7 @@ KVR_DEV void cta_fwht_rows(float* s, int rows) {
 // Returns the stored-space (rotated) dequantised elements of lane l in deq[side]
 // (dims 4l..4l+3); a non-finite row is flagged, not written, and reads as 0.
 template <int ORDER>
-KVR_DEV void append_rows_exact(const DecodeParams& p, const Signs& sg, int b, int h, float (&deq)[2][4],
+KVR_DEV bool append_rows_exact(const DecodeParams& p, const Signs& sg, int b, int h, float (&deq)[2][4],
                                unsigned long long* tr = nullptr) {
   const int lane = threadIdx.x & 31;
   const int64_t slot = p.new_slot[b];
@@ -204,12 +199,10 @@ KVR_DEV void append_rows_exact(const DecodeParams& p, const Signs& sg, int b, in
   }
   int ci;
   uint8_t* cell = cell_of(p.pool, slot >> p.log2P, h, (int)(slot & ((1 << p.log2P) - 1)), ci);
-#pragma unroll
-  for (int sd = 0; sd < 2; ++sd) {
-    fin[sd] = __all_sync(0xffffffffu, fin[sd]);
-    if (tr && sd == 0) tr[14] = clk64();  // rows landed
-    if (!fin[sd] && lane == 0 && p.flags) atomicOr(p.flags, (uint32_t)KVR_FLAG_NONFINITE);
-  }
+  // the token is all-or-nothing: a NaN/Inf in either row leaves both unwritten
+  const bool ok = __all_sync(0xffffffffu, fin[0] && fin[1]);
+  if (tr) tr[14] = clk64();  // rows landed
+  if (!ok && lane == 0 && p.flags) atomicOr(p.flags, (uint32_t)KVR_FLAG_NONFINITE);
   const bool rot[2] = {p.rotate != 0, p.rotate && p.rot_v};
 #pragma unroll
   for (int sd = 0; sd < 2; ++sd)
@@ -291,7 +284,7 @@ KVR_DEV void append_rows_exact(const DecodeParams& p, const Signs& sg, int b, in
 #pragma unroll
       for (int u = 0; u < 4; ++u) deq[sd][u] = scv;  // sentinel row: the offset
     }
-    if (!fin[sd]) {
+    if (!ok) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) deq[sd][u] = 0.f;
       continue;
@@ -303,6 +296,7 @@ KVR_DEV void append_rows_exact(const DecodeParams& p, const Signs& sg, int b, in
       cell[sd ? cell_vzp(p.pool, ci) : cell_kzp(p.pool, ci)] = (uint8_t)zpv;
     }
   }
+  return ok;
 }
 
 // named barriers (id 0 is __syncthreads): 1 = the tile warps after query prep,
@@ -587,8 +581,9 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   // and V rows bit-exactly (f64, reference arithmetic) right away, overlapping the
   // query prep and the main loop of the others; scored once the rotated q is in smem
   float newd[2][4];
+  bool new_ok = true;
   if (APPEND && warp == DW && app_owner) {
-    append_rows_exact<ORDER>(p, signs, b, h, newd, p.trace && lane == 0 ? p.trace + cta_id * 16 : nullptr);
+    new_ok = append_rows_exact<ORDER>(p, signs, b, h, newd, p.trace && lane == 0 ? p.trace + cta_id * 16 : nullptr);
     *reinterpret_cast<float4*>(s_vnew + 4 * lane) = make_float4(newd[1][0], newd[1][1], newd[1][2], newd[1][3]);
   }
   if (threadIdx.x == 0 && len_raw > p.max_len && p.flags && h == 0 && split == 0)
@@ -741,18 +736,18 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
       const float4 qv = *reinterpret_cast<const float4*>(s_qrot + j * 128 + 4 * lane);
       const float dot =
           warp_sum(qv.x * newd[0][0] + qv.y * newd[0][1] + qv.z * newd[0][2] + qv.w * newd[0][3]);
-      if (lane == 0) s_lnew[j] = dot * (LOG2E * (float)(1.0 / sqrt(128.0)));
+      // a rejected (non-finite) token is not attended: no phantom zero key / value
+      if (lane == 0) s_lnew[j] = new_ok ? dot * (LOG2E * (float)(1.0 / sqrt(128.0))) : -INFINITY;
     }
     __syncwarp();
   }
 
-  float M[NT], lsum[NT], Zs[NT];
+  float M[NT], lsum[NT];
   float acc[NT][8][4];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
     M[nt] = -INFINITY;
     lsum[nt] = 0.f;
-    Zs[nt] = 0.f;
 #pragma unroll
     for (int m = 0; m < 8; ++m)
 #pragma unroll
@@ -919,7 +914,6 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
         if (tm > M[nt] + 7.0f) {
           const float alpha = (M[nt] == -INFINITY) ? 0.f : ex2f(M[nt] - tm);
           lsum[nt] *= alpha;
-          Zs[nt] *= alpha;
 #pragma unroll
           for (int m = 0; m < 8; ++m)
 #pragma unroll
@@ -934,6 +928,14 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
       }
     }
 
+    // zero-point term of this group, sum_t w_t z_t per q head: folded into the
+    // accumulators every group (below), so they carry sum_t w_t (c_t - z_t) -- the
+    // output's own magnitude -- and never the ~7.5 sum_t w_t of the raw codes
+    // (a running code sum minus one final z-term cancels catastrophically over
+    // long contexts)
+    float zt[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) zt[nt] = 0.f;
 #pragma unroll
     for (int c = 0; c < C; ++c) {
       uint32_t wlo[NT], whi[NT];
@@ -942,7 +944,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
         const float p0 = pr0[c][nt], p1 = pr1[c][nt];  // = p_t * 2^(.)
         const float w0 = p0 * svc0[c], w1 = p1 * svc1[c];  // = p_t * s_v * 2^(.)
         lsum[nt] += p0 + p1;
-        Zs[nt] += w0 * zv0[c] + w1 * zv1[c];
+        zt[nt] = fmaf(w0, zv0[c], fmaf(w1, zv1[c], zt[nt]));
         // fp16 hi/lo of w * 2^8 (w <= 2^7): 22-bit weights, the lo half out of fp16
         // subnormals for weights down to ~2^-21 of the reference point
         const float w0s = w0 * 256.0f, w1s = w1 * 256.0f;
@@ -976,6 +978,22 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
         for (int nt = 0; nt < NT; ++nt)
           mma16816(acc[nt][m], xr[0][0][m], xr[0][1][m], xr[1][0][m], xr[1][1][m], wlo[nt], whi[nt]);
     }
+    // the fold: this q head's group z-term summed over the 8 lanes of its column
+    // (lanes i, i + 4, ...), subtracted from the hi column of every output row in
+    // accumulator units (x 2^24 codes / 2^8 weights; x 16 for the high-nibble tiles)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      float z = zt[nt];
+      z += __shfl_xor_sync(0xffffffffu, z, 4);
+      z += __shfl_xor_sync(0xffffffffu, z, 8);
+      z += __shfl_xor_sync(0xffffffffu, z, 16);
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const float u = (m & 1) ? -0x1p-12f : -0x1p-16f;
+        acc[nt][m][0] = fmaf(z, u, acc[nt][m][0]);
+        acc[nt][m][2] = fmaf(z, u, acc[nt][m][2]);
+      }
+    }
     if (++stg == NSTG) {
       stg = 0;
       phase ^= 1u;
@@ -994,10 +1012,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {
-      lsum[nt] += __shfl_xor_sync(0xffffffffu, lsum[nt], o);
-      Zs[nt] += __shfl_xor_sync(0xffffffffu, Zs[nt], o);
-    }
+    for (int o = 4; o < 32; o <<= 1) lsum[nt] += __shfl_xor_sync(0xffffffffu, lsum[nt], o);
     if (r == 0) s_m[warp * 8 + 4 * nt + i] = tile_warp ? M[nt] : -INFINITY;
   }
   if (APPEND && warp == DW && lane < 8)  // the writer warp's partial: the new token alone
@@ -1017,8 +1032,8 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
 #pragma unroll
       for (int m = 0; m < 8; ++m) {
         const float f = ((m & 1) ? 65536.0f / 16.0f : 65536.0f) * sc;  // undo 2^-24 (codes), 2^8 (w), x16 nibble
-        dst[m * 8] = (acc[nt][m][0] + acc[nt][m][1]) * f - Zs[nt] * sc;
-        dst[(m + 8) * 8] = (acc[nt][m][2] + acc[nt][m][3]) * f - Zs[nt] * sc;
+        dst[m * 8] = (acc[nt][m][0] + acc[nt][m][1]) * f;
+        dst[(m + 8) * 8] = (acc[nt][m][2] + acc[nt][m][3]) * f;
       }
       if (r == 0) s_lw[warp * 8 + j] = lsum[nt] * sc;
     }
@@ -1310,7 +1325,7 @@ __global__ void decode_generic_kernel(const __grid_constant__ DecodeParams p, co
   for (int k = 0; k < 8; ++k) o[k] = 0.f;
   for (int t = warp; t < len; t += nw) {
     int ci;
-    const uint8_t* cell = token_cell(p, b, t, h, ci);
+    const uint8_t* cell = cell_of(p.pool, p.bt[(int64_t)b * p.bt_stride + t / p.pool.P], h, t % p.pool.P, ci);
     const bool bf = p.pool.prec == KVR_PREC_BF16;  // raw bf16 rows (cache.py:115-118)
     const uint16_t* kb = reinterpret_cast<const uint16_t*>(cell + cell_bf16(p.pool, 0, ci));
     const uint16_t* vb = reinterpret_cast<const uint16_t*>(cell + cell_bf16(p.pool, 1, ci));
@@ -1446,13 +1461,14 @@ int kvr_pick_splits(int batch, int H, int max_len, int P) {
 template <int NT, int ORDER, bool APP, bool CL>
 static int launch_one(dim3 grid, size_t smem, cudaStream_t st, const DecodeParams& p, const Signs& sg) {
   auto kern = decode_tma_kernel<NT, ORDER, APP, NT == 1 ? 2 : KVR_NT2_CELLS, CL>;
-  static bool set = false;  // one flag per instantiation
-  if (!set) {
+  static bool set[KVR_MAX_DEVICES];  // per instantiation and device
+  const int dev = kvr_current_device();
+  if (!set[dev]) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return KVR_ERR_CUDA;
     if (CL && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
       return KVR_ERR_CUDA;
-    set = true;
+    set[dev] = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
@@ -1474,8 +1490,9 @@ static int launch_one(dim3 grid, size_t smem, cudaStream_t st, const DecodeParam
 // Can clusters of `splits` CTAs of this kernel be co-scheduled? (cached per size)
 template <int NT, int ORDER, bool APP>
 static bool cluster_ok(int splits, size_t smem) {
-  static int cache[17] = {0};  // 0 unknown, 1 yes, 2 no
+  static int cache_all[KVR_MAX_DEVICES][17];  // per device: 0 unknown, 1 yes, 2 no
   if (splits < 2 || splits > 16) return false;
+  int* cache = cache_all[kvr_current_device()];
   if (!cache[splits]) {
     auto kern = decode_tma_kernel<NT, ORDER, APP, NT == 1 ? 2 : KVR_NT2_CELLS, true>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1567,7 +1584,9 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
   // defaults are the measured best): one ring group per warp before the wait (a
   // full-ring burst queues the query load behind it), evict-first KV streaming,
   // inline split merge for 9..32 splits
-  p.pre_groups = KVR_PREWAIT_GROUPS;
+  // (pool cells read before griddepcontrol.wait are only those no preceding grid on
+  // the stream writes: after a store kernel on this stream the prefetch waits)
+  p.pre_groups = kvr_take_pool_written(st) ? 0 : KVR_PREWAIT_GROUPS;
   p.evict_first = KVR_EVICT_FIRST;
   int l2 = 0;
   while ((1 << l2) < pool.P) ++l2;
@@ -1575,8 +1594,7 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
   p.log2P = l2;
   Signs sg = s;
   if (!has) for (auto& x : sg.w) x = 0u;
-  if (!pow2) return KVR_ERR_UNSUPPORTED;
-  const bool tma_ok = pool.prec == KVR_PREC_INT4 && pool.d == 128 && pool.T == 16 &&
+  const bool tma_ok = pow2 && pool.prec == KVR_PREC_INT4 && pool.d == 128 && pool.T == 16 &&
                       (p.G == 1 || p.G == 2 || p.G == 4 || p.G == 8) &&
                       (reinterpret_cast<uintptr_t>(pool.base) & 15) == 0 && (pool.cell_bytes & 15) == 0;
   if (tma_ok) {
@@ -1607,7 +1625,7 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
     return p.G == 8 ? launch_tma<2, false>(p, sg, grid, smem, ord, st) : launch_tma<1, false>(p, sg, grid, smem, ord, st);
   }
   if (new_slot) return KVR_ERR_UNSUPPORTED;  // the fused append lives in the TMA kernel only
-  if (pool.d > 256 || (pool.d & 31)) return KVR_ERR_UNSUPPORTED;
+  if (pool.d > 256) return KVR_ERR_UNSUPPORTED;
   p.splits = 1;
   const int warps = 4;
   const size_t smem = (size_t)(pool.d + warps * pool.d + warps * 2) * sizeof(float);

@@ -26,6 +26,8 @@ int kvr_launch_store_bf16(const void* k, const void* v, int in_dtype, int64_t n_
                           const kvr::Pool& pool, uint32_t* flags, cudaStream_t st);
 int kvr_launch_dequant_pages(const kvr::Pool& pool, const int32_t* bt, int bt_stride, const int32_t* lens, int batch,
                              int max_len, void* k_out, void* v_out, int out_dtype, cudaStream_t st);
+int kvr_launch_decode_flat_f64(const double* q, const double* k, const double* v, int64_t t, int nq, int H, int d,
+                               double* out, cudaStream_t st);
 
 // Fast serving-path write (bf16/fp16 rows, head_dim 128): returns KVR_ERR_UNSUPPORTED
 // when the configuration has no specialised kernel (caller falls back to the exact path).
@@ -48,4 +50,15 @@ void kvr_set_decode_trace(void* trace);
 CUresult kvr_encode_tensor_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows,
                                   uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_rows,
                                   CUtensorMapSwizzle swz);
+// Per-device launch state: function attributes and occupancy answers are cached per
+// CUDA device (index = kvr_current_device()), so one process may drive several GPUs.
+constexpr int KVR_MAX_DEVICES = 64;
+int kvr_current_device();
 int kvr_num_sms();
+
+// Pool-write notes per stream (host side, mutex-protected): every launch that writes
+// pool cells marks its stream; the next decode launch on that stream takes the mark
+// and then issues no pool reads before its grid-dependency wait (griddepcontrol.wait
+// is the only point where a preceding grid's writes are guaranteed visible).
+void kvr_mark_pool_written(cudaStream_t st);
+bool kvr_take_pool_written(cudaStream_t st);

@@ -325,6 +325,73 @@ __global__ void dequant_bf16_kernel(Pool pool, const int32_t* bt, int bt_stride,
   }
 }
 
+// Flat full-precision decode (attention.decode_step_fp, attention.py:90-115): per q
+// head, softmax(K[:, kv] q / sqrt(d)) V[:, kv] over flat (t, H, d) f64 arrays, all in
+// f64.  One CTA per q head; warp w takes tokens w, w + nw, ... with lanes over the
+// dims (warp-reduced dot), an online max-subtracted softmax per warp, then the warps
+// merge through shared memory.
+__global__ void decode_flat_f64_kernel(const double* q, const double* k, const double* v, int64_t t, int H, int G,
+                                       int d, double* out) {
+  extern __shared__ double fsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int qh = blockIdx.x, kv = qh / G;
+  double* so = fsm;                // [nw][d]
+  double* sml = fsm + nw * d;      // [nw][2]
+  const double scale = 1.0 / sqrt((double)d);
+  double qr[8], o[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int x = lane + 32 * e;
+    qr[e] = x < d ? q[(int64_t)qh * d + x] : 0.0;
+    o[e] = 0.0;
+  }
+  double m = -INFINITY, l = 0.0;
+  for (int64_t tok = warp; tok < t; tok += nw) {
+    const double* kr = k + (tok * H + kv) * d;
+    const double* vr = v + (tok * H + kv) * d;
+    double dot = 0.0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int x = lane + 32 * e;
+      if (x < d) dot = fma(kr[x], qr[e], dot);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
+    dot *= scale;
+    const double mn = fmax(m, dot);
+    const double a = exp(m - mn), pw = exp(dot - mn);
+    l = l * a + pw;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int x = lane + 32 * e;
+      if (x < d) o[e] = fma(pw, vr[x], o[e] * a);
+    }
+    m = mn;
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int x = lane + 32 * e;
+    if (x < d) so[warp * d + x] = o[e];
+  }
+  if (lane == 0) {
+    sml[2 * warp] = m;
+    sml[2 * warp + 1] = l;
+  }
+  __syncthreads();
+  for (int x = threadIdx.x; x < d; x += blockDim.x) {
+    double mm = -INFINITY;
+    for (int w = 0; w < nw; ++w) mm = fmax(mm, sml[2 * w]);
+    double lt = 0.0, ot = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      if (sml[2 * w] == -INFINITY) continue;
+      const double f = exp(sml[2 * w] - mm);
+      lt += f * sml[2 * w + 1];
+      ot += f * so[w * d + x];
+    }
+    out[(int64_t)qh * d + x] = ot / lt;
+  }
+}
+
 }  // namespace kvr
 
 // ============================ host launchers ================================
@@ -493,5 +560,14 @@ int kvr_launch_dequant_pages(const Pool& pool, const int32_t* bt, int bt_stride,
       break;
     default: return KVR_ERR_ARG;
   }
+  return 0;
+}
+
+int kvr_launch_decode_flat_f64(const double* q, const double* k, const double* v, int64_t t, int nq, int H, int d,
+                               double* out, cudaStream_t st) {
+  if (d > 256 || nq % H) return KVR_ERR_UNSUPPORTED;
+  const int warps = 8;
+  const size_t smem = (size_t)(warps * d + 2 * warps) * sizeof(double);
+  decode_flat_f64_kernel<<<nq, warps * 32, smem, st>>>(q, k, v, t, H, nq / H, d, out);
   return 0;
 }

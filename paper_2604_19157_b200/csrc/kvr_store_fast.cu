@@ -487,7 +487,6 @@ __global__ void __launch_bounds__(FS_WARPS * 32, KVR_FS_MINB)
   // programmatic dependent launch: the setup above overlaps the previous kernel;
   // the inputs, slot ids and the pool may come from it
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   int tile = blockIdx.x * FS_WARPS + wib;
   if (tile < total_tiles && elect_one()) issue(tile, 0);
   uint32_t phases = 0u;  // bit b: parity of buffer b
@@ -540,10 +539,11 @@ static int launch_fast_impl(const void* k, const void* v, int64_t n_tok, const i
     return KVR_ERR_CUDA;
   const size_t smem = FS_WARPS * (2 * FS_TILE_BYTES + MS_STAGE) + 64 + 256 + 1024;
   auto kern = store_mma_kernel<ORDER, F16>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[KVR_MAX_DEVICES];  // per device (cudaFuncSetAttribute is per device)
+  const int dev = kvr_current_device();
+  if (!attr_set[dev]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_set = true;
+    attr_set[dev] = true;
   }
   const int total_tiles = 2 * prm.tiles_per_side;
   int grid = (total_tiles + FS_WARPS - 1) / FS_WARPS;

@@ -31,3 +31,9 @@ def rng():
 def golden_bf16():
     with np.load(os.path.join(GOLDEN_DIR, "golden_bf16.npz")) as z:
         return {k: z[k] for k in z.files}
+
+
+@pytest.fixture(scope="session")
+def golden_reads():
+    with np.load(os.path.join(GOLDEN_DIR, "golden_reads.npz")) as z:
+        return {k: z[k] for k in z.files}

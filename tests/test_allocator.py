@@ -34,10 +34,28 @@ def test_lowest_id_reuse_and_release():
     a.create(1)
     a.plan([0] * 9)
     a.plan([1])
-    assert a.release(0) == 3
+    assert a.release(0) == [0, 1, 2]
     a.create(2)
     a.plan([2])
     assert a.seq_pages[2] == [0]
+
+
+def test_unplan_restores_state():
+    """A step that fails after planning its slots is undone completely: lengths,
+    page lists and the free heap are as before (the reference never mutates on a
+    rejected append, cache.py:225-233)."""
+    a = PageAllocator(8, 4)
+    for s in (0, 1, 2):
+        a.create(s)
+    a.plan([0] * 4 + [1] * 3)
+    before = (sorted(a.free), {k: list(v) for k, v in a.seq_pages.items()}, dict(a.seq_len))
+    slots, fresh = a.plan([0, 1, 2])  # seq 0 and 2 take fresh pages, seq 1 fills its page
+    assert len(fresh) == 2
+    a.unplan([0, 1, 2], fresh)
+    assert (sorted(a.free), {k: list(v) for k, v in a.seq_pages.items()}, dict(a.seq_len)) == before
+    assert a.plan([0, 1, 2])[0].tolist() == slots.tolist()  # same slots again
+    fr = a.reserve(2, 9)
+    assert a.seq_len[2] == 10
 
 
 def test_all_or_nothing_on_exhaustion():

@@ -22,3 +22,8 @@ def test_reference_arm_json_line():
     assert line["cpu_baseline"]["kind"] in ("reference", "port") and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
     assert line["e2e"]["value"] == line["value"] and line["e2e"]["unit"] == line["unit"]
+    # both arms describe the same workload with the same config dict
+    sys.path.insert(0, ROOT)
+    import bench
+
+    assert line["config"] == bench.headline_config(1)
