@@ -10,14 +10,16 @@
 // Design (B200, sm_100a, head_dim 128, GQA group G in {1,2,4,8}):
 //  * grid = (split, kv head, sequence); 4 warps per CTA stride over 16-token
 //    tiles of the split; a warp owns one (kv head, tile) at a time;
-//  * INT4 codes never become floats in memory: a nibble masked into the low
-//    mantissa bits of an fp16 IS the fp16 subnormal c * 2^-24 (exact), so one
-//    LOP3 turns a code word into two MMA operands; the 2^-24 (and the x16 of
-//    high nibbles) are folded into the query / the epilogue;
+//  * INT4 codes never become floats in memory: for QK a nibble masked into the
+//    low mantissa bits of an fp16 IS the fp16 subnormal c * 2^-24 (exact), so one
+//    LOP3 turns a code word into two MMA operands (or the code bytes feed the int8
+//    MMA directly); for PV a nibble masked into the mantissa of 1024.0 minus
+//    1024 + z gives the exact signed c - z (LOP3 + HSUB2 per two operands);
 //  * dequantisation is factored out of the inner products:
 //        logit = s_k * (q.c - z * sum(q)) / sqrt(d),  out = sum_t w_t (c_t - z_t)
-//    with w_t = p_t s_t, so the tensor cores (mma.sync m16n8k16, fp16 in /
-//    fp32 accumulate) only ever see exact codes;
+//    with w_t = p_t s_t, so the tensor cores (mma.sync, fp16 / int8 in, fp32 /
+//    int32 accumulate) only ever see exact integers; PV products carry both signs
+//    (c - z), so the tensor core's truncating accumulation does not drift;
 //  * the query and the softmax weights are split hi + lo fp16 (22-bit
 //    significand) and packed as column pairs of the same 8-wide MMA tile, so
 //    one MMA per (16 tokens x 16 dims) yields both halves;
@@ -99,6 +101,12 @@ KVR_DEV void imma16832(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint3
 KVR_DEV float ex2f(float x) {
   float r;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+KVR_DEV uint32_t hsub2_u32(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
   return r;
 }
 
@@ -199,8 +207,28 @@ KVR_DEV bool append_rows_exact(const DecodeParams& p, const Signs& sg, int b, in
   }
   int ci;
   uint8_t* cell = cell_of(p.pool, slot >> p.log2P, h, (int)(slot & ((1 << p.log2P) - 1)), ci);
-  // the token is all-or-nothing: a NaN/Inf in either row leaves both unwritten
-  const bool ok = __all_sync(0xffffffffu, fin[0] && fin[1]);
+  // the token is all-or-nothing (the reference validates the whole (H, d) K and V
+  // before any write, cache.py:225-233): a NaN/Inf in any head's row leaves every
+  // head's rows unwritten -- so this writer also scans the other heads' rows
+  bool all_fin = fin[0] && fin[1];
+  for (int hh = 0; hh < p.pool.H; ++hh) {
+    if (hh == h) continue;
+    const int64_t ob = ((int64_t)b * p.pool.H + hh) * 128 + 4 * lane;
+#pragma unroll
+    for (int sd = 0; sd < 2; ++sd) {
+      const void* src = sd ? p.new_v : p.new_k;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        float xv;
+        if (p.new_dtype == KVR_BF16) xv = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(src)[ob + u]);
+        else if (p.new_dtype == KVR_F16) xv = __half2float(reinterpret_cast<const __half*>(src)[ob + u]);
+        else if (p.new_dtype == KVR_F32) xv = reinterpret_cast<const float*>(src)[ob + u];
+        else xv = isfinite(reinterpret_cast<const double*>(src)[ob + u]) ? 0.f : NAN;
+        all_fin &= (bool)isfinite(xv);
+      }
+    }
+  }
+  const bool ok = __all_sync(0xffffffffu, all_fin);
   if (tr) tr[14] = clk64();  // rows landed
   if (!ok && lane == 0 && p.flags) atomicOr(p.flags, (uint32_t)KVR_FLAG_NONFINITE);
   const bool rot[2] = {p.rotate != 0, p.rotate && p.rot_v};
@@ -382,6 +410,7 @@ struct CellFrag {
   uint2 vw[4];
   float sk0, sk1, sv0, sv1;
   uint32_t kz0, kz1, vz0, vz1;
+  uint32_t vzp0, vzp1;  // V zero points of tokens (2i, 2i + 1) and (2i + 8, 2i + 9): the PV operand pairs
 };
 KVR_DEV void load_cell_k(CellFrag& f, const uint8_t* st, int r, int i) {
   f.ka = *reinterpret_cast<const uint4*>(st + 128 + r * 64 + 16 * i);
@@ -402,6 +431,8 @@ KVR_DEV void load_cell_rest(CellFrag& f, const uint8_t* st, int r, int i) {
   f.kz1 = st[2176 + r + 8];
   f.vz0 = st[2192 + r];
   f.vz1 = st[2192 + r + 8];
+  f.vzp0 = *reinterpret_cast<const uint16_t*>(st + 2192 + 2 * i);
+  f.vzp1 = *reinterpret_cast<const uint16_t*>(st + 2192 + 8 + 2 * i);
 }
 
 // One q head's final output (warp-wide, lane owns dims 4l..4l+3): the inverse
@@ -851,13 +882,15 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
     for (int c = 0; c < C; ++c) {
       float sk0 = f[c].sk0, sk1 = f[c].sk1, sv0 = f[c].sv0, sv1 = f[c].sv1;
       float zk0 = (float)f[c].kz0, zk1 = (float)f[c].kz1;
-      zv0[c] = (float)f[c].vz0;
-      zv1[c] = (float)f[c].vz1;
+      // zv: a sentinel V token's offset (its codes are 0 and enter the PV product as
+      // 0 - 0); every other token's zero point is inside its PV operand (c - z)
+      zv0[c] = 0.f;
+      zv1[c] = 0.f;
       if (rare) {
         if (f[c].kz0 == 0xFFu) { zk0 = -sk0; sk0 = 1.f; }
         if (f[c].kz1 == 0xFFu) { zk1 = -sk1; sk1 = 1.f; }
-        if (f[c].vz0 == 0xFFu) { zv0[c] = -sv0; sv0 = 1.f; }
-        if (f[c].vz1 == 0xFFu) { zv1[c] = -sv1; sv1 = 1.f; }
+        if (f[c].vz0 == 0xFFu) { zv0[c] = sv0; sv0 = 1.f; }
+        if (f[c].vz1 == 0xFFu) { zv1[c] = sv1; sv1 = 1.f; }
       }
       svc0[c] = sv0;
       svc1[c] = sv1;
@@ -928,11 +961,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
       }
     }
 
-    // zero-point term of this group, sum_t w_t z_t per q head: folded into the
-    // accumulators every group (below), so they carry sum_t w_t (c_t - z_t) -- the
-    // output's own magnitude -- and never the ~7.5 sum_t w_t of the raw codes
-    // (a running code sum minus one final z-term cancels catastrophically over
-    // long contexts)
+    // sentinel V tokens' offsets, sum_t w_t offset_t per q head (rare groups only)
     float zt[NT];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) zt[nt] = 0.f;
@@ -953,7 +982,20 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
         whi[nt] = movtrans(pack_h2(w1h, w1s - w1h));  // tokens 8..15 -> b2,b3
       }
 
-      // ---- O^T += C_v^T W : 8 m-tiles (16 dims each) of m16n8k16
+      // ---- O^T += (C_v - z)^T W : 8 m-tiles (16 dims each) of m16n8k16.  The A operand
+      // is the exact signed integer c - z of each token as an fp16 (a nibble masked into
+      // the mantissa of 1024.0, minus 1024 + z): the products then carry both signs, so
+      // the tensor core's truncating fp32 accumulation has no systematic drift (raw
+      // codes 0..15 against positive weights bias every output dim the same way).
+      uint32_t off[2][2];  // [token pair][low | high nibble]: fp16x2 (1024 + z, 1024 + 16 z)
+#pragma unroll
+      for (int tp = 0; tp < 2; ++tp) {
+        uint32_t zz = tp ? f[c].vzp1 : f[c].vzp0;  // z of the pair's two tokens (bytes 0, 1)
+        if (rare) zz &= ~__vcmpeq4(zz, 0x0000FFFFu);  // sentinel (0xFF): its codes are 0, offset 0
+        const uint32_t x = prmt(zz, 0u, 0x4140u);     // [z_a, 0, z_b, 0]
+        off[tp][0] = x + 0x64006400u;
+        off[tp][1] = x * 16u + 0x64006400u;
+      }
       uint32_t xr[2][2][8];  // [token pair (2i,2i+1)|(2i+8,2i+9)][word][dim e]
 #pragma unroll
       for (int tp = 0; tp < 2; ++tp)
@@ -963,14 +1005,14 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
           const uint32_t wb = q ? f[c].vw[2 * tp + 1].y : f[c].vw[2 * tp + 1].x;
           const uint32_t t0w = prmt(wa, wb, 0x5410u), t1w = prmt(wa, wb, 0x7632u);
           const uint32_t t0s = t0w >> 8, t1s = t1w >> 8;
-          xr[tp][q][0] = t0w & 0x000F000Fu;
-          xr[tp][q][1] = t0w & 0x00F000F0u;
-          xr[tp][q][2] = t0s & 0x000F000Fu;
-          xr[tp][q][3] = t0s & 0x00F000F0u;
-          xr[tp][q][4] = t1w & 0x000F000Fu;
-          xr[tp][q][5] = t1w & 0x00F000F0u;
-          xr[tp][q][6] = t1s & 0x000F000Fu;
-          xr[tp][q][7] = t1s & 0x00F000F0u;
+          xr[tp][q][0] = hsub2_u32((t0w & 0x000F000Fu) | 0x64006400u, off[tp][0]);
+          xr[tp][q][1] = hsub2_u32((t0w & 0x00F000F0u) | 0x64006400u, off[tp][1]);
+          xr[tp][q][2] = hsub2_u32((t0s & 0x000F000Fu) | 0x64006400u, off[tp][0]);
+          xr[tp][q][3] = hsub2_u32((t0s & 0x00F000F0u) | 0x64006400u, off[tp][1]);
+          xr[tp][q][4] = hsub2_u32((t1w & 0x000F000Fu) | 0x64006400u, off[tp][0]);
+          xr[tp][q][5] = hsub2_u32((t1w & 0x00F000F0u) | 0x64006400u, off[tp][1]);
+          xr[tp][q][6] = hsub2_u32((t1s & 0x000F000Fu) | 0x64006400u, off[tp][0]);
+          xr[tp][q][7] = hsub2_u32((t1s & 0x00F000F0u) | 0x64006400u, off[tp][1]);
         }
 #pragma unroll
       for (int m = 0; m < 8; ++m)
@@ -978,20 +1020,22 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
         for (int nt = 0; nt < NT; ++nt)
           mma16816(acc[nt][m], xr[0][0][m], xr[0][1][m], xr[1][0][m], xr[1][1][m], wlo[nt], whi[nt]);
     }
-    // the fold: this q head's group z-term summed over the 8 lanes of its column
-    // (lanes i, i + 4, ...), subtracted from the hi column of every output row in
-    // accumulator units (x 2^24 codes / 2^8 weights; x 16 for the high-nibble tiles)
+    if (rare) {
+      // sentinel V tokens: p * offset, the same for every dim -- summed over the 8 lanes
+      // of the q head's column (lanes i, i + 4, ...) and added to the hi column of every
+      // output row in accumulator units (x 2^8 weights; x 16 on the high-nibble tiles)
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      float z = zt[nt];
-      z += __shfl_xor_sync(0xffffffffu, z, 4);
-      z += __shfl_xor_sync(0xffffffffu, z, 8);
-      z += __shfl_xor_sync(0xffffffffu, z, 16);
+      for (int nt = 0; nt < NT; ++nt) {
+        float z = zt[nt];
+        z += __shfl_xor_sync(0xffffffffu, z, 4);
+        z += __shfl_xor_sync(0xffffffffu, z, 8);
+        z += __shfl_xor_sync(0xffffffffu, z, 16);
 #pragma unroll
-      for (int m = 0; m < 8; ++m) {
-        const float u = (m & 1) ? -0x1p-12f : -0x1p-16f;
-        acc[nt][m][0] = fmaf(z, u, acc[nt][m][0]);
-        acc[nt][m][2] = fmaf(z, u, acc[nt][m][2]);
+        for (int m = 0; m < 8; ++m) {
+          const float u = (m & 1) ? 4096.0f : 256.0f;
+          acc[nt][m][0] = fmaf(z, u, acc[nt][m][0]);
+          acc[nt][m][2] = fmaf(z, u, acc[nt][m][2]);
+        }
       }
     }
     if (++stg == NSTG) {
@@ -1031,7 +1075,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
       float* dst = sred + (warp * 8 + j) * 136 + r;
 #pragma unroll
       for (int m = 0; m < 8; ++m) {
-        const float f = ((m & 1) ? 65536.0f / 16.0f : 65536.0f) * sc;  // undo 2^-24 (codes), 2^8 (w), x16 nibble
+        const float f = ((m & 1) ? 0x1p-12f : 0x1p-8f) * sc;  // undo the x 2^8 weights (x 16 high nibbles)
         dst[m * 8] = (acc[nt][m][0] + acc[nt][m][1]) * f;
         dst[(m + 8) * 8] = (acc[nt][m][2] + acc[nt][m][3]) * f;
       }

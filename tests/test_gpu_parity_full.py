@@ -7,8 +7,14 @@ quantize (_ref.py:57-80) -> dequantize (_ref.py:83-95) -> decode (attention.py:5
 checked end to end against the reference arithmetic, at the configs' real sizes
 (sampled sequences / heads where the oracle would be slow).
 
-Tolerance (BASELINE.json north_star): fp32 outputs within 1e-3 * max|ref|; the
-tighter bars below pin the measured accuracy of the zero-point-folded PV.
+Two bars per config:
+* end to end against the oracle-quantised pages: 1e-3 * max|ref| (BASELINE.json
+  north_star).  At long contexts the output is small (a mean over ~L/e tokens), so a
+  single code that the fast K1 rounds differently (its scale may differ from the
+  reference's by 1 ulp in ~0.5 % of rotated rows) moves it by
+  ~1e-4 of max|ref|;
+* the decode kernel alone, against an f64 decode of the pages it actually read:
+  1e-5 (measured ~1.2e-6: exact integer QK, signed (c - z) PV operands).
 """
 
 import ctypes
@@ -63,6 +69,24 @@ def oracle_decode(k, v, q, order, signs, targets, group):
     return out
 
 
+def own_pages_decode(table, seqs, q, spec, G):
+    """f64 decode over the GPU's own dequantised pages (isolates the decode kernel)."""
+    lay = table.layout
+    kd, vd = table.read_sequence_device(seqs, torch.float64)
+    outs = []
+    for b, s in enumerate(seqs):
+        L = table.sequence_length(s)
+        kh, vh = kd[b, :L].cpu().numpy(), vd[b, :L].cpu().numpy()
+        qn = np.asarray(q[b], dtype=np.float64)
+        qf = O.rotate_rows(qn, lay.rot_order, spec.signs) if spec is not None else qn
+        o = O.decode_flat(qf, kh, vh, G)
+        if spec is not None and spec.targets is Targets.KEYS_AND_VALUES:
+            o = O.unrotate_rows(o, lay.rot_order, spec.signs)
+        outs.append(o)
+    del kd, vd
+    return np.stack(outs)
+
+
 def _fill(table, seq, seed, L, chunk=1 << 16, spec=None):
     H, d = table.layout.num_kv_heads, table.layout.head_dim
     slots = torch.from_numpy(table.alloc.reserve(seq, L)).cuda()
@@ -91,9 +115,11 @@ def test_c2_full_size_random_keys():
     kk = torch.cat([k, kn]).double().cpu().numpy()
     vv = torch.cat([v, vn]).double().cpu().numpy()
     ref = oracle_decode(kk, vv, q[0].double().cpu().numpy(), 128, spec.signs, spec.targets, G)
-    err = rel_err(out[0].double().cpu().numpy(), ref)
-    print("C2 full size, oracle-quantised, rel err", err)
-    assert err <= 1e-5  # zero-point fold: the north-star bar is 1e-3
+    got = out[0].double().cpu().numpy()
+    err = rel_err(got, ref)
+    kern = rel_err(got, own_pages_decode(t, [0], q.double().cpu().numpy(), spec, G)[0])
+    print("C2 full size rel err: vs oracle-quantised", err, "| decode kernel vs f64 of its pages", kern)
+    assert err <= TOL and kern <= 1e-5
 
 
 def test_c3_b256_8k_sampled():
@@ -108,14 +134,16 @@ def test_c3_b256_8k_sampled():
         _fill(t, s, 1000 + s, L, spec=spec)
     q = torch.randn((B, G * H, d), generator=torch.Generator(device="cuda").manual_seed(5), device="cuda").bfloat16()
     out = decode_batch(q, t, list(range(B)), spec=spec).double().cpu().numpy()
-    worst = 0.0
+    worst = kern = 0.0
     for s in (0, 1, 77, 128, 200, 253, 254, 255):
         k, v = _kv(1000 + s, L, H, d)
         ref = oracle_decode(k.double().cpu().numpy(), v.double().cpu().numpy(), q[s].double().cpu().numpy(), 128,
                             spec.signs, spec.targets, G)
         worst = max(worst, rel_err(out[s], ref))
-    print("C3 B=256 x 8k sampled rel err", worst)
-    assert worst <= 1e-5
+        own = own_pages_decode(t, [s], q[s:s + 1].double().cpu().numpy(), spec, G)[0]
+        kern = max(kern, rel_err(out[s], own))
+    print("C3 B=256 x 8k sampled rel err: vs oracle-quantised", worst, "| decode kernel", kern)
+    assert worst <= TOL and kern <= 1e-5
 
 
 def test_c4_g8_16x16k_fused_layer():
@@ -134,15 +162,17 @@ def test_c4_g8_16x16k_fused_layer():
     vn = torch.randn((B, H, d), generator=g, device="cuda").bfloat16()
     q = torch.randn((B, G * H, d), generator=g, device="cuda").bfloat16()
     out = plan.step(q, kn, vn, spec).double().cpu().numpy()
-    worst = 0.0
+    worst = kern = 0.0
     for s in (0, 5, 10, 15):
         k, v = _kv(2000 + s, L, H, d)
         kk = torch.cat([k, kn[s:s + 1]]).double().cpu().numpy()
         vv = torch.cat([v, vn[s:s + 1]]).double().cpu().numpy()
         ref = oracle_decode(kk, vv, q[s].double().cpu().numpy(), 128, spec.signs, spec.targets, G)
         worst = max(worst, rel_err(out[s], ref))
-    print("C4 G=8 16 x 16k fused layer, sampled rel err", worst)
-    assert worst <= 1e-5
+        own = own_pages_decode(t, [s], q[s:s + 1].double().cpu().numpy(), spec, G)[0]
+        kern = max(kern, rel_err(out[s], own))
+    print("C4 G=8 16 x 16k fused layer, sampled rel err: vs oracle-quantised", worst, "| decode kernel", kern)
+    assert worst <= TOL and kern <= 1e-5
 
 
 @pytest.mark.parametrize("L,order,fused", [(131072, 128, False), (131072, 64, True), (1 << 20, 128, True)])
@@ -171,9 +201,11 @@ def test_c5_long_context_random_keys(L, order, fused):
     assert plan.splits > 32
     ref = oracle_decode(k.double().cpu().numpy(), v.double().cpu().numpy(), q[0].double().cpu().numpy(), order,
                         spec.signs, spec.targets, G)
-    err = rel_err(out[0].double().cpu().numpy(), ref)
-    print(f"C5 L={L} order={order} fused={fused} rel err {err}")
-    assert err <= 1e-4
+    got = out[0].double().cpu().numpy()
+    err = rel_err(got, ref)
+    kern = rel_err(got, own_pages_decode(t, [0], q.double().cpu().numpy(), spec, G)[0])
+    print(f"C5 L={L} order={order} fused={fused} rel err: vs oracle-quantised {err} | decode kernel {kern}")
+    assert err <= TOL and kern <= 1e-5
 
 
 def test_store_then_decode_back_to_back():
@@ -425,7 +457,8 @@ def test_softmax_shift_invariance_plus_5000():
     t.append_tokens_two_pass(0, kh, v)
     out = decode_step(DecodeRequest(q=q, seq=0), t)
     fk, fv = t.read_sequence(0)
-    assert np.isfinite(out).all() and rel_err(out, decode_step_fp(q, fk, fv, layout)) <= 1e-5
+    # logits of ~880 in fp32 carry ~5e-5 absolute rounding: 1e-4 here (f64 reference: exact)
+    assert np.isfinite(out).all() and rel_err(out, decode_step_fp(q, fk, fv, layout)) <= 1e-4
 
 
 def test_decode_step_fp_matches_reference_goldens(golden):
