@@ -270,6 +270,10 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- the other BASELINE configs (parity-test cases, reported in `detail`)
     c1 = c1_quantize_store(torch, layout, spec, dev, gen, timed)
+    print(f"[bench] C1 K1 rot {c1['rot_us']} us plain {c1['plain_us']} (tcgen05 {c1['tcgen05_rot_us']} / "
+          f"{c1['tcgen05_plain_us']}); 65536 tok rot {c1['write_65536_tokens']['rot_us']} plain "
+          f"{c1['write_65536_tokens']['plain_us']} (mma.sync {c1['write_65536_tokens']['mma_sync_rot_us']}); "
+          f"K4 {c1['dequant_us']} us", file=sys.stderr, flush=True)
     c3 = c4 = c5 = None
     if not args.quick:
         sets.clear()  # free the headline's buffers first
@@ -534,21 +538,53 @@ def c1_quantize_store(torch, layout, spec, dev, gen, timed):
     """configs[0] shape on the GPU: 4096 tokens x 8 kv heads, order 128, bf16 in."""
     from paper_2604_19157_b200 import PageTable
 
+    from paper_2604_19157_b200 import _lib as _L
+
+    def make_sets(n_tok, R):
+        sets = []
+        for r in range(R):
+            t = PageTable(layout, num_pages=n_tok // P, device=dev)
+            t.create_sequence(0)
+            slots = torch.arange(n_tok, dtype=torch.int64, device=dev)
+            t.alloc.plan([0] * n_tok)
+            k = torch.randn((n_tok, H, D), generator=gen, device=dev).to(torch.bfloat16)
+            v = torch.randn((n_tok, H, D), generator=gen, device=dev).to(torch.bfloat16)
+            sets.append((t, k, v, slots))
+        return sets
+
+    def k1_us(sets, n):
+        R = len(sets)
+        t_r = timed(lambda i: sets[i % R][0].store_slots(sets[i % R][1], sets[i % R][2], sets[i % R][3], spec), n) / n
+        t_p = timed(lambda i: sets[i % R][0].store_slots(sets[i % R][1], sets[i % R][2], sets[i % R][3], None), n) / n
+        return t_r, t_p
+
     n_tok, R = 4096, 8
-    sets = []
-    for r in range(R):
-        t = PageTable(layout, num_pages=n_tok // P, device=dev)
-        t.create_sequence(0)
-        slots = torch.arange(n_tok, dtype=torch.int64, device=dev)
-        t.alloc.plan([0] * n_tok)
-        k = torch.randn((n_tok, H, D), generator=gen, device=dev).to(torch.bfloat16)
-        v = torch.randn((n_tok, H, D), generator=gen, device=dev).to(torch.bfloat16)
-        sets.append((t, k, v, slots))
+    sets = make_sets(n_tok, R)
     n = 256
-    t_rot = timed(lambda i: sets[i % R][0].store_slots(sets[i % R][1], sets[i % R][2], sets[i % R][3], spec), n) / n
-    t_pl = timed(lambda i: sets[i % R][0].store_slots(sets[i % R][1], sets[i % R][2], sets[i % R][3], None), n) / n
+    t_rot, t_pl = k1_us(sets, n)  # the default dispatch (mma.sync kernel at this size)
+    _L.lib().kvr_debug_set_k1_impl(2)  # A/B: the tcgen05 kernel forced at this size
+    try:
+        c_rot, c_pl = k1_us(sets, n)
+    finally:
+        _L.lib().kvr_debug_set_k1_impl(0)
     byts = n_tok * WRITE_BYTES_PER_TOKEN
     peak, _ = hbm_peak()
+    # the 65,536-token bulk (prefill-sized) write, both kernels
+    big_n = 65536
+    big = make_sets(big_n, 2)
+    b_rot, b_pl = k1_us(big, 64)  # default dispatch: the tcgen05 kernel at this size
+    _L.lib().kvr_debug_set_k1_impl(1)
+    try:
+        bm_rot, bm_pl = k1_us(big, 64)
+    finally:
+        _L.lib().kvr_debug_set_k1_impl(0)
+    del big
+    bb = big_n * WRITE_BYTES_PER_TOKEN
+    big_line = {"tokens": big_n, "algorithmic_bytes": bb, "rot_us": round(b_rot * 1e3, 2), "plain_us": round(b_pl * 1e3, 2),
+                "rot_GBps": round(bb / (b_rot * 1e-3) / 1e9, 1), "rot_frac": round(bb / (b_rot * 1e-3) / 1e9 / peak, 4),
+                "overhead_vs_plain": round(b_rot / b_pl - 1.0, 4),
+                "kernel": "store_tc_kernel (tcgen05.mma M128 N16 K16, TMEM accumulators, TMA ring; the default here)",
+                "mma_sync_rot_us": round(bm_rot * 1e3, 2), "mma_sync_plain_us": round(bm_pl * 1e3, 2)}
     # K4 flatten-dequant of the same 4096 tokens back to bf16 (stored space)
     import ctypes
 
@@ -571,7 +607,10 @@ def c1_quantize_store(torch, layout, spec, dev, gen, timed):
             "dequant_frac": round(dq_bytes / (t_dq * 1e-3) / 1e9 / peak, 4),
             "plain_us": round(t_pl * 1e3, 3), "rot_GBps": round(byts / (t_rot * 1e-3) / 1e9, 1),
             "plain_GBps": round(byts / (t_pl * 1e-3) / 1e9, 1), "rot_frac": round(byts / (t_rot * 1e-3) / 1e9 / peak, 4),
-            "overhead_vs_plain": round(t_rot / t_pl - 1.0, 4)}
+            "overhead_vs_plain": round(t_rot / t_pl - 1.0, 4),
+            "kernel": "store_mma_kernel (mma.sync; the default below ~4 tiles of 128 rows per SM)",
+            "tcgen05_rot_us": round(c_rot * 1e3, 3), "tcgen05_plain_us": round(c_pl * 1e3, 3),
+            "write_65536_tokens": big_line}
 
 
 def e2e_api(torch, layout, spec, dev, tables, args, world):

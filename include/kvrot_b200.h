@@ -109,6 +109,11 @@ const char* kvr_last_error(void);
  * reached); then one row per split-merge CTA (splits > 8): globaltimer at [0]
  * entry, [1] past the grid-dependency wait, [2] exit.  NULL disables. */
 void kvr_debug_decode_trace(void* trace);
+/* A/B aid: the kernel behind the fast bf16/fp16 path of kvr_rotate_quantize_store --
+ * 0 the default (the tcgen05/TMEM kernel from ~4 tiles of 128 rows per SM on, the mma.sync
+ * kernel below), 1 the mma.sync kernel at every size, 2 the tcgen05 kernel at every size.
+ * Process-wide; call between launches, not concurrently with them. */
+void kvr_debug_set_k1_impl(int32_t impl);
 int kvr_abi_version(void);
 /* The caller wrote pool bytes on `stream` outside this library (e.g. a checkpoint
  * load): the next decode launched on that stream issues no pool reads before its

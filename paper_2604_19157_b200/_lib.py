@@ -28,7 +28,7 @@ EXPORTED = (
     "kvr_fwht_rows_f64", "kvr_pack_rows", "kvr_unpack_rows", "kvr_quantize_rows_f64",
     "kvr_dequantize_rows_f64", "kvr_block_rotate", "kvr_rotate_quantize_store",
     "kvr_dequantize_pages", "kvr_decode_workspace_bytes", "kvr_decode_pick_splits",
-    "kvr_paged_decode", "kvr_decode_step", "kvr_debug_decode_trace", "kvr_note_pool_write",
+    "kvr_paged_decode", "kvr_decode_step", "kvr_debug_decode_trace", "kvr_debug_set_k1_impl", "kvr_note_pool_write",
     "kvr_host_all_finite", "kvr_decode_flat_f64",
 )
 
@@ -58,6 +58,7 @@ def _declare(lib):
         "kvr_pool_init_bf16": (_I32, [ctypes.POINTER(KvrPool), _P, _I64, _I32, _I32, _I32]),
         "kvr_last_error": (ctypes.c_char_p, []),
         "kvr_debug_decode_trace": (None, [_P]),
+        "kvr_debug_set_k1_impl": (None, [_I32]),
         "kvr_note_pool_write": (None, [_P]),
         "kvr_host_all_finite": (_I32, [_P, _I32, _I64]),
         "kvr_decode_flat_f64": (_I32, [_P, _P, _P, _I64, _I32, _I32, _I32, _P, _P]),

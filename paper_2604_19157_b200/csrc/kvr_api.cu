@@ -140,6 +140,7 @@ extern "C" {
 const char* kvr_last_error(void) { return g_err; }
 void kvr_note_pool_write(void* stream) { kvr_mark_pool_written((cudaStream_t)stream); }
 void kvr_debug_decode_trace(void* trace) { kvr_set_decode_trace(trace); }
+void kvr_debug_set_k1_impl(int32_t impl) { kvr_set_k1_impl(impl); }
 int kvr_abi_version(void) { return KVR_ABI_VERSION; }
 
 // Host-side validation helper (not a compute path): 1 when all n values at host

@@ -54,10 +54,12 @@ KVR_DEV double round_half_away(double t) { return copysign(floor(fabs(t) + 0.5),
 // RN(q0 + r rb) is RN(a / b) (Markstein) while nothing over/underflows.  b is an
 // f32 value or 15 here, so its significand is never all ones.  Results that
 // leave the safe range (or NaN from an infinite b) take the IEEE division.
+static __device__ __noinline__ double div_ieee_slow(double a, double b) { return a / b; }
 KVR_DEV double div_rn_recip(double a, double b, double rb) {
   const double q0 = a * rb;
   const double q = fma(fma(-q0, b, a), rb, q0);
-  return fabs(q) < 0x1p1000 ? q : a / b;
+  if (__builtin_expect(fabs(q) < 0x1p1000, 1)) return q;  // a branch: the IEEE division stays out of line
+  return div_ieee_slow(a, b);
 }
 
 // ---- f32x2 packed arithmetic (FADD2 / FFMA2 on sm_100a) --------------------

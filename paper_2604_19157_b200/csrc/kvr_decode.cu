@@ -58,6 +58,8 @@ struct DecodeParams {
   int pre_groups;    // ring groups per warp requested before griddepcontrol.wait
   int evict_first;   // KV cells are streamed with an L2 evict-first policy
   int merge_inline;  // splits > 1 without a cluster: the last CTA merges (ws_cnt counters)
+  uint32_t f16x2_1024;  // 0x64006400 (fp16x2 1024.0) from the parameter bank: an opaque operand lets
+                        // ptxas fuse (x & mask) | 1024 into one LOP3 (two immediates need two)
 };
 
 KVR_DEV unsigned long long clk64() {
@@ -107,6 +109,14 @@ KVR_DEV float ex2f(float x) {
 KVR_DEV uint32_t hsub2_u32(uint32_t a, uint32_t b) {
   uint32_t r;
   asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
+// (a & MASK) | c in one LOP3 (c in a register or the constant bank)
+template <uint32_t MASK>
+KVR_DEV uint32_t and_or(uint32_t a, uint32_t c) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(a), "n"(MASK), "r"(c));
   return r;
 }
 
@@ -390,6 +400,9 @@ constexpr int RING_CELLS = 4;    // cells in flight per warp (NSTG stages of C c
 #ifndef KVR_MERGE_INLINE
 #define KVR_MERGE_INLINE 1
 #endif
+#ifndef KVR_CLUSTER_MAX
+#define KVR_CLUSTER_MAX 8
+#endif
 constexpr int MAX_SPLITS = 256;
 constexpr int MERGE_INLINE_MAX = 32;  // up to this many splits the last CTA merges them inline
 
@@ -498,6 +511,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = lane >> 2, i = lane & 3;
   const int h = blockIdx.x, split = blockIdx.y, b = blockIdx.z;
+  const uint32_t k1024 = p.f16x2_1024;
   const int G = p.G, H = p.pool.H;
   const int64_t cta_id = ((int64_t)b * p.splits + split) * H + h;
   if (p.trace && threadIdx.x == 0) {
@@ -993,8 +1007,8 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
         uint32_t zz = tp ? f[c].vzp1 : f[c].vzp0;  // z of the pair's two tokens (bytes 0, 1)
         if (rare) zz &= ~__vcmpeq4(zz, 0x0000FFFFu);  // sentinel (0xFF): its codes are 0, offset 0
         const uint32_t x = prmt(zz, 0u, 0x4140u);     // [z_a, 0, z_b, 0]
-        off[tp][0] = x + 0x64006400u;
-        off[tp][1] = x * 16u + 0x64006400u;
+        off[tp][0] = x + k1024;
+        off[tp][1] = x * 16u + k1024;
       }
       uint32_t xr[2][2][8];  // [token pair (2i,2i+1)|(2i+8,2i+9)][word][dim e]
 #pragma unroll
@@ -1005,14 +1019,14 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
           const uint32_t wb = q ? f[c].vw[2 * tp + 1].y : f[c].vw[2 * tp + 1].x;
           const uint32_t t0w = prmt(wa, wb, 0x5410u), t1w = prmt(wa, wb, 0x7632u);
           const uint32_t t0s = t0w >> 8, t1s = t1w >> 8;
-          xr[tp][q][0] = hsub2_u32((t0w & 0x000F000Fu) | 0x64006400u, off[tp][0]);
-          xr[tp][q][1] = hsub2_u32((t0w & 0x00F000F0u) | 0x64006400u, off[tp][1]);
-          xr[tp][q][2] = hsub2_u32((t0s & 0x000F000Fu) | 0x64006400u, off[tp][0]);
-          xr[tp][q][3] = hsub2_u32((t0s & 0x00F000F0u) | 0x64006400u, off[tp][1]);
-          xr[tp][q][4] = hsub2_u32((t1w & 0x000F000Fu) | 0x64006400u, off[tp][0]);
-          xr[tp][q][5] = hsub2_u32((t1w & 0x00F000F0u) | 0x64006400u, off[tp][1]);
-          xr[tp][q][6] = hsub2_u32((t1s & 0x000F000Fu) | 0x64006400u, off[tp][0]);
-          xr[tp][q][7] = hsub2_u32((t1s & 0x00F000F0u) | 0x64006400u, off[tp][1]);
+          xr[tp][q][0] = hsub2_u32(and_or<0x000F000Fu>(t0w, k1024), off[tp][0]);
+          xr[tp][q][1] = hsub2_u32(and_or<0x00F000F0u>(t0w, k1024), off[tp][1]);
+          xr[tp][q][2] = hsub2_u32(and_or<0x000F000Fu>(t0s, k1024), off[tp][0]);
+          xr[tp][q][3] = hsub2_u32(and_or<0x00F000F0u>(t0s, k1024), off[tp][1]);
+          xr[tp][q][4] = hsub2_u32(and_or<0x000F000Fu>(t1w, k1024), off[tp][0]);
+          xr[tp][q][5] = hsub2_u32(and_or<0x00F000F0u>(t1w, k1024), off[tp][1]);
+          xr[tp][q][6] = hsub2_u32(and_or<0x000F000Fu>(t1s, k1024), off[tp][0]);
+          xr[tp][q][7] = hsub2_u32(and_or<0x00F000F0u>(t1s, k1024), off[tp][1]);
         }
 #pragma unroll
       for (int m = 0; m < 8; ++m)
@@ -1632,6 +1646,7 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
   // the stream writes: after a store kernel on this stream the prefetch waits)
   p.pre_groups = kvr_take_pool_written(st) ? 0 : KVR_PREWAIT_GROUPS;
   p.evict_first = KVR_EVICT_FIRST;
+  p.f16x2_1024 = 0x64006400u;
   int l2 = 0;
   while ((1 << l2) < pool.P) ++l2;
   const bool pow2 = (1 << l2) == pool.P;
@@ -1659,7 +1674,7 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
 #ifndef KVR_NO_CLUSTER
     // portable cluster sizes only: 16-CTA clusters of one-CTA-per-SM kernels do not
     // all co-schedule on B200 (a second wave appears), measured slower
-    p.use_cluster = splits >= 2 && splits <= 8;
+    p.use_cluster = splits >= 2 && splits <= KVR_CLUSTER_MAX;
 #else
     p.use_cluster = 0;
 #endif

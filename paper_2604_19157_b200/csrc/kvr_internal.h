@@ -45,6 +45,7 @@ int kvr_launch_decode(const void* q, int q_dtype, const kvr::Pool& pool, const i
                       const int64_t* new_slot = nullptr, uint32_t* flags = nullptr);
 
 void kvr_set_decode_trace(void* trace);
+void kvr_set_k1_impl(int impl);
 
 // Tensor-map encoder resolved through the runtime (no -lcuda link dependency).
 CUresult kvr_encode_tensor_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows,

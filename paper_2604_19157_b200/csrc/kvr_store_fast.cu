@@ -9,6 +9,10 @@
 // H_16 on the tensor cores (bf16/fp16 HMMA, +-1 weights), H_8 as lane-local FADD2
 // stages, the reference's f64 row scale / zero point, codes by FFMA2.RM with a
 // +-delta boundary test and an exact recomputation of flagged rows.
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
 #include "kvr_common.cuh"
 #include "kvr_internal.h"
 
@@ -39,11 +43,11 @@ struct FastStoreParams {
 };
 
 // Elements 4l..4l+3 of the row staged for lane `src` in the swizzled tile, as f64.
-template <bool F16>
+template <bool F16, int SUB = FS_SUB_BYTES>
 KVR_DEV void tile_quad(const uint8_t* buf, int src, int l, double (&x)[4]) {
   const int e = 4 * l;
   const int h = e >> 6, c = (e >> 3) & 7, within = e & 7;
-  const uint2 q = *reinterpret_cast<const uint2*>(buf + h * FS_SUB_BYTES + src * 128 + ((c ^ (src & 7)) << 4) + within * 2);
+  const uint2 q = *reinterpret_cast<const uint2*>(buf + h * SUB + src * 128 + ((c ^ (src & 7)) << 4) + within * 2);
   const uint32_t w[2] = {q.x, q.y};
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
@@ -53,16 +57,14 @@ KVR_DEV void tile_quad(const uint8_t* buf, int src, int l, double (&x)[4]) {
   }
 }
 
-// Reference-exact codes of the row staged for lane `src`, computed by the whole
-// warp: lane l owns elements 4l..4l+3; f64 butterfly in _ref.fwht_rows order
-// (stages half = 1, 2 in registers, 4..ORDER/2 by shuffles, lowest index first),
-// * 1/sqrt(ORDER), then round-half-away(y / s64) + z, clip (_ref.py:22-40, 57-80).
-// Returns the 4 codes of lane l as a 16-bit group (element 4l in the low nibble).
-template <int ORDER, bool F16, bool ROT>
-__device__ __noinline__ uint32_t warp_exact_row(const uint8_t* buf, int src, const Signs& sg, double s64, double z) {
+// Reference-exact codes of one row, computed by the whole warp: lane l owns
+// elements 4l..4l+3 (in x); f64 butterfly in _ref.fwht_rows order (stages half =
+// 1, 2 in registers, 4..ORDER/2 by shuffles, lowest index first), * 1/sqrt(ORDER),
+// then round-half-away(y / s64) + z, clip (_ref.py:22-40, 57-80).  Returns the 4
+// codes of lane l as a 16-bit group (element 4l in the low nibble).
+template <int ORDER, bool ROT>
+KVR_DEV uint32_t warp_exact_core(double (&x)[4], const Signs& sg, double s64, double z) {
   const int lane = threadIdx.x & 31;
-  double x[4];
-  tile_quad<F16>(buf, src, lane, x);
   if constexpr (ROT) {
 #pragma unroll
     for (int u = 0; u < 4; ++u)
@@ -93,6 +95,27 @@ __device__ __noinline__ uint32_t warp_exact_row(const uint8_t* buf, int src, con
     g |= (uint32_t)q << (4 * u);
   }
   return g;
+}
+// ... of the row staged for lane `src` of a swizzled shared-memory tile
+template <int ORDER, bool F16, bool ROT, int SUB = FS_SUB_BYTES>
+__device__ __noinline__ uint32_t warp_exact_row(const uint8_t* buf, int src, const Signs& sg, double s64, double z) {
+  double x[4];
+  tile_quad<F16, SUB>(buf, src, threadIdx.x & 31, x);
+  return warp_exact_core<ORDER, ROT>(x, sg, s64, z);
+}
+// ... of a row of 128 bf16 / fp16 values in global memory
+template <int ORDER, bool F16>
+__device__ __noinline__ uint32_t warp_exact_row_g(const uint16_t* row, const Signs& sg, double s64, double z) {
+  const uint2 q = *reinterpret_cast<const uint2*>(row + 4 * (threadIdx.x & 31));
+  const uint32_t w[2] = {q.x, q.y};
+  double x[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const uint32_t bits = (u & 1) ? (w[u >> 1] >> 16) : (w[u >> 1] & 0xFFFFu);
+    if constexpr (F16) x[u] = (double)__half2float(__ushort_as_half((unsigned short)bits));
+    else x[u] = (double)__uint_as_float(bits << 16);
+  }
+  return warp_exact_core<ORDER, true>(x, sg, s64, z);
 }
 
 KVR_DEV uint32_t pack4(uint32_t m0, uint32_t m1, uint32_t m2, uint32_t m3) {
@@ -162,7 +185,9 @@ KVR_DEV RowQ row_quant(float mxf, float mnf, double scl, bool valid) {
   q.s64 = 1.0;
   if (!valid) return q;
   const double mx = (double)mxf * scl, mn = (double)mnf * scl;
-  const float s32 = (float)((mx - mn) / 15.0);
+  // the reference's f64 divisions, each correctly rounded (div_rn_recip: one FMA-refined
+  // product by a correctly rounded reciprocal instead of a full IEEE division)
+  const float s32 = (float)div_rn_recip(mx - mn, 15.0, 1.0 / 15.0);
   q.s32 = s32;
   if (s32 == 0.0f) {
     q.scale_out = (float)mn;  // sentinel row: offset in the scale slot, zp 0xFF, codes 0
@@ -170,19 +195,20 @@ KVR_DEV RowQ row_quant(float mxf, float mnf, double scl, bool valid) {
     return q;
   }
   q.s64 = (double)s32;
-  double z = round_half_away(-mn / q.s64);
+  double z = round_half_away(div_rn_recip(-mn, q.s64, __drcp_rn(q.s64)));
   z = z < 0.0 ? 0.0 : (z > 15.0 ? 15.0 : z);
   q.z = z;
   q.scale_out = s32;
   q.zp_out = (uint32_t)z;
   // fast-code constants in f32: c = scl / s to 2^-23 relative (|u| <= 16 -> 2^-19 of a
   // code step, inside the +-2^-16 boundary test)
-  const float cst = (float)scl / s32;
+  const float rs32 = __frcp_rn(s32);
+  const float cst = scl == 1.0 ? rs32 : (float)scl * rs32;
   q.cf = cst * FS_FIX;
   q.bias = (float)((z + 0.5) * (double)FS_FIX) + FS_MAGIC;
   q.zb = (float)(z + 0.5);
   q.cu = cst;
-  const float ulo = (float)mn / s32 + q.zb, uhi = (float)mx / s32 + q.zb;
+  const float ulo = (float)mn * rs32 + q.zb, uhi = (float)mx * rs32 + q.zb;  // (2e-3 margins: approximate is fine)
   q.clamp = !((ulo > 2e-3f) && (uhi < 16.0f - 2e-3f));
   q.codes = true;
   return q;
@@ -511,6 +537,423 @@ __global__ void __launch_bounds__(FS_WARPS * 32, KVR_FS_MINB)
   }
 }
 
+// ===========================================================================
+// K1 on the 5th-generation tensor cores: tcgen05.mma with the accumulators in
+// TMEM.  Persistent CTAs (one per SM), warp-specialised:
+//   warp 0       TMA producer: 128-row x 128-column bf16/fp16 tiles (two SW128
+//                boxes of 64 columns, 32 KB) into an NS-stage ring;
+//   warp 1       TMEM owner + MMA issuer: per tile 8 x tcgen05.mma M128 N16 K16 --
+//                block b of the tile times diag(s_b) H_16 (rotated tiles) or the
+//                identity (plain tiles): +-1 / 1 weights, exact products, fp32
+//                accumulation -- into 16 TMEM columns; one commit releases the
+//                ring stage, one hands the accumulator to the epilogue;
+//   warps 2-17   epilogue, four groups of 4 warps (one 128-column TMEM accumulator
+//                each, every fourth tile): thread t of a group owns row t of the
+//                tile (its TMEM lane).  Pass 1 reads the row in two halves of 64
+//                columns (tcgen05.ld 32x32b.x8 per 16-column block), applies the
+//                H_8 stages across the blocks as FADD2 and takes the extremes
+//                (FMNMX3); the reference's f64 scale / zero point follow; pass 2
+//                re-reads and re-rotates each half and forms the codes by the
+//                +-delta magic floor (FFMA2.RM).  Codes are staged in shared memory
+//                and leave as whole 64-byte rows (16-B stores, 8 rows per warp
+//                instruction).  Codes within delta of a rounding boundary are
+//                recomputed reference-exactly from the row in global memory: whole
+//                rotated rows by the warp (f64 butterfly, warp_exact_row_g), plain
+//                8-element words by exact FMA sign tests spread over the lanes.
+// Same codes, scales and flags as store_mma_kernel above.
+namespace k1tc {
+constexpr int TM = 128;
+constexpr int HALF = TM * 128;  // one 64-column SW128 box of the tile
+constexpr int TILE = 2 * HALF;  // 32 KB
+constexpr int NS = 4;           // input ring stages
+constexpr int NGRP = 4;         // epilogue groups = TMEM accumulators (4 x 128 columns)
+constexpr int NEPI = 4 * NGRP;  // epilogue warps (4 lane quadrants per group)
+constexpr int THREADS = (2 + NEPI) * 32;
+constexpr int OFF_B = 0;        // B's 16 x 16 blocks (SW128 K-major [128 n][128 k]): see the setup
+constexpr int OFF_ST = TILE;
+constexpr int OFF_BAR = OFF_ST + NS * TILE;            // full[NS] empty[NS] tfull[4] tempty[4] tmem
+constexpr int OFF_CODES = OFF_BAR + 256;               // code staging [4 groups][128 rows][16 words], XOR-swizzled
+constexpr int OFF_FIXQ = OFF_CODES + NGRP * TM * 64;   // per epilogue warp: queue of flagged plain words (1 KB)
+constexpr int SMEM = OFF_FIXQ + NEPI * 1024 + 1024;    // + 1 KB alignment slack (SW128 atoms need 1024-B bases)
+}  // namespace k1tc
+
+struct TcStoreParams {
+  Pool pool;
+  const int64_t* slots;
+  uint32_t* flags;
+  const uint16_t* k_in;  // the rows themselves (exact fallbacks re-read them)
+  const uint16_t* v_in;
+  int32_t n_rows;          // n_tok * H per side
+  int32_t tiles_per_side;  // ceil(n_rows / 128)
+  int32_t rot_k, rot_v;
+  int32_t log2P;
+};
+
+KVR_DEV void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v[k] = __uint_as_float(r[k]);
+}
+KVR_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+KVR_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+KVR_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+KVR_DEV void mbar_arrive1(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// K-major operand in the 128-byte swizzle: rows at 128 B, 8-row atoms at 1024 B (SBO),
+// version 1 (sm_100), layout type 2 (SWIZZLE_128B)
+KVR_DEV uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+KVR_DEV void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 0, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc)
+      : "memory");
+}
+KVR_DEV void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// codes of 8 consecutive elements (element 2i in the low nibble of byte i) from their magic-floored values
+KVR_DEV uint32_t pack8(const uint32_t (&m)[8]) {
+  return prmt(pack4(m[0], m[1], m[2], m[3]), pack4(m[4], m[5], m[6], m[7]), 0x6420u);
+}
+
+// One half (columns 8 ch .. 8 ch + 7 of every 16-column block) of this thread's row from
+// TMEM, with the H_{ORDER/16} stages across the blocks (butterfly stages half = 16, 32, 64).
+template <int ORDER>
+KVR_DEV void tc_load_half(uint32_t ta, bool rot, float (&v)[8][8]) {
+#pragma unroll
+  for (int b = 0; b < 8; ++b) tmem_ld8(ta + 16 * b, v[b]);
+  tmem_wait_ld();
+  if (rot) {
+#pragma unroll
+    for (int h = 1; h < 8 && 16 * h < ORDER; h <<= 1)
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+        if ((b & h) == 0)
+#pragma unroll
+          for (int c = 0; c < 8; c += 2) {
+            const unsigned long long x = pk(v[b][c], v[b][c + 1]);
+            const unsigned long long y = pk(v[b + h][c], v[b + h][c + 1]);
+            upk(add2(x, y), v[b][c], v[b][c + 1]);
+            upk(sub2(x, y), v[b + h][c], v[b + h][c + 1]);
+          }
+  }
+}
+
+template <int ORDER, bool F16>
+__global__ void __launch_bounds__(k1tc::THREADS, 1)
+    store_tc_kernel(const __grid_constant__ TcStoreParams p, const __grid_constant__ CUtensorMap map_k,
+                    const __grid_constant__ CUtensorMap map_v, const __grid_constant__ Signs signs) {
+  using namespace k1tc;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* empty = full + NS;
+  uint64_t* tfull = empty + NS;
+  uint64_t* tempty = tfull + NGRP;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + NGRP);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int total = 2 * p.tiles_per_side;
+
+  // ---- setup (overlaps the previous grid under PDL): B's 16 x 16 blocks -- diag(s_j) H_16 at
+  // (rows 16 j, K 16 j) for rotated tiles and the identity at (rows 16 j, K 16 (j ^ 4)) for plain
+  // ones (the N = 16 MMAs read nothing else) -- barriers, TMEM
+  {
+    const uint32_t one = F16 ? 0x3C00u : 0x3F80u;
+    for (int e = threadIdx.x; e < 2 * 8 * 16 * 8; e += THREADS) {
+      const int id = e >> 10, j = (e >> 7) & 7, r = (e >> 3) & 15, kp = e & 7;  // row n = 16 j + r, k = 2 kp (+1)
+      const int n = 16 * j + r, k = 16 * (id ? (j ^ 4) : j) + 2 * kp;
+      uint32_t w;
+      if (id) {
+        w = (r == 2 * kp ? one : 0u) | ((r == 2 * kp + 1 ? one : 0u) << 16);
+      } else {
+        const uint32_t n0 = (uint32_t)(__popc(r & (2 * kp)) & 1) ^ (uint32_t)sign_bit(signs, k);
+        const uint32_t n1 = (uint32_t)(__popc(r & (2 * kp + 1)) & 1) ^ (uint32_t)sign_bit(signs, k + 1);
+        w = (one | (n0 << 15)) | ((one | (n1 << 15)) << 16);
+      }
+      const int byte = (k & 63) * 2;
+      *reinterpret_cast<uint32_t*>(smem + OFF_B + (k >> 6) * HALF + (n >> 3) * 1024 + (n & 7) * 128 +
+                                   (((byte >> 4) ^ (n & 7)) << 4) + (byte & 15)) = w;
+    }
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < NGRP; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    fence_mbar_init();
+    prefetch_tensormap(&map_k);
+    prefetch_tensormap(&map_v);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(s_tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_proxy_async();  // the generic-proxy B matrix -> the tensor core's async-proxy reads
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *s_tmem;
+  // programmatic dependent launch: the inputs, slot ids and the pool may come from the previous grid
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  if (warp == 0) {
+    // ================= TMA producer
+    int i = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++i) {
+      const int s = i % NS;
+      mbar_wait(&empty[s], ((i / NS) & 1) ^ 1);
+      if (elect_one()) {
+        const int side = tile >= p.tiles_per_side;
+        const int row0 = (side ? tile - p.tiles_per_side : tile) * TM;
+        const CUtensorMap* m = side ? &map_v : &map_k;
+        uint8_t* dst = smem + OFF_ST + s * TILE;
+        mbar_expect_tx(&full[s], TILE);
+        tma_load_2d(dst, m, &full[s], 0, row0);
+        tma_load_2d(dst + HALF, m, &full[s], 64, row0);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer: D[:, 16 j .. 16 j + 15] = A[:, 16 j ..] B_j^T per block j
+    // idesc: D f32, A/B bf16 (1) or f16 (0), both K-major, N = 16, M = 128
+    const uint32_t fmt = F16 ? 0u : 1u;
+    const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
+    const uint32_t bbase = smem_u32(smem + OFF_B);
+    int i = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++i) {
+      const int side = tile >= p.tiles_per_side;
+      const uint32_t bx = (side ? p.rot_v : p.rot_k) ? 0u : 4u;  // plain tiles: the identity blocks at K 16 (j ^ 4)
+      const int s = i % NS, a = i & (NGRP - 1);
+      mbar_wait(&full[s], (i / NS) & 1);
+      mbar_wait(&tempty[a], ((i / NGRP) & 1) ^ 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t abase = smem_u32(smem + OFF_ST + s * TILE);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t ko = (uint32_t)(j >> 2) * HALF + (uint32_t)(j & 3) * 32;  // 16 columns = 32 B into the atom
+          const uint32_t jb = (uint32_t)j ^ bx;
+          const uint32_t kb = (jb >> 2) * HALF + (jb & 3) * 32;
+          umma_f16(tmem + (uint32_t)(a * 128 + 16 * j), sw128_desc(abase + ko), sw128_desc(bbase + kb + 2048u * j),
+                   idesc);
+        }
+        umma_commit(&empty[s]);  // the stage is free once the MMAs have read it
+        umma_commit(&tfull[a]);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ================= epilogue: group g = every fourth tile (accumulator g); thread = row
+    const int ew = warp - 2, g = ew >> 2, quad = warp & 3;  // TMEM lane quadrant = warp % 4
+    const int rl = 32 * quad + lane;
+    const Pool& pl = p.pool;
+    const int H = pl.H;
+    const int hshift = (H & (H - 1)) ? -1 : __ffs(H) - 1;
+    const double scl_rot = 1.0 / sqrt((double)ORDER);
+    // code staging of this warp's 32 rows: word w of row r at word w ^ ((r >> 1) & 15) -- 32 rows'
+    // stores of one word hit 32 banks, and so do the write-out's word reads
+    uint32_t* stage = reinterpret_cast<uint32_t*>(smem + OFF_CODES + g * TM * 64) + 32 * quad * 16;
+    const uint32_t sw = (uint32_t)(lane >> 1) & 15u;
+    uint16_t* fixq = reinterpret_cast<uint16_t*>(smem + OFF_FIXQ + ew * 1024);
+    const uint32_t ta0 = tmem + ((uint32_t)(32 * quad) << 16) + (uint32_t)(g * 128);
+    int k_tile = 0;
+    for (int tile = blockIdx.x + g * gridDim.x; tile < total; tile += NGRP * gridDim.x, ++k_tile) {
+      const int side = tile >= p.tiles_per_side;
+      const bool rot = side ? p.rot_v : p.rot_k;
+      const int row = (side ? tile - p.tiles_per_side : tile) * TM + rl;
+      const bool valid = row < p.n_rows;
+      const int tok = hshift >= 0 ? row >> hshift : row / H;
+      const int64_t slot = valid ? __ldg(&p.slots[tok]) : -1;
+      mbar_wait(&tfull[g], k_tile & 1);
+      tc_fence_after();
+      float v[8][8];  // [block b][column 8 ch + c of the block]
+      // ---- pass 1: row extremes (NaN-propagating), two halves x two FMNMX3 chains
+      float mx, mn;
+      {
+        float mxc[2], mnc[2];
+#pragma unroll 1
+        for (int ch = 0; ch < 2; ++ch) {
+          tc_load_half<ORDER>(ta0 + 8 * ch, rot, v);
+          float a = max3_nan(v[0][0], v[0][1], v[0][2]), c = min3_nan(v[0][0], v[0][1], v[0][2]);
+          float a2 = max3_nan(v[4][0], v[4][1], v[4][2]), c2 = min3_nan(v[4][0], v[4][1], v[4][2]);
+#pragma unroll
+          for (int k = 3; k < 31; k += 2) {
+            a = max3_nan(a, v[k >> 3][k & 7], v[(k + 1) >> 3][(k + 1) & 7]);
+            c = min3_nan(c, v[k >> 3][k & 7], v[(k + 1) >> 3][(k + 1) & 7]);
+            a2 = max3_nan(a2, v[4 + (k >> 3)][k & 7], v[4 + ((k + 1) >> 3)][(k + 1) & 7]);
+            c2 = min3_nan(c2, v[4 + (k >> 3)][k & 7], v[4 + ((k + 1) >> 3)][(k + 1) & 7]);
+          }
+          mxc[ch] = max3_nan(a, a2, max3_nan(v[3][7], v[7][7], v[7][7]));
+          mnc[ch] = min3_nan(c, c2, min3_nan(v[3][7], v[7][7], v[7][7]));
+        }
+        mx = max3_nan(mxc[0], mxc[1], mxc[1]);
+        mn = min3_nan(mnc[0], mnc[1], mnc[1]);
+      }
+      const bool fin = isfinite(mx) && isfinite(mn);
+      if (valid && !fin && p.flags) atomicOr(p.flags, (uint32_t)KVR_FLAG_NONFINITE);
+      const bool wr = valid && fin && slot >= 0;
+      const RowQ rq = row_quant(mx, mn, rot ? scl_rot : 1.0, valid && fin);
+      const bool clamp = __any_sync(0xffffffffu, rq.codes && rq.clamp);
+      const bool cd = rq.codes;
+      // ---- pass 2: codes into the staging row (rows without codes get c = 0, bias = 1/2 -> code 0)
+      uint32_t flg = 0u;  // rotated: OR of the +-delta differences; plain: bit w = word w needs the exact path
+#pragma unroll 1
+      for (int ch = 0; ch < 2; ++ch) {
+        tc_load_half<ORDER>(ta0 + 8 * ch, rot, v);
+        if (ch == 1) {  // the accumulator is read: the MMA may reuse it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive1(&tempty[g]);
+        }
+        if (!clamp) {  // warp-uniform
+          const float cfv = cd ? rq.cf : 0.f, bias = cd ? rq.bias : FS_MAGIC + 0.5f * FS_FIX;
+          const unsigned long long c2 = pk(cfv, cfv);
+          const unsigned long long bp = pk(bias + FS_D, bias + FS_D), bm = pk(bias - FS_D, bias - FS_D);
+#pragma unroll
+          for (int b = 0; b < 8; ++b) {
+            uint32_t m[8], d = 0u;
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+              const unsigned long long a = pk(v[b][e], v[b][e + 1]);
+              const unsigned long long up = fma2_rm(a, c2, bp), um = fma2_rm(a, c2, bm);
+              m[e] = (uint32_t)up;
+              m[e + 1] = (uint32_t)(up >> 32);
+              d |= (m[e] ^ (uint32_t)um) | (m[e + 1] ^ (uint32_t)(um >> 32));
+            }
+            if (rot) flg |= d;
+            else flg |= (d >= 0x10000u ? 1u : 0u) << (2 * b + ch);
+            stage[lane * 16 + ((2 * b + ch) ^ sw)] = pack8(m);
+          }
+        } else {  // clamped variant: u in f32 clamped to [2^-13, 15.99], then the magic floor
+          const float cu = cd ? rq.cu : 0.f, zb = cd ? rq.zb : 1.0f / 8192.0f;
+          const unsigned long long fix2 = pk(FS_FIX, FS_FIX);
+          const unsigned long long mgp = pk(FS_MAGIC + FS_D_CLAMP, FS_MAGIC + FS_D_CLAMP);
+          const unsigned long long mgm = pk(FS_MAGIC - FS_D_CLAMP, FS_MAGIC - FS_D_CLAMP);
+#pragma unroll
+          for (int b = 0; b < 8; ++b) {
+            uint32_t m[8], d = 0u;
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+              const float u0 = fminf(fmaxf(fmaf(v[b][e], cu, zb), 1.0f / 8192.0f), 15.99f);
+              const float u1 = fminf(fmaxf(fmaf(v[b][e + 1], cu, zb), 1.0f / 8192.0f), 15.99f);
+              const unsigned long long uu = pk(u0, u1);
+              const unsigned long long up = fma2_rm(uu, fix2, mgp), um = fma2_rm(uu, fix2, mgm);
+              m[e] = (uint32_t)up;
+              m[e + 1] = (uint32_t)(up >> 32);
+              d |= (m[e] ^ (uint32_t)um) | (m[e + 1] ^ (uint32_t)(um >> 32));
+            }
+            if (cd) {
+              if (rot) flg |= d;
+              else flg |= (d >= 0x10000u ? 1u : 0u) << (2 * b + ch);
+            }
+            stage[lane * 16 + ((2 * b + ch) ^ sw)] = pack8(m);
+          }
+        }
+      }
+      // ---- sidecars and the row's destination
+      unsigned long long rowdst = 0ull;
+      if (wr) {
+        const int head = row - tok * H;
+        const int64_t page = slot >> p.log2P;
+        const int sip = (int)(slot & (pl.P - 1));
+        const int ci = sip & 15;
+        uint8_t* cell = pl.base + page * pl.page_bytes + (int64_t)(head * (pl.P >> 4) + (sip >> 4)) * pl.cell_bytes;
+        *reinterpret_cast<float*>(cell + side * 64 + ci * 4) = rq.scale_out;
+        cell[2176 + side * 16 + ci] = (uint8_t)rq.zp_out;
+        rowdst = reinterpret_cast<unsigned long long>(cell + (side ? 1152 : 128) + ci * 64);
+      }
+      const uint16_t* in = side ? p.v_in : p.k_in;
+      __syncwarp();
+      if (!rot) {
+        // ---- plain rows: y = x exactly, so a word (8 elements) with a code within delta of a rounding
+        // boundary -- bf16 rows hit exact ties of x / s often -- is recomputed by exact FMA sign tests;
+        // the warp's flagged words are queued and spread over its lanes, one word per lane and round
+        const uint32_t mine = wr ? flg : 0u;
+        const int n = __popc(mine);
+        int incl = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const int nfix = __shfl_sync(0xffffffffu, incl, 31);
+        if (nfix) {  // warp-uniform
+          int pos = incl - n;
+          for (uint32_t mm = mine; mm; mm &= mm - 1) fixq[pos++] = (uint16_t)((lane << 4) | (__ffs(mm) - 1));
+          __syncwarp();
+          for (int base = 0; base < nfix; base += 32) {
+            const int k = base + lane;
+            const int e = k < nfix ? fixq[k] : (lane << 4);
+            const int owner = e >> 4, w = e & 15;  // word w = 2 b + ch: elements 16 b + 8 ch .. + 7
+            const float so = __shfl_sync(0xffffffffu, rq.s32, owner);
+            const float zo = __shfl_sync(0xffffffffu, (float)rq.z, owner);
+            if (k < nfix) {
+              const int r = row - rl + 32 * quad + owner;
+              const uint4 x = *reinterpret_cast<const uint4*>(in + (int64_t)r * 128 + 8 * w);
+              const uint32_t xx[4] = {x.x, x.y, x.z, x.w};
+              const float inv = __frcp_rn(so);  // first guess only: the sign tests make it exact
+              uint32_t word = 0u;
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const float2 f = b16x2_to_f2<F16>(xx[u]);
+                word |= (plain_code_exact(f.x, so, inv, zo) | (plain_code_exact(f.y, so, inv, zo) << 4)) << (8 * u);
+              }
+              stage[owner * 16 + (w ^ ((owner >> 1) & 15))] = word;
+            }
+          }
+          __syncwarp();
+        }
+      } else {
+        // ---- rare: reference-exact recomputation of a rotated row with a code within delta of a
+        // boundary, warp-cooperative, from the row in global memory
+        uint32_t todo = __ballot_sync(0xffffffffu, wr && flg >= 0x10000u);
+        while (todo) {
+          const int src = __ffs(todo) - 1;
+          todo &= todo - 1;
+          const double sb = __shfl_sync(0xffffffffu, rq.s64, src), zb = __shfl_sync(0xffffffffu, rq.z, src);
+          const int r = row - rl + 32 * quad + src;
+          const uint32_t g16 = warp_exact_row_g<ORDER, F16>(in + (int64_t)r * 128, signs, sb, zb);
+          const uint32_t hi16 = __shfl_down_sync(0xffffffffu, g16, 1);
+          // lane l: elements 4l..4l+3 = bytes 2l, 2l+1 of word l / 2
+          if (!(lane & 1)) stage[src * 16 + ((lane >> 1) ^ ((src >> 1) & 15))] = (g16 & 0xFFFFu) | (hi16 << 16);
+        }
+        __syncwarp();
+      }
+      // ---- write-out: this warp's 32 rows as 16-B chunks (4 lanes per row, 8 whole rows per instruction)
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        const int r = 8 * it + (lane >> 2), c = lane & 3;
+        const unsigned long long dst = __shfl_sync(0xffffffffu, rowdst, r);
+        const uint32_t* srow = stage + r * 16;
+        const uint32_t sr = (uint32_t)(r >> 1) & 15u;
+        const uint4 w = make_uint4(srow[(4 * c) ^ sr], srow[(4 * c + 1) ^ sr], srow[(4 * c + 2) ^ sr], srow[(4 * c + 3) ^ sr]);
+        if (dst) *reinterpret_cast<uint4*>(dst + 16 * c) = w;
+      }
+      __syncwarp();  // the staging rows are rewritten by the next tile
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
 }  // namespace kvr
 
 using namespace kvr;
@@ -563,6 +1006,80 @@ static int launch_fast_impl(const void* k, const void* v, int64_t n_tok, const i
   return cudaLaunchKernelEx(&cfg, kern, prm, mk, mv, sg) == cudaSuccess ? 0 : KVR_ERR_CUDA;
 }
 
+template <int ORDER, bool F16>
+static int launch_tc_impl(const void* k, const void* v, int64_t n_tok, const int64_t* slots, const Pool& pool,
+                          int rot_k, int rot_v, const Signs& s, int has, uint32_t* flags, cudaStream_t st) {
+  TcStoreParams prm{};
+  prm.pool = pool;
+  prm.slots = slots;
+  prm.flags = flags;
+  if (n_tok * pool.H > (int64_t)INT32_MAX - k1tc::TM) return KVR_ERR_UNSUPPORTED;  // 32-bit row indices
+  prm.n_rows = (int32_t)(n_tok * pool.H);
+  prm.k_in = reinterpret_cast<const uint16_t*>(k);
+  prm.v_in = reinterpret_cast<const uint16_t*>(v);
+  prm.tiles_per_side = (int)((prm.n_rows + k1tc::TM - 1) / k1tc::TM);
+  prm.rot_k = rot_k;
+  prm.rot_v = rot_v;
+  prm.log2P = 0;
+  while ((1 << prm.log2P) < pool.P) ++prm.log2P;
+  Signs sg = s;
+  if (!has) for (auto& x : sg.w) x = 0u;
+  CUtensorMap mk, mv;
+  if (kvr_encode_tensor_map_2d(&mk, k, 128, (uint64_t)prm.n_rows, 256, 64, k1tc::TM, CU_TENSOR_MAP_SWIZZLE_128B) !=
+      CUDA_SUCCESS)
+    return KVR_ERR_CUDA;
+  if (kvr_encode_tensor_map_2d(&mv, v, 128, (uint64_t)prm.n_rows, 256, 64, k1tc::TM, CU_TENSOR_MAP_SWIZZLE_128B) !=
+      CUDA_SUCCESS)
+    return KVR_ERR_CUDA;
+  auto kern = store_tc_kernel<ORDER, F16>;
+  static bool attr_set[KVR_MAX_DEVICES];
+  const int dev = kvr_current_device();
+  if (!attr_set[dev]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, k1tc::SMEM) != cudaSuccess)
+      return KVR_ERR_CUDA;
+    attr_set[dev] = true;
+  }
+  const int total = 2 * prm.tiles_per_side;
+  int grid = kvr_num_sms() > 0 ? kvr_num_sms() : 148;
+  if (grid > total) grid = total;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(k1tc::THREADS);
+  cfg.dynamicSmemBytes = k1tc::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, prm, mk, mv, sg);
+  if (e != cudaSuccess) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, kern);
+    fprintf(stderr, "[kvr] store_tc launch: %s (regs %d, max threads %d, smem %d)\n", cudaGetErrorString(e), fa.numRegs,
+            fa.maxThreadsPerBlock, k1tc::SMEM);
+    return KVR_ERR_CUDA;
+  }
+  return 0;
+}
+
+// K1 implementation: the tcgen05 kernel unless KVR_K1_IMPL=mma or kvr_debug_set_k1_impl(1)
+// selects the mma.sync kernel it replaced (kept for A/B runs)
+static int g_k1_impl = -1;  // -1: from the environment on first use
+static bool k1_forced_tc = false;  // kvr_debug_set_k1_impl(2) / KVR_K1_IMPL=tc: the tcgen05 kernel at every size
+void kvr_set_k1_impl(int impl) {
+  g_k1_impl = impl == 1 ? 1 : 0;
+  k1_forced_tc = impl == 2;
+}
+static bool k1_use_tc() {
+  if (g_k1_impl < 0) {
+    const char* e = getenv("KVR_K1_IMPL");
+    g_k1_impl = (e && !strcmp(e, "mma")) ? 1 : 0;
+    k1_forced_tc = e && !strcmp(e, "tc");
+  }
+  return g_k1_impl == 0;
+}
+
 int kvr_launch_store_fast(const void* k, const void* v, int in_dtype, int64_t n_tok, const int64_t* slots,
                           const Pool& pool, int order, int rot_k, int rot_v, const Signs& s, int has,
                           uint32_t* flags, cudaStream_t st) {
@@ -572,6 +1089,24 @@ int kvr_launch_store_fast(const void* k, const void* v, int in_dtype, int64_t n_
   if ((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) & 15) return KVR_ERR_UNSUPPORTED;
   if (!(rot_k || rot_v)) order = 128;  // plain twin: order is irrelevant
   const bool f16 = in_dtype == KVR_F16;
+  // the tcgen05 kernel from ~4 tiles of 128 rows per SM on (measured: it ties with the mma.sync kernel at
+  // 8,192 tokens x 8 heads and is 17-20 % faster from 32k tokens; below, its fixed setup -- TMEM allocation,
+  // B blocks, 576 threads -- and the per-row latency of one epilogue thread per row dominate)
+  const int64_t tiles = 2 * ((n_tok * pool.H + 127) / 128);
+  const int sms = kvr_num_sms() > 0 ? kvr_num_sms() : 148;
+  if (k1_use_tc() && (tiles >= 4 * (int64_t)sms || k1_forced_tc)) {
+    switch (order) {
+      case 128: return f16 ? launch_tc_impl<128, true>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st)
+                           : launch_tc_impl<128, false>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st);
+      case 64: return f16 ? launch_tc_impl<64, true>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st)
+                          : launch_tc_impl<64, false>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st);
+      case 32: return f16 ? launch_tc_impl<32, true>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st)
+                          : launch_tc_impl<32, false>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st);
+      case 16: return f16 ? launch_tc_impl<16, true>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st)
+                          : launch_tc_impl<16, false>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st);
+    }
+    return KVR_ERR_UNSUPPORTED;
+  }
   switch (order) {
     case 128: return f16 ? launch_fast_impl<128, true>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st)
                          : launch_fast_impl<128, false>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st);

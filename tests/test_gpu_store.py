@@ -31,6 +31,17 @@ CASES = {
 }
 
 
+@pytest.fixture(params=["default", "tcgen05"], autouse=True)
+def k1_impl(request):
+    """Every test runs under the default K1 dispatch (the mma.sync kernel at these sizes)
+    and with the tcgen05/TMEM kernel forced (kvr_debug_set_k1_impl(2))."""
+    from paper_2604_19157_b200 import _lib
+
+    _lib.lib().kvr_debug_set_k1_impl(2 if request.param == "tcgen05" else 0)
+    yield request.param
+    _lib.lib().kvr_debug_set_k1_impl(0)
+
+
 def _spec(tag):
     lay, _, _, sargs, targets = CASES[tag]
     if sargs is None:
@@ -79,7 +90,7 @@ def test_fast_bf16_batch_on_golden(golden, tag):
         zpm = int(np.count_nonzero(fa[f"{side}_zp"] != fb[f"{side}_zp"]))
         ulp = ulp_distance_f32(fa[f"{side}_scale"], fb[f"{side}_scale"])
         print(f"{tag} {side}: nibble mismatches {mism}, zp mismatches {zpm}, scale ulp max {ulp.max()}")
-        assert zpm == 0 and ulp.max() <= 2 and mism <= 2
+        assert zpm == 0 and ulp.max() <= 2 and mism == 0  # measured: 0 nibble / 0 zp mismatches
     if CASES[tag][3] is None:
         assert ours == ref  # plain INT4 twin is bit-exact
 
@@ -138,12 +149,23 @@ def test_fast_rotated_c1(kind, targets):
     print(kind, targets, st)
     for side in ("k", "v"):
         s = st[side]
-        # documented reassociation tolerance: scale <= 2 ulp; codes/zp rare
+        # the fp32 butterfly may move a row's scale by <= 2 ulp (counted);
+        # codes and zero points are the reference's -- measured 0 / 0 on every family, both kernels
         assert s["scale_ulp_max"] <= 2
-        assert s["zp"] <= max(2, s["rows"] // 2000)
-        assert s["nibbles"] <= max(4, s["rows"] * 128 // 100000)
+        assert s["zp"] == 0
+        assert s["nibbles"] == 0
     if targets is Targets.KEYS_ONLY:
         assert st["v"]["nibbles"] == 0 and st["v"]["scale_rows_off"] == 0
+
+
+@pytest.mark.parametrize("rotate", [True, False])
+@pytest.mark.parametrize("kind", ["gaussian", "outlier"])
+def test_fast_large_write_default_dispatch(kind, rotate):
+    """8,192 tokens x 8 heads: large enough that the default dispatch picks the tcgen05 kernel."""
+    st = _fast_vs_oracle(kind, 8192, 8, 128, 128, rotate=rotate, targets=Targets.KEYS_AND_VALUES, seed=17)
+    print(kind, rotate, st)
+    for side in ("k", "v"):
+        assert st[side]["nibbles"] == 0 and st[side]["zp"] == 0 and st[side]["scale_ulp_max"] <= (2 if rotate else 0)
 
 
 @pytest.mark.parametrize("kind", ["gaussian", "outlier", "adversarial"])
@@ -158,14 +180,14 @@ def test_fast_lower_orders(order):
     st = _fast_vs_oracle("gaussian", 1024, 8, 128, order, rotate=True, targets=Targets.KEYS_AND_VALUES, seed=11)
     print(order, st)
     for side in ("k", "v"):
-        assert st[side]["scale_ulp_max"] <= 2 and st[side]["zp"] <= 2 and st[side]["nibbles"] <= 8
+        assert st[side]["scale_ulp_max"] <= 2 and st[side]["zp"] == 0 and st[side]["nibbles"] == 0
 
 
 def test_fast_fp16_input():
     st = _fast_vs_oracle("gaussian", 1024, 8, 128, 128, rotate=True, targets=Targets.KEYS_AND_VALUES, seed=13,
                          dtype=torch.float16)
     for side in ("k", "v"):
-        assert st[side]["scale_ulp_max"] <= 2 and st[side]["zp"] <= 2 and st[side]["nibbles"] <= 8
+        assert st[side]["scale_ulp_max"] <= 2 and st[side]["zp"] == 0 and st[side]["nibbles"] == 0
 
 
 def test_fast_nonfinite_flag():
