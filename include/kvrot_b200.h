@@ -48,7 +48,8 @@ typedef enum {
   KVR_ERR_ORDER = 2,        /* maps to kvrot.errors.InvalidOrderError     */
   KVR_ERR_UNSUPPORTED = 3,  /* configuration not built into this library  */
   KVR_ERR_CUDA = 4,         /* CUDA runtime failure (see kvr_last_error)  */
-  KVR_ERR_ARG = 5           /* null pointer / negative size / bad enum    */
+  KVR_ERR_ARG = 5,          /* null pointer / negative size / bad enum    */
+  KVR_ERR_NONFINITE = 6     /* a host input holds NaN/Inf (maps to NonFiniteInputError); nothing launched */
 } kvr_status;
 
 typedef enum { KVR_F64 = 0, KVR_F32 = 1, KVR_BF16 = 2, KVR_F16 = 3 } kvr_dtype;
@@ -122,6 +123,49 @@ void kvr_note_pool_write(void* stream);
 /* Host validation helper: 1 when the n values (dtype F64/F32/BF16/F16) at HOST
  * pointer p are all finite, 0 when one is NaN/Inf, -1 on a bad argument. */
 int kvr_host_all_finite(const void* p, int32_t dtype, int64_t n);
+/* Per-step host helpers of a graph-replayed serving step (DecodePlan.step; host code only).
+ * kvr_step_stage: waits for `ring_event` (the last launch that read this staging slot), then
+ * -- when `check` -- scans the HOST inputs q / k / v (any may be NULL) for NaN/Inf and copies
+ * them into the pinned `staging` buffer at their offsets.  Returns 1 (staged), 0 (a non-finite
+ * value: nothing was copied), < 0 on an error.
+ * kvr_step_launch: enqueues on `stream` the staging -> `dev_buf` copy of `bytes` (slot ids,
+ * lengths and the staged inputs), a launch of the instantiated CUDA graph `graph_exec`
+ * (cudaGraphExec_t; NULL = none) and a record of `ring_event`. */
+int kvr_step_stage(void* ring_event, void* staging, const void* q, int64_t q_off, int64_t q_bytes, int32_t q_dtype,
+                   const void* k, int64_t k_off, const void* v, int64_t v_off, int64_t kv_bytes, int32_t kv_dtype,
+                   int32_t check);
+int kvr_step_launch(void* dev_buf, const void* staging, int64_t bytes, void* graph_exec, void* ring_event,
+                    void* stream);
+/* A staging ring bound to fixed host inputs q / k / v (any may be NULL: not staged) and, per slot,
+ * a pinned staging buffer, its device twin, an instantiated CUDA graph and an event: then
+ * kvr_step_ring_run(ring, slot, meta) is the whole per-step host work of a graph-replayed serving
+ * step -- kvr_step_stage (wait for the slot's event, NaN/Inf scan when `check`, copy-in), the
+ * `meta_bytes` of step metadata (slot ids, lengths) copied to the front of the staging buffer,
+ * then kvr_step_launch.  Returns KVR_ERR_NONFINITE (nothing launched) on a NaN/Inf input. */
+typedef struct kvr_step_ring kvr_step_ring;
+kvr_step_ring* kvr_step_ring_create(int32_t n_slots, const void* q, int64_t q_off, int64_t q_bytes, int32_t q_dtype,
+                                    const void* k, int64_t k_off, const void* v, int64_t v_off, int64_t kv_bytes,
+                                    int32_t kv_dtype, int64_t meta_bytes, int64_t bytes, int32_t check, void* stream);
+int kvr_step_ring_set_slot(kvr_step_ring* ring, int32_t slot, void* staging, void* dev, void* graph_exec, void* event);
+int kvr_step_ring_run(kvr_step_ring* ring, int32_t slot, const void* meta);
+void kvr_step_ring_destroy(kvr_step_ring* ring);
+/* Direct modes: each kvr_step_ring_run launches kvr_decode_step itself (no graph), consecutive
+ * steps chained by programmatic dependent launch; new_slot / seq_lens point into the pinned slot.
+ *   mode 1: q / new_k / new_v are read by the kernel in place from the pinned slot (over the bus;
+ *           the query before the grid-dependency wait: a staged query is immutable for that launch);
+ *   mode 2: a one-CTA copy kernel chained in front of the decode moves the slot to its device twin
+ *           (overlapping the previous step) and the decode reads q / k / v there.
+ * The other arguments are kvr_decode_step's, fixed for the ring. */
+int kvr_step_ring_set_decode(kvr_step_ring* ring, int32_t q_dtype, int32_t kv_dtype, const kvr_pool* pool,
+                             const int32_t* block_table, int32_t bt_stride, int32_t batch, int32_t num_q_heads,
+                             int32_t max_seq_len, int32_t rot_order, int32_t rotate, int32_t targets,
+                             const uint32_t* sign_words, float* out, void* workspace, size_t workspace_bytes,
+                             int32_t num_splits, uint32_t* flags, int32_t mode);
+/* Profiling aid: mean host ns per kvr_step_ring_run since load -- stage (slot wait, scan, copy-in),
+ * metadata copy, decode launch, event record. */
+void kvr_debug_step_ring_times(double* out4);
+/* Optional: stage-in copies go on `copy_stream` (the step stream waits for each); NULL = same stream. */
+int kvr_step_ring_set_copy_stream(kvr_step_ring* ring, void* copy_stream);
 /* Number of SMs of the current device (0 if no device). */
 int kvr_device_sms(void);
 

@@ -29,7 +29,9 @@ EXPORTED = (
     "kvr_dequantize_rows_f64", "kvr_block_rotate", "kvr_rotate_quantize_store",
     "kvr_dequantize_pages", "kvr_decode_workspace_bytes", "kvr_decode_pick_splits",
     "kvr_paged_decode", "kvr_decode_step", "kvr_debug_decode_trace", "kvr_debug_set_k1_impl", "kvr_note_pool_write",
-    "kvr_host_all_finite", "kvr_decode_flat_f64",
+    "kvr_host_all_finite", "kvr_decode_flat_f64", "kvr_step_stage", "kvr_step_launch",
+    "kvr_step_ring_create", "kvr_step_ring_set_slot", "kvr_step_ring_run", "kvr_step_ring_destroy",
+    "kvr_step_ring_set_copy_stream", "kvr_step_ring_set_decode", "kvr_debug_step_ring_times",
 )
 
 
@@ -61,6 +63,16 @@ def _declare(lib):
         "kvr_debug_set_k1_impl": (None, [_I32]),
         "kvr_note_pool_write": (None, [_P]),
         "kvr_host_all_finite": (_I32, [_P, _I32, _I64]),
+        "kvr_step_stage": (_I32, [_P, _P, _P, _I64, _I64, _I32, _P, _I64, _P, _I64, _I64, _I32, _I32]),
+        "kvr_step_launch": (_I32, [_P, _P, _I64, _P, _P, _P]),
+        "kvr_step_ring_create": (_P, [_I32, _P, _I64, _I64, _I32, _P, _I64, _P, _I64, _I64, _I32, _I64, _I64, _I32, _P]),
+        "kvr_step_ring_set_slot": (_I32, [_P, _I32, _P, _P, _P, _P]),
+        "kvr_step_ring_run": (_I32, [_P, _I32, _P]),
+        "kvr_step_ring_destroy": (None, [_P]),
+        "kvr_step_ring_set_copy_stream": (_I32, [_P, _P]),
+        "kvr_debug_step_ring_times": (None, [_P]),
+        "kvr_step_ring_set_decode": (_I32, [_P, _I32, _I32, ctypes.POINTER(KvrPool), _P, _I32, _I32, _I32, _I32, _I32,
+                                            _I32, _I32, _P, _P, _P, _SZ, _I32, _P, _I32]),
         "kvr_decode_flat_f64": (_I32, [_P, _P, _P, _I64, _I32, _I32, _I32, _P, _P]),
         "kvr_abi_version": (_I32, []),
         "kvr_device_sms": (_I32, []),
@@ -105,6 +117,7 @@ _STATUS = {
     3: errors.UnsupportedConfigError,
     4: errors.DeviceError,
     5: errors.ShapeError,
+    6: errors.NonFiniteInputError,
 }
 
 

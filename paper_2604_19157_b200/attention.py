@@ -10,6 +10,7 @@ output when values were stored rotated.
 from __future__ import annotations
 
 import ctypes
+import os
 import math
 from dataclasses import dataclass
 from typing import Optional, Sequence
@@ -98,8 +99,12 @@ class DecodePlan:
         self.lens.copy_(lens)
         self._copy_stream = None
         self.side_copy = False  # True: staged inputs go over on a side stream (measured slower end to end)
+        self.fast_copy_stream = os.environ.get("KVR_STEP_SIDE_COPY", "0") == "1"  # the native ring's copies (A/B)
+        # the native ring launches the fused step itself on pinned inputs (no graph, no copy); A/B switch
+        self.fast_direct = int(os.environ.get("KVR_STEP_DIRECT", "2"))  # 0 graph replay, 1 in place, 2 copy kernel
         self._lens_stale = False  # step() passes its own device copy of the lengths
         self._layouts = {}
+        self._fast = None  # native step ring bound to the last graph step's host tensors
         if num_splits <= 0:
             num_splits = _lib.lib().kvr_decode_pick_splits(B, lay.num_kv_heads, self.max_len, P)
         self.splits = num_splits
@@ -258,6 +263,107 @@ class DecodePlan:
 
     def step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, spec: Optional[RotationSpec],
              out: Optional[torch.Tensor] = None, graph: bool = False, check: bool = True) -> torch.Tensor:
+        """One serving decode step (see _step_general for the contract).  Repeated graph
+        steps with the same host tensors take a native fast path: the slot ids and
+        lengths are planned here (no new page: every page_tokens-th step takes the
+        general path, which allocates it) and one kvr_step_ring_run call stages,
+        checks and copies the inputs and replays the step's CUDA graph."""
+        fr = self._fast
+        if (graph and fr is not None and fr["q"] is q and fr["k"] is k_new and fr["v"] is v_new and fr["out"] is out
+                and fr["spec"] is spec and fr["check"] == check):
+            r = self._fast_step(fr)
+            if r is not None:
+                return r
+        return self._step_general(q, k_new, v_new, spec, out, graph, check)
+
+    def _fast_step(self, fr: dict) -> Optional[torch.Tensor]:
+        if (fr["max_len"] != self.max_len or fr["q"].data_ptr() != fr["qp"] or fr["k"].data_ptr() != fr["kp"]
+                or fr["v"].data_ptr() != fr["vp"]
+                or torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice()) != fr["stream"]):
+            self._drop_fast()
+            return None
+        alloc = self.table.alloc
+        P = alloc.page_tokens
+        seq_len, seq_pages = alloc.seq_len, alloc.seq_pages
+        slots, lens, known = fr["slots"], fr["lens"], self._known_pages
+        for n, s in enumerate(self.seqs):
+            t = seq_len[s]
+            # a new page, the capacity error, pages the block table has not seen: the general path
+            if t % P == 0 or t + 1 > self.max_len or len(seq_pages[s]) != known[n]:
+                return None
+            slots[n] = seq_pages[s][t // P] * P + t % P
+            lens[n] = t + 1
+        for n, s in enumerate(self.seqs):
+            seq_len[s] = int(lens[n])
+        sl = fr["layout"]
+        i = sl["i"]
+        sl["i"] = (i + 1) % self._RING
+        rc = _lib.lib().kvr_step_ring_run(fr["handle"], i, fr["meta_ptr"])
+        if rc:
+            for n, s in enumerate(self.seqs):
+                seq_len[s] = int(lens[n]) - 1  # nothing of a rejected step stays behind
+            _lib.check(rc)
+        self._lens_stale = True
+        return fr["out"]
+
+    def _drop_fast(self) -> None:
+        if self._fast is not None:
+            _lib.lib().kvr_step_ring_destroy(self._fast["handle"])
+            self._fast = None
+
+    def __del__(self):
+        try:
+            self._drop_fast()
+        except Exception:
+            pass
+
+    def _arm_fast(self, q, k_new, v_new, spec, out, check, lay, stream) -> None:
+        """After a general graph step: when every staging slot has its graph, bind a native
+        step ring to these host tensors (kvr_step_ring_create)."""
+        B = len(self.seqs)
+        if not (q.is_contiguous() and k_new.is_contiguous() and v_new.is_contiguous()):
+            return
+        execs = []
+        for i, ring in enumerate(lay["ring"]):
+            dq, dk, dv = ring[5]["inputs"]
+            g = lay.get("graphs", {}).get((i, out.data_ptr(), id(spec), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
+                                           self.max_len, self.splits))
+            if g is None or g[1] is None:
+                return
+            execs.append(g[1])
+        self._drop_fast()
+        meta = np.zeros(12 * B, dtype=np.uint8)
+        h = _lib.lib().kvr_step_ring_create(
+            self._RING, q.data_ptr(), lay["offs"][0], q.numel() * q.element_size(), _KV_CODE[q.dtype],
+            k_new.data_ptr(), lay["offs"][1], v_new.data_ptr(), lay["offs"][2], k_new.numel() * k_new.element_size(),
+            _KV_CODE[k_new.dtype], 12 * B, lay["bytes"], 1 if check else 0, stream)
+        if not h:
+            return
+        for i, ring in enumerate(lay["ring"]):
+            _lib.check(_lib.lib().kvr_step_ring_set_slot(h, i, ring[2], ring[4], execs[i], ring[3].cuda_event))
+        if self.fast_direct and lay["bytes"] <= 65536 and fused_step_supported(self.table.layout, self.table.precision) and not (
+                spec is not None and spec.learned is not None):
+            # direct mode: the kernel reads q / k / v / slot ids / lengths from the pinned slot
+            rotate = spec is not None and self.table.precision == INT4
+            lay_ = self.table.layout
+            targets = _lib.KVR_KEYS_ONLY if (rotate and spec.targets is Targets.KEYS_ONLY) else _lib.KVR_KEYS_AND_VALUES
+            _lib.check(_lib.lib().kvr_step_ring_set_decode(
+                h, _Q_CODE[q.dtype], _KV_CODE[k_new.dtype], ctypes.byref(self.table.desc), self.bt.data_ptr(),
+                self.bt.shape[1], B, lay_.num_q_heads, self.max_len, spec.order if rotate else 1, 1 if rotate else 0,
+                targets, spec.sign_words(lay_.head_dim) if rotate else None, out.data_ptr(), self.ws.data_ptr(),
+                self.ws.numel(), self.splits, self.table.flags.data_ptr(), self.fast_direct))
+        elif self.fast_copy_stream:  # stage-in copies on a side stream (they may overlap the previous step)
+            if self._copy_stream is None:
+                self._copy_stream = torch.cuda.Stream(device=self.table.device)
+            _lib.check(_lib.lib().kvr_step_ring_set_copy_stream(h, self._copy_stream.cuda_stream))
+        self._fast = {"q": q, "k": k_new, "v": v_new, "out": out, "spec": spec, "check": check,
+                      "qp": q.data_ptr(), "kp": k_new.data_ptr(), "vp": v_new.data_ptr(), "stream": stream,
+                      "max_len": self.max_len, "layout": lay, "handle": h, "meta": meta,
+                      "meta_ptr": meta.ctypes.data, "slots": meta[:8 * B].view(np.int64),
+                      "lens": meta[8 * B:].view(np.int32)}
+
+    def _step_general(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, spec: Optional[RotationSpec],
+                      out: Optional[torch.Tensor] = None, graph: bool = False, check: bool = True) -> torch.Tensor:
         """One serving decode step for every sequence of the plan: allocate the new
         token's slot (reference page order), then one fused append + decode launch.
         q (B, nq, d) and k_new/v_new (B, H, d) may be host tensors: they are staged
@@ -283,13 +389,16 @@ class DecodePlan:
         lay = table.layout
         B = len(self.seqs)
         stream = torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
-        if (tuple(q.shape) != (B, lay.num_q_heads, lay.head_dim) or tuple(k_new.shape) != (B, lay.num_kv_heads,
-                lay.head_dim) or tuple(v_new.shape) != tuple(k_new.shape)):
+        kv_shape = (B, lay.num_kv_heads, lay.head_dim)
+        if q.shape != (B, lay.num_q_heads, lay.head_dim) or k_new.shape != kv_shape or v_new.shape != kv_shape:
             raise ShapeError(f"expected q ({B}, {lay.num_q_heads}, {lay.head_dim}) and k/v ({B}, {lay.num_kv_heads}, "
                              f"{lay.head_dim}), got {tuple(q.shape)}, {tuple(k_new.shape)}, {tuple(v_new.shape)}")
+        if k_new.dtype != v_new.dtype:
+            raise ShapeError(f"k_new and v_new dtypes differ ({k_new.dtype}, {v_new.dtype})")
         if out is not None and not out.is_cuda and not out.is_pinned():
             raise ShapeError("out must be a CUDA tensor or a pinned host tensor")
-        if check and not (_all_finite(q) and _all_finite(k_new) and _all_finite(v_new)):
+        host = [not t.is_cuda for t in (q, k_new, v_new)]
+        if check and not all(_all_finite(t) for t, h in zip((q, k_new, v_new), host) if not h):
             raise NonFiniteInputError("q / k_new / v_new contain NaN or Inf")
         cur = [table.sequence_length(s) for s in self.seqs]
         mx = max(cur) + 1
@@ -300,36 +409,65 @@ class DecodePlan:
         if mx > self.max_len and graph:
             raise ShapeError(f"sequence length {mx} passed the plan's capacity {self.max_len}; "
                              f"build a new DecodePlan (extra_tokens)")
+        # stage the host inputs into the next pinned ring slot (once its last reader has run)
+        # and scan them for NaN/Inf -- one native call, before any allocator state changes
+        host_in = [t if t.is_contiguous() else t.contiguous() for t, h in zip((q, k_new, v_new), host) if h]
+        lkey = tuple((t.shape, t.dtype) for t in host_in)
+        sl = self._layouts.get(lkey) or self._step_layout(host_in)
+        slot_i = sl["i"]
+        ring = sl["ring"][slot_i]
+        sl["i"] = (slot_i + 1) % self._RING
+        ptrs, offs = [None, None, None], [0, 0, 0]
+        j = 0
+        for r in range(3):
+            if host[r]:
+                ptrs[r], offs[r] = host_in[j].data_ptr(), sl["offs"][j]
+                j += 1
+        rc = _lib.lib().kvr_step_stage(ring[3].cuda_event, ring[2], ptrs[0], offs[0],
+                                       q.numel() * q.element_size(), _KV_CODE.get(q.dtype, -1), ptrs[1], offs[1],
+                                       ptrs[2], offs[2], k_new.numel() * k_new.element_size(),
+                                       _KV_CODE.get(k_new.dtype, -1), 1 if check else 0)
+        if rc == 0:
+            raise NonFiniteInputError("q / k_new / v_new contain NaN or Inf")
+        _lib.check(rc if rc < 0 else 0)
         slots, fresh = table.alloc.plan(self.seqs)  # commit (pages on the free heap are zero)
         known = list(self._known_pages)
         try:
-            return self._step_committed(q, k_new, v_new, spec, out, graph, slots, fresh, cur, mx, stream)
+            res = self._step_committed(q, k_new, v_new, spec, out, graph, slots, fresh, cur, mx, stream, sl, slot_i)
         except BaseException:
             table.alloc.unplan(self.seqs, fresh)  # nothing of a failed step stays behind
             self._known_pages = known
             raise
+        if graph and out is not None and all(host) and not self.side_copy and (
+                self._fast is None or self._fast["q"] is not q or self._fast["out"] is not out):
+            self._arm_fast(q, k_new, v_new, spec, out, check, sl, stream)
+        return res
 
-    def _step_committed(self, q, k_new, v_new, spec, out, graph, slots, fresh, cur, mx, stream):
+    def _step_committed(self, q, k_new, v_new, spec, out, graph, slots, fresh, cur, mx, stream, lay, slot_i):
         table = self.table
         B = len(self.seqs)
         if fresh:
             self._patch_pages(stream)
-        lens = np.fromiter((c + 1 for c in cur), dtype=np.int32, count=B)
         if mx > self.max_len:
             self.max_len = mx
-        host_in = [t for t in (q, k_new, v_new) if not t.is_cuda]
-        lkey = tuple((t.shape, t.dtype) for t in host_in)
-        lay = self._layouts.get(lkey) or self._step_layout(host_in)
-        slot_i = lay["i"]
         buf, buf_np, buf_ptr, ev, dptr, dviews, cev = lay["ring"][slot_i]
-        lay["i"] = (slot_i + 1) % self._RING
-        _kernels.event_sync(ev)  # the kernel that last read this slot (host and device side) has run
         buf_np[:8 * B] = slots.view(np.uint8)
-        buf_np[8 * B:12 * B] = lens.view(np.uint8)
-        for t, off, n in zip(host_in, lay["offs"], lay["sizes"]):
-            t = t if t.is_contiguous() else t.contiguous()
-            ctypes.memmove(buf_ptr + off, t.data_ptr(), n)
+        lens = buf_np[8 * B:12 * B].view(np.int32)
+        for i, c in enumerate(cur):
+            lens[i] = c + 1
+        self._lens_stale = True  # the plan's own device lengths are refreshed on demand
+        staged = iter(dviews["inputs"])
+        q, k_new, v_new = (t if t.is_cuda else next(staged) for t in (q, k_new, v_new))
+        if out is None:
+            out = torch.empty(q.shape, dtype=torch.float32, device=table.device)
         side = self.side_copy
+        if graph and not side:
+            gkey = (slot_i, out.data_ptr(), id(spec), q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(),
+                    self.max_len, self.splits)
+            g = lay.setdefault("graphs", {}).get(gkey)
+            if g is not None and g[1] is not None:  # the common path: copy + graph + event in one native call
+                _lib.check(_lib.lib().kvr_step_launch(dptr, buf_ptr, lay["bytes"], g[1], ev.cuda_event, stream))
+                return out
         if side:  # the staged bytes go over on the side stream; the compute stream waits for them
             if self._copy_stream is None:
                 self._copy_stream = torch.cuda.Stream(device=table.device)
@@ -337,13 +475,7 @@ class DecodePlan:
             _kernels.h2d_async(dptr, buf_ptr, lay["bytes"], cs)
             _kernels.event_record(cev, cs)
             _kernels.stream_wait(stream, cev)
-        self._lens_stale = True  # the plan's own device lengths are refreshed on demand
-        staged = iter(dviews["inputs"])
-        q, k_new, v_new = (t if t.is_cuda else next(staged) for t in (q, k_new, v_new))
-        if out is None:
-            out = torch.empty(q.shape, dtype=torch.float32, device=table.device)
-
-        if not side:  # the staged bytes go over on the compute stream, ahead of the kernel
+        else:  # the staged bytes go over on the compute stream, ahead of the kernel
             _kernels.h2d_async(dptr, buf_ptr, lay["bytes"], stream)
 
         def device_part():
@@ -353,8 +485,10 @@ class DecodePlan:
             device_part()
         else:
             graphs = lay.setdefault("graphs", {})
-            gkey = (slot_i, side, out.data_ptr(), id(spec), q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(),
+            gkey = (slot_i, out.data_ptr(), id(spec), q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(),
                     self.max_len, self.splits)
+            if side:
+                gkey = gkey + ("side",)
             g = graphs.get(gkey)
             if g is not None:
                 if g[1] is not None:

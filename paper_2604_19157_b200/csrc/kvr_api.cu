@@ -3,7 +3,9 @@
 // entry point replaces.
 #include <cstdarg>
 #include <cstdio>
+#include <chrono>
 #include <cstring>
+#include <new>
 #include <mutex>
 #include <vector>
 
@@ -135,6 +137,13 @@ bool kvr_take_pool_written(cudaStream_t st) {
   return false;
 }
 
+static int decode_step_impl(const void* q, int32_t q_dtype, const void* new_k, const void* new_v, int32_t kv_dtype,
+                            const int64_t* new_slot, const kvr_pool* pool, const int32_t* block_table,
+                            int32_t bt_stride, const int32_t* seq_lens, int32_t batch, int32_t num_q_heads,
+                            int32_t max_seq_len, int32_t rot_order, int32_t rotate, int32_t targets,
+                            const uint32_t* sign_words, float* out, void* workspace, size_t workspace_bytes,
+                            int32_t num_splits, uint32_t* flags, void* stream, int q_host_staged);
+
 extern "C" {
 
 const char* kvr_last_error(void) { return g_err; }
@@ -151,14 +160,22 @@ int kvr_host_all_finite(const void* p, int32_t dtype, int64_t n) {
   if (!p) return -1;
   uint32_t bad = 0u;
   switch (dtype) {
-    case KVR_BF16: {  // exponent all ones
+    case KVR_BF16:    // exponent all ones
+    case KVR_F16: {   // four 16-bit values per 64-bit word: a lane with the exponent mask all set
+      const uint64_t m = dtype == KVR_BF16 ? 0x7F807F807F807F80ull : 0x7C007C007C007C00ull;
       const uint16_t* u = static_cast<const uint16_t*>(p);
-      for (int64_t i = 0; i < n; ++i) bad |= ((u[i] & 0x7F80u) == 0x7F80u);
-      return bad ? 0 : 1;
-    }
-    case KVR_F16: {
-      const uint16_t* u = static_cast<const uint16_t*>(p);
-      for (int64_t i = 0; i < n; ++i) bad |= ((u[i] & 0x7C00u) == 0x7C00u);
+      int64_t i = 0;
+      if (!(reinterpret_cast<uintptr_t>(p) & 7)) {
+        const uint64_t* w = static_cast<const uint64_t*>(p);
+        uint64_t acc = 0;
+        for (; i + 4 <= n; i += 4) {
+          const uint64_t x = (w[i >> 2] & m) ^ m;  // 16-bit lane == 0 <=> non-finite
+          acc |= (x - 0x0001000100010001ull) & ~x & 0x8000800080008000ull;
+        }
+        bad |= acc != 0;
+      }
+      const uint16_t e = (uint16_t)(m & 0xFFFF);
+      for (; i < n; ++i) bad |= ((u[i] & e) == e);
       return bad ? 0 : 1;
     }
     case KVR_F32: {
@@ -175,6 +192,214 @@ int kvr_host_all_finite(const void* p, int32_t dtype, int64_t n) {
   return -1;
 }
 int kvr_device_sms(void) { return kvr_num_sms(); }
+
+// ---- DecodePlan.step's per-step host work in two calls (Python keeps only the
+// allocator bookkeeping between them)
+static int host_finite_bytes(const void* p, int32_t dtype, int64_t n) { return kvr_host_all_finite(p, dtype, n); }
+
+int kvr_step_stage(void* ring_event, void* staging, const void* q, int64_t q_off, int64_t q_bytes, int32_t q_dtype,
+                   const void* k, int64_t k_off, const void* v, int64_t v_off, int64_t kv_bytes, int32_t kv_dtype,
+                   int32_t check) {
+  if (!staging) return fail(KVR_ERR_ARG, "step_stage: null staging buffer");
+  if (ring_event && cudaEventSynchronize((cudaEvent_t)ring_event) != cudaSuccess)
+    return fail(KVR_ERR_CUDA, "step_stage: cudaEventSynchronize failed");
+  const int esz[] = {8, 4, 2, 2};  // KVR_F64, F32, BF16, F16
+  if (check) {
+    if (q && q_dtype >= KVR_F64 && q_dtype <= KVR_F16 && host_finite_bytes(q, q_dtype, q_bytes / esz[q_dtype]) != 1)
+      return 0;
+    if (kv_dtype >= KVR_F64 && kv_dtype <= KVR_F16) {
+      if (k && host_finite_bytes(k, kv_dtype, kv_bytes / esz[kv_dtype]) != 1) return 0;
+      if (v && host_finite_bytes(v, kv_dtype, kv_bytes / esz[kv_dtype]) != 1) return 0;
+    }
+  }
+  uint8_t* st = static_cast<uint8_t*>(staging);
+  if (q) memcpy(st + q_off, q, (size_t)q_bytes);
+  if (k) memcpy(st + k_off, k, (size_t)kv_bytes);
+  if (v) memcpy(st + v_off, v, (size_t)kv_bytes);
+  return 1;
+}
+
+// A pinned staging ring bound to fixed host inputs and captured graphs: one call per step.
+struct kvr_step_ring {
+  void* q;
+  void* k;
+  void* v;
+  int64_t q_off, q_bytes, k_off, v_off, kv_bytes, meta_bytes, bytes;
+  int32_t q_dtype, kv_dtype, check, n;
+  void* stream;
+  void* copy_stream;  // non-NULL: the copy goes on this stream and `stream` waits for it (copy_event)
+  void* copy_event[16];
+  // direct mode (kvr_step_ring_set_decode): each run launches the fused decode step itself, its
+  // inputs read by the kernel from the pinned staging slot (no graph, no stage-in copy)
+  int direct;
+  int32_t d_q_dtype, d_kv_dtype, d_bt_stride, d_batch, d_nq, d_max_len, d_rot_order, d_rotate, d_targets, d_splits,
+      d_has_signs;
+  kvr_pool d_pool;
+  const int32_t* d_bt;
+  uint32_t d_signs[KVR_MAX_HEAD_DIM / 32];
+  float* d_out;
+  void* d_ws;
+  size_t d_ws_bytes;
+  uint32_t* d_flags;
+  void* staging[16];
+  void* dev[16];
+  void* exec[16];
+  void* event[16];
+};
+
+kvr_step_ring* kvr_step_ring_create(int32_t n_slots, const void* q, int64_t q_off, int64_t q_bytes, int32_t q_dtype,
+                                    const void* k, int64_t k_off, const void* v, int64_t v_off, int64_t kv_bytes,
+                                    int32_t kv_dtype, int64_t meta_bytes, int64_t bytes, int32_t check, void* stream) {
+  if (n_slots < 1 || n_slots > 16) {
+    fail(KVR_ERR_ARG, "step_ring_create: 1..16 slots");
+    return nullptr;
+  }
+  kvr_step_ring* r = new (std::nothrow) kvr_step_ring();
+  if (!r) return nullptr;
+  r->q = const_cast<void*>(q);
+  r->k = const_cast<void*>(k);
+  r->v = const_cast<void*>(v);
+  r->q_off = q_off;
+  r->q_bytes = q_bytes;
+  r->k_off = k_off;
+  r->v_off = v_off;
+  r->kv_bytes = kv_bytes;
+  r->q_dtype = q_dtype;
+  r->kv_dtype = kv_dtype;
+  r->meta_bytes = meta_bytes;
+  r->bytes = bytes;
+  r->check = check;
+  r->n = n_slots;
+  r->stream = stream;
+  return r;
+}
+
+int kvr_step_ring_set_slot(kvr_step_ring* r, int32_t i, void* staging, void* dev, void* graph_exec, void* event) {
+  if (!r || i < 0 || i >= r->n) return fail(KVR_ERR_ARG, "step_ring_set_slot: bad ring or slot");
+  r->staging[i] = staging;
+  r->dev[i] = dev;
+  r->exec[i] = graph_exec;
+  r->event[i] = event;
+  return KVR_OK;
+}
+
+void kvr_step_ring_destroy(kvr_step_ring* r) {
+  if (!r) return;
+  for (int i = 0; i < 16; ++i)
+    if (r->copy_event[i]) cudaEventDestroy((cudaEvent_t)r->copy_event[i]);
+  delete r;
+}
+
+int kvr_step_ring_set_decode(kvr_step_ring* r, int32_t q_dtype, int32_t kv_dtype, const kvr_pool* pool,
+                             const int32_t* block_table, int32_t bt_stride, int32_t batch, int32_t num_q_heads,
+                             int32_t max_seq_len, int32_t rot_order, int32_t rotate, int32_t targets,
+                             const uint32_t* sign_words, float* out, void* workspace, size_t workspace_bytes,
+                             int32_t num_splits, uint32_t* flags, int32_t mode) {
+  if (!r || !pool) return fail(KVR_ERR_ARG, "step_ring_set_decode: null ring / pool");
+  if (mode < 1 || mode > 2) return fail(KVR_ERR_ARG, "step_ring_set_decode: mode 1 or 2");
+  r->d_q_dtype = q_dtype;
+  r->d_kv_dtype = kv_dtype;
+  r->d_pool = *pool;
+  r->d_bt = block_table;
+  r->d_bt_stride = bt_stride;
+  r->d_batch = batch;
+  r->d_nq = num_q_heads;
+  r->d_max_len = max_seq_len;
+  r->d_rot_order = rot_order;
+  r->d_rotate = rotate;
+  r->d_targets = targets;
+  r->d_has_signs = sign_words != nullptr;
+  if (sign_words) memcpy(r->d_signs, sign_words, sizeof(r->d_signs[0]) * ((pool->head_dim + 31) / 32));
+  r->d_out = out;
+  r->d_ws = workspace;
+  r->d_ws_bytes = workspace_bytes;
+  r->d_splits = num_splits;
+  r->d_flags = flags;
+  r->direct = mode;
+  return KVR_OK;
+}
+
+static double g_ring_ns[4];
+static long g_ring_calls;
+static inline double now_ns() {
+  return (double)std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+void kvr_debug_step_ring_times(double* out4) {  // profiling aid: mean ns per run (stage, meta, launch, record)
+  for (int k = 0; k < 4; ++k) out4[k] = g_ring_calls ? g_ring_ns[k] / g_ring_calls : 0.0;
+}
+int kvr_step_ring_run(kvr_step_ring* r, int32_t i, const void* meta) {
+  if (!r || i < 0 || i >= r->n || !(r->exec[i] || r->direct)) return fail(KVR_ERR_ARG, "step_ring_run: bad ring or slot");
+  const double t0 = now_ns();
+  ++g_ring_calls;
+  const int rc = kvr_step_stage(r->event[i], r->staging[i], r->q, r->q_off, r->q_bytes, r->q_dtype, r->k, r->k_off,
+                                r->v, r->v_off, r->kv_bytes, r->kv_dtype, r->check);
+  if (rc != 1) return rc == 0 ? KVR_ERR_NONFINITE : rc;
+  const double t1 = now_ns();
+  g_ring_ns[0] += t1 - t0;
+  memcpy(r->staging[i], meta, (size_t)r->meta_bytes);
+  if (r->direct) {  // slot ids | lengths | q | k | v all in the pinned slot: the kernel reads them in place
+    uint8_t* st = static_cast<uint8_t*>(r->staging[i]);
+    const int B = r->d_batch;
+    const uint8_t* in = st;  // where the kernel reads q / k / v
+    int q_staged = 1;
+    if (r->direct == 2) {
+      // the slot (ids, lengths, q, k, v) goes to its device twin through a one-CTA copy kernel chained
+      // in front of the decode: the copy overlaps the previous step; the decode reads it all after its
+      // grid-dependency wait (pinned-memory reads in its prologue cost ~12 us a step, measured)
+      if (int e = kvr_launch_stage_copy(r->dev[i], st, r->bytes, (cudaStream_t)r->stream))
+        return fail(e, "step_ring_run: stage copy launch failed");
+      in = static_cast<const uint8_t*>(r->dev[i]);
+      q_staged = 2;  // slot ids / lengths too come from the copy: the decode reads them after its wait
+    }
+    const uint8_t* meta_in = r->direct == 2 ? in : st;
+    const double t2 = now_ns();
+    g_ring_ns[1] += t2 - t1;
+    if (int e = decode_step_impl(in + r->q_off, r->d_q_dtype, in + r->k_off, in + r->v_off, r->d_kv_dtype,
+                                 reinterpret_cast<const int64_t*>(meta_in), &r->d_pool, r->d_bt, r->d_bt_stride,
+                                 reinterpret_cast<const int32_t*>(meta_in + 8 * B), B, r->d_nq, r->d_max_len,
+                                 r->d_rot_order, r->d_rotate, r->d_targets, r->d_has_signs ? r->d_signs : nullptr,
+                                 r->d_out, r->d_ws, r->d_ws_bytes, r->d_splits, r->d_flags, r->stream, q_staged))
+      return e;
+    const double t3 = now_ns();
+    g_ring_ns[2] += t3 - t2;
+    if (cudaEventRecord((cudaEvent_t)r->event[i], (cudaStream_t)r->stream) != cudaSuccess)
+      return fail(KVR_ERR_CUDA, "step_ring_run: cudaEventRecord failed");
+    g_ring_ns[3] += now_ns() - t3;
+    return KVR_OK;
+  }
+  if (!r->copy_stream) return kvr_step_launch(r->dev[i], r->staging[i], r->bytes, r->exec[i], r->event[i], r->stream);
+  // side-stream copy: it may overlap the previous step's kernel (the slot's last reader is done)
+  cudaStream_t cs = (cudaStream_t)r->copy_stream, st = (cudaStream_t)r->stream;
+  if (cudaMemcpyAsync(r->dev[i], r->staging[i], (size_t)r->bytes, cudaMemcpyHostToDevice, cs) != cudaSuccess ||
+      cudaEventRecord((cudaEvent_t)r->copy_event[i], cs) != cudaSuccess ||
+      cudaStreamWaitEvent(st, (cudaEvent_t)r->copy_event[i], 0) != cudaSuccess)
+    return fail(KVR_ERR_CUDA, "step_ring_run: side-stream copy failed");
+  return kvr_step_launch(nullptr, nullptr, 0, r->exec[i], r->event[i], r->stream);
+}
+
+int kvr_step_ring_set_copy_stream(kvr_step_ring* r, void* copy_stream) {
+  if (!r) return fail(KVR_ERR_ARG, "step_ring_set_copy_stream: null ring");
+  if (copy_stream)
+    for (int i = 0; i < r->n; ++i)
+      if (!r->copy_event[i] &&
+          cudaEventCreateWithFlags((cudaEvent_t*)&r->copy_event[i], cudaEventDisableTiming) != cudaSuccess)
+        return fail(KVR_ERR_CUDA, "step_ring_set_copy_stream: cudaEventCreate failed");
+  r->copy_stream = copy_stream;
+  return KVR_OK;
+}
+
+int kvr_step_launch(void* dev_buf, const void* staging, int64_t bytes, void* graph_exec, void* ring_event,
+                    void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (bytes > 0 && cudaMemcpyAsync(dev_buf, staging, (size_t)bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return fail(KVR_ERR_CUDA, "step_launch: cudaMemcpyAsync failed");
+  if (graph_exec && cudaGraphLaunch((cudaGraphExec_t)graph_exec, st) != cudaSuccess)
+    return fail(KVR_ERR_CUDA, "step_launch: cudaGraphLaunch failed");
+  if (ring_event && cudaEventRecord((cudaEvent_t)ring_event, st) != cudaSuccess)
+    return fail(KVR_ERR_CUDA, "step_launch: cudaEventRecord failed");
+  return KVR_OK;
+}
 
 int kvr_pool_init(kvr_pool* pool, void* base, int64_t num_pages, int32_t page_tokens, int32_t num_kv_heads,
                   int32_t head_dim) {
@@ -371,6 +596,19 @@ int kvr_decode_step(const void* q, int32_t q_dtype, const void* new_k, const voi
                     const int32_t* seq_lens, int32_t batch, int32_t num_q_heads, int32_t max_seq_len,
                     int32_t rot_order, int32_t rotate, int32_t targets, const uint32_t* sign_words, float* out,
                     void* workspace, size_t workspace_bytes, int32_t num_splits, uint32_t* flags, void* stream) {
+  return decode_step_impl(q, q_dtype, new_k, new_v, kv_dtype, new_slot, pool, block_table, bt_stride, seq_lens, batch,
+                          num_q_heads, max_seq_len, rot_order, rotate, targets, sign_words, out, workspace,
+                          workspace_bytes, num_splits, flags, stream, 0);
+}
+
+}  // extern "C"
+
+static int decode_step_impl(const void* q, int32_t q_dtype, const void* new_k, const void* new_v, int32_t kv_dtype,
+                            const int64_t* new_slot, const kvr_pool* pool, const int32_t* block_table,
+                            int32_t bt_stride, const int32_t* seq_lens, int32_t batch, int32_t num_q_heads,
+                            int32_t max_seq_len, int32_t rot_order, int32_t rotate, int32_t targets,
+                            const uint32_t* sign_words, float* out, void* workspace, size_t workspace_bytes,
+                            int32_t num_splits, uint32_t* flags, void* stream, int q_host_staged) {
   Pool pl;
   if (int rc = to_pool(pool, pl)) return rc;
   if (batch < 0 || num_q_heads < 1 || num_q_heads % pl.H != 0)
@@ -407,10 +645,8 @@ int kvr_decode_step(const void* q, int32_t q_dtype, const void* new_k, const voi
   const int rot_v = (rotate && targets == KVR_KEYS_AND_VALUES) ? 1 : 0;
   int rc = kvr_launch_decode(q, q_dtype, pl, block_table, bt_stride, seq_lens, batch, num_q_heads, max_seq_len,
                              rot_order, rotate, rot_v, s, has, out, workspace, workspace_bytes, num_splits,
-                             (cudaStream_t)stream, new_k, new_v, kv_dtype, new_slot, flags);
+                             (cudaStream_t)stream, new_k, new_v, kv_dtype, new_slot, flags, q_host_staged);
   if (rc == KVR_ERR_ARG) return fail(rc, "decode workspace too small");
   if (rc) return fail(rc, "decode_step: unsupported geometry (needs d=128, page_tokens>=16, G in 1/2/4/8)");
   return check_launch("decode_step");
 }
-
-}  // extern "C"

@@ -58,6 +58,8 @@ struct DecodeParams {
   int pre_groups;    // ring groups per warp requested before griddepcontrol.wait
   int evict_first;   // KV cells are streamed with an L2 evict-first policy
   int merge_inline;  // splits > 1 without a cluster: the last CTA merges (ws_cnt counters)
+  int q_pre_wait;       // the query is host-staged for this launch (immutable): load it before the wait
+  int meta_post_wait;   // lengths / slot ids come from the previous grid: read them after the wait
   uint32_t f16x2_1024;  // 0x64006400 (fp16x2 1024.0) from the parameter bank: an opaque operand lets
                         // ptxas fuse (x & mask) | 1024 into one LOP3 (two immediates need two)
 };
@@ -194,6 +196,13 @@ KVR_DEV void cta_fwht_rows(float* s, int rows) {
 // then _ref.quantize_rows (_ref.py:22-40, 57-80) and the paged store.
 // Returns the stored-space (rotated) dequantised elements of lane l in deq[side]
 // (dims 4l..4l+3); a non-finite row is flagged, not written, and reads as 0.
+KVR_DEV double load_any(const void* src, int dtype, int64_t i) {
+  if (dtype == KVR_BF16) return (double)__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(src)[i]);
+  if (dtype == KVR_F16) return (double)__half2float(reinterpret_cast<const __half*>(src)[i]);
+  if (dtype == KVR_F32) return (double)reinterpret_cast<const float*>(src)[i];
+  return reinterpret_cast<const double*>(src)[i];
+}
+
 template <int ORDER>
 KVR_DEV bool append_rows_exact(const DecodeParams& p, const Signs& sg, int b, int h, float (&deq)[2][4],
                                unsigned long long* tr = nullptr) {
@@ -201,40 +210,66 @@ KVR_DEV bool append_rows_exact(const DecodeParams& p, const Signs& sg, int b, in
   const int64_t slot = p.new_slot[b];
   const int64_t base = ((int64_t)b * p.pool.H + h) * 128 + 4 * lane;
   double x[2][4];
-  bool fin[2];
-#pragma unroll
-  for (int sd = 0; sd < 2; ++sd) {
-    const void* src = sd ? p.new_v : p.new_k;
-    fin[sd] = true;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (p.new_dtype == KVR_BF16) x[sd][u] = (double)__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(src)[base + u]);
-      else if (p.new_dtype == KVR_F16) x[sd][u] = (double)__half2float(reinterpret_cast<const __half*>(src)[base + u]);
-      else if (p.new_dtype == KVR_F32) x[sd][u] = (double)reinterpret_cast<const float*>(src)[base + u];
-      else x[sd][u] = reinterpret_cast<const double*>(src)[base + u];
-      fin[sd] &= (bool)isfinite(x[sd][u]);
-    }
-  }
   int ci;
   uint8_t* cell = cell_of(p.pool, slot >> p.log2P, h, (int)(slot & ((1 << p.log2P) - 1)), ci);
   // the token is all-or-nothing (the reference validates the whole (H, d) K and V
   // before any write, cache.py:225-233): a NaN/Inf in any head's row leaves every
   // head's rows unwritten -- so this writer also scans the other heads' rows
-  bool all_fin = fin[0] && fin[1];
-  for (int hh = 0; hh < p.pool.H; ++hh) {
-    if (hh == h) continue;
-    const int64_t ob = ((int64_t)b * p.pool.H + hh) * 128 + 4 * lane;
+  bool all_fin = true;
+  if ((p.new_dtype == KVR_BF16 || p.new_dtype == KVR_F16) &&
+      !((reinterpret_cast<uintptr_t>(p.new_k) | reinterpret_cast<uintptr_t>(p.new_v)) & 7)) {
+    // every head's K and V quad of this lane as one batch of independent 8-byte loads (the
+    // rows may come over the bus from a pinned staging buffer: one round trip, not one per head)
+    const bool bf = p.new_dtype == KVR_BF16;
+    const uint32_t em = bf ? 0x7F80u : 0x7C00u;  // exponent all ones <=> NaN / Inf
+    const uint16_t* kq = reinterpret_cast<const uint16_t*>(p.new_k) + (int64_t)b * p.pool.H * 128 + 4 * lane;
+    const uint16_t* vq = reinterpret_cast<const uint16_t*>(p.new_v) + (int64_t)b * p.pool.H * 128 + 4 * lane;
+    for (int h0 = 0; h0 < p.pool.H; h0 += 8) {
+      uint2 wk[8], wv[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (h0 + j < p.pool.H) {
+          wk[j] = *reinterpret_cast<const uint2*>(kq + (h0 + j) * 128);
+          wv[j] = *reinterpret_cast<const uint2*>(vq + (h0 + j) * 128);
+        }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (h0 + j < p.pool.H) {
+          const uint32_t w4[4] = {wk[j].x, wk[j].y, wv[j].x, wv[j].y};
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            all_fin &= ((w4[u] & em) != em) && (((w4[u] >> 16) & em) != em);
+          if (h0 + j == h) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const uint32_t hk = (u & 1) ? (w4[u >> 1] >> 16) : (w4[u >> 1] & 0xFFFFu);
+              const uint32_t hv = (u & 1) ? (w4[2 + (u >> 1)] >> 16) : (w4[2 + (u >> 1)] & 0xFFFFu);
+              x[0][u] = bf ? (double)__uint_as_float(hk << 16) : (double)__half2float(__ushort_as_half((unsigned short)hk));
+              x[1][u] = bf ? (double)__uint_as_float(hv << 16) : (double)__half2float(__ushort_as_half((unsigned short)hv));
+            }
+          }
+        }
+    }
+  } else {
 #pragma unroll
     for (int sd = 0; sd < 2; ++sd) {
       const void* src = sd ? p.new_v : p.new_k;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        float xv;
-        if (p.new_dtype == KVR_BF16) xv = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(src)[ob + u]);
-        else if (p.new_dtype == KVR_F16) xv = __half2float(reinterpret_cast<const __half*>(src)[ob + u]);
-        else if (p.new_dtype == KVR_F32) xv = reinterpret_cast<const float*>(src)[ob + u];
-        else xv = isfinite(reinterpret_cast<const double*>(src)[ob + u]) ? 0.f : NAN;
-        all_fin &= (bool)isfinite(xv);
+        x[sd][u] = load_any(src, p.new_dtype, base + u);
+        all_fin &= (bool)isfinite(x[sd][u]);
+      }
+    }
+    for (int hh = 0; hh < p.pool.H; ++hh) {
+      if (hh == h) continue;
+      const int64_t ob = ((int64_t)b * p.pool.H + hh) * 128 + 4 * lane;
+#pragma unroll
+      for (int sd = 0; sd < 2; ++sd) {
+        const void* src = sd ? p.new_v : p.new_k;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          all_fin &= (bool)isfinite(load_any(src, p.new_dtype, ob + u));
+        }
       }
     }
   }
@@ -520,6 +555,11 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
     for (int k = 2; k < 16; ++k) p.trace[cta_id * 16 + k] = 0ull;
   }
 
+  // a host-staged query (kvr_step_ring) cannot change during this launch: its read (over the bus
+  // from pinned memory) goes out first, beside the length's, and overlaps the previous grid's tail
+  float qx[4] = {0.f, 0.f, 0.f, 0.f};
+  if (p.q_pre_wait && warp < G) load_q4(p.q, p.q_dtype, ((int64_t)b * p.nq + (int64_t)h * G + warp) * 128 + 4 * lane, qx);
+
   // ---- prologue (independent of the previous grid): split range from max_len,
   // the cell addresses of this warp's first 64 tiles, barrier init.
   // Warp w owns the groups g = w, w + DW, ... of C consecutive tiles of the split;
@@ -549,6 +589,9 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   // load per CTA, broadcast through shared memory (they may live in mapped host memory)
   int* s_len = reinterpret_cast<int*>(s_sumq + 58);
   long long* s_slot = reinterpret_cast<long long*>(s_sumq + 60);
+  // ... unless the previous grid writes them (meta_post_wait: the step ring's stage-copy kernel):
+  // then everything waits here, and no cell is requested before the wait either (pre_groups = 0)
+  if (p.meta_post_wait) pdl_wait();
   if (threadIdx.x == 0) {
     *s_len = __ldg(&p.lens[b]);
     if (APPEND) *s_slot = __ldg(&p.new_slot[b]);
@@ -634,8 +677,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   if (threadIdx.x == 0 && len_raw > p.max_len && p.flags && h == 0 && split == 0)
     atomicOr(p.flags, KVR_FLAG_LEN_OVERFLOW);
 
-  float qx[4] = {0.f, 0.f, 0.f, 0.f};
-  if (warp < G) load_q4(p.q, p.q_dtype, ((int64_t)b * p.nq + (int64_t)h * G + warp) * 128 + 4 * lane, qx);
+  if (!p.q_pre_wait && warp < G) load_q4(p.q, p.q_dtype, ((int64_t)b * p.nq + (int64_t)h * G + warp) * 128 + 4 * lane, qx);
   if (p.trace) {  // q landed
     asm volatile("" ::"f"(qx[0]), "f"(qx[1]), "f"(qx[2]), "f"(qx[3]));
     KVR_STAMP(13);
@@ -1248,6 +1290,27 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   KVR_STAMP(10);
 }
 
+// Stage-in of one serving step's host inputs (kvr_step_ring): pinned staging -> its device twin,
+// 16 B per thread.  Launched with programmatic dependent launch right after the previous step's
+// decode: the copy (the slot's last reader finished long ago) overlaps that decode, then the grid
+// waits for it, so the next decode -- chained to this grid -- still starts after the previous one.
+__global__ void __launch_bounds__(1024) stage_copy_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, int n16) {
+  // all of a thread's loads before its stores: one round trip over the bus for up to 64 KB
+  uint4 v[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int i = threadIdx.x + u * 1024;
+    if (i < n16) v[u] = src[i];
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int i = threadIdx.x + u * 1024;
+    if (i < n16) dst[i] = v[u];
+  }
+  pdl_launch_dependents();
+  pdl_wait();
+}
+
 // Split merge (K3), launched right after a split decode with programmatic
 // dependent launch: one CTA per (q head j, kv head, sequence), 512 threads =
 // 128 dims x 4 split slices.  LSE-weighted sum of the splits' (o, lse)
@@ -1608,6 +1671,24 @@ static int launch_tma(const DecodeParams& p, const Signs& sg, dim3 grid, size_t 
   return KVR_ERR_UNSUPPORTED;
 }
 
+int kvr_launch_stage_copy(void* dst, const void* src, int64_t bytes, cudaStream_t st) {
+  if ((bytes & 15) || bytes > 65536 || ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15))
+    return KVR_ERR_ARG;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(1024);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, stage_copy_kernel, reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src),
+                            (int)(bytes >> 4)) == cudaSuccess
+             ? 0
+             : KVR_ERR_CUDA;
+}
+
 static unsigned long long* g_trace = nullptr;
 void kvr_set_decode_trace(void* trace) { g_trace = reinterpret_cast<unsigned long long*>(trace); }
 
@@ -1615,8 +1696,10 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
                       const int32_t* lens, int batch, int nq, int max_len, int order, int rotate, int rot_v,
                       const Signs& s, int has, float* out, void* ws, size_t ws_bytes, int splits, cudaStream_t st,
                       const void* new_k, const void* new_v, int new_dtype, const int64_t* new_slot,
-                      uint32_t* flags) {
+                      uint32_t* flags, int q_host_staged) {
   DecodeParams p{};
+  p.q_pre_wait = q_host_staged == 1;
+  p.meta_post_wait = q_host_staged == 2;
   p.pool = pool;
   p.q = q;
   p.q_dtype = q_dtype;
@@ -1644,7 +1727,7 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
   // inline split merge for 9..32 splits
   // (pool cells read before griddepcontrol.wait are only those no preceding grid on
   // the stream writes: after a store kernel on this stream the prefetch waits)
-  p.pre_groups = kvr_take_pool_written(st) ? 0 : KVR_PREWAIT_GROUPS;
+  p.pre_groups = (kvr_take_pool_written(st) || p.meta_post_wait) ? 0 : KVR_PREWAIT_GROUPS;
   p.evict_first = KVR_EVICT_FIRST;
   p.f16x2_1024 = 0x64006400u;
   int l2 = 0;

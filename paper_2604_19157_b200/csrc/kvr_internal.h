@@ -42,9 +42,12 @@ int kvr_launch_decode(const void* q, int q_dtype, const kvr::Pool& pool, const i
                       const int32_t* lens, int batch, int nq, int max_len, int order, int rotate, int rot_v,
                       const kvr::Signs& s, int has, float* out, void* ws, size_t ws_bytes, int splits,
                       cudaStream_t st, const void* new_k = nullptr, const void* new_v = nullptr, int new_dtype = 0,
-                      const int64_t* new_slot = nullptr, uint32_t* flags = nullptr);
+                      const int64_t* new_slot = nullptr, uint32_t* flags = nullptr, int q_host_staged = 0);
+// q_host_staged: 0 plain; 1 the query is host-staged (read before the wait); 2 lengths / slot ids
+// are written by the preceding grid (read after the wait; no pre-wait cell requests)
 
 void kvr_set_decode_trace(void* trace);
+int kvr_launch_stage_copy(void* dst, const void* src, int64_t bytes, cudaStream_t st);
 void kvr_set_k1_impl(int impl);
 
 // Tensor-map encoder resolved through the runtime (no -lcuda link dependency).
