@@ -803,7 +803,8 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   const uint2* sfrag2 = reinterpret_cast<const uint2*>(sfrag);
   uint2 bq[BQ_REG ? (QK_INT8 ? NTL * 4 : 8 * NT) : 1];
   float sumq[NT], kscale[NT];
-  if (BQ_REG) {
+  // (tile warps only: the writer warp is not ordered after the query prep by barrier 1)
+  if (BQ_REG && tile_warp) {
 #pragma unroll
     for (int s = 0; s < (QK_INT8 ? NTL * 4 : 8 * NT); ++s) bq[BQ_REG ? s : 0] = sfrag2[s * 32 + lane];
   }
@@ -811,8 +812,8 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   for (int nt = 0; nt < NT; ++nt) {
     // the int8 QK yields 16 S (integer combination of the nibble planes): fold the
     // 1/16 into the query sum and the scale (powers of two: the same roundings)
-    sumq[nt] = s_sumq[4 * nt + i] * (QK_INT8 ? 16.0f : 1.0f);
-    kscale[nt] = s_ksc[4 * nt + i] * (QK_INT8 ? 0.0625f : 1.0f);
+    sumq[nt] = tile_warp ? s_sumq[4 * nt + i] * (QK_INT8 ? 16.0f : 1.0f) : 0.f;
+    kscale[nt] = tile_warp ? s_ksc[4 * nt + i] * (QK_INT8 ? 0.0625f : 1.0f) : 0.f;
   }
 
   // ---- the writer warp scores the new token (logits in log2 units)

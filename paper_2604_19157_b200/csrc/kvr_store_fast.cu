@@ -400,6 +400,7 @@ KVR_DEV void mma_tile(const uint8_t* buf, uint8_t* stage, const uint2* smask, co
       fl[rh] |= __shfl_xor_sync(0xffffffffu, fl[rh], 2);
     }
     uint32_t todo = __ballot_sync(0xffffffffu, t == 0 && (fl[0] | fl[1]) != 0u);
+    if (todo) __syncwarp();  // the lanes' staged bytes before the rows' exact rewrite
     while (todo) {
       const int src = __ffs(todo) - 1;  // lane 4 g' of row pair (g', g' + 8)
       todo &= todo - 1;
