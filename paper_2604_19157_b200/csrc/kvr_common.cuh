@@ -81,6 +81,11 @@ KVR_DEV unsigned long long sub2(unsigned long long a, unsigned long long b) {
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
+KVR_DEV unsigned long long mul2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 // fl_RM(a*b + c) elementwise: the magic-number floor (exact product-sum, one rounding)
 KVR_DEV unsigned long long fma2_rm(unsigned long long a, unsigned long long b, unsigned long long c) {
   unsigned long long r;

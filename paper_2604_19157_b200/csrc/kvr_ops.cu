@@ -202,56 +202,72 @@ __global__ void dequant_pages_kernel(Pool pool, const int32_t* bt, int bt_stride
   }
 }
 
-// Fast flatten-dequant for the serving geometry (d = 128, 16-token cells): one warp
-// per cell (16 tokens of one head); lane pair (2r, 2r+1) owns token r, 64 dims each,
-// reads 32 code bytes as two 16-B loads and writes 64 outputs as full 16-B stores
-// (a token's 128 outputs are one contiguous 256-B (bf16) / 512-B (f32) run).
+// Fast flatten-dequant for the serving geometry (d = 128, 16-token cells): four warps
+// per cell (16 tokens of one head), four tokens each; a lane owns 32 dims of one token's
+// K or V row (a token's 128 outputs are one contiguous 256-B (bf16) / 512-B (f32) run,
+// written by 4 adjacent lanes as whole 64-B groups per store instruction).
 // Arithmetic: f32 s * (q - z) (q - z exact, one rounding), then the output cast.
 template <typename TOut>
 __global__ void __launch_bounds__(256) dequant_cells_kernel(Pool pool, const int32_t* bt, int bt_stride,
                                                             const int32_t* lens, int batch, int max_len, int cps_log2,
                                                             TOut* k_out, TOut* v_out) {
   const int lane = threadIdx.x & 31;
-  const int64_t cell_id = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t wid = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int H = pool.H, ntiles = (max_len + 15) >> 4;
+  const int64_t cell_id = wid >> 2;  // four warps per cell, four tokens each
   if (cell_id >= (int64_t)batch * ntiles * H) return;
   const int head = (int)(cell_id % H);
   const int64_t bt_ = cell_id / H;
   const int tile = (int)(bt_ % ntiles), b = (int)(bt_ / ntiles);
-  const int r = lane >> 1, hf = lane & 1, t = tile * 16 + r;
+  // lane: token r of the cell, side (K | V), 32-dim quarter qt of the row
+  const int r = 4 * (int)(wid & 3) + (lane >> 3), side = (lane >> 2) & 1, qt = lane & 3, t = tile * 16 + r;
   if (t >= __ldg(&lens[b]) || t >= max_len) return;
   const int page = __ldg(&bt[(int64_t)b * bt_stride + (t >> (4 + cps_log2))]);
   const uint8_t* cell = pool.base + (int64_t)page * pool.page_bytes +
                         (int64_t)((head << cps_log2) + (tile & ((1 << cps_log2) - 1))) * pool.cell_bytes;
+  // lane qt takes code bytes 16 i + 4 qt .. + 3 of the row (dims 32 i + 8 qt .. + 7), i = 0..3: its
+  // outputs then sit at 16-B chunk qt of every 64-B group, so each store instruction of the row's four
+  // lanes writes 64 contiguous bytes (whole sectors)
+  const uint32_t* crow = reinterpret_cast<const uint32_t*>(cell + (side ? 1152 : 128) + r * 64) + qt;
+  const uint32_t w[4] = {__ldg(crow), __ldg(crow + 4), __ldg(crow + 8), __ldg(crow + 12)};
+  const float sc = __ldg(reinterpret_cast<const float*>(cell + side * 64 + r * 4));
+  const uint32_t zp = __ldg(cell + 2176 + side * 16 + r);
+  // a code c as the float 2^23 + c (nibble in the low mantissa bits), minus 2^23 + z: the exact
+  // c - z, then one f32 product by the scale (FADD2 / FMUL2 on element pairs); sentinel rows
+  // (zp 0xFF, codes 0) output their offset, held in the scale slot
+  const bool sent = zp == 0xFFu;
+  const float zf = 8388608.0f + (float)(sent ? 0u : zp);
+  const unsigned long long z2 = pk(zf, zf), s2 = pk(sc, sc);
+  float f[32];  // f[8 i + j] = dim 32 i + 8 qt + j
 #pragma unroll
-  for (int side = 0; side < 2; ++side) {
-    const uint4* src = reinterpret_cast<const uint4*>(cell + (side ? 1152 : 128) + r * 64 + hf * 32);
-    const uint4 c0 = __ldg(src), c1 = __ldg(src + 1);
-    const float sc = __ldg(reinterpret_cast<const float*>(cell + side * 64 + r * 4));
-    const uint32_t zp = __ldg(cell + 2176 + side * 16 + r);
-    const uint32_t w[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-    float f[64];
+  for (int i = 0; i < 16; ++i) {  // byte i: elements 2i (low nibble), 2i + 1 (high nibble)
+    const uint32_t byte = (w[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+    const unsigned long long x = pk(__uint_as_float(0x4B000000u | (byte & 15u)), __uint_as_float(0x4B000000u | (byte >> 4)));
+    const unsigned long long y = mul2(sub2(x, z2), s2);
+    upk(y, f[2 * i], f[2 * i + 1]);
+  }
+  if (sent) {
 #pragma unroll
-    for (int i = 0; i < 64; ++i) {
-      const float q = (float)((w[i >> 3] >> (4 * (i & 7))) & 15u);
-      f[i] = zp == 0xFFu ? sc : sc * (q - (float)zp);
-    }
-    TOut* dst = (side ? v_out : k_out) + (((int64_t)b * max_len + t) * H + head) * 128 + hf * 64;
-    if constexpr (sizeof(TOut) == 2) {
+    for (int i = 0; i < 32; ++i) f[i] = sc;
+  }
+  TOut* dst = (side ? v_out : k_out) + (((int64_t)b * max_len + t) * H + head) * 128 + qt * 8;
+  if constexpr (sizeof(TOut) == 2) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        uint32_t u[4];
+    for (int i = 0; i < 4; ++i) {
+      uint32_t u[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const __nv_bfloat162 h2 = __floats2bfloat162_rn(f[8 * i + 2 * k], f[8 * i + 2 * k + 1]);
-          u[k] = *reinterpret_cast<const uint32_t*>(&h2);
-        }
-        reinterpret_cast<uint4*>(dst)[i] = make_uint4(u[0], u[1], u[2], u[3]);
+      for (int k = 0; k < 4; ++k) {
+        const __nv_bfloat162 h2 = __floats2bfloat162_rn(f[8 * i + 2 * k], f[8 * i + 2 * k + 1]);
+        u[k] = *reinterpret_cast<const uint32_t*>(&h2);
       }
-    } else {
+      *reinterpret_cast<uint4*>(dst + 32 * i) = make_uint4(u[0], u[1], u[2], u[3]);
+    }
+  } else {
 #pragma unroll
-      for (int i = 0; i < 16; ++i)
-        reinterpret_cast<float4*>(dst)[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
+    for (int i = 0; i < 4; ++i) {
+      float4* d4 = reinterpret_cast<float4*>(dst + 32 * i);
+      d4[0] = make_float4(f[8 * i], f[8 * i + 1], f[8 * i + 2], f[8 * i + 3]);
+      d4[1] = make_float4(f[8 * i + 4], f[8 * i + 5], f[8 * i + 6], f[8 * i + 7]);
     }
   }
 }
@@ -534,7 +550,7 @@ int kvr_launch_dequant_pages(const Pool& pool, const int32_t* bt, int bt_stride,
                     ((reinterpret_cast<uintptr_t>(k_out) | reinterpret_cast<uintptr_t>(v_out)) & 15) == 0;
   if (fast && (out_dtype == KVR_BF16 || out_dtype == KVR_F32)) {
     const int64_t cells = (int64_t)batch * ((max_len + 15) / 16) * pool.H;
-    const int g = (int)((cells + 7) / 8);
+    const int g = (int)((cells * 4 + 7) / 8);  // four warps per cell, eight warps per block
     if (out_dtype == KVR_BF16)
       dequant_cells_kernel<__nv_bfloat16><<<g, 256, 0, st>>>(pool, bt, bt_stride, lens, batch, max_len, cl,
                                                               (__nv_bfloat16*)k_out, (__nv_bfloat16*)v_out);
