@@ -270,6 +270,8 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- the other BASELINE configs (parity-test cases, reported in `detail`)
     c1 = c1_quantize_store(torch, layout, spec, dev, gen, timed)
+    c2v = c2_variants(torch, layout, spec, dev, gen, timed)
+    print(f"[bench] C2 variants {c2v}", file=sys.stderr, flush=True)
     print(f"[bench] C1 K1 rot {c1['rot_us']} us plain {c1['plain_us']} (tcgen05 {c1['tcgen05_rot_us']} / "
           f"{c1['tcgen05_plain_us']}); 65536 tok rot {c1['write_65536_tokens']['rot_us']} plain "
           f"{c1['write_65536_tokens']['plain_us']} (mma.sync {c1['write_65536_tokens']['mma_sync_rot_us']}); "
@@ -331,6 +333,7 @@ def run_ours(args, rank, world, local_rank):
             "fused_step_us": round(t_fr * 1e3, 3), "fused_step_plain_us": round(t_fp * 1e3, 3),
             "fused_step_overhead_vs_plain": round(t_fr / t_fp - 1.0, 4),
             "c1_quantize_store": c1,
+            "c2_input_variants": c2v,
             "c3_concurrency_sweep": c3,
             "c4_llama70b": c4,
             "c5_long_context_1kv_per_gpu": c5,
@@ -418,6 +421,67 @@ def decode_case(torch, dev, tables, spec, timed, fused=False, n=256, gen=None):
             "GBps": round(byts / (t_rot * 1e-3) / 1e9, 1), "frac": round(byts / (t_rot * 1e-3) / 1e9 / peak, 4),
             "overhead_vs_plain": round(t_rot / t_pl - 1.0, 4), "tok_per_s": round(B / (t_rot * 1e-3), 1),
             "l2": f"{R} rotating table(s) of {byts / 1e6:.0f} MB"}
+
+
+def kv_profile(torch, kind, n, Hh, Dd, gen, dev):
+    """K/V rows (bf16) of the reference harness's profiles (harness.py:82-176), generated on
+    the device: 'outlier' -- Rademacher bulk with one fixed +-27 hot channel per head;
+    'correlated' -- Student-t(4)/sqrt(2) rows through a dense rank-4 mixing, two x100 channels."""
+    if kind == "outlier":
+        x = torch.where(torch.rand((n, Hh, Dd), generator=gen, device=dev) < 0.5, -1.0, 1.0)
+        ch = torch.randint(0, Dd, (Hh,), generator=gen, device=dev)
+        sgn = torch.where(torch.rand((n, Hh), generator=gen, device=dev) < 0.5, -27.0, 27.0)
+        x[:, torch.arange(Hh, device=dev), ch] = sgn
+    else:
+        z = torch.randn((n, Hh, Dd), generator=gen, device=dev)
+        chi = sum(torch.randn((n, Hh, 1), generator=gen, device=dev) ** 2 for _ in range(4)) / 4.0
+        x = z / chi.sqrt() / 2.0 ** 0.5
+        a = torch.randn((Dd, 4), generator=gen, device=dev)
+        b = torch.randn((4, Dd), generator=gen, device=dev)
+        mix = torch.eye(Dd, device=dev) + (0.75 / (4 * Dd) ** 0.5) * (a @ b)
+        x = x @ mix.T
+        ch = torch.randperm(Dd, generator=gen, device=dev)[:2]
+        x[:, :, ch] *= 100.0
+    return x.to(torch.bfloat16)
+
+
+def c2_variants(torch, layout, spec, dev, gen, timed):
+    """the C2 fused step on the harness's outlier and correlated K/V
+    profiles, and on a pool whose pages are randomly permuted (block tables point all over
+    the pool instead of in allocation order)."""
+    from paper_2604_19157_b200 import PageTable
+
+    P, Hh, Dd, L = layout.page_tokens, layout.num_kv_heads, layout.head_dim, CTX
+    res = {}
+    for kind in ("outlier", "correlated", "gaussian_shuffled_pages"):
+        tables = []
+        for _ in range(4):
+            t = PageTable(layout, num_pages=-(-(L + 1) // P) + 1, device=dev)
+            t.create_sequence(0)
+            slots = torch.from_numpy(t.alloc.reserve(0, L)).to(dev)
+            for c0 in range(0, L, 8192):
+                n = min(8192, L - c0)
+                if kind == "gaussian_shuffled_pages":
+                    k = torch.randn((n, Hh, Dd), generator=gen, device=dev).to(torch.bfloat16)
+                    v = torch.randn((n, Hh, Dd), generator=gen, device=dev).to(torch.bfloat16)
+                else:
+                    k, v = kv_profile(torch, kind, n, Hh, Dd, gen, dev), kv_profile(torch, kind, n, Hh, Dd, gen, dev)
+                t.store_slots(k, v, slots[c0:c0 + n], spec)
+            if kind == "gaussian_shuffled_pages":  # move every page to a random physical place
+                pages = t.alloc.seq_pages[0]
+                perm = torch.randperm(t.num_pages, generator=gen, device=dev)
+                new = t.pool.clone()
+                new[perm[torch.tensor(pages, device=dev)]] = t.pool[torch.tensor(pages, device=dev)]
+                t.pool.copy_(new)
+                t.alloc.seq_pages[0] = [int(x) for x in perm[torch.tensor(pages, device=dev)].cpu()]
+                used = set(t.alloc.seq_pages[0])
+                t.alloc.free = sorted(p for p in range(t.num_pages) if p not in used)
+            tables.append(t)
+        r = decode_case(torch, dev, tables, spec, timed, fused=True, n=256, gen=gen)
+        res[kind] = {"us": r["us"], "plain_us": r["plain_us"], "frac": r["frac"],
+                     "overhead_vs_plain": r["overhead_vs_plain"]}
+        del tables
+    return res
 
 
 def c3_sweep(torch, dev, gen, timed):
