@@ -626,7 +626,7 @@ class PageTable:
             self._ws_cnt = 0
         # the split counters sit at the start of the workspace and are left at
         # zero by every launch; bytes first used as counters are zeroed once here
-        cnt = (batch * self.layout.num_kv_heads * 4 + 255) // 256 * 256
+        cnt = (batch * self.layout.num_kv_heads * 4 * 9 + 255) // 256 * 256  # counters + merge epochs
         if cnt > self._ws_cnt:
             self._ws[:cnt].zero_()
             self._ws_cnt = cnt

@@ -58,6 +58,12 @@ struct DecodeParams {
   int pre_groups;    // ring groups per warp requested before griddepcontrol.wait
   int evict_first;   // KV cells are streamed with an L2 evict-first policy
   int merge_inline;  // splits > 1 without a cluster: the last CTA merges (ws_cnt counters)
+  // flag-in-data split merge (the grid is one wave): every split stores its (o, lse) as 64-bit
+  // words (value bits | epoch + 1) with relaxed stores; CTA j < G polls the words of q head j
+  int merge_ll;
+  uint32_t* ws_epoch;             // [B][H][8] epochs, bumped by each head's merger
+  unsigned long long* ll_lse;     // [B][H][8][32]
+  unsigned long long* ll_o;       // [B][H][8][32][128]
   int q_pre_wait;       // the query is host-staged for this launch (immutable): load it before the wait
   int meta_post_wait;   // lengths / slot ids come from the previous grid: read them after the wait
   uint32_t f16x2_1024;  // 0x64006400 (fp16x2 1024.0) from the parameter bank: an opaque operand lets
@@ -372,6 +378,15 @@ KVR_DEV bool append_rows_exact(const DecodeParams& p, const Signs& sg, int b, in
   return ok;
 }
 
+KVR_DEV void st_relaxed_u64(unsigned long long* a, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+KVR_DEV unsigned long long ld_relaxed_u64(const unsigned long long* a) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+  return v;
+}
+
 // named barriers (id 0 is __syncthreads): 1 = the tile warps after query prep,
 // 2 = query-prep warps -> writer warp (rotated q in smem for scoring the new token)
 KVR_DEV void named_bar_sync(int id, int threads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory"); }
@@ -437,6 +452,9 @@ constexpr int RING_CELLS = 4;    // cells in flight per warp (NSTG stages of C c
 #endif
 #ifndef KVR_CLUSTER_MAX
 #define KVR_CLUSTER_MAX 8
+#endif
+#ifndef KVR_MERGE_LL
+#define KVR_MERGE_LL 1
 #endif
 constexpr int MAX_SPLITS = 256;
 constexpr int MERGE_INLINE_MAX = 32;  // up to this many splits the last CTA merges them inline
@@ -664,6 +682,8 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
 
   pdl_wait();  // q, the new token, the workspace and recent pages may come from the previous grid
   pdl_launch_dependents();
+  uint32_t* s_ep = reinterpret_cast<uint32_t*>(s_sumq + 16);  // [8] merge epochs of this (sequence, kv head)
+  if (p.merge_ll && threadIdx.x < 8) s_ep[threadIdx.x] = p.ws_epoch[((int64_t)b * H + h) * 8 + threadIdx.x];
   KVR_STAMP(11);  // past the grid-dependency wait
   // ---- the writer warp (no tiles of its own) quantizes + stores the new token's K
   // and V rows bit-exactly (f64, reference arithmetic) right away, overlapping the
@@ -1174,6 +1194,11 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
     if (p.splits == 1 || CL) {
       obuf[j * 128 + dd] = o;
       if (CL && pp == 0) s_lse[j] = lse;
+    } else if (p.merge_ll) {
+      const int64_t hj = (((int64_t)b * H + h) * 8 + j) * 32 + split;
+      const unsigned long long tag = (unsigned long long)(s_ep[j] + 1u) << 32;
+      st_relaxed_u64(p.ll_o + hj * 128 + dd, tag | __float_as_uint(o));
+      if (pp == 0) st_relaxed_u64(p.ll_lse + hj, tag | __float_as_uint(lse));
     } else {
       __stcg(&p.ws_o[(hbase + (int64_t)split * 8 + j) * 128 + dd], o);
       if (pp == 0) __stcg(&p.ws_lse[hbase + (int64_t)split * 8 + j], lse);
@@ -1221,6 +1246,80 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   }
   if (p.splits > 1 && !p.merge_inline) {  // the partial is final: decode_merge_kernel (next in the stream) merges
     KVR_STAMP(6);
+    return;
+  }
+  if (p.merge_ll) {
+    // ---- flag-in-data split merge: CTA j < G merges q head j.  No fence, no counter: each
+    // 64-bit word carries its split's epoch tag, and the merger's threads poll (split, 4 dims)
+    // words until every tag is this launch's (the whole grid is resident: one wave).
+    const int S = p.splits, j = split;
+    if (j >= G) return;
+    __syncthreads();  // the rings / reduction space are free; this CTA's own words are out
+    const uint32_t want = s_ep[j] + 1u;
+    const int64_t hj = (((int64_t)b * H + h) * 8 + j) * 32;
+    float* so = reinterpret_cast<float*>(sm);  // [S][128]
+    float* sl = so + 32 * 128;                 // [S]
+
+#pragma unroll 1
+    for (int k = threadIdx.x; k < S * 33; k += blockDim.x) {
+      if (k < S * 32) {
+        const int sp = k >> 5, l = k & 31;
+        const unsigned long long* a = p.ll_o + (hj + sp) * 128 + 4 * l;
+        unsigned long long v0, v1, v2, v3;
+        do {
+          v0 = ld_relaxed_u64(a);
+          v1 = ld_relaxed_u64(a + 1);
+          v2 = ld_relaxed_u64(a + 2);
+          v3 = ld_relaxed_u64(a + 3);
+        } while ((uint32_t)(v0 >> 32) != want || (uint32_t)(v1 >> 32) != want || (uint32_t)(v2 >> 32) != want ||
+                 (uint32_t)(v3 >> 32) != want);
+        *reinterpret_cast<float4*>(so + sp * 128 + 4 * l) =
+            make_float4(__uint_as_float((uint32_t)v0), __uint_as_float((uint32_t)v1), __uint_as_float((uint32_t)v2),
+                        __uint_as_float((uint32_t)v3));
+      } else {
+        const int sp = k - S * 32;
+        unsigned long long v;
+        do {
+          v = ld_relaxed_u64(p.ll_lse + hj + sp);
+        } while ((uint32_t)(v >> 32) != want);
+        sl[sp] = __uint_as_float((uint32_t)v);
+      }
+    }
+    __syncthreads();
+    KVR_STAMP(7);  // merge inputs landed
+    if (warp == 0) {
+      // lane l: dims 4l..4l+3 of q head j, the S partials LSE-weighted in one pass (no shuffles)
+      // (S <= 32: a fixed trip count of independent pairs keeps the chains short)
+      float m2[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+      for (int sp = 0; sp < 32; ++sp)
+        if (sp < S) m2[sp & 1] = fmaxf(m2[sp & 1], sl[sp]);
+      const float mx = fmaxf(m2[0], m2[1]);
+      float tot[2] = {0.f, 0.f}, o4[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      if (mx != -INFINITY) {
+#pragma unroll 4
+        for (int sp = 0; sp < S; ++sp) {
+          const float l = sl[sp];
+          const float w = (l == -INFINITY) ? 0.f : ex2f(l - mx);
+          const float4 v = *reinterpret_cast<const float4*>(so + sp * 128 + 4 * lane);
+          const int e = sp & 1;
+          tot[e] += w;
+          o4[e][0] = fmaf(w, v.x, o4[e][0]);
+          o4[e][1] = fmaf(w, v.y, o4[e][1]);
+          o4[e][2] = fmaf(w, v.z, o4[e][2]);
+          o4[e][3] = fmaf(w, v.w, o4[e][3]);
+        }
+      }
+      const float tt = tot[0] + tot[1];
+      const float inv = tt > 0.f ? 1.0f / tt : 0.f;
+      *reinterpret_cast<float4*>(obuf + 4 * lane) =
+          make_float4((o4[0][0] + o4[1][0]) * inv, (o4[0][1] + o4[1][1]) * inv, (o4[0][2] + o4[1][2]) * inv,
+                      (o4[0][3] + o4[1][3]) * inv);
+      __syncwarp();
+      emit_head<ORDER>(p, sgw, b, h, j, obuf, lane);
+    }
+    if (threadIdx.x == 0) p.ws_epoch[((int64_t)b * H + h) * 8 + j] = want;  // read again only by the next launch
+    KVR_STAMP(9);  // merged + stored
     return;
   }
   if (p.splits > 1) {
@@ -1534,13 +1633,22 @@ using namespace kvr;
 // Workspace: split counters u32[B][H] first (padded to 256 B, so a workspace reused
 // with another split count still finds them at zero), then lse f32[B][H][S][8],
 // then o f32[B][H][S][8][128].
-static size_t ws_cnt_bytes(int batch, int H) { return ((size_t)batch * H * sizeof(uint32_t) + 255) & ~size_t(255); }
+// (counters u32[B][H] | merge epochs u32[B][H][8]) -- zeroed once by the owner, left consistent by
+// every launch -- padded to 256 B
+static size_t ws_cnt_bytes(int batch, int H) { return ((size_t)batch * H * 9 * sizeof(uint32_t) + 255) & ~size_t(255); }
+// the flag-in-data merge's words: split-count independent slots [B][H][8][32] lse and [.][128] o
+static bool ws_has_ll(int batch, int H, int splits) {
+  return splits > 8 && splits <= MERGE_INLINE_MAX && (long)batch * H * splits <= 256;
+}
+static size_t ws_ll_bytes(int batch, int H) { return (size_t)batch * H * 8 * 32 * 129 * sizeof(unsigned long long); }
 size_t kvr_decode_ws_bytes(int batch, int H, int nq, int d, int splits) {
   (void)nq;
   (void)d;
   if (splits < 1) splits = 1;
   const size_t units = (size_t)batch * H * splits * 8;
   size_t bytes = ws_cnt_bytes(batch, H) + units * sizeof(float) + units * 128 * sizeof(float);
+  bytes = (bytes + 255) & ~size_t(255);
+  if (ws_has_ll(batch, H, splits)) bytes += ws_ll_bytes(batch, H);
   return (bytes + 255) & ~size_t(255);
 }
 
@@ -1747,8 +1855,14 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
     p.splits = splits;
     const size_t units = (size_t)batch * pool.H * splits * 8;
     p.ws_cnt = reinterpret_cast<uint32_t*>(ws);
+    p.ws_epoch = p.ws_cnt + (size_t)batch * pool.H;
     p.ws_lse = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + ws_cnt_bytes(batch, pool.H));
     p.ws_o = p.ws_lse + units;
+    {
+      const size_t base = (ws_cnt_bytes(batch, pool.H) + units * sizeof(float) * 129 + 255) & ~size_t(255);
+      p.ll_lse = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(ws) + base);
+      p.ll_o = p.ll_lse + (size_t)batch * pool.H * 8 * 32;
+    }
     dim3 grid(pool.H, splits, batch);
     const int ord = rotate ? order : 128;
     const size_t smem = decode_smem_bytes();
@@ -1763,6 +1877,9 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
     p.use_cluster = 0;
 #endif
     p.merge_inline = KVR_MERGE_INLINE && !p.use_cluster && splits > 1 && splits <= MERGE_INLINE_MAX;
+    // flag-in-data merge when the grid is one wave (the merger CTAs spin on the others' words)
+    p.merge_ll = KVR_MERGE_LL && p.merge_inline && ws_has_ll(batch, pool.H, splits) &&
+                 (long)batch * pool.H * splits <= (kvr_num_sms() > 0 ? kvr_num_sms() : 148) && p.G <= 8;
     if (new_slot)
       return p.G == 8 ? launch_tma<2, true>(p, sg, grid, smem, ord, st) : launch_tma<1, true>(p, sg, grid, smem, ord, st);
     return p.G == 8 ? launch_tma<2, false>(p, sg, grid, smem, ord, st) : launch_tma<1, false>(p, sg, grid, smem, ord, st);

@@ -53,8 +53,8 @@ def run(plan, k):
 
 
 out_lines = []
-names = {11: "past wait", 14: "wr rows landed", 15: "wr rotated", 8: "wr append done", 13: "q landed", 12: "q prep done", 2: "loop start", 3: "loop end", 4: "M published", 5: "warp partials", 6: "partial stored", 7: "merge in",
-         9: "merged", 10: "exit"}
+names = {11: "past wait", 14: "wr rows landed", 15: "wr rotated", 8: "wr append done", 13: "q landed", 12: "q prep done", 2: "loop start", 3: "loop end", 4: "M published", 5: "warp partials", 6: "partial stored / split weights", 7: "merge in",
+         10: "exit / merged in smem", 9: "merged"}
 MHZ = float(os.environ.get("SM_MHZ", "1965"))
 lib = _lib.lib()
 for splits in split_list:
