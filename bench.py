@@ -195,8 +195,48 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         return g
 
+    def timed_in_graph(fn, count):
+        """Device time of `count` calls of fn inside ONE graph that also holds the timing events
+        (recorded as graph nodes) after one untimed step: the graph's own launch is outside the
+        window and the first timed step has a predecessor to overlap with, as in steady state."""
+        import ctypes as _ct
+        from paper_2604_19157_b200 import _kernels as _K
+        rt = _K._cudart()
+        rt.cudaEventRecordWithFlags.argtypes = [_ct.c_void_p, _ct.c_void_p, _ct.c_uint]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        e1.record()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        stream = torch.cuda.Stream()
+        stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(stream):
+            for i in range(2):
+                fn(i)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=stream):
+                fn(count)  # untimed predecessor
+                rt.cudaEventRecordWithFlags(e0.cuda_event, stream.cuda_stream, 1)  # cudaEventRecordExternal
+                for i in range(count):
+                    fn(i)
+                rt.cudaEventRecordWithFlags(e1.cuda_event, stream.cuda_stream, 1)
+        torch.cuda.current_stream().wait_stream(stream)
+        torch.cuda.synchronize()
+        # the window holds exactly `count` steps; it is replayed 5 times and the median reported
+        # (one short window alone is at the mercy of a single clock / scheduling hiccup)
+        samples = []
+        for _ in range(5):
+            if world > 1:
+                torch.distributed.barrier()
+            g.replay()
+            torch.cuda.synchronize()
+            samples.append(e0.elapsed_time(e1))
+        return max_over_ranks(float(np.median(samples)), dev)
+
     def timed(fn, count, chunk_steps=256):
         """Device time of `count` calls of fn (replayed from CUDA graphs), max over ranks."""
+        if count < chunk_steps:
+            return timed_in_graph(fn, count)
         n_full, rem = divmod(count, chunk_steps)
         gf = graph_of(fn, chunk_steps) if n_full else None
         gr = graph_of(fn, rem) if rem else None
@@ -221,6 +261,11 @@ def run_ours(args, rank, world, local_rank):
         step(i)
     torch.cuda.synchronize()
     with ClockSampler(local_rank) as clk:
+        # untimed: bring clocks and the launch path to steady state (~0.2 s of steps) so a short
+        # K measures the same per-step time as a long one
+        t0 = time.time()
+        while time.time() - t0 < 0.2:
+            timed(step, 256)
         ms = timed(step, args.steps)
         # keep the sampler fed while it is running: repeat a short loop for >= 0.5 s
         t0 = time.time()
