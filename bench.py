@@ -321,7 +321,7 @@ def run_ours(args, rank, world, local_rank):
           f"{c1['tcgen05_plain_us']}); 65536 tok rot {c1['write_65536_tokens']['rot_us']} plain "
           f"{c1['write_65536_tokens']['plain_us']} (mma.sync {c1['write_65536_tokens']['mma_sync_rot_us']}); "
           f"K4 {c1['dequant_us']} us", file=sys.stderr, flush=True)
-    c3 = c4 = c5 = None
+    c3 = c4 = c5 = bf = None
     if not args.quick:
         sets.clear()  # free the headline's buffers first
         torch.cuda.empty_cache()
@@ -331,6 +331,8 @@ def run_ours(args, rank, world, local_rank):
         print(f"[bench] C5 {[(r['ctx'], r['rot_order'], r['us'], r['frac']) for r in c5]}", file=sys.stderr, flush=True)
         c4 = c4_llama70b(torch, dev, gen, timed, world, rank)
         print(f"[bench] C4 step {c4['step_us']} us, {c4['tok_per_s_per_gpu']} tok/s/GPU", file=sys.stderr, flush=True)
+        bf = bf16_pool_decode(torch, dev, gen, timed, round(t_k2 * 1e3, 3), c3[1]["us"] if len(c3) > 1 else None)
+        print(f"[bench] BF16 pool decode {bf}", file=sys.stderr, flush=True)
 
     cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu:  # the CPU legs: rank 0 at N = 1 only, after timing
@@ -382,6 +384,7 @@ def run_ours(args, rank, world, local_rank):
             "c3_concurrency_sweep": c3,
             "c4_llama70b": c4,
             "c5_long_context_1kv_per_gpu": c5,
+            "bf16_pool_decode": bf,
         },
     }
     print(json.dumps(line), flush=True)
@@ -526,6 +529,41 @@ def c2_variants(torch, layout, spec, dev, gen, timed):
         res[kind] = {"us": r["us"], "plain_us": r["plain_us"], "frac": r["frac"],
                      "overhead_vs_plain": r["overhead_vs_plain"]}
         del tables
+    return res
+
+
+def bf16_pool_decode(torch, dev, gen, timed, int4_c2_us, int4_c3_b16_us):
+    """the BF16 baseline pool (raw bf16 rows, cache.py:115-118) decoded by the
+    tensor-core BF16 kernel at the C2 shape and at C3 B = 16 x 8k, beside the INT4 decode."""
+    from paper_2604_19157_b200 import DecodePlan, HeadLayout, PageTable
+    from paper_2604_19157_b200.cache import BF16
+
+    lay = HeadLayout(num_q_heads=NQ, num_kv_heads=H, head_dim=D, rot_order=ORDER, page_tokens=P)
+    res = {}
+    peak, _ = hbm_peak()
+    for name, B, L, int4_us in (("c2_b1_32k", 1, CTX, int4_c2_us), ("c3_b16_8k", 16, 8192, int4_c3_b16_us)):
+        R = max(2, -(-300_000_000 // (B * L * H * D * 4)))  # > 2x L2 of rotating tables
+        tables = []
+        for _ in range(R):
+            t = PageTable(lay, precision=BF16, num_pages=B * (-(-L // P)), device=dev)
+            for b in range(B):
+                t.create_sequence(b)
+                sl = torch.from_numpy(t.alloc.reserve(b, L)).to(dev)
+                for c0 in range(0, L, 8192):
+                    n = min(8192, L - c0)
+                    t.store_slots(torch.randn((n, H, D), generator=gen, device=dev).to(torch.bfloat16),
+                                  torch.randn((n, H, D), generator=gen, device=dev).to(torch.bfloat16), sl[c0:c0 + n], None)
+            tables.append(t)
+        plans = [DecodePlan(t, list(range(B))) for t in tables]
+        q = torch.randn((B, NQ, D), generator=gen, device=dev).to(torch.bfloat16)
+        outs = [torch.empty((B, NQ, D), dtype=torch.float32, device=dev) for _ in tables]
+        us = timed(lambda i: plans[i % R].run(q, None, out=outs[i % R]), 256) / 256 * 1e3
+        byts = B * (L * H * D * 4 + -(-L // P) * 4 + NQ * D * (2 + 4))
+        res[name] = {"us": round(us, 3), "GBps": round(byts / (us * 1e-6) / 1e9, 1),
+                     "frac": round(byts / (us * 1e-6) / 1e9 / peak, 4), "splits": plans[0].splits,
+                     "int4_decode_us": int4_us, "int4_speedup": round(us / int4_us, 3) if int4_us else None,
+                     "kernel": "decode_bf16_kernel (mma.sync bf16, SW128 TMA cells, split-K)"}
+        del tables, plans
     return res
 
 

@@ -27,6 +27,8 @@
 //    operand with movmatrix.trans (no shared memory round trip);
 //  * per-split (lse, o) partials go to a workspace; the last CTA of a
 //    (sequence, kv head) merges them and applies the inverse rotation.
+#include <cstdlib>
+
 #include "kvr_common.cuh"
 #include "kvr_internal.h"
 
@@ -1390,6 +1392,255 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   KVR_STAMP(10);
 }
 
+// ---------------------------------------------------------------------------
+// BF16-pool decode (the reference's BF16 baseline pool: raw bf16 K / V rows, no rotation,
+// cache.py:115-118, attention.py:67-71) -- the comparison point for the INT4 kernel.
+// A 16-token cell of one head is 32 rows of 256 B (16 K | 16 V).  Grid (kv head, split,
+// sequence), 8 warps; each warp streams its cells as two SW128 TMA boxes (the pool viewed
+// as a 2-D tensor of 256-B rows) through a 2-stage ring, and per cell runs
+//   S = K q on mma.sync m16n8k16 bf16 (K fragments by ldmatrix from the swizzled tile,
+//       q split hi + lo bf16 in the columns of an 8-wide tile),
+//   an online softmax in log2 units,
+//   O^T += V^T P (V^T fragments by ldmatrix.trans, P hi + lo bf16 via movmatrix),
+// then the CTA merge and, with splits, decode_merge_kernel (no inverse rotation).
+namespace bfd {
+constexpr int NW = 8;
+constexpr int TILE = 8192;
+constexpr int NSTG = 2;
+constexpr int OFF_BARS = NW * NSTG * TILE;  // 128 KB of rings
+constexpr int SM_M = OFF_BARS + 256;        // [NW][8] reference points
+constexpr int SM_L = SM_M + NW * 8 * 4;    // [NW][8] softmax sums
+constexpr int SM_RED = SM_L + NW * 8 * 4;  // [NW][8][128] partials
+constexpr int SM_MSTAR = SM_RED + NW * 8 * 128 * 4;
+constexpr int SM_TOTAL = SM_MSTAR + 64 + 1024;
+}  // namespace bfd
+
+KVR_DEV void ldsm_x4_u(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+KVR_DEV void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+KVR_DEV void mma_bf16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+KVR_DEV uint32_t pack_bf2(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+// hi + lo bf16 split of x: (bf16(x), bf16(x - bf16(x)))
+KVR_DEV void split_bf(float x, float& hi, float& lo) {
+  hi = __bfloat162float(__float2bfloat16_rn(x));
+  lo = x - hi;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(bfd::NW * 32, 1)
+    decode_bf16_kernel(const __grid_constant__ DecodeParams p, const __grid_constant__ CUtensorMap map) {
+  using namespace bfd;
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = sm_raw + ((1024u - (smem_u32(sm_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + OFF_BARS);
+  float* s_m = reinterpret_cast<float*>(sm + SM_M);
+  float* s_lw = reinterpret_cast<float*>(sm + SM_L);
+  float* sred = reinterpret_cast<float*>(sm + SM_RED);
+  float* s_mstar = reinterpret_cast<float*>(sm + SM_MSTAR);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = lane >> 2, i = lane & 3;
+  const int h = blockIdx.x, split = blockIdx.y, b = blockIdx.z;
+  const int G = p.G, H = p.pool.H;
+  if (threadIdx.x < NW * NSTG) mbar_init(&bars[threadIdx.x], 1);
+  fence_mbar_init();
+  if (threadIdx.x == 0) prefetch_tensormap(&map);
+  __syncthreads();
+  pdl_wait();
+  pdl_launch_dependents();
+
+  const int len = min(__ldg(&p.lens[b]), p.max_len);
+  const int n_tiles = (len + 15) >> 4;
+  const int per = (((p.max_len + 15) >> 4) + p.splits - 1) / p.splits;
+  const int lo = min(n_tiles, split * per), hi = min(n_tiles, lo + per);
+  const int my = hi - lo - warp > 0 ? (hi - lo - warp + NW - 1) / NW : 0;
+  const int32_t* btrow = p.bt + (int64_t)b * p.bt_stride;
+  const int cpp = p.pool.P >> 4;  // cells of a head per page
+  uint8_t* ring = sm + warp * NSTG * TILE;
+  uint64_t* bw = bars + warp * NSTG;
+  auto issue = [&](int k) {
+    if (elect_one()) {
+      const int t = lo + warp + k * NW;
+      const int page = __ldg(&btrow[t / cpp]);
+      const int64_t row = ((int64_t)page * p.pool.page_bytes + (int64_t)(h * cpp + t % cpp) * p.pool.cell_bytes) >> 8;
+      uint8_t* dst = ring + (k % NSTG) * TILE;
+      mbar_expect_tx(&bw[k % NSTG], TILE);
+      tma_load_2d(dst, &map, &bw[k % NSTG], 0, (int32_t)row);
+      tma_load_2d(dst + TILE / 2, &map, &bw[k % NSTG], 64, (int32_t)row);
+    }
+    __syncwarp();
+  };
+  for (int k = 0; k < NSTG && k < my; ++k) issue(k);
+
+  // q as the B operand: column n = lane >> 2 of tile nt is (head 4 nt + n / 2, hi | lo); the
+  // 1/sqrt(d) and log2(e) are applied to S
+  uint32_t qb[NT][8][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int head = 4 * nt + (r >> 1);
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        float v[2] = {0.f, 0.f};
+        if (head < G) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+            v[u] = load_q(p.q, p.q_dtype, ((int64_t)b * p.nq + (int64_t)h * G + head) * 128 + 16 * ks + 8 * hf + 2 * i + u);
+        }
+        float h0, l0, h1, l1;
+        split_bf(v[0], h0, l0);
+        split_bf(v[1], h1, l1);
+        qb[nt][ks][hf] = (r & 1) ? pack_bf2(l0, l1) : pack_bf2(h0, h1);
+      }
+  }
+  const float qk = LOG2E * (float)(1.0 / sqrt(128.0));
+  float M[NT], lsum[NT], acc[NT][8][4];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    M[nt] = -INFINITY;
+    lsum[nt] = 0.f;
+#pragma unroll
+    for (int m = 0; m < 8; ++m)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[nt][m][c] = 0.f;
+  }
+  const int arow = (lane & 7) + 8 * ((lane >> 3) & 1), acol = lane >> 4;  // K: ldmatrix.x4 lane -> (token, chunk)
+  const int vrow = (lane & 7) + 8 * (lane >> 4), vcol = (lane >> 3) & 1;  // V: ldmatrix.x4.trans
+#pragma unroll 1
+  for (int k = 0; k < my; ++k) {
+    const int st = k % NSTG;
+    mbar_wait(&bw[st], (k / NSTG) & 1);
+    const uint8_t* tile = ring + st * TILE;
+    const uint32_t tb = smem_u32(tile);
+    const int t0 = (lo + warp + k * NW) * 16;
+    if (t0 + 16 > len) {  // the last, partial cell: zero the V rows past the length (stale slots)
+      for (int x = lane; x < 16 * 16; x += 32) {
+        const int tok = x >> 4, c = x & 15;
+        if (t0 + tok >= len)
+          *reinterpret_cast<uint4*>(const_cast<uint8_t*>(tile) + (c >> 3) * (TILE / 2) + (16 + tok) * 128 +
+                                    (((c & 7) ^ ((16 + tok) & 7)) << 4)) = make_uint4(0u, 0u, 0u, 0u);
+      }
+      __syncwarp();
+    }
+    // ---- S = K q
+    float sa[NT][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) sa[nt][c] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const int ch = 2 * ks + acol;
+      uint32_t a[4];
+      ldsm_x4_u(tb + (ch >> 3) * (TILE / 2) + arow * 128 + (((ch & 7) ^ (arow & 7)) << 4), a);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) mma_bf16(sa[nt], a, qb[nt][ks][0], qb[nt][ks][1]);
+    }
+    // ---- online softmax (lane: tokens r, r + 8 of head 4 nt + i)
+    float p0[NT], p1[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      float l0 = (sa[nt][0] + sa[nt][1]) * qk, l1 = (sa[nt][2] + sa[nt][3]) * qk;
+      if (t0 + r >= len) l0 = -INFINITY;
+      if (t0 + r + 8 >= len) l1 = -INFINITY;
+      float mx = fmaxf(l0, l1);
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+      if (mx > M[nt]) {
+        const float alpha = (M[nt] == -INFINITY) ? 0.f : ex2f(M[nt] - mx);
+        lsum[nt] *= alpha;
+#pragma unroll
+        for (int m = 0; m < 8; ++m)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[nt][m][c] *= alpha;
+        M[nt] = mx;
+      }
+      p0[nt] = (l0 == -INFINITY) ? 0.f : ex2f(l0 - M[nt]);
+      p1[nt] = (l1 == -INFINITY) ? 0.f : ex2f(l1 - M[nt]);
+      lsum[nt] += p0[nt] + p1[nt];
+    }
+    // ---- O^T += V^T P
+    uint32_t wlo[NT], whi[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      float h0, l0, h1, l1;
+      split_bf(p0[nt], h0, l0);
+      split_bf(p1[nt], h1, l1);
+      wlo[nt] = movtrans(pack_bf2(h0, l0));  // tokens 0..7
+      whi[nt] = movtrans(pack_bf2(h1, l1));  // tokens 8..15
+    }
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const int ch = 2 * m + vcol, row = 16 + vrow;
+      uint32_t a[4];
+      ldsm_x4_t(tb + (ch >> 3) * (TILE / 2) + row * 128 + (((ch & 7) ^ (row & 7)) << 4), a);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) mma_bf16(acc[nt][m], a, wlo[nt], whi[nt]);
+    }
+    __syncwarp();
+    if (k + NSTG < my) issue(k + NSTG);
+  }
+
+  // ---- CTA merge (reference points, rescaled partials, one summing pass)
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) lsum[nt] += __shfl_xor_sync(0xffffffffu, lsum[nt], o);
+    if (r == 0) s_m[warp * 8 + 4 * nt + i] = M[nt];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int j = 4 * nt + i;
+    float mstar = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) mstar = fmaxf(mstar, s_m[w * 8 + j]);
+    if (warp == 0 && r == 0) s_mstar[j] = mstar;
+    const float sc = (M[nt] == -INFINITY) ? 0.f : ex2f(M[nt] - mstar);
+    float* dst = sred + (warp * 8 + j) * 128;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      dst[16 * m + r] = (acc[nt][m][0] + acc[nt][m][1]) * sc;
+      dst[16 * m + r + 8] = (acc[nt][m][2] + acc[nt][m][3]) * sc;
+    }
+    if (r == 0) s_lw[warp * 8 + j] = lsum[nt] * sc;
+  }
+  __syncthreads();
+  const int64_t hbase = (((int64_t)b * H + h) * p.splits) * 8;
+  for (int x = threadIdx.x; x < G * 128; x += blockDim.x) {
+    const int j = x >> 7, dd = x & 127;
+    float lt = 0.f, ot = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      lt += s_lw[w * 8 + j];
+      ot += sred[(w * 8 + j) * 128 + dd];
+    }
+    const float o = lt > 0.f ? ot / lt : 0.f;
+    if (p.splits == 1) {
+      p.out[((int64_t)b * p.nq + (int64_t)h * G + j) * 128 + dd] = o;
+    } else {
+      __stcg(&p.ws_o[(hbase + (int64_t)split * 8 + j) * 128 + dd], o);
+      if (dd == 0) __stcg(&p.ws_lse[hbase + (int64_t)split * 8 + j], lt > 0.f ? s_mstar[j] + __log2f(lt) : -INFINITY);
+    }
+  }
+}
+
 // Stage-in of one serving step's host inputs (kvr_step_ring): pinned staging -> its device twin,
 // 16 B per thread.  Launched with programmatic dependent launch right after the previous step's
 // decode: the copy (the slot's last reader finished long ago) overlaps that decode, then the grid
@@ -1885,6 +2136,53 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
     return p.G == 8 ? launch_tma<2, false>(p, sg, grid, smem, ord, st) : launch_tma<1, false>(p, sg, grid, smem, ord, st);
   }
   if (new_slot) return KVR_ERR_UNSUPPORTED;  // the fused append lives in the TMA kernel only
+  if (pool.prec == KVR_PREC_BF16 && pool.d == 128 && pool.T == 16 && pool.P % 16 == 0 && p.G >= 1 && p.G <= 8 &&
+      (reinterpret_cast<uintptr_t>(pool.base) & 255) == 0 && (pool.page_bytes & 255) == 0 && pool.cell_bytes == 8192 &&
+      !getenv("KVR_BF16_DECODE_GENERIC")) {
+    if (splits <= 0) splits = kvr_pick_splits(batch, pool.H, max_len, pool.P);
+    if (splits > MAX_SPLITS) splits = MAX_SPLITS;
+    if (splits > 1 && kvr_decode_ws_bytes(batch, pool.H, nq, 128, splits) > ws_bytes) return KVR_ERR_ARG;
+    p.splits = splits;
+    const size_t units = (size_t)batch * pool.H * splits * 8;
+    p.ws_cnt = reinterpret_cast<uint32_t*>(ws);
+    p.ws_lse = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + ws_cnt_bytes(batch, pool.H));
+    p.ws_o = p.ws_lse + units;
+    p.rotate = 0;
+    p.rot_v = 0;
+    CUtensorMap map;
+    const uint64_t rows = (uint64_t)pool.num_pages * (uint64_t)pool.page_bytes / 256;
+    if (kvr_encode_tensor_map_2d(&map, pool.base, 128, rows, 256, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B) != CUDA_SUCCESS)
+      return KVR_ERR_CUDA;
+    const size_t smem = bfd::SM_TOTAL;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(pool.H, splits, batch);
+    cfg.blockDim = dim3(bfd::NW * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    static bool attr_set[KVR_MAX_DEVICES][2];
+    const int dev = kvr_current_device();
+    cudaError_t e;
+    if (p.G > 4) {
+      if (!attr_set[dev][1]) {
+        cudaFuncSetAttribute(decode_bf16_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set[dev][1] = true;
+      }
+      e = cudaLaunchKernelEx(&cfg, decode_bf16_kernel<2>, p, map);
+    } else {
+      if (!attr_set[dev][0]) {
+        cudaFuncSetAttribute(decode_bf16_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set[dev][0] = true;
+      }
+      e = cudaLaunchKernelEx(&cfg, decode_bf16_kernel<1>, p, map);
+    }
+    if (e != cudaSuccess) return KVR_ERR_CUDA;
+    return splits > 1 ? launch_merge<128>(p, sg, st) : 0;
+  }
   if (pool.d > 256) return KVR_ERR_UNSUPPORTED;
   p.splits = 1;
   const int warps = 4;

@@ -104,3 +104,35 @@ def test_bf16_batch_write_and_load(tmp_path, dtype, golden_bf16):
     t2 = PageTable.load(path)
     assert t2.precision == BF16 and t2.dump_bytes() == path.read_bytes()
     np.testing.assert_array_equal(t2.read_sequence(0)[0], kh)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("L,G,splits", [(37, 4, 1), (300, 4, 0), (4096, 4, 0), (4096, 8, 0), (32768, 4, 0), (1000, 1, 3)])
+def test_bf16_tuned_decode_vs_f64(L, G, splits):
+    """The tensor-core BF16-pool decode (d = 128, 16-token cells) against an f64 decode of
+    the same raw bf16 rows, any split count; the ragged last cell holds stale NaN rows."""
+    from paper_2604_19157_b200 import DecodePlan, HeadLayout, PageTable
+    from paper_2604_19157_b200.cache import BF16
+
+    H, d = 2, 128
+    layout = HeadLayout(num_q_heads=G * H, num_kv_heads=H, head_dim=d, rot_order=128, page_tokens=16)
+    t = PageTable(layout, precision=BF16, num_pages=(L + 15) // 16 + 1)
+    t.pool.fill_(0xFF)  # unwritten slots: NaN bit patterns
+    t.create_sequence(0)
+    g = torch.Generator(device="cuda").manual_seed(L + G)
+    k = torch.randn((L, H, d), generator=g, device="cuda").bfloat16()
+    v = torch.randn((L, H, d), generator=g, device="cuda").bfloat16()
+    t.store_slots(k, v, torch.from_numpy(t.alloc.reserve(0, L)).cuda(), None)
+    q = torch.randn((1, G * H, d), generator=g, device="cuda").bfloat16()
+    out = DecodePlan(t, [0], num_splits=splits).run(q, None)
+    torch.cuda.synchronize()
+    kk, vv, qq = k.double().cpu(), v.double().cpu(), q[0].double().cpu()
+    ref = torch.empty((G * H, d), dtype=torch.float64)
+    for qh in range(G * H):
+        s = kk[:, qh // G] @ qq[qh] / np.sqrt(d)
+        w = torch.softmax(s, 0)
+        ref[qh] = w @ vv[:, qh // G]
+    got = out[0].double().cpu()
+    err = float((got - ref).abs().max() / ref.abs().max())
+    print(f"L={L} G={G} splits={splits}: rel err {err:.2e}")
+    assert torch.isfinite(got).all() and err <= 1e-4
