@@ -321,6 +321,7 @@ def run_ours(args, rank, world, local_rank):
           f"{c1['tcgen05_plain_us']}); 65536 tok rot {c1['write_65536_tokens']['rot_us']} plain "
           f"{c1['write_65536_tokens']['plain_us']} (mma.sync {c1['write_65536_tokens']['mma_sync_rot_us']}); "
           f"K4 {c1['dequant_us']} us", file=sys.stderr, flush=True)
+    print(f"[bench] learned R fused K1 {c1['learned_r_fused']}", file=sys.stderr, flush=True)
     c3 = c4 = c5 = bf = None
     if not args.quick:
         sets.clear()  # free the headline's buffers first
@@ -725,6 +726,33 @@ def c1_quantize_store(torch, layout, spec, dev, gen, timed):
         bm_rot, bm_pl = k1_us(big, 64)
     finally:
         _L.lib().kvr_debug_set_k1_impl(0)
+    # row f3: the learned R fused into the tcgen05 K1 (T = diag(s) H_blk R as three bf16 parts, 24 MMAs
+    # of M128 N128 K16 per tile) vs the unfused route (f64 FWHT + cuBLAS DGEMM, then the exact store)
+    import numpy as _np
+
+    from paper_2604_19157_b200 import RotationSpec as _RS
+    from paper_2604_19157_b200.rotation import learned_on, learned_store_operands
+    qm, rm = _np.linalg.qr(_np.random.default_rng(7).standard_normal((D, D)))
+    lspec = _RS(order=spec.order, signs=spec.signs, learned=qm * _np.sign(_np.diag(rm)), learned_values=True)
+    learned_store_operands(lspec, layout, dev)
+    learned_on(lspec, dev)
+
+    def kl_us(sets_, n_, exact=False):
+        R_ = len(sets_)
+        return timed(lambda i: sets_[i % R_][0].store_slots(sets_[i % R_][1], sets_[i % R_][2], sets_[i % R_][3], lspec,
+                                                          exact=exact), n_) / n_
+
+    l_small, l_small_unf = kl_us(sets, n), kl_us(sets, 32, exact=True)
+    l_big, l_big_unf = kl_us(big, 64), kl_us(big, 8, exact=True)
+    learned_line = {"kernel": "store_tc_kernel<LEARNED> (tcgen05.mma M128 N128 K16 x 24 per tile, T in shared memory)",
+                    "c1_us": round(l_small * 1e3, 3), "c1_GBps": round(byts / (l_small * 1e-3) / 1e9, 1),
+                    "c1_frac": round(byts / (l_small * 1e-3) / 1e9 / peak, 4),
+                    "c1_unfused_us": round(l_small_unf * 1e3, 2),
+                    "t65536_us": round(l_big * 1e3, 2),
+                    "t65536_GBps": round(big_n * WRITE_BYTES_PER_TOKEN / (l_big * 1e-3) / 1e9, 1),
+                    "t65536_frac": round(big_n * WRITE_BYTES_PER_TOKEN / (l_big * 1e-3) / 1e9 / peak, 4),
+                    "t65536_unfused_us": round(l_big_unf * 1e3, 2),
+                    "t65536_vs_hadamard_only": round(l_big / b_rot - 1.0, 4)}
     del big
     bb = big_n * WRITE_BYTES_PER_TOKEN
     big_line = {"tokens": big_n, "algorithmic_bytes": bb, "rot_us": round(b_rot * 1e3, 2), "plain_us": round(b_pl * 1e3, 2),
@@ -757,7 +785,7 @@ def c1_quantize_store(torch, layout, spec, dev, gen, timed):
             "overhead_vs_plain": round(t_rot / t_pl - 1.0, 4),
             "kernel": "store_mma_kernel (mma.sync; the default below ~4 tiles of 128 rows per SM)",
             "tcgen05_rot_us": round(c_rot * 1e3, 3), "tcgen05_plain_us": round(c_pl * 1e3, 3),
-            "write_65536_tokens": big_line}
+            "write_65536_tokens": big_line, "learned_r_fused": learned_line}
 
 
 def e2e_api(torch, layout, spec, dev, tables, args, world):

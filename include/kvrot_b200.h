@@ -207,6 +207,25 @@ int kvr_rotate_quantize_store(const void* k, const void* v, int32_t in_dtype, in
                               void* stream);
 
 /*
+ * Row f3, K1 with a learned R fused: y = x diag(s) H_blk R (rotation.py:118-142) for the K
+ * rows and for V per value_branch_spec (rotation.py:162-168: learned_values=1 the same T,
+ * 0 the Hadamard part only; targets KVR_KEYS_ONLY leaves V plain).  One tcgen05 kernel: T as
+ * three bf16 parts in shared memory (24 mantissa bits), fp32 accumulation in TMEM, codes
+ * within a margin of a rounding boundary recomputed in f64 (FWHT then R).
+ *   t_img : device image of T, 98,304 bytes (kvr_learned_pack_image)
+ *   r_t   : device R^T, f64 [d][d] row-major (r_t[n * d + k] = R[k][n])
+ * Only bf16 rows, d = 128, T = 16, power-of-two pages: KVR_ERR_UNSUPPORTED otherwise (the
+ * caller rotates in f64 and stores through kvr_rotate_quantize_store(exact=1)).
+ */
+int kvr_rotate_quantize_store_learned(const void* k, const void* v, int32_t in_dtype, int64_t n_tok,
+                                      const int64_t* slot_mapping, const kvr_pool* pool, int32_t rot_order,
+                                      int32_t targets, int32_t learned_values, const uint32_t* sign_words,
+                                      const void* t_img, const double* r_t, uint32_t* flags, void* stream);
+/* Host helper: the kernel's shared-memory image of T (host f64 [128][128] row-major, the dense
+ * compose_transform, rotation.py:171-184) into `img` (host, 49,152 uint16: three bf16 parts). */
+void kvr_learned_pack_image(const double* t, uint16_t* img);
+
+/*
  * K4: flatten-dequant of sequences into dense stored-space rows.
  *   block_table : int32[batch][bt_stride] page ids; seq_lens: int32[batch]
  *   k_out/v_out : (batch, max_len, H, d) of out_dtype (F64/F32/BF16); rows past a

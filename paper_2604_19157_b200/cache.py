@@ -392,8 +392,10 @@ class PageTable:
         if rotate:
             if spec.order != self.layout.rot_order:
                 raise ShapeError(f"spec order {spec.order} != layout rot_order {self.layout.rot_order}")
-            if spec.learned is not None:  # row f3: learned R after H, unfused f64 transform on the device
-                from .rotation import rotate_kv_learned
+            if spec.learned is not None:  # row f3: learned R after H
+                if not exact and self._store_learned(k, v, slot_t, spec):
+                    return
+                from .rotation import rotate_kv_learned  # unfused: f64 transform on the device, exact store
 
                 k, v = rotate_kv_learned(k, v, self.layout, spec)
                 spec, rotate, exact = None, False, True
@@ -403,6 +405,26 @@ class PageTable:
             _kernels.ptr(k), _kernels.ptr(v), _TORCH_DTYPE_CODE[k.dtype], n, _kernels.ptr(slot_t),
             ctypes.byref(self.desc), spec.order if rotate else 1, 1 if rotate else 0, targets, words,
             1 if exact else 0, _kernels.ptr(self.flags), _kernels.stream_ptr()))
+
+    def _store_learned(self, k: torch.Tensor, v: torch.Tensor, slot_t: torch.Tensor, spec: RotationSpec) -> bool:
+        """Row f3 fused: the tcgen05 K1 with T = diag(s) H_blk R in shared memory (bf16 rows,
+        head_dim 128).  False when the kernel does not cover the configuration (the caller
+        takes the unfused path)."""
+        if k.dtype != torch.bfloat16 or self.layout.head_dim != 128 or cell_tokens(self.layout) != 16:
+            return False
+        from .rotation import learned_store_operands
+
+        img, rt = learned_store_operands(spec, self.layout, self.device)
+        targets = _lib.KVR_KEYS_ONLY if spec.targets is Targets.KEYS_ONLY else _lib.KVR_KEYS_AND_VALUES
+        rc = _lib.lib().kvr_rotate_quantize_store_learned(
+            _kernels.ptr(k), _kernels.ptr(v), _TORCH_DTYPE_CODE[k.dtype], k.shape[0], _kernels.ptr(slot_t),
+            ctypes.byref(self.desc), spec.order, targets, 1 if spec.learned_values else 0,
+            spec.sign_words(self.layout.head_dim), _kernels.ptr(img), _kernels.ptr(rt), _kernels.ptr(self.flags),
+            _kernels.stream_ptr())
+        if rc == _lib.KVR_ERR_UNSUPPORTED:
+            return False
+        _lib.check(rc)
+        return True
 
     def _check_kv_host(self, k, v, ndim: int):
         h, d = self.layout.num_kv_heads, self.layout.head_dim
@@ -488,7 +510,9 @@ class PageTable:
             raise ShapeError("slots must be an int64 CUDA tensor")
         if self.precision == BF16:
             spec = None
-        if spec is not None and spec.learned is not None:  # row f3, unfused (see _store)
+        if spec is not None and spec.learned is not None:  # row f3 (see _store)
+            if not exact and self._store_learned(k, v, slots, spec):
+                return
             from .rotation import rotate_kv_learned
 
             k, v = rotate_kv_learned(k, v, self.layout, spec)

@@ -526,6 +526,37 @@ int kvr_rotate_quantize_store(const void* k, const void* v, int32_t in_dtype, in
   return check_launch("rotate_quantize_store");
 }
 
+int kvr_rotate_quantize_store_learned(const void* k, const void* v, int32_t in_dtype, int64_t n_tok,
+                                      const int64_t* slot_mapping, const kvr_pool* pool, int32_t rot_order,
+                                      int32_t targets, int32_t learned_values, const uint32_t* sign_words,
+                                      const void* t_img, const double* r_t, uint32_t* flags, void* stream) {
+  Pool pl;
+  if (int rc = to_pool(pool, pl)) return rc;
+  if (n_tok < 0) return fail(KVR_ERR_SHAPE, "n_tok < 0");
+  if (!k || !v || !slot_mapping || !t_img || !r_t) return fail(KVR_ERR_ARG, "null k/v/slot_mapping/t_img/r_t");
+  if (in_dtype < KVR_F64 || in_dtype > KVR_F16) return fail(KVR_ERR_ARG, "bad dtype %d", in_dtype);
+  if (targets != KVR_KEYS_ONLY && targets != KVR_KEYS_AND_VALUES) return fail(KVR_ERR_ARG, "bad targets %d", targets);
+  if (int rc = check_order(pl.d, rot_order)) return rc;
+  if (pl.prec != KVR_PREC_INT4) return fail(KVR_ERR_UNSUPPORTED, "learned store: INT4 pools only");
+  Signs s;
+  int has;
+  if (int rc = make_signs(sign_words, pl.d, s, has)) return rc;
+  if (n_tok == 0) return KVR_OK;
+  const int mode_v = targets == KVR_KEYS_ONLY ? 0 : (learned_values ? 2 : 1);
+  cudaStream_t st = (cudaStream_t)stream;
+  kvr_mark_pool_written(st);
+  const int rc = kvr_launch_store_learned(k, v, in_dtype, n_tok, slot_mapping, pl, rot_order, mode_v, s, has, t_img,
+                                          r_t, flags, st);
+  if (rc == KVR_ERR_UNSUPPORTED)
+    return fail(rc, "learned store: bf16 rows, d = 128, 16-token cells, power-of-two pages, 16-B aligned only");
+  if (rc) return fail(rc, "rotate_quantize_store_learned: launch failed (%d)", rc);
+  return check_launch("rotate_quantize_store_learned");
+}
+
+void kvr_learned_pack_image(const double* t, uint16_t* img) {
+  if (t && img) kvr_pack_learned_image(t, img);
+}
+
 int kvr_dequantize_pages(const kvr_pool* pool, const int32_t* block_table, int32_t bt_stride,
                          const int32_t* seq_lens, int32_t batch, int32_t max_len, void* k_out, void* v_out,
                          int32_t out_dtype, void* stream) {

@@ -34,6 +34,12 @@ int kvr_launch_decode_flat_f64(const double* q, const double* k, const double* v
 int kvr_launch_store_fast(const void* k, const void* v, int in_dtype, int64_t n_tok, const int64_t* slots,
                           const kvr::Pool& pool, int order, int rot_k, int rot_v, const kvr::Signs& s, int has,
                           uint32_t* flags, cudaStream_t st);
+// Row f3: the tcgen05 K1 with the learned R fused (bf16 rows, head_dim 128); K tiles through T,
+// V tiles in mode_v (0 plain, 1 block Hadamard, 2 T).  KVR_ERR_UNSUPPORTED otherwise.
+int kvr_launch_store_learned(const void* k, const void* v, int in_dtype, int64_t n_tok, const int64_t* slots,
+                             const kvr::Pool& pool, int order, int mode_v, const kvr::Signs& s, int has,
+                             const void* t_img, const double* rt, uint32_t* flags, cudaStream_t st);
+void kvr_pack_learned_image(const double* t, uint16_t* img);
 
 // Decode (kvr_decode.cu)
 size_t kvr_decode_ws_bytes(int batch, int H, int nq, int d, int splits);

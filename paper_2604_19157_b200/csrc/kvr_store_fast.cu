@@ -62,38 +62,41 @@ KVR_DEV void tile_quad(const uint8_t* buf, int src, int l, double (&x)[4]) {
 // 1, 2 in registers, 4..ORDER/2 by shuffles, lowest index first), * 1/sqrt(ORDER),
 // then round-half-away(y / s64) + z, clip (_ref.py:22-40, 57-80).  Returns the 4
 // codes of lane l as a 16-bit group (element 4l in the low nibble).
+template <int ORDER>
+KVR_DEV void warp_fwht_f64(double (&x)[4], const Signs& sg) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    if (sign_bit(sg, 4 * lane + u)) x[u] = x[u] * -1.0;
+  const double a0 = x[0] + x[1], a1 = x[0] - x[1], a2 = x[2] + x[3], a3 = x[2] - x[3];  // half = 1
+  x[0] = a0 + a2;                                                                     // half = 2
+  x[1] = a1 + a3;
+  x[2] = a0 - a2;
+  x[3] = a1 - a3;
+#pragma unroll
+  for (int k = 0; (4 << k) < ORDER; ++k) {
+    const double sgn = ((lane >> k) & 1) ? -1.0 : 1.0;  // upper half of the pair: o - x
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double o = __shfl_xor_sync(0xffffffffu, x[u], 1 << k);
+      x[u] = fma(sgn, x[u], o);  // o -+ x, one rounding
+    }
+  }
+  const double inv = 1.0 / sqrt((double)ORDER);
+#pragma unroll
+  for (int u = 0; u < 4; ++u) x[u] = x[u] * inv;
+}
+KVR_DEV uint32_t code_f64(double y, double s64, double z) {
+  double q = round_half_away(y / s64) + z;
+  q = q < 0.0 ? 0.0 : (q > 15.0 ? 15.0 : q);
+  return (uint32_t)q;
+}
 template <int ORDER, bool ROT>
 KVR_DEV uint32_t warp_exact_core(double (&x)[4], const Signs& sg, double s64, double z) {
-  const int lane = threadIdx.x & 31;
-  if constexpr (ROT) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (sign_bit(sg, 4 * lane + u)) x[u] = x[u] * -1.0;
-    const double a0 = x[0] + x[1], a1 = x[0] - x[1], a2 = x[2] + x[3], a3 = x[2] - x[3];  // half = 1
-    x[0] = a0 + a2;                                                                     // half = 2
-    x[1] = a1 + a3;
-    x[2] = a0 - a2;
-    x[3] = a1 - a3;
-#pragma unroll
-    for (int k = 0; (4 << k) < ORDER; ++k) {
-      const double sgn = ((lane >> k) & 1) ? -1.0 : 1.0;  // upper half of the pair: o - x
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const double o = __shfl_xor_sync(0xffffffffu, x[u], 1 << k);
-        x[u] = fma(sgn, x[u], o);  // o -+ x, one rounding
-      }
-    }
-    const double inv = 1.0 / sqrt((double)ORDER);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) x[u] = x[u] * inv;
-  }
+  if constexpr (ROT) warp_fwht_f64<ORDER>(x, sg);
   uint32_t g = 0u;
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    double q = round_half_away(x[u] / s64) + z;
-    q = q < 0.0 ? 0.0 : (q > 15.0 ? 15.0 : q);
-    g |= (uint32_t)q << (4 * u);
-  }
+  for (int u = 0; u < 4; ++u) g |= code_f64(x[u], s64, z) << (4 * u);
   return g;
 }
 // ... of the row staged for lane `src` of a swizzled shared-memory tile
@@ -562,21 +565,29 @@ __global__ void __launch_bounds__(FS_WARPS * 32, KVR_FS_MINB)
 //                rotated rows by the warp (f64 butterfly, warp_exact_row_g), plain
 //                8-element words by exact FMA sign tests spread over the lanes.
 // Same codes, scales and flags as store_mma_kernel above.
-namespace k1tc {
-constexpr int TM = 128;
-constexpr int HALF = TM * 128;  // one 64-column SW128 box of the tile
-constexpr int TILE = 2 * HALF;  // 32 KB
-constexpr int NS = 4;           // input ring stages
-constexpr int NGRP = 4;         // epilogue groups = TMEM accumulators (4 x 128 columns)
-constexpr int NEPI = 4 * NGRP;  // epilogue warps (4 lane quadrants per group)
-constexpr int THREADS = (2 + NEPI) * 32;
-constexpr int OFF_B = 0;        // B's 16 x 16 blocks (SW128 K-major [128 n][128 k]): see the setup
-constexpr int OFF_ST = TILE;
-constexpr int OFF_BAR = OFF_ST + NS * TILE;            // full[NS] empty[NS] tfull[4] tempty[4] tmem
-constexpr int OFF_CODES = OFF_BAR + 256;               // code staging [4 groups][128 rows][16 words], XOR-swizzled
-constexpr int OFF_FIXQ = OFF_CODES + NGRP * TM * 64;   // per epilogue warp: queue of flagged plain words (1 KB)
-constexpr int SMEM = OFF_FIXQ + NEPI * 1024 + 1024;    // + 1 KB alignment slack (SW128 atoms need 1024-B bases)
-}  // namespace k1tc
+// LEARNED (row f3): a third tile mode, y = x T with the dense T = diag(s) H_blk R / sqrt(order) as three
+// bf16 parts (hi + mid + lo, 24 mantissa bits) in shared memory: 3 x 8 MMAs of M128 N128 K16 per tile
+template <bool LEARNED>
+struct K1Cfg {
+  static constexpr int TM = 128;
+  static constexpr int HALF = TM * 128;  // one 64-column SW128 box of the tile
+  static constexpr int TILE = 2 * HALF;  // 32 KB
+  static constexpr int NS = LEARNED ? 2 : 4;    // input ring stages
+  static constexpr int NGRP = LEARNED ? 3 : 4;  // epilogue groups = TMEM accumulators (128 columns each)
+  static constexpr int NEPI = 4 * NGRP;         // epilogue warps (4 lane quadrants per group)
+  static constexpr int THREADS = (2 + NEPI) * 32;
+  static constexpr int TMEM_COLS = 512;         // NGRP x 128 columns, allocated as a power of two
+  static constexpr int OFF_B = 0;  // B's 16 x 16 blocks (SW128 K-major [128 n][128 k]): see the setup
+  static constexpr int OFF_T = TILE;                            // learned: the three parts of T (B[n][k] = T[k][n])
+  static constexpr int OFF_ST = OFF_T + (LEARNED ? 3 * TILE : 0);
+  static constexpr int OFF_BAR = OFF_ST + NS * TILE;            // full[NS] empty[NS] tfull[NGRP] tempty[NGRP] tmem
+  static constexpr int OFF_CODES = OFF_BAR + 256;               // code staging [groups][128 rows][16 words], swizzled
+  static constexpr int OFF_FIXQ = OFF_CODES + NGRP * TM * 64;   // per epilogue warp: queue of flagged words
+  static constexpr int FIXQ = LEARNED ? 512 : 1024;            // bytes per warp: learned rows queue <= 8 words each
+  static constexpr int SMEM = OFF_FIXQ + NEPI * FIXQ + 1024;    // + 1 KB alignment slack (SW128 atoms: 1024-B bases)
+};
+static_assert(K1Cfg<true>::SMEM <= 232448, "learned K1 shared memory");
+static_assert(K1Cfg<false>::SMEM <= 232448, "K1 shared memory");
 
 struct TcStoreParams {
   Pool pool;
@@ -586,8 +597,11 @@ struct TcStoreParams {
   const uint16_t* v_in;
   int32_t n_rows;          // n_tok * H per side
   int32_t tiles_per_side;  // ceil(n_rows / 128)
-  int32_t rot_k, rot_v;
+  int32_t rot_k, rot_v;    // tile modes: 0 plain, 1 block Hadamard, 2 learned (T)
   int32_t log2P;
+  const uint4* t_img;      // learned: the SW128 image of T's three bf16 parts (kvr_learned_pack), 96 KB
+  const double* rt;        // learned: R^T, f64 [128 n][128 k], for the exact recomputation
+  float kappa_units;       // learned: boundary margin per unit of ||y||_2 / s, in 2^-16 code steps
 };
 
 KVR_DEV void tmem_ld8(uint32_t taddr, float (&v)[8]) {
@@ -615,6 +629,13 @@ KVR_DEV void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t 
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 0, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc)
+      : "memory");
+}
+KVR_DEV void umma_f16_acc(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
 }
 KVR_DEV void umma_commit(uint64_t* bar) {
@@ -650,11 +671,86 @@ KVR_DEV void tc_load_half(uint32_t ta, bool rot, float (&v)[8][8]) {
   }
 }
 
-template <int ORDER, bool F16>
-__global__ void __launch_bounds__(k1tc::THREADS, 1)
+// Queue this warp's flagged 8-element words (bit w of `mine` = word w of this lane's row) as
+// u16 entries lane << 4 | w in lane order; returns the warp's count (warp-uniform).
+KVR_DEV int queue_words(uint32_t mine, uint16_t* fixq) {
+  const int lane = threadIdx.x & 31;
+  const int n = __popc(mine);
+  int incl = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const int nfix = __shfl_sync(0xffffffffu, incl, 31);
+  if (nfix) {
+    int pos = incl - n;
+    for (uint32_t mm = mine; mm; mm &= mm - 1) fixq[pos++] = (uint16_t)((lane << 4) | (__ffs(mm) - 1));
+    __syncwarp();
+  }
+  return nfix;
+}
+
+// Row f3: codes of elements 8 w .. 8 w + 7 of a learned-rotated bf16 row y = FWHT(x o s) R
+// (rotation.py:118-142), in f64 by the whole warp: the row's quad and R^T's 8 rows are loaded up front,
+// the f64 butterfly gives h (lane l holds h[4 l .. 4 l + 3]), then y_n = sum over lanes of
+// h[4 l ..] . R^T[n][4 l ..] by a transposing reduction (16 -> 8 -> 4 lanes keep 4, 2, 1 of the 8
+// sums, then xor 2, 1: lanes 4 j' .. 4 j' + 3 end with the same sum).  The reference's x @ R goes
+// through a BLAS with its own summation order: codes agree except within ~1e-16 of a boundary.
+template <int ORDER>
+__device__ __noinline__ uint32_t warp_learned_word(const uint16_t* xrow, const Signs& sg, const double* rt, int w,
+                                                   double s64, double z) {
+  const int lane = threadIdx.x & 31;
+  const uint2 q = *reinterpret_cast<const uint2*>(xrow + 4 * lane);
+  double2 r[8][2];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const double2* rp = reinterpret_cast<const double2*>(rt + (size_t)(8 * w + j) * 128 + 4 * lane);
+    r[j][0] = __ldg(rp);
+    r[j][1] = __ldg(rp + 1);
+  }
+  double h[4];
+  const uint32_t xw[2] = {q.x, q.y};
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const uint32_t bits = (u & 1) ? (xw[u >> 1] >> 16) : (xw[u >> 1] & 0xFFFFu);
+    h[u] = (double)__uint_as_float(bits << 16);
+  }
+  warp_fwht_f64<ORDER>(h, sg);
+  double y[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    y[j] = fma(h[3], r[j][1].y, fma(h[2], r[j][1].x, fma(h[1], r[j][0].y, h[0] * r[j][0].x)));
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  double z4[4], z2[2];
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) {
+    const double keep = b4 ? y[jj + 4] : y[jj], give = b4 ? y[jj] : y[jj + 4];
+    z4[jj] = keep + __shfl_xor_sync(0xffffffffu, give, 16);
+  }
+#pragma unroll
+  for (int jj = 0; jj < 2; ++jj) {
+    const double keep = b3 ? z4[jj + 2] : z4[jj], give = b3 ? z4[jj] : z4[jj + 2];
+    z2[jj] = keep + __shfl_xor_sync(0xffffffffu, give, 8);
+  }
+  double t = (b2 ? z2[1] : z2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? z2[0] : z2[1], 4);
+  t += __shfl_xor_sync(0xffffffffu, t, 2);
+  t += __shfl_xor_sync(0xffffffffu, t, 1);
+  const int j = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);  // this lane's element 8 w + j
+  const uint32_t c = (lane & 3) ? 0u : code_f64(t, s64, z) << (4 * j);
+  return __reduce_or_sync(0xffffffffu, c);
+}
+
+template <int ORDER, bool F16, bool LEARNED>
+__global__ void __launch_bounds__(K1Cfg<LEARNED>::THREADS, 1)
     store_tc_kernel(const __grid_constant__ TcStoreParams p, const __grid_constant__ CUtensorMap map_k,
                     const __grid_constant__ CUtensorMap map_v, const __grid_constant__ Signs signs) {
-  using namespace k1tc;
+  static_assert(!(LEARNED && F16), "the learned K1 takes bf16 rows");
+  using Cfg = K1Cfg<LEARNED>;
+  constexpr int TM = Cfg::TM, HALF = Cfg::HALF, TILE = Cfg::TILE, NS = Cfg::NS, NGRP = Cfg::NGRP;
+  constexpr int THREADS = Cfg::THREADS;
+  constexpr int OFF_B = Cfg::OFF_B, OFF_T = Cfg::OFF_T, OFF_ST = Cfg::OFF_ST, OFF_BAR = Cfg::OFF_BAR;
+  constexpr int OFF_CODES = Cfg::OFF_CODES, OFF_FIXQ = Cfg::OFF_FIXQ;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
@@ -667,7 +763,7 @@ __global__ void __launch_bounds__(k1tc::THREADS, 1)
 
   // ---- setup (overlaps the previous grid under PDL): B's 16 x 16 blocks -- diag(s_j) H_16 at
   // (rows 16 j, K 16 j) for rotated tiles and the identity at (rows 16 j, K 16 (j ^ 4)) for plain
-  // ones (the N = 16 MMAs read nothing else) -- barriers, TMEM
+  // ones (the N = 16 MMAs read nothing else) -- T's parts (learned), barriers, TMEM
   {
     const uint32_t one = F16 ? 0x3C00u : 0x3F80u;
     for (int e = threadIdx.x; e < 2 * 8 * 16 * 8; e += THREADS) {
@@ -686,6 +782,7 @@ __global__ void __launch_bounds__(k1tc::THREADS, 1)
                                    (((byte >> 4) ^ (n & 7)) << 4) + (byte & 15)) = w;
     }
   }
+  uint64_t* tbar = reinterpret_cast<uint64_t*>(s_tmem + 2);  // learned: T's parts have landed
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
       mbar_init(&full[i], 1);
@@ -695,12 +792,19 @@ __global__ void __launch_bounds__(k1tc::THREADS, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 4);
     }
+    if (LEARNED) mbar_init(tbar, 1);
     fence_mbar_init();
+    if constexpr (LEARNED) {  // T's three parts by bulk copy (a one-time upload, not the previous grid's output)
+      mbar_expect_tx(tbar, 3 * TILE);
+      for (int pp = 0; pp < 3; ++pp)
+        bulk_g2s(smem + OFF_T + pp * TILE, reinterpret_cast<const uint8_t*>(p.t_img) + pp * TILE, TILE, tbar);
+    }
     prefetch_tensormap(&map_k);
     prefetch_tensormap(&map_v);
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(s_tmem)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
+                 "n"(Cfg::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   fence_proxy_async();  // the generic-proxy B matrix -> the tensor core's async-proxy reads
@@ -730,35 +834,56 @@ __global__ void __launch_bounds__(k1tc::THREADS, 1)
     }
   } else if (warp == 1) {
     // ================= MMA issuer: D[:, 16 j .. 16 j + 15] = A[:, 16 j ..] B_j^T per block j
-    // idesc: D f32, A/B bf16 (1) or f16 (0), both K-major, N = 16, M = 128
+    // (learned tiles: D = A T, 8 K-steps per part, accumulated over the three parts)
+    // idesc: D f32, A/B bf16 (1) or f16 (0), both K-major, N = 16 (128), M = 128
     const uint32_t fmt = F16 ? 0u : 1u;
     const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
+    const uint32_t idesc_l = (1u << 4) | (fmt << 7) | (fmt << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
     const uint32_t bbase = smem_u32(smem + OFF_B);
+    bool t_ready = false;
     int i = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++i) {
       const int side = tile >= p.tiles_per_side;
-      const uint32_t bx = (side ? p.rot_v : p.rot_k) ? 0u : 4u;  // plain tiles: the identity blocks at K 16 (j ^ 4)
-      const int s = i % NS, a = i & (NGRP - 1);
+      const int mode = side ? p.rot_v : p.rot_k;
+      const uint32_t bx = mode ? 0u : 4u;  // plain tiles: the identity blocks at K 16 (j ^ 4)
+      const int s = i % NS, a = i % NGRP;
       mbar_wait(&full[s], (i / NS) & 1);
       mbar_wait(&tempty[a], ((i / NGRP) & 1) ^ 1);
       tc_fence_after();
       if (elect_one()) {
         const uint32_t abase = smem_u32(smem + OFF_ST + s * TILE);
+        if (LEARNED && mode == 2) {
+          if (!t_ready) {
+            mbar_wait(tbar, 0);
+            t_ready = true;
+          }
+          const uint32_t tbase = smem_u32(smem + OFF_T);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint32_t ko = (uint32_t)(j >> 2) * HALF + (uint32_t)(j & 3) * 32;  // 16 columns = 32 B into the atom
-          const uint32_t jb = (uint32_t)j ^ bx;
-          const uint32_t kb = (jb >> 2) * HALF + (jb & 3) * 32;
-          umma_f16(tmem + (uint32_t)(a * 128 + 16 * j), sw128_desc(abase + ko), sw128_desc(bbase + kb + 2048u * j),
-                   idesc);
+          for (int pp = 0; pp < 3; ++pp)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint32_t ko = (uint32_t)(j >> 2) * HALF + (uint32_t)(j & 3) * 32;
+              umma_f16_acc(tmem + (uint32_t)(a * 128), sw128_desc(abase + ko),
+                           sw128_desc(tbase + (uint32_t)pp * TILE + ko), idesc_l, (uint32_t)(pp | j));
+            }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t ko = (uint32_t)(j >> 2) * HALF + (uint32_t)(j & 3) * 32;  // 16 columns = 32 B into the atom
+            const uint32_t jb = (uint32_t)j ^ bx;
+            const uint32_t kb = (jb >> 2) * HALF + (jb & 3) * 32;
+            umma_f16(tmem + (uint32_t)(a * 128 + 16 * j), sw128_desc(abase + ko), sw128_desc(bbase + kb + 2048u * j),
+                     idesc);
+          }
         }
         umma_commit(&empty[s]);  // the stage is free once the MMAs have read it
         umma_commit(&tfull[a]);
       }
       __syncwarp();
     }
+    if (LEARNED && !t_ready) mbar_wait(tbar, 0);  // no bulk copy may outlive the CTA
   } else {
-    // ================= epilogue: group g = every fourth tile (accumulator g); thread = row
+    // ================= epilogue: group g = every NGRP-th tile (accumulator g); thread = row
     const int ew = warp - 2, g = ew >> 2, quad = warp & 3;  // TMEM lane quadrant = warp % 4
     const int rl = 32 * quad + lane;
     const Pool& pl = p.pool;
@@ -769,12 +894,13 @@ __global__ void __launch_bounds__(k1tc::THREADS, 1)
     // stores of one word hit 32 banks, and so do the write-out's word reads
     uint32_t* stage = reinterpret_cast<uint32_t*>(smem + OFF_CODES + g * TM * 64) + 32 * quad * 16;
     const uint32_t sw = (uint32_t)(lane >> 1) & 15u;
-    uint16_t* fixq = reinterpret_cast<uint16_t*>(smem + OFF_FIXQ + ew * 1024);
+    uint16_t* fixq = reinterpret_cast<uint16_t*>(smem + OFF_FIXQ + ew * Cfg::FIXQ);
     const uint32_t ta0 = tmem + ((uint32_t)(32 * quad) << 16) + (uint32_t)(g * 128);
     int k_tile = 0;
     for (int tile = blockIdx.x + g * gridDim.x; tile < total; tile += NGRP * gridDim.x, ++k_tile) {
       const int side = tile >= p.tiles_per_side;
-      const bool rot = side ? p.rot_v : p.rot_k;
+      const int mode = side ? p.rot_v : p.rot_k;
+      const bool rot = mode == 1, lrn = LEARNED && mode == 2;
       const int row = (side ? tile - p.tiles_per_side : tile) * TM + rl;
       const bool valid = row < p.n_rows;
       const int tok = hshift >= 0 ? row >> hshift : row / H;
@@ -782,8 +908,9 @@ __global__ void __launch_bounds__(k1tc::THREADS, 1)
       mbar_wait(&tfull[g], k_tile & 1);
       tc_fence_after();
       float v[8][8];  // [block b][column 8 ch + c of the block]
-      // ---- pass 1: row extremes (NaN-propagating), two halves x two FMNMX3 chains
-      float mx, mn;
+      // ---- pass 1: row extremes (NaN-propagating), two halves x two FMNMX3 chains; learned rows
+      // also sum y^2 (the boundary margin scales with ||y||_2)
+      float mx, mn, ss = 0.f;
       {
         float mxc[2], mnc[2];
 #pragma unroll 1
@@ -800,6 +927,17 @@ __global__ void __launch_bounds__(k1tc::THREADS, 1)
           }
           mxc[ch] = max3_nan(a, a2, max3_nan(v[3][7], v[7][7], v[7][7]));
           mnc[ch] = min3_nan(c, c2, min3_nan(v[3][7], v[7][7], v[7][7]));
+          if (lrn) {
+            float q0 = 0.f, q1 = 0.f;
+#pragma unroll
+            for (int b = 0; b < 8; ++b)
+#pragma unroll
+              for (int e = 0; e < 8; e += 2) {
+                q0 = fmaf(v[b][e], v[b][e], q0);
+                q1 = fmaf(v[b][e + 1], v[b][e + 1], q1);
+              }
+            ss += q0 + q1;
+          }
         }
         mx = max3_nan(mxc[0], mxc[1], mxc[1]);
         mn = min3_nan(mnc[0], mnc[1], mnc[1]);
@@ -810,8 +948,16 @@ __global__ void __launch_bounds__(k1tc::THREADS, 1)
       const RowQ rq = row_quant(mx, mn, rot ? scl_rot : 1.0, valid && fin);
       const bool clamp = __any_sync(0xffffffffu, rq.codes && rq.clamp);
       const bool cd = rq.codes;
+      // boundary margin: exact products, f32 accumulation -- plain / Hadamard rows one 2^-16 step;
+      // learned rows (T is dense, the sums round) kappa ||y||_2 / s more, capped where every code is
+      // flagged anyway
+      float dlt = FS_D, dltc = FS_D_CLAMP;
+      if (lrn && cd) {
+        dlt = fminf(FS_D + ceilf(p.kappa_units * sqrtf(ss) * __frcp_rn(rq.s32)), 131072.f);
+        dltc = dlt;
+      }
       // ---- pass 2: codes into the staging row (rows without codes get c = 0, bias = 1/2 -> code 0)
-      uint32_t flg = 0u;  // rotated: OR of the +-delta differences; plain: bit w = word w needs the exact path
+      uint32_t flg = 0u;  // Hadamard: OR of the +-delta differences; plain / learned: bit w = word w to redo
 #pragma unroll 1
       for (int ch = 0; ch < 2; ++ch) {
         tc_load_half<ORDER>(ta0 + 8 * ch, rot, v);
@@ -823,7 +969,7 @@ __global__ void __launch_bounds__(k1tc::THREADS, 1)
         if (!clamp) {  // warp-uniform
           const float cfv = cd ? rq.cf : 0.f, bias = cd ? rq.bias : FS_MAGIC + 0.5f * FS_FIX;
           const unsigned long long c2 = pk(cfv, cfv);
-          const unsigned long long bp = pk(bias + FS_D, bias + FS_D), bm = pk(bias - FS_D, bias - FS_D);
+          const unsigned long long bp = pk(bias + dlt, bias + dlt), bm = pk(bias - dlt, bias - dlt);
 #pragma unroll
           for (int b = 0; b < 8; ++b) {
             uint32_t m[8], d = 0u;
@@ -842,8 +988,8 @@ __global__ void __launch_bounds__(k1tc::THREADS, 1)
         } else {  // clamped variant: u in f32 clamped to [2^-13, 15.99], then the magic floor
           const float cu = cd ? rq.cu : 0.f, zb = cd ? rq.zb : 1.0f / 8192.0f;
           const unsigned long long fix2 = pk(FS_FIX, FS_FIX);
-          const unsigned long long mgp = pk(FS_MAGIC + FS_D_CLAMP, FS_MAGIC + FS_D_CLAMP);
-          const unsigned long long mgm = pk(FS_MAGIC - FS_D_CLAMP, FS_MAGIC - FS_D_CLAMP);
+          const unsigned long long mgp = pk(FS_MAGIC + dltc, FS_MAGIC + dltc);
+          const unsigned long long mgm = pk(FS_MAGIC - dltc, FS_MAGIC - dltc);
 #pragma unroll
           for (int b = 0; b < 8; ++b) {
             uint32_t m[8], d = 0u;
@@ -879,23 +1025,36 @@ __global__ void __launch_bounds__(k1tc::THREADS, 1)
       }
       const uint16_t* in = side ? p.v_in : p.k_in;
       __syncwarp();
-      if (!rot) {
+      if (lrn) {
+        // ---- learned rows: flagged words recomputed in f64 by the whole warp, one word at a time;
+        // rows with more than 8 flagged words (near-constant rows) redo all 16 (keeps the queue <= 256)
+        const uint32_t mine = wr ? flg : 0u;
+        const bool bulk = __popc(mine) > 8;
+        const int nfix = queue_words(bulk ? 0u : mine, fixq);
+        uint32_t bulkrows = __ballot_sync(0xffffffffu, bulk);
+        for (int k = 0; k < nfix || bulkrows; ++k) {  // warp-uniform
+          int owner, w;
+          if (k < nfix) {
+            const int e = fixq[k];
+            owner = e >> 4;
+            w = e & 15;
+          } else {
+            owner = __ffs(bulkrows) - 1;
+            w = (k - nfix) & 15;
+            if (w == 15) bulkrows &= bulkrows - 1;
+          }
+          const double sb = __shfl_sync(0xffffffffu, rq.s64, owner), zb = __shfl_sync(0xffffffffu, rq.z, owner);
+          const int r = row - rl + 32 * quad + owner;
+          const uint32_t word = warp_learned_word<ORDER>(in + (int64_t)r * 128, signs, p.rt, w, sb, zb);
+          if (lane == 0) stage[owner * 16 + (w ^ ((owner >> 1) & 15))] = word;
+        }
+        __syncwarp();
+      } else if (!rot) {
         // ---- plain rows: y = x exactly, so a word (8 elements) with a code within delta of a rounding
         // boundary -- bf16 rows hit exact ties of x / s often -- is recomputed by exact FMA sign tests;
         // the warp's flagged words are queued and spread over its lanes, one word per lane and round
-        const uint32_t mine = wr ? flg : 0u;
-        const int n = __popc(mine);
-        int incl = n;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int t = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += t;
-        }
-        const int nfix = __shfl_sync(0xffffffffu, incl, 31);
+        const int nfix = queue_words(wr ? flg : 0u, fixq);
         if (nfix) {  // warp-uniform
-          int pos = incl - n;
-          for (uint32_t mm = mine; mm; mm &= mm - 1) fixq[pos++] = (uint16_t)((lane << 4) | (__ffs(mm) - 1));
-          __syncwarp();
           for (int base = 0; base < nfix; base += 32) {
             const int k = base + lane;
             const int e = k < nfix ? fixq[k] : (lane << 4);
@@ -951,7 +1110,7 @@ __global__ void __launch_bounds__(k1tc::THREADS, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Cfg::TMEM_COLS));
   }
 }
 
@@ -1007,36 +1166,49 @@ static int launch_fast_impl(const void* k, const void* v, int64_t n_tok, const i
   return cudaLaunchKernelEx(&cfg, kern, prm, mk, mv, sg) == cudaSuccess ? 0 : KVR_ERR_CUDA;
 }
 
-template <int ORDER, bool F16>
+struct LearnedArgs {
+  const void* t_img;
+  const double* rt;
+  float kappa_units;
+};
+
+template <int ORDER, bool F16, bool LEARNED>
 static int launch_tc_impl(const void* k, const void* v, int64_t n_tok, const int64_t* slots, const Pool& pool,
-                          int rot_k, int rot_v, const Signs& s, int has, uint32_t* flags, cudaStream_t st) {
+                          int rot_k, int rot_v, const Signs& s, int has, uint32_t* flags, cudaStream_t st,
+                          const LearnedArgs* la = nullptr) {
+  using Cfg = K1Cfg<LEARNED>;
   TcStoreParams prm{};
   prm.pool = pool;
   prm.slots = slots;
   prm.flags = flags;
-  if (n_tok * pool.H > (int64_t)INT32_MAX - k1tc::TM) return KVR_ERR_UNSUPPORTED;  // 32-bit row indices
+  if (n_tok * pool.H > (int64_t)INT32_MAX - Cfg::TM) return KVR_ERR_UNSUPPORTED;  // 32-bit row indices
   prm.n_rows = (int32_t)(n_tok * pool.H);
   prm.k_in = reinterpret_cast<const uint16_t*>(k);
   prm.v_in = reinterpret_cast<const uint16_t*>(v);
-  prm.tiles_per_side = (int)((prm.n_rows + k1tc::TM - 1) / k1tc::TM);
+  prm.tiles_per_side = (int)((prm.n_rows + Cfg::TM - 1) / Cfg::TM);
   prm.rot_k = rot_k;
   prm.rot_v = rot_v;
   prm.log2P = 0;
   while ((1 << prm.log2P) < pool.P) ++prm.log2P;
+  if (la) {
+    prm.t_img = reinterpret_cast<const uint4*>(la->t_img);
+    prm.rt = la->rt;
+    prm.kappa_units = la->kappa_units;
+  }
   Signs sg = s;
   if (!has) for (auto& x : sg.w) x = 0u;
   CUtensorMap mk, mv;
-  if (kvr_encode_tensor_map_2d(&mk, k, 128, (uint64_t)prm.n_rows, 256, 64, k1tc::TM, CU_TENSOR_MAP_SWIZZLE_128B) !=
+  if (kvr_encode_tensor_map_2d(&mk, k, 128, (uint64_t)prm.n_rows, 256, 64, Cfg::TM, CU_TENSOR_MAP_SWIZZLE_128B) !=
       CUDA_SUCCESS)
     return KVR_ERR_CUDA;
-  if (kvr_encode_tensor_map_2d(&mv, v, 128, (uint64_t)prm.n_rows, 256, 64, k1tc::TM, CU_TENSOR_MAP_SWIZZLE_128B) !=
+  if (kvr_encode_tensor_map_2d(&mv, v, 128, (uint64_t)prm.n_rows, 256, 64, Cfg::TM, CU_TENSOR_MAP_SWIZZLE_128B) !=
       CUDA_SUCCESS)
     return KVR_ERR_CUDA;
-  auto kern = store_tc_kernel<ORDER, F16>;
+  auto kern = store_tc_kernel<ORDER, F16, LEARNED>;
   static bool attr_set[KVR_MAX_DEVICES];
   const int dev = kvr_current_device();
   if (!attr_set[dev]) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, k1tc::SMEM) != cudaSuccess)
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess)
       return KVR_ERR_CUDA;
     attr_set[dev] = true;
   }
@@ -1045,8 +1217,8 @@ static int launch_tc_impl(const void* k, const void* v, int64_t n_tok, const int
   if (grid > total) grid = total;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(k1tc::THREADS);
-  cfg.dynamicSmemBytes = k1tc::SMEM;
+  cfg.blockDim = dim3(Cfg::THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1058,7 +1230,7 @@ static int launch_tc_impl(const void* k, const void* v, int64_t n_tok, const int
     cudaFuncAttributes fa{};
     cudaFuncGetAttributes(&fa, kern);
     fprintf(stderr, "[kvr] store_tc launch: %s (regs %d, max threads %d, smem %d)\n", cudaGetErrorString(e), fa.numRegs,
-            fa.maxThreadsPerBlock, k1tc::SMEM);
+            fa.maxThreadsPerBlock, Cfg::SMEM);
     return KVR_ERR_CUDA;
   }
   return 0;
@@ -1097,14 +1269,14 @@ int kvr_launch_store_fast(const void* k, const void* v, int in_dtype, int64_t n_
   const int sms = kvr_num_sms() > 0 ? kvr_num_sms() : 148;
   if (k1_use_tc() && (tiles >= 4 * (int64_t)sms || k1_forced_tc)) {
     switch (order) {
-      case 128: return f16 ? launch_tc_impl<128, true>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st)
-                           : launch_tc_impl<128, false>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st);
-      case 64: return f16 ? launch_tc_impl<64, true>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st)
-                          : launch_tc_impl<64, false>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st);
-      case 32: return f16 ? launch_tc_impl<32, true>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st)
-                          : launch_tc_impl<32, false>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st);
-      case 16: return f16 ? launch_tc_impl<16, true>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st)
-                          : launch_tc_impl<16, false>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st);
+      case 128: return f16 ? launch_tc_impl<128, true, false>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st)
+                           : launch_tc_impl<128, false, false>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st);
+      case 64: return f16 ? launch_tc_impl<64, true, false>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st)
+                          : launch_tc_impl<64, false, false>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st);
+      case 32: return f16 ? launch_tc_impl<32, true, false>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st)
+                          : launch_tc_impl<32, false, false>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st);
+      case 16: return f16 ? launch_tc_impl<16, true, false>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st)
+                          : launch_tc_impl<16, false, false>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st);
     }
     return KVR_ERR_UNSUPPORTED;
   }
@@ -1120,3 +1292,60 @@ int kvr_launch_store_fast(const void* k, const void* v, int in_dtype, int64_t n_
   }
   return KVR_ERR_UNSUPPORTED;
 }
+
+// Row f3: K1 with the learned R fused (bf16 rows, d = 128; K mode 2, V mode 0 / 1 / 2).
+int kvr_launch_store_learned(const void* k, const void* v, int in_dtype, int64_t n_tok, const int64_t* slots,
+                             const Pool& pool, int order, int mode_v, const Signs& s, int has, const void* t_img,
+                             const double* rt, uint32_t* flags, cudaStream_t st) {
+  if (pool.d != 128 || pool.T != 16 || (pool.P & (pool.P - 1)) || (pool.cell_bytes & 15)) return KVR_ERR_UNSUPPORTED;
+  if (in_dtype != KVR_BF16) return KVR_ERR_UNSUPPORTED;
+  if ((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(t_img) |
+       reinterpret_cast<uintptr_t>(rt)) & 15)
+    return KVR_ERR_UNSUPPORTED;
+  static float kappa = -1.f;  // margin per unit of ||y||_2 / s: 2^-20 (KVR_K1L_KAPPA_LOG2 overrides, for tests)
+  if (kappa < 0.f) {
+    const char* e = getenv("KVR_K1L_KAPPA_LOG2");
+    const int l2 = e ? atoi(e) : -20;
+    kappa = ldexpf(1.0f, l2 + 16);
+    if (e && l2 <= -64) kappa = 0.f;
+  }
+  const LearnedArgs la{t_img, rt, kappa};
+  switch (order) {
+    case 128: return launch_tc_impl<128, false, true>(k, v, n_tok, slots, pool, 2, mode_v, s, has, flags, st, &la);
+    case 64: return launch_tc_impl<64, false, true>(k, v, n_tok, slots, pool, 2, mode_v, s, has, flags, st, &la);
+    case 32: return launch_tc_impl<32, false, true>(k, v, n_tok, slots, pool, 2, mode_v, s, has, flags, st, &la);
+    case 16: return launch_tc_impl<16, false, true>(k, v, n_tok, slots, pool, 2, mode_v, s, has, flags, st, &la);
+  }
+  return KVR_ERR_UNSUPPORTED;
+}
+
+// The shared-memory image of T's three bf16 parts: part p at p * 32 KB, B[n][k] = T[k][n] in the SW128
+// K-major layout of the kernel's B operand (two 64-column boxes of 128 rows x 128 B).
+static uint16_t bf16_rn(double x) {
+  const float f = (float)x;
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+static double bf16_val(uint16_t b) {
+  const uint32_t u = (uint32_t)b << 16;
+  float f;
+  memcpy(&f, &u, 4);
+  return (double)f;
+}
+void kvr_pack_learned_image(const double* t, uint16_t* img) {
+  for (int kk = 0; kk < 128; ++kk)
+    for (int n = 0; n < 128; ++n) {
+      double r = t[kk * 128 + n];
+      const int byte = (kk & 63) * 2;
+      const size_t off = (size_t)(kk >> 6) * 16384 + (n >> 3) * 1024 + (n & 7) * 128 + (((byte >> 4) ^ (n & 7)) << 4) +
+                         (byte & 15);
+      for (int pp = 0; pp < 3; ++pp) {
+        const uint16_t b = bf16_rn(r);
+        img[(pp * 32768 + off) / 2] = b;
+        r -= bf16_val(b);
+      }
+    }
+}
+

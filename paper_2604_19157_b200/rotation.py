@@ -127,6 +127,22 @@ def learned_on(spec: RotationSpec, device) -> Optional[torch.Tensor]:
     return cache[key]
 
 
+def learned_store_operands(spec: RotationSpec, layout: HeadLayout, device):
+    """Row f3, fused K1 operands (memoised per device and layout): the kernel's
+    shared-memory image of the dense T = diag(s) H_blk R (compose_transform,
+    rotation.py:171-184) as three bf16 parts, and R^T in f64 for the kernel's exact
+    recomputation of codes near a rounding boundary."""
+    cache = spec.__dict__.setdefault("_learned_store", {})
+    key = (str(torch.device(device)), layout.head_dim, layout.rot_order)
+    if key not in cache:
+        t = np.ascontiguousarray(compose_transform(spec, layout), dtype=np.float64)
+        img = np.zeros(3 * t.shape[0] * t.shape[1], dtype=np.uint16)
+        _lib.lib().kvr_learned_pack_image(t.ctypes.data, img.ctypes.data)
+        rt = np.ascontiguousarray(np.asarray(spec.learned, dtype=np.float64).T)
+        cache[key] = (torch.from_numpy(img).to(device), torch.from_numpy(rt).to(device))
+    return cache[key]
+
+
 def rotate_kv_learned(k: torch.Tensor, v: torch.Tensor, layout: HeadLayout, spec: RotationSpec):
     """Row f3 (learned R composed after the Hadamard), unfused on the device: the
     K rows through the full transform, the V rows through value_branch_spec

@@ -14,7 +14,7 @@ import torch
 
 pytestmark = pytest.mark.gpu
 
-from kvtest_util import gen_rows, page_fields  # noqa: E402
+from kvtest_util import bf16_round, gen_rows, page_fields  # noqa: E402
 from oracle import kvrot_oracle as O  # noqa: E402
 from paper_2604_19157_b200.attention import DecodePlan, decode_batch  # noqa: E402
 from paper_2604_19157_b200.cache import PageTable  # noqa: E402
@@ -116,3 +116,96 @@ def test_learned_serving_step():
             o = O.decode_flat(_ref_rotate(q[b], spec, False), kd[b, :L].cpu().numpy(), vd[b, :L].cpu().numpy(), G)
             o = O.unrotate_rows(o @ spec.learned.T, spec.order, spec.signs)
             assert np.abs(out[b] - o).max() / np.abs(o).max() <= TOL
+
+
+def _bf16(a):
+    return torch.tensor(bf16_round(a), dtype=torch.float64).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("order", [128, 32])
+@pytest.mark.parametrize("targets,learned_values", [(Targets.KEYS_AND_VALUES, False), (Targets.KEYS_AND_VALUES, True),
+                                                    (Targets.KEYS_ONLY, False)])
+def test_learned_fused_store_bf16(monkeypatch, order, targets, learned_values):
+    """Row f3 fused: bf16 rows through the tcgen05 K1 with T = diag(s) H_blk R in shared memory.
+    Bars: codes at most one step from the reference composition (f64 FWHT then R), with the
+    mismatch count reported and <= 1e-4 of the nibbles; zero points at most one step, in
+    <= 1e-4 of the rows; scales within rtol 1e-5 (f32 accumulation of the dense product; the
+    stated tolerance is 1e-3)."""
+    import paper_2604_19157_b200.rotation as rotmod
+
+    def _no_unfused(*a, **kw):
+        raise AssertionError("the fused learned K1 must take bf16 rows")
+
+    monkeypatch.setattr(rotmod, "rotate_kv_learned", _no_unfused)
+    H, G, d, P = 8, 4, 128, 16
+    lens = [7, 40, 1500, 2049]
+    layout = HeadLayout(num_q_heads=G * H, num_kv_heads=H, head_dim=d, rot_order=order, page_tokens=P)
+    t = PageTable(layout, num_pages=sum((L + P - 1) // P for L in lens) + 2)
+    spec = RotationSpec(order=order, signs=make_signs(4, 0, d, order), learned=_orth(d, 21), targets=targets,
+                        learned_values=learned_values)
+    kinds = ["gaussian", "outlier", "correlated", "gaussian"]
+    seqs, ks, vs = [], [], []
+    for s, L in enumerate(lens):
+        t.create_sequence(s)
+        seqs += [s] * L
+        ks.append(bf16_round(gen_rows(kinds[s], L * H, d, 300 + s)).reshape(L, H, d))
+        vs.append(bf16_round(gen_rows(kinds[3 - s], L * H, d, 400 + s)).reshape(L, H, d))
+    k, v = np.concatenate(ks), np.concatenate(vs)
+    t.append_batch(seqs, _bf16(k), _bf16(v), spec=spec)
+    t.check_flags()
+    kr = _ref_rotate(k.reshape(-1, d), spec, values=False)
+    vr = _ref_rotate(v.reshape(-1, d), spec, values=True)
+    mism = total = zmis = rows = 0
+    worst = 0.0
+    row = 0
+    for s, L in enumerate(lens):
+        f = page_fields(t.page_records(t.sequence_pages(s)), P, H, d)
+        for side, ref in (("k", kr), ("v", vr)):
+            pk_, sk, zk = O.quantize_rows(ref[row * H:(row + L) * H])
+            got = f[f"{side}_payload"].reshape(-1, H, d // 2)[:L].reshape(-1, d // 2)
+            dl = np.abs((got & 15).astype(int) - (pk_ & 15)) + np.abs((got >> 4).astype(int) - (pk_ >> 4))
+            assert dl.max() <= 1
+            mism += int((dl > 0).sum())
+            total += dl.size * 2
+            gz = f[f"{side}_zp"].reshape(-1, H)[:L].reshape(-1).astype(int)
+            assert np.abs(gz - zk.astype(int)).max() <= 1
+            zmis += int((gz != zk).sum())
+            rows += gz.size
+            gs = f[f"{side}_scale"].reshape(-1, H)[:L].reshape(-1).astype(np.float64)
+            worst = max(worst, float(np.max(np.abs(gs - sk) / np.abs(sk))))
+        row += L
+    print(f"learned fused (order {order}, {targets.name}, lv={learned_values}): nibble mismatches {mism} of {total}, "
+          f"zp {zmis} of {rows}, scale max rel {worst:.2e}")
+    assert mism <= total * 1e-4
+    assert zmis <= rows * 1e-4
+    assert worst <= 1e-5
+
+
+def test_learned_fused_nonfinite_and_skip():
+    """A NaN row is not written and raises the flag; negative slots are skipped; the other
+    rows are stored."""
+    H, d, P = 2, 128, 16
+    layout = HeadLayout(num_q_heads=4 * H, num_kv_heads=H, head_dim=d, rot_order=128, page_tokens=P)
+    t = PageTable(layout, num_pages=4)
+    spec = RotationSpec(order=128, signs=make_signs(4, 0, d, 128), learned=_orth(d, 5), learned_values=True)
+    t.create_sequence(0)
+    k = bf16_round(gen_rows("gaussian", 3 * H, d, 1)).reshape(3, H, d)
+    v = bf16_round(gen_rows("gaussian", 3 * H, d, 2)).reshape(3, H, d)
+    k[1, 0, 17] = np.nan
+    t.append_batch([0, 0, 0], _bf16(k), _bf16(v), spec=spec, check=False)
+    with pytest.raises(Exception):
+        t.check_flags()
+    f = page_fields(t.page_records(t.sequence_pages(0)), P, H, d)
+    kr = _ref_rotate(k.reshape(-1, d), spec, values=False)
+    pk_, sk, zk = O.quantize_rows(np.nan_to_num(kr))
+    got = f["k_payload"].reshape(-1, H, d // 2)[:3].reshape(-1, d // 2)
+    for r in (0, 1, 3, 4, 5):  # row 2 = token 1, head 0: the NaN row
+        dl = np.abs((got[r] & 15).astype(int) - (pk_[r] & 15)) + np.abs((got[r] >> 4).astype(int) - (pk_[r] >> 4))
+        assert dl.max() <= 1
+    assert not got[2].any()
+    # skipped slots: nothing written
+    slots = torch.full((2,), -1, dtype=torch.int64, device="cuda")
+    before = t.page_records(t.sequence_pages(0)).copy()
+    t.store_slots(_bf16(k[:2]).cuda(), _bf16(v[:2]).cuda(), slots, spec=spec)
+    torch.cuda.synchronize()
+    assert np.array_equal(before, t.page_records(t.sequence_pages(0)))
