@@ -288,7 +288,19 @@ def run_ours(args, rank, world, local_rank):
     t_k2 = timed(lambda i: k2(sets[i % R]), n_k) / n_k
     t_k1p = timed(lambda i: k1(sets[i % R], None), n_k) / n_k
     t_k2p = timed(lambda i: k2(sets[i % R], None), n_k) / n_k
-    # restore the rotated token in every set (the plain twin overwrote slot L)
+    # row f3 at C2: a learned spec (same signs, an orthogonal R, learned_values) -- the decode with
+    # the query through T and the output through T^T (one row-matmul launch each), and the serving
+    # step (new token through the exact f64 transform + store, then that decode).  Same bytes read;
+    # the values decoded are not meaningful (the pool was written with the Hadamard spec).
+    qm_, rm_ = np.linalg.qr(np.random.default_rng(7).standard_normal((D, D)))
+    lspec = RotationSpec(order=ORDER, signs=spec.signs, learned=qm_ * np.sign(np.diag(rm_)), learned_values=True)
+    t_k2l = timed(lambda i: k2(sets[i % R], lspec), n_k) / n_k
+    t_fl = timed(lambda i: fused(sets[i % R], lspec), n_k) / n_k
+    learned_c2 = {"decode_us": round(t_k2l * 1e3, 3), "step_us": round(t_fl * 1e3, 3),
+                  "hadamard_decode_us": round(t_k2 * 1e3, 3), "hadamard_step_us": round(t_fused * 1e3, 3),
+                  "launches_decode": "rows_matmul(q T) + decode + rows_matmul(out T^T)"}
+    print(f"[bench] learned R at C2 {learned_c2}", file=sys.stderr, flush=True)
+    # restore the rotated token in every set (the plain / learned twins overwrote slot L)
     for s in sets:
         k1(s)
     torch.cuda.synchronize()
@@ -381,6 +393,7 @@ def run_ours(args, rank, world, local_rank):
             "fused_step_us": round(t_fr * 1e3, 3), "fused_step_plain_us": round(t_fp * 1e3, 3),
             "fused_step_overhead_vs_plain": round(t_fr / t_fp - 1.0, 4),
             "c1_quantize_store": c1,
+            "c2_learned_r": learned_c2,
             "c2_input_variants": c2v,
             "c3_concurrency_sweep": c3,
             "c4_llama70b": c4,

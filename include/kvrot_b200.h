@@ -191,6 +191,17 @@ int kvr_block_rotate(const void* x, int32_t in_dtype, void* out, int32_t out_dty
                      void* stream);
 
 /*
+ * Dense factor of a rotation spec (row f3): y = x M for rows (n, d), M a device f64
+ * [d][d] row-major matrix, f64 arithmetic (k ascending).  Replaces the learned R's
+ * `out @ spec.learned` / `out @ spec.learned.T` (rotation.py:140-141, 154-155) and applies
+ * the composed T = diag(s) H_blk R (compose_transform, rotation.py:171-184) to decode
+ * queries and T^T to outputs in one launch.  in_dtype {F64, F32, BF16, F16}, out_dtype
+ * {F64, F32}; x and y must not alias; d <= 768.
+ */
+int kvr_rows_matmul_f64(const void* x, int32_t in_dtype, const double* m, void* y, int32_t out_dtype, int64_t n,
+                        int32_t d, void* stream);
+
+/*
  * K1: fused rotate -> token-wise INT4 quantize -> paged store.
  *   k, v         : (n_tok, H, d) rows of in_dtype (F64/F32/BF16/F16), contiguous
  *   slot_mapping : int64[n_tok] device, page_id * P + slot; negative = skip

@@ -33,7 +33,7 @@ EXPORTED = (
     "kvr_host_all_finite", "kvr_decode_flat_f64", "kvr_step_stage", "kvr_step_launch",
     "kvr_step_ring_create", "kvr_step_ring_set_slot", "kvr_step_ring_run", "kvr_step_ring_destroy",
     "kvr_step_ring_set_copy_stream", "kvr_step_ring_set_decode", "kvr_debug_step_ring_times",
-    "kvr_rotate_quantize_store_learned", "kvr_learned_pack_image",
+    "kvr_rotate_quantize_store_learned", "kvr_learned_pack_image", "kvr_rows_matmul_f64",
 )
 
 
@@ -89,6 +89,7 @@ def _declare(lib):
         "kvr_rotate_quantize_store_learned": (_I32, [_P, _P, _I32, _I64, _P, ctypes.POINTER(KvrPool), _I32, _I32,
                                                      _I32, _P, _P, _P, _P, _P]),
         "kvr_learned_pack_image": (None, [_P, _P]),
+        "kvr_rows_matmul_f64": (_I32, [_P, _I32, _P, _P, _I32, _I64, _I32, _P]),
         "kvr_dequantize_pages": (_I32, [ctypes.POINTER(KvrPool), _P, _I32, _P, _I32, _I32, _P, _P, _I32, _P]),
         "kvr_decode_workspace_bytes": (_SZ, [_I32, _I32, _I32, _I32, _I32]),
         "kvr_decode_pick_splits": (_I32, [_I32, _I32, _I32, _I32]),

@@ -22,7 +22,7 @@ from . import _kernels, _lib
 from .cache import INT4, PageTable
 from .errors import EmptySequenceError, NonFiniteInputError, ShapeError
 from .layout import HeadLayout
-from .rotation import RotationSpec, Targets, apply_block_rotation, apply_inverse_rotation, value_branch_spec
+from .rotation import RotationSpec, Targets, composed_on, rows_matmul
 
 _Q_CODE = {torch.float32: _lib.KVR_F32, torch.bfloat16: _lib.KVR_BF16, torch.float16: _lib.KVR_F16}
 _KV_CODE = {torch.float64: _lib.KVR_F64, **_Q_CODE}
@@ -173,16 +173,21 @@ class DecodePlan:
 
 
     def _run_learned(self, q: torch.Tensor, spec: RotationSpec, out: torch.Tensor) -> torch.Tensor:
-        """Row f3, unfused: q through the full transform (signs, H, learned R) in f64
-        on the device, the INT4 decode kernel on the pre-rotated query, then the
-        value branch's inverse transform on the output (attention.py:63-85)."""
+        """Row f3: the query through the composed T = diag(s) H_blk R (one f64
+        row-matmul launch, f32 out), the INT4 decode kernel on the pre-rotated query,
+        then the value branch's T^T on the output (one launch) (attention.py:63-85)."""
         lay = self.table.layout
-        d = lay.head_dim
-        qr = apply_block_rotation(q.reshape(-1, d), lay, spec).reshape(q.shape).float()
-        self.run(qr, None, out)
-        vspec = value_branch_spec(spec)
-        if vspec is not None:
-            out.copy_(apply_inverse_rotation(out.reshape(-1, d), lay, vspec).reshape(out.shape))
+        dev = self.table.device
+        qr = getattr(self, "_lq", None)
+        if qr is None or qr.shape != q.shape:
+            qr = self._lq = torch.empty(q.shape, dtype=torch.float32, device=dev)
+            self._lo = torch.empty(q.shape, dtype=torch.float32, device=dev)
+        rows_matmul(q, composed_on(spec, lay, dev), out=qr)
+        tv = composed_on(spec, lay, dev, transpose=True, values=True)
+        if tv is None:
+            return self.run(qr, None, out)
+        self.run(qr, None, self._lo)
+        rows_matmul(self._lo, tv, out=out)
         return out
 
     def run_step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, slots: torch.Tensor,

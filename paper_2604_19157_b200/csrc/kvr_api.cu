@@ -488,6 +488,18 @@ int kvr_block_rotate(const void* x, int32_t in_dtype, void* out, int32_t out_dty
   return check_launch("block_rotate");
 }
 
+int kvr_rows_matmul_f64(const void* x, int32_t in_dtype, const double* m, void* y, int32_t out_dtype, int64_t n,
+                        int32_t d, void* stream) {
+  if (n < 0 || d < 1) return fail(KVR_ERR_SHAPE, "rows_matmul: bad shape (n=%lld, d=%d)", (long long)n, d);
+  if (d > 768) return fail(KVR_ERR_UNSUPPORTED, "rows_matmul: dim %d > 768", d);
+  if (n == 0) return KVR_OK;
+  if (!x || !m || !y) return fail(KVR_ERR_ARG, "rows_matmul: null pointer");
+  if (x == y) return fail(KVR_ERR_ARG, "rows_matmul: in-place (x == y) is not supported");
+  int rc = kvr_launch_rows_matmul(x, in_dtype, m, y, out_dtype, n, d, (cudaStream_t)stream);
+  if (rc) return fail(rc, "rows_matmul: unsupported dtype combination (%d -> %d)", in_dtype, out_dtype);
+  return check_launch("rows_matmul_f64");
+}
+
 int kvr_rotate_quantize_store(const void* k, const void* v, int32_t in_dtype, int64_t n_tok,
                               const int64_t* slot_mapping, const kvr_pool* pool, int32_t rot_order, int32_t rotate,
                               int32_t targets, const uint32_t* sign_words, int32_t exact, uint32_t* flags,

@@ -29,6 +29,9 @@ int kvr_launch_dequant_pages(const kvr::Pool& pool, const int32_t* bt, int bt_st
 int kvr_launch_decode_flat_f64(const double* q, const double* k, const double* v, int64_t t, int nq, int H, int d,
                                double* out, cudaStream_t st);
 
+int kvr_launch_rows_matmul(const void* x, int in_dtype, const double* m, void* y, int out_dtype, int64_t n, int d,
+                           cudaStream_t st);
+
 // Fast serving-path write (bf16/fp16 rows, head_dim 128): returns KVR_ERR_UNSUPPORTED
 // when the configuration has no specialised kernel (caller falls back to the exact path).
 int kvr_launch_store_fast(const void* k, const void* v, int in_dtype, int64_t n_tok, const int64_t* slots,

@@ -116,6 +116,99 @@ __global__ void block_rotate_kernel(const TIn* x, TOut* out, int64_t n, int d, i
   }
 }
 
+// Row f3's dense factor: y = x M in f64 (M [d][d] row-major), the learned R of
+// rotation.py:140-141 / 154-155 (M = R or R^T) and the composed transforms of the query
+// prep and the output's value branch (M = T = diag(s) H_blk R, or T^T).  Latency-shaped
+// for the few rows of a decode step: a CTA owns 8 rows (staged in shared memory as f64)
+// and 32 output columns; its 16 warps split k (warp = k group, lane = column: every M
+// read is a coalesced 256-B row segment), the first 8 M values per thread are loaded
+// before the grid-dependency wait (M is constant, x may be the previous kernel's output),
+// and the 16 partial sums are added in k-group order through shared memory.
+constexpr int RM_ROWS = 8, RM_COLS = 32, RM_KG = 16;
+template <typename TIn, typename TOut>
+__global__ void __launch_bounds__(RM_COLS * RM_KG) rows_matmul_kernel(const TIn* x, const double* __restrict__ m,
+                                                                       TOut* y, int64_t n, int d) {
+  extern __shared__ double rm_sm[];  // xs [RM_ROWS][d] | part [RM_KG][RM_ROWS][RM_COLS]
+  double* xs = rm_sm;
+  double* part = rm_sm + RM_ROWS * d;
+  const int c = threadIdx.x & (RM_COLS - 1), kg = threadIdx.x / RM_COLS;
+  const int col = blockIdx.y * RM_COLS + c;
+  const int kq = (d + RM_KG - 1) / RM_KG, k0 = kg * kq, k1 = min(d, k0 + kq);
+  const bool live = col < d;
+  double mk[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) mk[u] = (live && k0 + u < k1) ? __ldg(m + (size_t)(k0 + u) * d + col) : 0.0;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int64_t r0 = (int64_t)blockIdx.x * RM_ROWS;
+  const int nr = (int)((n - r0) < RM_ROWS ? (n - r0) : RM_ROWS);
+  for (int i = threadIdx.x; i < RM_ROWS * d; i += blockDim.x) {
+    const int r = i / d, k = i - r * d;
+    xs[i] = r < nr ? load_as_f64<TIn>(x, (r0 + r) * d + k) : 0.0;
+  }
+  __syncthreads();
+  double acc[RM_ROWS];
+#pragma unroll
+  for (int r = 0; r < RM_ROWS; ++r) acc[r] = 0.0;
+  if (live) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (k0 + u < k1)
+#pragma unroll
+        for (int r = 0; r < RM_ROWS; ++r) acc[r] = fma(xs[r * d + k0 + u], mk[u], acc[r]);
+    for (int k = k0 + 8; k < k1; ++k) {
+      const double mv = __ldg(m + (size_t)k * d + col);
+#pragma unroll
+      for (int r = 0; r < RM_ROWS; ++r) acc[r] = fma(xs[r * d + k], mv, acc[r]);
+    }
+  }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#pragma unroll
+  for (int r = 0; r < RM_ROWS; ++r) part[(kg * RM_ROWS + r) * RM_COLS + c] = acc[r];
+  __syncthreads();
+  if (threadIdx.x < RM_ROWS * RM_COLS) {
+    const int r = threadIdx.x / RM_COLS, cc = threadIdx.x & (RM_COLS - 1);
+    const int oc = blockIdx.y * RM_COLS + cc;
+    if (r < nr && oc < d) {
+      double v = part[r * RM_COLS + cc];
+#pragma unroll
+      for (int g = 1; g < RM_KG; ++g) v += part[(g * RM_ROWS + r) * RM_COLS + cc];
+      y[(r0 + r) * d + oc] = (TOut)v;
+    }
+  }
+}
+
+template <typename TIn>
+static int rows_matmul_out(const void* x, const double* m, void* y, int out_dtype, int64_t n, int d, cudaStream_t st) {
+  const size_t sm = (size_t)RM_ROWS * d * 8 + (size_t)RM_KG * RM_ROWS * RM_COLS * 8;
+  auto kd = rows_matmul_kernel<TIn, double>;
+  auto kf = rows_matmul_kernel<TIn, float>;
+  static bool attr_set[KVR_MAX_DEVICES];
+  const int dev = kvr_current_device();
+  if (!attr_set[dev]) {  // up to d = 768: 48 KB + 32 KB
+    cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    attr_set[dev] = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((n + RM_ROWS - 1) / RM_ROWS), (unsigned)((d + RM_COLS - 1) / RM_COLS));
+  cfg.blockDim = dim3(RM_COLS * RM_KG);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  if (out_dtype == KVR_F64)
+    e = cudaLaunchKernelEx(&cfg, kd, (const TIn*)x, m, (double*)y, n, d);
+  else if (out_dtype == KVR_F32)
+    e = cudaLaunchKernelEx(&cfg, kf, (const TIn*)x, m, (float*)y, n, d);
+  else
+    return KVR_ERR_UNSUPPORTED;
+  return e == cudaSuccess ? 0 : KVR_ERR_CUDA;
+}
+
 // Generic exact fused write: warp per (token, head, side) row, f64 arithmetic.
 // Row order: all K rows (token-major, head-minor) then all V rows.
 template <typename TIn>
@@ -477,6 +570,17 @@ int kvr_launch_block_rotate(const void* x, int in_dtype, void* out, int out_dtyp
     case KVR_F32: return rotate_dispatch_out<float>(x, out, out_dtype, n, d, order, s, has, inv, st);
     case KVR_BF16: return rotate_dispatch_out<__nv_bfloat16>(x, out, out_dtype, n, d, order, s, has, inv, st);
     case KVR_F16: return rotate_dispatch_out<__half>(x, out, out_dtype, n, d, order, s, has, inv, st);
+  }
+  return KVR_ERR_ARG;
+}
+
+int kvr_launch_rows_matmul(const void* x, int in_dtype, const double* m, void* y, int out_dtype, int64_t n, int d,
+                           cudaStream_t st) {
+  switch (in_dtype) {
+    case KVR_F64: return rows_matmul_out<double>(x, m, y, out_dtype, n, d, st);
+    case KVR_F32: return rows_matmul_out<float>(x, m, y, out_dtype, n, d, st);
+    case KVR_BF16: return rows_matmul_out<__nv_bfloat16>(x, m, y, out_dtype, n, d, st);
+    case KVR_F16: return rows_matmul_out<__half>(x, m, y, out_dtype, n, d, st);
   }
   return KVR_ERR_ARG;
 }

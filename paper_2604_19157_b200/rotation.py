@@ -3,8 +3,10 @@
 Row convention as in the reference (rotation.py:118-159):
     forward  x -> x diag(s) H_blk R      inverse  x -> x R^T H_blk diag(s)
 The block butterfly runs in the native library in f64 (bit-identical to the
-reference).  The optional learned factor R (Hessian calibration, out of scope
-for the serving kernels) is applied as an f64 GEMM on the device.
+reference).  The optional learned factor R (row f3; its Hessian calibration is out
+of scope) is applied by the library's f64 row-matmul kernel (kvr_rows_matmul_f64),
+composed with the butterfly into one dense T for decode queries and outputs, and
+fused into the tcgen05 K1 for bf16 writes (kvr_rotate_quantize_store_learned).
 """
 
 from __future__ import annotations
@@ -103,27 +105,61 @@ def _rotate(x, layout: HeadLayout, spec: RotationSpec, inverse: bool):
         raise ShapeError(f"expected (n, {layout.head_dim}) rows, got {tuple(t.shape)}")
     _check_spec_layout(spec, layout)
     n, d = t.shape
-    learned = learned_on(spec, t.device)
-    if inverse and learned is not None:
-        t = (t @ learned.T).contiguous()
+    if inverse and spec.learned is not None:
+        t = rows_matmul(t, learned_on(spec, t.device, transpose=True))
     out = torch.empty_like(t)
     _lib.check(_lib.lib().kvr_block_rotate(_kernels.ptr(t), _lib.KVR_F64, _kernels.ptr(out), _lib.KVR_F64, n, d,
                                            spec.order, spec.sign_words(d), 1 if inverse else 0,
                                            _kernels.stream_ptr()))
-    if not inverse and learned is not None:
-        out = out @ learned
+    if not inverse and spec.learned is not None:
+        out = rows_matmul(out, learned_on(spec, t.device))
     return out.cpu().numpy() if is_np else out
 
 
-def learned_on(spec: RotationSpec, device) -> Optional[torch.Tensor]:
-    """The learned factor as an f64 device tensor (memoised per device, so graph
-    capture and steady-state steps do no host->device copy)."""
+def rows_matmul(x: torch.Tensor, m: torch.Tensor, out: Optional[torch.Tensor] = None,
+                out_dtype=torch.float64) -> torch.Tensor:
+    """y = x @ m on the device in f64 arithmetic (kvr_rows_matmul_f64): the learned
+    factor of row f3 (rotation.py:140-141, 154-155) and the composed transforms."""
+    x = x.contiguous()
+    n, d = x.shape[0], x.shape[-1]
+    if out is None:
+        out = torch.empty(x.shape, dtype=out_dtype, device=x.device)
+    code = {torch.float64: _lib.KVR_F64, torch.float32: _lib.KVR_F32, torch.bfloat16: _lib.KVR_BF16,
+            torch.float16: _lib.KVR_F16}
+    _lib.check(_lib.lib().kvr_rows_matmul_f64(_kernels.ptr(x), code[x.dtype], _kernels.ptr(m), _kernels.ptr(out),
+                                              code[out.dtype], x.numel() // d, d, _kernels.stream_ptr()))
+    return out
+
+
+def learned_on(spec: RotationSpec, device, transpose: bool = False) -> Optional[torch.Tensor]:
+    """The learned factor (or its transpose) as a contiguous f64 device tensor (memoised
+    per device, so graph capture and steady-state steps do no host->device copy)."""
     if spec.learned is None:
         return None
     cache = spec.__dict__.setdefault("_learned_dev", {})
-    key = str(torch.device(device))
+    key = (str(torch.device(device)), transpose)
     if key not in cache:
-        cache[key] = torch.from_numpy(np.array(spec.learned, dtype=np.float64)).to(device)
+        r = np.array(spec.learned, dtype=np.float64)
+        cache[key] = torch.from_numpy(np.ascontiguousarray(r.T if transpose else r)).to(device)
+    return cache[key]
+
+
+def composed_on(spec: RotationSpec, layout: HeadLayout, device, transpose: bool = False,
+                values: bool = False) -> Optional[torch.Tensor]:
+    """The dense T = diag(s) H_blk R (compose_transform, rotation.py:171-184), or T^T,
+    as a contiguous f64 device tensor (memoised on the spec per device and layout): one
+    kvr_rows_matmul_f64 launch applies the whole transform to decode queries (T) or
+    maps decode outputs back (T^T, T orthogonal).  values=True: the value branch's
+    transform (value_branch_spec, rotation.py:162-168); None when values stay raw."""
+    cache = spec.__dict__.setdefault("_composed_dev", {})
+    key = (str(torch.device(device)), layout.head_dim, layout.rot_order, transpose, values)
+    if key not in cache:
+        sp = value_branch_spec(spec) if values else spec
+        if sp is None:
+            cache[key] = None
+        else:
+            t = compose_transform(sp, layout)
+            cache[key] = torch.from_numpy(np.ascontiguousarray(t.T if transpose else t)).to(device)
     return cache[key]
 
 
@@ -148,9 +184,9 @@ def rotate_kv_learned(k: torch.Tensor, v: torch.Tensor, layout: HeadLayout, spec
     K rows through the full transform, the V rows through value_branch_spec
     (rotation.py:118-142, 162-168).  Returns f64 tensors shaped like k / v."""
     d = layout.head_dim
-    kr = apply_block_rotation(k.reshape(-1, d), layout, spec).reshape(k.shape)
-    vspec = value_branch_spec(spec)
-    vr = v.to(torch.float64) if vspec is None else apply_block_rotation(v.reshape(-1, d), layout, vspec).reshape(v.shape)
+    kr = rows_matmul(k.reshape(-1, d), composed_on(spec, layout, k.device)).reshape(k.shape)
+    tv = composed_on(spec, layout, v.device, values=True)
+    vr = v.to(torch.float64) if tv is None else rows_matmul(v.reshape(-1, d), tv).reshape(v.shape)
     return kr.contiguous(), vr.contiguous()
 
 

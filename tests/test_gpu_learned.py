@@ -209,3 +209,34 @@ def test_learned_fused_nonfinite_and_skip():
     t.store_slots(_bf16(k[:2]).cuda(), _bf16(v[:2]).cuda(), slots, spec=spec)
     torch.cuda.synchronize()
     assert np.array_equal(before, t.page_records(t.sequence_pages(0)))
+
+
+@pytest.mark.parametrize("n,d,dt", [(1, 128, torch.float64), (37, 128, torch.float32), (300, 64, torch.bfloat16),
+                                    (9, 256, torch.float16)])
+def test_rows_matmul_f64(n, d, dt):
+    """kvr_rows_matmul_f64 (the learned factor and the composed transforms) vs numpy f64."""
+    from paper_2604_19157_b200.rotation import rows_matmul
+
+    rng = np.random.default_rng(n + d)
+    x = torch.tensor(rng.standard_normal((n, d))).to(dt).cuda()
+    m = torch.tensor(_orth(d, 3)).cuda()
+    y = rows_matmul(x, m).cpu().numpy()
+    ref = x.double().cpu().numpy() @ m.cpu().numpy()
+    assert np.abs(y - ref).max() <= 1e-12 * np.abs(ref).max()
+    y32 = rows_matmul(x, m, out_dtype=torch.float32).cpu().numpy()
+    assert np.abs(y32 - ref).max() <= 1e-6 * np.abs(ref).max()
+
+
+def test_learned_composed_matches_reference_order():
+    """The composed T (one launch) agrees with the reference's FWHT-then-R order to f64 rounding."""
+    from paper_2604_19157_b200.rotation import composed_on, rows_matmul
+
+    d = 128
+    layout = HeadLayout(num_q_heads=8, num_kv_heads=2, head_dim=d, rot_order=64, page_tokens=16)
+    spec = RotationSpec(order=64, signs=make_signs(2, 1, d, 64), learned=_orth(d, 8), learned_values=True)
+    x = np.random.default_rng(1).standard_normal((50, d))
+    got = rows_matmul(torch.tensor(x).cuda(), composed_on(spec, layout, "cuda")).cpu().numpy()
+    ref = _ref_rotate(x, spec, values=False)
+    assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
+    back = rows_matmul(torch.tensor(got).cuda(), composed_on(spec, layout, "cuda", transpose=True)).cpu().numpy()
+    assert np.abs(back - x).max() <= 1e-13 * np.abs(x).max()
