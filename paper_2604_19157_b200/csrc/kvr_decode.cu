@@ -1289,37 +1289,33 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
     }
     __syncthreads();
     KVR_STAMP(7);  // merge inputs landed
-    if (warp == 0) {
-      // lane l: dims 4l..4l+3 of q head j, the S partials LSE-weighted in one pass (no shuffles)
-      // (S <= 32: a fixed trip count of independent pairs keeps the chains short)
-      float m2[2] = {-INFINITY, -INFINITY};
+    {
+      // all 16 warps: warp w owns dims 8 w .. 8 w + 7, lane = (split group sg = lane >> 3, dim); lane l
+      // also holds split l's LSE (S <= 32), so the max and the weight sum are warp reductions and
+      // each split's weight a shuffle.  Runs once per launch with no other warps to hide latency:
+      // short per-warp instruction streams, every load independent.
+      const float lv = lane < S ? sl[lane] : -INFINITY;
+      float mx = lv;
 #pragma unroll
-      for (int sp = 0; sp < 32; ++sp)
-        if (sp < S) m2[sp & 1] = fmaxf(m2[sp & 1], sl[sp]);
-      const float mx = fmaxf(m2[0], m2[1]);
-      float tot[2] = {0.f, 0.f}, o4[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-      if (mx != -INFINITY) {
-#pragma unroll 4
-        for (int sp = 0; sp < S; ++sp) {
-          const float l = sl[sp];
-          const float w = (l == -INFINITY) ? 0.f : ex2f(l - mx);
-          const float4 v = *reinterpret_cast<const float4*>(so + sp * 128 + 4 * lane);
-          const int e = sp & 1;
-          tot[e] += w;
-          o4[e][0] = fmaf(w, v.x, o4[e][0]);
-          o4[e][1] = fmaf(w, v.y, o4[e][1]);
-          o4[e][2] = fmaf(w, v.z, o4[e][2]);
-          o4[e][3] = fmaf(w, v.w, o4[e][3]);
-        }
+      for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      const float wl = (lv == -INFINITY) ? 0.f : ex2f(lv - mx);
+      float tot = wl;
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+      const int sg = lane >> 3, dd = 8 * warp + (lane & 7);
+      float acc = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int sp = sg + 4 * k;
+        const float w = __shfl_sync(0xffffffffu, wl, sp & 31);
+        if (sp < S) acc = fmaf(w, so[sp * 128 + dd], acc);
       }
-      const float tt = tot[0] + tot[1];
-      const float inv = tt > 0.f ? 1.0f / tt : 0.f;
-      *reinterpret_cast<float4*>(obuf + 4 * lane) =
-          make_float4((o4[0][0] + o4[1][0]) * inv, (o4[0][1] + o4[1][1]) * inv, (o4[0][2] + o4[1][2]) * inv,
-                      (o4[0][3] + o4[1][3]) * inv);
-      __syncwarp();
-      emit_head<ORDER>(p, sgw, b, h, j, obuf, lane);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 8);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 16);
+      if (sg == 0) obuf[dd] = tot > 0.f ? acc / tot : 0.f;
     }
+    __syncthreads();  // the merged row is in obuf
+    if (warp == 0) emit_head<ORDER>(p, sgw, b, h, j, obuf, lane);
     if (threadIdx.x == 0) p.ws_epoch[((int64_t)b * H + h) * 8 + j] = want;  // read again only by the next launch
     KVR_STAMP(9);  // merged + stored
     return;

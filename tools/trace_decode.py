@@ -99,6 +99,10 @@ for splits in split_list:
         if ok.any():
             t = (g0[ok] + (raw[ok, k] - raw[ok, 1]) * 1e3 / MHZ) / 1e3
             out_lines.append(f"{nm:16s}: n {ok.sum():4d} min {t.min():6.2f} med {np.median(t):6.2f} max {t.max():6.2f} us")
+    if os.environ.get("TR_MERGE_ROWS"):  # per merger CTA: stamps (ns) relative to 'merge in' (7)
+        for r_ in raw[(raw[:, 7] > raw[:, 1])][:6]:
+            rel = {k: round((r_[k] - r_[7]) * 1e3 / MHZ, 0) for k in (5, 6, 9) if r_[k] > r_[1]}
+            out_lines.append(f"  merger row: {rel}")
     mg = raw_all[nd:]
     mg = mg[mg[:, 0] > 0]
     for k, nm in ((0, "merge entry"), (1, "merge past wait"), (3, "merge lse in"), (2, "merge exit")):
