@@ -334,7 +334,7 @@ def run_ours(args, rank, world, local_rank):
           f"{c1['write_65536_tokens']['plain_us']} (mma.sync {c1['write_65536_tokens']['mma_sync_rot_us']}); "
           f"K4 {c1['dequant_us']} us", file=sys.stderr, flush=True)
     print(f"[bench] learned R fused K1 {c1['learned_r_fused']}", file=sys.stderr, flush=True)
-    c3 = c4 = c5 = bf = None
+    c3 = c4 = c5 = bf = pf = None
     if not args.quick:
         sets.clear()  # free the headline's buffers first
         torch.cuda.empty_cache()
@@ -346,6 +346,9 @@ def run_ours(args, rank, world, local_rank):
         print(f"[bench] C4 step {c4['step_us']} us, {c4['tok_per_s_per_gpu']} tok/s/GPU", file=sys.stderr, flush=True)
         bf = bf16_pool_decode(torch, dev, gen, timed, round(t_k2 * 1e3, 3), c3[1]["us"] if len(c3) > 1 else None)
         print(f"[bench] BF16 pool decode {bf}", file=sys.stderr, flush=True)
+        pf = prefill_sweep(torch, dev, gen, timed)
+        print(f"[bench] prefill write sweep {[(r['tokens'], r['rotk_us'], r['plain_us'], r['dequant_us']) for r in pf['rows']]}",
+              file=sys.stderr, flush=True)
 
     cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu:  # the CPU legs: rank 0 at N = 1 only, after timing
@@ -399,6 +402,7 @@ def run_ours(args, rank, world, local_rank):
             "c4_llama70b": c4,
             "c5_long_context_1kv_per_gpu": c5,
             "bf16_pool_decode": bf,
+            "prefill_write_sweep": pf,
         },
     }
     print(json.dumps(line), flush=True)
@@ -544,6 +548,61 @@ def c2_variants(torch, layout, spec, dev, gen, timed):
                      "overhead_vs_plain": r["overhead_vs_plain"]}
         del tables
     return res
+
+
+# PAPER.md Table (prefill kernel profiling, Qwen3-32B on 2x H100, tp = 2, one layer): the
+# _quantized_set_kv_int4_kernel (INT4, INT4-Fused-RotateK) and flatten_dequant rows, us
+PAPER_PREFILL = {8192: (22.05, 29.44, 7.65, 21.63), 16384: (39.04, 52.13, 15.87, 38.69),
+                 32768: (74.11, 98.18, 33.18, 75.39), 65536: (135.87, 212.32, 69.22, 165.47),
+                 131072: (253.47, 402.33, 137.34, 313.79)}
+
+
+def prefill_sweep(torch, dev, gen, timed):
+    """Row f2: the prefill-sized write (K1) and flatten-dequant (K4) at 8k-128k tokens on the
+    paper's prefill shape (Qwen3-32B at tp = 2: 4 kv heads x 128 per GPU), rotated K only
+    ("Fused-RotateK", Targets.KEYS_ONLY) and plain, beside the paper's H100 numbers
+    (other hardware: context, not a target).  Each size's inputs are larger than L2."""
+    import ctypes
+
+    from paper_2604_19157_b200 import HeadLayout, PageTable, RotationSpec, Targets, _kernels, _lib, make_signs
+    Hq, Dq = 4, 128
+    lay = HeadLayout(num_q_heads=32, num_kv_heads=Hq, head_dim=Dq, rot_order=128, page_tokens=P)
+    spk = RotationSpec(order=128, signs=make_signs(0, 0, Dq, 128), targets=Targets.KEYS_ONLY)
+    peak, _ = hbm_peak()
+    rows = []
+    for n_tok in sorted(PAPER_PREFILL):
+        t = PageTable(lay, num_pages=n_tok // P, device=dev)
+        t.create_sequence(0)
+        t.alloc.plan([0] * n_tok)
+        slots = torch.arange(n_tok, dtype=torch.int64, device=dev)
+        k = torch.randn((n_tok, Hq, Dq), generator=gen, device=dev).to(torch.bfloat16)
+        v = torch.randn((n_tok, Hq, Dq), generator=gen, device=dev).to(torch.bfloat16)
+        n = 16
+        t_r = timed(lambda i: t.store_slots(k, v, slots, spk), n) / n
+        t_p = timed(lambda i: t.store_slots(k, v, slots, None), n) / n
+        bt, lens, ml = t.block_table([0])
+        ko = torch.empty((1, n_tok, Hq, Dq), dtype=torch.bfloat16, device=dev)
+        vo = torch.empty_like(ko)
+
+        def deq(i):
+            _lib.check(_lib.lib().kvr_dequantize_pages(ctypes.byref(t.desc), _kernels.ptr(bt), bt.shape[1],
+                                                       _kernels.ptr(lens), 1, ml, _kernels.ptr(ko), _kernels.ptr(vo),
+                                                       _lib.KVR_BF16, _kernels.stream_ptr()))
+        t_d = timed(deq, n) / n
+        wb = n_tok * (2 * Hq * Dq * 2 + Hq * (Dq + 10) + 8)
+        db = n_tok * (Hq * (Dq + 10) + 2 * Hq * Dq * 2)
+        pp = PAPER_PREFILL[n_tok]
+        rows.append({"tokens": n_tok, "rotk_us": round(t_r * 1e3, 2), "plain_us": round(t_p * 1e3, 2),
+                     "dequant_us": round(t_d * 1e3, 2),
+                     "write_frac": round(wb / (t_r * 1e-3) / 1e9 / peak, 4),
+                     "dequant_frac": round(db / (t_d * 1e-3) / 1e9 / peak, 4),
+                     "paper_h100_int4_us": pp[0], "paper_h100_fused_rotatek_us": pp[1],
+                     "paper_h100_dequant_int4_us": pp[2], "paper_h100_dequant_rotatek_us": pp[3]})
+        del t, k, v, ko, vo
+        torch.cuda.empty_cache()
+    return {"shape": "Qwen3-32B tp=2 prefill: 4 kv heads x 128 per GPU, page 16, bf16 in, one layer",
+            "rotation": "block Hadamard order 128 on K (Targets.KEYS_ONLY), as the paper's Fused-RotateK",
+            "paper_source": "PAPER.md prefill kernel profiling table (2x H100, SGLang)", "rows": rows}
 
 
 def bf16_pool_decode(torch, dev, gen, timed, int4_c2_us, int4_c3_b16_us):
