@@ -1267,7 +1267,10 @@ int kvr_launch_store_fast(const void* k, const void* v, int in_dtype, int64_t n_
   // B blocks, 576 threads -- and the per-row latency of one epilogue thread per row dominate)
   const int64_t tiles = 2 * ((n_tok * pool.H + 127) / 128);
   const int sms = kvr_num_sms() > 0 ? kvr_num_sms() : 148;
-  if (k1_use_tc() && (tiles >= 4 * (int64_t)sms || k1_forced_tc)) {
+  // plain twins (no rotation anywhere) switch earlier: bf16 rows hit exact ties of x / s often and the
+  // tcgen05 kernel spreads their exact fixes over the warp (C1: 13.4 vs 15.9 us on the mma.sync kernel)
+  const int64_t tc_from = (rot_k || rot_v) ? 4 * (int64_t)sms : (int64_t)sms;
+  if (k1_use_tc() && (tiles >= tc_from || k1_forced_tc)) {
     switch (order) {
       case 128: return f16 ? launch_tc_impl<128, true, false>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st)
                            : launch_tc_impl<128, false, false>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st);

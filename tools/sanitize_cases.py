@@ -50,4 +50,27 @@ oh = torch.empty(1, H * G, D).pin_memory()
 for _ in range(12):
     plan.step(qh, kh, vh, spec, out=oh, graph=True)
 torch.cuda.synchronize()
+# row f3: the learned-R K1 (tcgen05, T in shared memory; V plain / Hadamard / T) and the
+# row-matmul query / output transforms around the decode
+from paper_2604_19157_b200 import Targets  # noqa: E402
+
+qr_, rr_ = np.linalg.qr(np.random.default_rng(5).standard_normal((D, D)))
+R = qr_ * np.sign(np.diag(rr_))
+for tg, lv in ((Targets.KEYS_AND_VALUES, False), (Targets.KEYS_AND_VALUES, True), (Targets.KEYS_ONLY, False)):
+    lspec = RotationSpec(order=128, signs=spec.signs, learned=R, targets=tg, learned_values=lv)
+    t.alloc.seq_len[0] = 0
+    t.alloc.seq_pages[0] = []
+    t.alloc.free = list(range(t.num_pages))
+    t.store_slots(k, v, torch.from_numpy(t.alloc.reserve(0, L)).to(dev), lspec)
+    DecodePlan(t, [0], num_splits=12).run(q, lspec)
+    torch.cuda.synchronize()
+# BF16 pool: the tuned decode (TMA cells, split-K + merge)
+from paper_2604_19157_b200.cache import BF16  # noqa: E402
+
+tb = PageTable(layout, num_pages=L // P + 4, device=dev, precision=BF16)
+tb.create_sequence(0)
+tb.store_slots(k, v, torch.from_numpy(tb.alloc.reserve(0, L)).to(dev), None)
+for splits in (1, 12):
+    DecodePlan(tb, [0], num_splits=splits).run(q, None)
+torch.cuda.synchronize()
 print("sanitize cases done")
