@@ -99,6 +99,14 @@ for splits in split_list:
         if ok.any():
             t = (g0[ok] + (raw[ok, k] - raw[ok, 1]) * 1e3 / MHZ) / 1e3
             out_lines.append(f"{nm:16s}: n {ok.sum():4d} min {t.min():6.2f} med {np.median(t):6.2f} max {t.max():6.2f} us")
+    if os.environ.get("TR_BY_SPLIT"):  # rows are cta_id = (b * S + split) * H + h
+        rs = raw.reshape(-1, S, H, 16)[0]
+        st = (rs[:, :, 0] - t0) / 1e3
+        le = st + (rs[:, :, 3] - rs[:, :, 1]) * 1e3 / MHZ / 1e3
+        pw = st + (rs[:, :, 11] - rs[:, :, 1]) * 1e3 / MHZ / 1e3
+        out_lines.append("  by split: start / past wait / loop end (us, mean over heads)")
+        for sp in range(S):
+            out_lines.append(f"   split {sp:2d}: {st[sp].mean():6.2f} {pw[sp].mean():6.2f} {le[sp].mean():6.2f}")
     if os.environ.get("TR_MERGE_ROWS"):  # per merger CTA: stamps (ns) relative to 'merge in' (7)
         for r_ in raw[(raw[:, 7] > raw[:, 1])][:6]:
             rel = {k: round((r_[k] - r_[7]) * 1e3 / MHZ, 0) for k in (5, 6, 9) if r_[k] > r_[1]}
