@@ -314,8 +314,15 @@ __global__ void __launch_bounds__(256) dequant_cells_kernel(Pool pool, const int
   const int tile = (int)(bt_ % ntiles), b = (int)(bt_ / ntiles);
   // lane: token r of the cell, side (K | V), 32-dim quarter qt of the row
   const int r = 4 * (int)(wid & 3) + (lane >> 3), side = (lane >> 2) & 1, qt = lane & 3, t = tile * 16 + r;
-  if (t >= __ldg(&lens[b]) || t >= max_len) return;
+  // programmatic dependent launch: the index math above overlaps the previous grid's tail; the
+  // lengths, the block table and the pool may be its output.  This kernel writes no pool cell, so
+  // its dependents may be scheduled at once (they wait for its completion before reading)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (t >= max_len) return;
+  const int len_b = __ldg(&lens[b]);  // the length and the page id load side by side
   const int page = __ldg(&bt[(int64_t)b * bt_stride + (t >> (4 + cps_log2))]);
+  if (t >= len_b) return;
   const uint8_t* cell = pool.base + (int64_t)page * pool.page_bytes +
                         (int64_t)((head << cps_log2) + (tile & ((1 << cps_log2) - 1))) * pool.cell_bytes;
   // lane qt takes code bytes 16 i + 4 qt .. + 3 of the row (dims 32 i + 8 qt .. + 7), i = 0..3: its
@@ -655,13 +662,23 @@ int kvr_launch_dequant_pages(const Pool& pool, const int32_t* bt, int bt_stride,
   if (fast && (out_dtype == KVR_BF16 || out_dtype == KVR_F32)) {
     const int64_t cells = (int64_t)batch * ((max_len + 15) / 16) * pool.H;
     const int g = (int)((cells * 4 + 7) / 8);  // four warps per cell, eight warps per block
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e;
     if (out_dtype == KVR_BF16)
-      dequant_cells_kernel<__nv_bfloat16><<<g, 256, 0, st>>>(pool, bt, bt_stride, lens, batch, max_len, cl,
-                                                              (__nv_bfloat16*)k_out, (__nv_bfloat16*)v_out);
+      e = cudaLaunchKernelEx(&cfg, dequant_cells_kernel<__nv_bfloat16>, pool, bt, bt_stride, lens, batch, max_len, cl,
+                             (__nv_bfloat16*)k_out, (__nv_bfloat16*)v_out);
     else
-      dequant_cells_kernel<float><<<g, 256, 0, st>>>(pool, bt, bt_stride, lens, batch, max_len, cl, (float*)k_out,
-                                                      (float*)v_out);
-    return 0;
+      e = cudaLaunchKernelEx(&cfg, dequant_cells_kernel<float>, pool, bt, bt_stride, lens, batch, max_len, cl,
+                             (float*)k_out, (float*)v_out);
+    return e == cudaSuccess ? 0 : KVR_ERR_CUDA;
   }
   const int64_t work = 2LL * batch * max_len * pool.H * (pool.d / 2);
   const int g = grid_for(work, 256);
