@@ -40,6 +40,7 @@ struct FastStoreParams {
   int32_t tiles_per_side;  // ceil(n_rows / 32)
   int32_t rot_k, rot_v;
   int32_t log2P;        // page_tokens = 2^log2P (tensor-core path)
+  int32_t hshift;       // log2(H) when H is a power of two, else -1 (row -> token / head without a division)
 };
 
 // Elements 4l..4l+3 of the row staged for lane `src` in the swizzled tile, as f64.
@@ -427,7 +428,7 @@ KVR_DEV void mma_tile(const uint8_t* buf, uint8_t* stage, const uint2* smask, co
   for (int rh = 0; rh < 2; ++rh) {
     if (!(wr[rh] && slot[rh] >= 0)) continue;
     const int row = (int)(row0 + g + 8 * rh);
-    const int head = row % pl.H;
+    const int head = p.hshift >= 0 ? row & (pl.H - 1) : row % pl.H;
     const int64_t page = slot[rh] >> p.log2P;
     const int ci = (int)(slot[rh] & (pl.P - 1)) & 15;
     uint8_t* cell = pl.base + page * pl.page_bytes +
@@ -509,7 +510,7 @@ __global__ void __launch_bounds__(FS_WARPS * 32, KVR_FS_MINB)
       if (tile < total_tiles) {
         const int side = tile >= p.tiles_per_side;
         const int row = (side ? tile - p.tiles_per_side : tile) * FS_TILE_ROWS + g + 8 * rh;
-        if (row < p.n_rows) sl[rh] = __ldg(&p.slots[row / H]);
+        if (row < p.n_rows) sl[rh] = __ldg(&p.slots[p.hshift >= 0 ? row >> p.hshift : row / H]);
       }
     }
   };
@@ -1129,6 +1130,7 @@ static int launch_fast_impl(const void* k, const void* v, int64_t n_tok, const i
   prm.tiles_per_side = (int)((prm.n_rows + FS_TILE_ROWS - 1) / FS_TILE_ROWS);
   prm.rot_k = rot_k;
   prm.rot_v = rot_v;
+  prm.hshift = (pool.H & (pool.H - 1)) ? -1 : __builtin_ctz((unsigned)pool.H);
   prm.log2P = 0;
   while ((1 << prm.log2P) < pool.P) ++prm.log2P;
   Signs sg = s;
