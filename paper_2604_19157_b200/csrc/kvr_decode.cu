@@ -45,6 +45,7 @@ struct DecodeParams {
   const int32_t* lens;
   int batch, nq, G, splits, order, rotate, rot_v, has_signs, log2P, max_len;
   int cps_log2;       // log2(cells of one head per page) = log2(P / 16) on the TMA path
+  int split_tiles;    // ceil(ceil(max_len / 16) / splits): the tiles of one split (host-computed: no division in-kernel)
   int use_cluster;    // 2..16 splits: merge them in a thread-block cluster
   float* out;
   float* ws_o;       // [B][H][S][8][128]
@@ -458,6 +459,9 @@ constexpr int RING_CELLS = 4;    // cells in flight per warp (NSTG stages of C c
 #ifndef KVR_MERGE_LL
 #define KVR_MERGE_LL 1
 #endif
+#ifndef KVR_PRMT_SENT
+#define KVR_PRMT_SENT 1  // sentinel zero points cleared by a sign-replicating PRMT (no predicated compare)
+#endif
 constexpr int MAX_SPLITS = 256;
 constexpr int MERGE_INLINE_MAX = 32;  // up to this many splits the last CTA merges them inline
 
@@ -585,7 +589,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   // Warp w owns the groups g = w, w + DW, ... of C consecutive tiles of the split;
   // its j-th tile is t = lo + C (w + DW (j / C)) + j % C.
   const int n_tiles_max = (p.max_len + 15) >> 4;
-  const int per = (n_tiles_max + p.splits - 1) / p.splits;
+  const int per = p.split_tiles;
   const int lo = min(n_tiles_max, split * per);
   const int hi_max = min(n_tiles_max, lo + per);
   const bool tile_warp = warp < DW;
@@ -1069,9 +1073,14 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
       uint32_t off[2][2];  // [token pair][low | high nibble]: fp16x2 (1024 + z, 1024 + 16 z)
 #pragma unroll
       for (int tp = 0; tp < 2; ++tp) {
-        uint32_t zz = tp ? f[c].vzp1 : f[c].vzp0;  // z of the pair's two tokens (bytes 0, 1)
-        if (rare) zz &= ~__vcmpeq4(zz, 0x0000FFFFu);  // sentinel (0xFF): its codes are 0, offset 0
-        const uint32_t x = prmt(zz, 0u, 0x4140u);     // [z_a, 0, z_b, 0]
+        const uint32_t zz = tp ? f[c].vzp1 : f[c].vzp0;  // z of the pair's two tokens (bytes 0, 1)
+        // [z_a, 0, z_b, 0]; a sentinel's 0xFF (its codes are 0, its offset is handled apart) -> 0: the
+        // second PRMT replicates each byte's bit 7, set only by 0xFF (valid z <= 15)
+#if KVR_PRMT_SENT
+        const uint32_t x = prmt(zz, 0u, 0x4140u) & ~prmt(zz, 0u, 0x4948u);
+#else
+        const uint32_t x = prmt(rare ? (zz & ~__vcmpeq4(zz, 0x0000FFFFu)) : zz, 0u, 0x4140u);
+#endif
         off[tp][0] = x + k1024;
         off[tp][1] = x * 16u + k1024;
       }
@@ -2100,6 +2109,7 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
     if (splits > MAX_SPLITS) splits = MAX_SPLITS;
     if (splits > 1 && kvr_decode_ws_bytes(batch, pool.H, nq, 128, splits) > ws_bytes) return KVR_ERR_ARG;
     p.splits = splits;
+    p.split_tiles = (((max_len + 15) >> 4) + splits - 1) / splits;
     const size_t units = (size_t)batch * pool.H * splits * 8;
     p.ws_cnt = reinterpret_cast<uint32_t*>(ws);
     p.ws_epoch = p.ws_cnt + (size_t)batch * pool.H;
