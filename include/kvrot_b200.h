@@ -28,6 +28,11 @@
  *                               decode step (cache.py:235-270 then attention.py:50-87)
  *   kvr_decode_flat_f64      <- attention.decode_step_fp (attention.py:90-115), the flat
  *                               full-precision decode (paged-vs-flat exactness oracle)
+ *   kvr_rows_matmul_f64      <- the learned factor's `out @ spec.learned` / `@ spec.learned.T`
+ *                               (rotation.py:140-141, 154-155) and compose_transform's T
+ *                               (rotation.py:171-184) applied to queries / outputs
+ *   kvr_rotate_quantize_store_learned <- append with a learned spec (rotation.py:118-168 then
+ *                               cache.py:235-270), R fused into the write kernel
  */
 #ifndef KVROT_B200_H
 #define KVROT_B200_H
