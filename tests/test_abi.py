@@ -85,3 +85,45 @@ def test_split_count_model(libpath):
     for b, h, L in ((1, 8, 32769), (2, 8, 32768), (1, 1, 1 << 20), (4, 8, 4096)):
         s = pick(b, h, L, 16)
         assert 1 <= s <= 256 and (b * h * s <= 148 or s == 1)
+
+
+def test_learned_entry_points_validate_without_device(libpath):
+    """Row f3's entry points reject bad arguments before any CUDA call (reference-style
+    exceptions through _lib.check), and the host image packer is a pure host function."""
+    import numpy as np
+
+    from paper_2604_19157_b200 import _lib
+
+    lib = _lib.lib()
+    pool = _lib.KvrPool()
+    assert lib.kvr_pool_init(ctypes.byref(pool), ctypes.c_void_p(16), 4, 16, 8, 128) == 0
+    dummy = ctypes.c_void_p(256)
+    args = (dummy, dummy, _lib.KVR_BF16, 16, dummy, ctypes.byref(pool), 128, _lib.KVR_KEYS_AND_VALUES, 1, None)
+    assert lib.kvr_rotate_quantize_store_learned(*args, None, dummy, None, None) == 5  # null t_img
+    assert lib.kvr_rotate_quantize_store_learned(*args[:7], 7, *args[8:], dummy, dummy, None, None) == 5  # targets
+    assert lib.kvr_rotate_quantize_store_learned(*args[:6], 48, *args[7:], dummy, dummy, None, None) == 2  # order
+    bf = _lib.KvrPool()
+    assert lib.kvr_pool_init_bf16(ctypes.byref(bf), ctypes.c_void_p(16), 4, 16, 8, 128) == 0
+    a2 = list(args)
+    a2[5] = ctypes.byref(bf)
+    assert lib.kvr_rotate_quantize_store_learned(*a2, dummy, dummy, None, None) == 3  # BF16 pool
+    # rows_matmul: shape, size, aliasing and null checks
+    assert lib.kvr_rows_matmul_f64(dummy, _lib.KVR_F64, dummy, dummy, _lib.KVR_F64, -1, 128, None) == 1
+    assert lib.kvr_rows_matmul_f64(dummy, _lib.KVR_F64, dummy, ctypes.c_void_p(512), _lib.KVR_F64, 4, 1024,
+                                   None) == 3
+    assert lib.kvr_rows_matmul_f64(dummy, _lib.KVR_F64, dummy, dummy, _lib.KVR_F64, 4, 128, None) == 5
+    assert lib.kvr_rows_matmul_f64(None, _lib.KVR_F64, dummy, ctypes.c_void_p(512), _lib.KVR_F64, 4, 128, None) == 5
+    assert lib.kvr_rows_matmul_f64(dummy, _lib.KVR_F64, dummy, ctypes.c_void_p(512), _lib.KVR_F64, 0, 128, None) == 0
+    # the T image: part p of element (n, k) sits at the SW128 K-major offset; hi + mid + lo == T to ~2^-24
+    t = np.random.default_rng(0).standard_normal((128, 128)) * 0.1
+    img = np.zeros(3 * 128 * 128, dtype=np.uint16)
+    lib.kvr_learned_pack_image(t.ctypes.data, img.ctypes.data)
+
+    def bf(u):
+        return (u.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+    for n, k in ((0, 0), (5, 70), (127, 127), (64, 3)):
+        byte = (k & 63) * 2
+        off = (k >> 6) * 16384 + (n >> 3) * 1024 + (n & 7) * 128 + (((byte >> 4) ^ (n & 7)) << 4) + (byte & 15)
+        parts = [bf(img[(p * 32768 + off) // 2:(p * 32768 + off) // 2 + 1])[0] for p in range(3)]
+        assert abs(sum(parts) - t[k, n]) <= 2.0 ** -24 * abs(t[k, n]) + 1e-30
