@@ -240,3 +240,36 @@ def test_learned_composed_matches_reference_order():
     assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
     back = rows_matmul(torch.tensor(got).cuda(), composed_on(spec, layout, "cuda", transpose=True)).cpu().numpy()
     assert np.abs(back - x).max() <= 1e-13 * np.abs(x).max()
+
+
+@pytest.mark.parametrize("P,H,dt", [(64, 8, torch.bfloat16), (16, 2, torch.float16), (32, 4, torch.bfloat16)])
+def test_learned_store_geometries_and_dtypes(P, H, dt):
+    """The fused learned K1 at other page sizes / head counts (bf16), and fp16 rows through the
+    unfused route (the fused kernel takes bf16 only): the same bars as the bf16 fused test."""
+    d = 128
+    L = 700
+    layout = HeadLayout(num_q_heads=4 * H, num_kv_heads=H, head_dim=d, rot_order=128, page_tokens=P)
+    t = PageTable(layout, num_pages=L // P + 2)
+    spec = RotationSpec(order=128, signs=make_signs(9, 2, d, 128), learned=_orth(d, 31), learned_values=True)
+    t.create_sequence(0)
+    rnd = bf16_round if dt == torch.bfloat16 else (lambda a: np.asarray(a, dtype=np.float16).astype(np.float64))
+    k = rnd(gen_rows("gaussian", L * H, d, 41)).reshape(L, H, d)
+    v = rnd(gen_rows("outlier", L * H, d, 42)).reshape(L, H, d)
+    t.append_batch([0] * L, torch.tensor(k).to(dt), torch.tensor(v).to(dt), spec=spec)
+    t.check_flags()
+    f = page_fields(t.page_records(t.sequence_pages(0)), P, H, d)
+    mism = total = 0
+    for side, x in (("k", k), ("v", v)):
+        ref = _ref_rotate(x.reshape(-1, d), spec, values=side == "v")
+        pk_, sk, zk = O.quantize_rows(ref)
+        got = f[f"{side}_payload"].reshape(-1, H, d // 2)[:L].reshape(-1, d // 2)
+        dl = np.abs((got & 15).astype(int) - (pk_ & 15)) + np.abs((got >> 4).astype(int) - (pk_ >> 4))
+        assert dl.max() <= 1
+        mism += int((dl > 0).sum())
+        total += dl.size * 2
+        gz = f[f"{side}_zp"].reshape(-1, H)[:L].reshape(-1).astype(int)
+        assert np.abs(gz - zk.astype(int)).max() <= 1
+        gs = f[f"{side}_scale"].reshape(-1, H)[:L].reshape(-1).astype(np.float64)
+        assert np.max(np.abs(gs - sk) / np.abs(sk)) <= 1e-5
+    print(f"learned P={P} H={H} {dt}: nibble mismatches {mism} of {total}")
+    assert mism <= total * 1e-4
