@@ -617,8 +617,17 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   // then everything waits here, and no cell is requested before the wait either (pre_groups = 0)
   if (p.meta_post_wait) pdl_wait();
   if (threadIdx.x == 0) {
-    *s_len = __ldg(&p.lens[b]);
-    if (APPEND) *s_slot = __ldg(&p.new_slot[b]);
+    if (p.meta_post_wait) {
+      // coherent loads, not the read-only (.nc) path: the lengths / slot ids were written by the
+      // stage-copy kernel, a grid this one may have been launched beside (PDL); the .nc path returned
+      // a previous step's values there (tools/soak_step.py: a step every few hundred decoded an older
+      // length).  (Host-written metadata -- pinned or copied in before the launch -- keeps __ldg.)
+      *s_len = *reinterpret_cast<const volatile int32_t*>(&p.lens[b]);
+      if (APPEND) *s_slot = *reinterpret_cast<const volatile long long*>(&p.new_slot[b]);
+    } else {
+      *s_len = __ldg(&p.lens[b]);
+      if (APPEND) *s_slot = __ldg(&p.new_slot[b]);
+    }
   }
   // this lane's word of the sign vector (dims 4l..4l+3), read from the parameter
   // bank before the dependency wait (0 = no flips)

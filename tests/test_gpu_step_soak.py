@@ -1,0 +1,21 @@
+"""A long run of the serving step through the native step ring (pinned host q / k / v / out,
+page boundaries on the general path, NaN steps rejected), checked against a fresh decode of the
+same table state: catches ordering races between consecutive steps that short tests miss."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("mode", ["1", "2"])
+def test_step_ring_soak(mode):
+    env = dict(os.environ, KVR_STEP_DIRECT=mode)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "soak_step.py"), "3000"], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "soak: 3000 steps" in r.stdout
