@@ -19,3 +19,14 @@ def test_step_ring_soak(mode):
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "soak: 3000 steps" in r.stdout
+
+
+@pytest.mark.parametrize("device_inputs", [False, True])
+def test_serving_soak_with_prefill(device_inputs):
+    """Decode steps interleaved on one stream with bulk prefill writes of another sequence and its
+    decodes (the pool-write notes gating pre-wait reads), checked against fresh decodes."""
+    args = [sys.executable, os.path.join(ROOT, "tools", "soak_serving.py"), "1000"] + (["--device"] if device_inputs
+                                                                                        else [])
+    r = subprocess.run(args, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "serving soak" in r.stdout and "1000 steps" in r.stdout
