@@ -162,7 +162,7 @@ class DecodePlan:
             if spec.order != lay.rot_order:
                 raise ShapeError(f"spec order {spec.order} != layout rot_order {lay.rot_order}")
             if spec.learned is not None:
-                return self._run_learned(q, spec, out)
+                return self._run_learned(q, spec, out, lens)
         targets = _lib.KVR_KEYS_ONLY if (rotate and spec.targets is Targets.KEYS_ONLY) else _lib.KVR_KEYS_AND_VALUES
         _lib.check(_lib.lib().kvr_paged_decode(
             _kernels.ptr(q), _Q_CODE[q.dtype], ctypes.byref(table.desc), _kernels.ptr(self.bt), self.bt.shape[1],
@@ -172,7 +172,8 @@ class DecodePlan:
         return out
 
 
-    def _run_learned(self, q: torch.Tensor, spec: RotationSpec, out: torch.Tensor) -> torch.Tensor:
+    def _run_learned(self, q: torch.Tensor, spec: RotationSpec, out: torch.Tensor,
+                     lens: Optional[torch.Tensor] = None) -> torch.Tensor:
         """Row f3: the query through the composed T = diag(s) H_blk R (one f64
         row-matmul launch, f32 out), the INT4 decode kernel on the pre-rotated query,
         then the value branch's T^T on the output (one launch) (attention.py:63-85)."""
@@ -184,9 +185,11 @@ class DecodePlan:
             self._lo = torch.empty(q.shape, dtype=torch.float32, device=dev)
         rows_matmul(q, composed_on(spec, lay, dev), out=qr)
         tv = composed_on(spec, lay, dev, transpose=True, values=True)
+        # the caller's lengths go through (a serving step's staged ones: nothing host-side may run
+        # inside a captured step graph)
         if tv is None:
-            return self.run(qr, None, out)
-        self.run(qr, None, self._lo)
+            return self.run(qr, None, out, lens=lens)
+        self.run(qr, None, self._lo, lens=lens)
         rows_matmul(self._lo, tv, out=out)
         return out
 

@@ -30,3 +30,13 @@ def test_serving_soak_with_prefill(device_inputs):
     r = subprocess.run(args, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "serving soak" in r.stdout and "1000 steps" in r.stdout
+
+
+def test_learned_step_soak():
+    """Row f3 through DecodePlan.step(graph=True): the learned step's graphs must take the staged
+    lengths (a graph captured around a host-side length refresh replayed stale lengths)."""
+    env = dict(os.environ, SOAK_LEARNED="1")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "soak_step.py"), "1000"], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "soak: 1000 steps" in r.stdout

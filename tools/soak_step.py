@@ -20,6 +20,9 @@ B, H, G, D = 3, 8, 4, 128
 dev = torch.device("cuda")
 layout = HeadLayout(num_q_heads=H * G, num_kv_heads=H, head_dim=D, rot_order=128, page_tokens=16)
 spec = RotationSpec(order=128, signs=make_signs(1, 0, D, 128))
+if os.environ.get("SOAK_LEARNED"):  # row f3: a learned R (unfused exact write + row-matmul query / output)
+    _q, _r = np.linalg.qr(np.random.default_rng(3).standard_normal((D, D)))
+    spec = RotationSpec(order=128, signs=spec.signs, learned=_q * np.sign(np.diag(_r)), learned_values=True)
 t = PageTable(layout, num_pages=(B * (2000 + N // 1)) // 16 + 16, device=dev)
 rng = np.random.default_rng(0)
 for s in range(B):
