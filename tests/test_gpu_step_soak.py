@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.parametrize("mode", ["1", "2"])
 def test_step_ring_soak(mode):
-    env = dict(os.environ, KVR_STEP_DIRECT=mode)
+    env = dict(os.environ, KVR_STEP_DIRECT=mode, SOAK_EVERY="25")
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "soak_step.py"), "3000"], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
@@ -35,7 +35,7 @@ def test_serving_soak_with_prefill(device_inputs):
 def test_learned_step_soak():
     """Row f3 through DecodePlan.step(graph=True): the learned step's graphs must take the staged
     lengths (a graph captured around a host-side length refresh replayed stale lengths)."""
-    env = dict(os.environ, SOAK_LEARNED="1")
+    env = dict(os.environ, SOAK_LEARNED="1", SOAK_EVERY="25")
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "soak_step.py"), "1000"], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]

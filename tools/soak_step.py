@@ -16,14 +16,20 @@ from paper_2604_19157_b200.attention import decode_batch  # noqa: E402
 from paper_2604_19157_b200.errors import NonFiniteInputError  # noqa: E402
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 20000
-B, H, G, D = 3, 8, 4, 128
+EVERY = int(os.environ.get("SOAK_EVERY", "500"))  # steps between full checks
+B, H, D = 3, 8, 128
+G = int(os.environ.get("SOAK_G", "4"))
+P = int(os.environ.get("SOAK_P", "16"))
 dev = torch.device("cuda")
-layout = HeadLayout(num_q_heads=H * G, num_kv_heads=H, head_dim=D, rot_order=128, page_tokens=16)
-spec = RotationSpec(order=128, signs=make_signs(1, 0, D, 128))
+layout = HeadLayout(num_q_heads=H * G, num_kv_heads=H, head_dim=D, rot_order=128, page_tokens=P)
+from paper_2604_19157_b200 import Targets  # noqa: E402
+spec = RotationSpec(order=128, signs=make_signs(1, 0, D, 128),
+                    targets=Targets.KEYS_ONLY if os.environ.get("SOAK_KEYS_ONLY") else Targets.KEYS_AND_VALUES)
 if os.environ.get("SOAK_LEARNED"):  # row f3: a learned R (unfused exact write + row-matmul query / output)
     _q, _r = np.linalg.qr(np.random.default_rng(3).standard_normal((D, D)))
     spec = RotationSpec(order=128, signs=spec.signs, learned=_q * np.sign(np.diag(_r)), learned_values=True)
-t = PageTable(layout, num_pages=(B * (2000 + N // 1)) // 16 + 16, device=dev)
+prec = "bf16" if os.environ.get("SOAK_BF16") else "int4"
+t = PageTable(layout, precision=prec, num_pages=(B * (2000 + N // 1)) // P + 16, device=dev)
 rng = np.random.default_rng(0)
 for s in range(B):
     t.create_sequence(s)
@@ -52,7 +58,7 @@ for i in range(N):
         assert [t.sequence_length(s) for s in range(B)] == lens0
         continue
     plan.step(qh, kh, vh, spec, out=oh, graph=True)
-    if i % 500 == 499:
+    if i % EVERY == EVERY - 1:
         torch.cuda.synchronize()
         ref = decode_batch(qh.cuda().float(), t, list(range(B)), spec=spec).cpu()
         err = float((oh - ref).abs().max() / ref.abs().max())
