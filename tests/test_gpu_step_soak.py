@@ -40,3 +40,13 @@ def test_learned_step_soak():
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "soak: 1000 steps" in r.stdout
+
+
+def test_k1_randomised_stress():
+    """Random token counts across both K1 kernels' dispatch range, slot permutations, head counts,
+    orders, targets and row families: the fast write equals the exact path (codes / zp bit-exact,
+    scales within 2 ulp)."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "stress_k1.py"), "16"], capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "stress_k1: 16 cases" in r.stdout
