@@ -50,3 +50,12 @@ def test_k1_randomised_stress():
                        text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert "stress_k1: 16 cases" in r.stdout
+
+
+def test_decode_randomised_stress():
+    """Random ragged batches, head counts, GQA groups, page sizes, orders, targets and split counts:
+    the INT4 decode against the flat f64 decode of the same pages, within 1e-5 of max|ref|."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "stress_decode.py"), "20"], capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "stress_decode: 20 cases" in r.stdout
