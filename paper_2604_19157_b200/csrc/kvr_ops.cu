@@ -302,16 +302,21 @@ __global__ void dequant_pages_kernel(Pool pool, const int32_t* bt, int bt_stride
 // Arithmetic: f32 s * (q - z) (q - z exact, one rounding), then the output cast.
 template <typename TOut>
 __global__ void __launch_bounds__(256) dequant_cells_kernel(Pool pool, const int32_t* bt, int bt_stride,
-                                                            const int32_t* lens, int batch, int max_len, int cps_log2,
-                                                            TOut* k_out, TOut* v_out) {
+                                                            const int32_t* lens, int max_len, int cps_log2,
+                                                            int h_log2, TOut* k_out, TOut* v_out) {
   const int lane = threadIdx.x & 31;
-  const int64_t wid = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int H = pool.H, ntiles = (max_len + 15) >> 4;
-  const int64_t cell_id = wid >> 2;  // four warps per cell, four tokens each
-  if (cell_id >= (int64_t)batch * ntiles * H) return;
-  const int head = (int)(cell_id % H);
-  const int64_t bt_ = cell_id / H;
-  const int tile = (int)(bt_ % ntiles), b = (int)(bt_ / ntiles);
+  const uint32_t wid = blockIdx.x * 8u + (threadIdx.x >> 5);  // grid (cells of one sequence / 2, sequence)
+  const int H = pool.H, ntiles = (max_len + 15) >> 4, b = blockIdx.y;
+  const uint32_t cell_id = wid >> 2;  // four warps per cell, four tokens each
+  if (cell_id >= (uint32_t)(ntiles * H)) return;
+  int head, tile;
+  if (h_log2 >= 0) {  // the usual power-of-two head count: no integer division
+    head = (int)(cell_id & (uint32_t)(H - 1));
+    tile = (int)(cell_id >> h_log2);
+  } else {
+    tile = (int)(cell_id / (uint32_t)H);
+    head = (int)cell_id - tile * H;
+  }
   // lane: token r of the cell, side (K | V), 32-dim quarter qt of the row
   const int r = 4 * (int)(wid & 3) + (lane >> 3), side = (lane >> 2) & 1, qt = lane & 3, t = tile * 16 + r;
   // programmatic dependent launch: the index math above overlaps the previous grid's tail; the
@@ -329,45 +334,40 @@ __global__ void __launch_bounds__(256) dequant_cells_kernel(Pool pool, const int
   // outputs then sit at 16-B chunk qt of every 64-B group, so each store instruction of the row's four
   // lanes writes 64 contiguous bytes (whole sectors)
   const uint32_t* crow = reinterpret_cast<const uint32_t*>(cell + (side ? 1152 : 128) + r * 64) + qt;
-  const uint32_t w[4] = {__ldg(crow), __ldg(crow + 4), __ldg(crow + 8), __ldg(crow + 12)};
+  uint32_t w[4] = {__ldg(crow), __ldg(crow + 4), __ldg(crow + 8), __ldg(crow + 12)};
   const float sc = __ldg(reinterpret_cast<const float*>(cell + side * 64 + r * 4));
   const uint32_t zp = __ldg(cell + 2176 + side * 16 + r);
-  // a code c as the float 2^23 + c (nibble in the low mantissa bits), minus 2^23 + z: the exact
-  // c - z, then one f32 product by the scale (FADD2 / FMUL2 on element pairs); sentinel rows
-  // (zp 0xFF, codes 0) output their offset, held in the scale slot
+  // a code c as the float 2^23 + c (one PRMT puts the nibble under the exponent byte 0x4B), minus
+  // 2^23 + z: the exact c - z, then one f32 product by the scale (FADD2 / FMUL2 on the element pair of
+  // one code byte).  A sentinel row (zp 0xFF) outputs its offset, held in the scale slot: its codes
+  // are taken as 0 and its zero point as -1, so every element is (0 + 1) * offset.
   const bool sent = zp == 0xFFu;
-  const float zf = 8388608.0f + (float)(sent ? 0u : zp);
+  const float zf = sent ? 8388607.0f : 8388608.0f + (float)zp;
   const unsigned long long z2 = pk(zf, zf), s2 = pk(sc, sc);
-  float f[32];  // f[8 i + j] = dim 32 i + 8 qt + j
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {  // byte i: elements 2i (low nibble), 2i + 1 (high nibble)
-    const uint32_t byte = (w[i >> 2] >> (8 * (i & 3))) & 0xFFu;
-    const unsigned long long x = pk(__uint_as_float(0x4B000000u | (byte & 15u)), __uint_as_float(0x4B000000u | (byte >> 4)));
-    const unsigned long long y = mul2(sub2(x, z2), s2);
-    upk(y, f[2 * i], f[2 * i + 1]);
-  }
-  if (sent) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) f[i] = sc;
-  }
   TOut* dst = (side ? v_out : k_out) + (((int64_t)b * max_len + t) * H + head) * 128 + qt * 8;
-  if constexpr (sizeof(TOut) == 2) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 4; ++i) {  // word i: dims 32 i + 8 qt + 2 j (low nibble of byte j), + 2 j + 1 (high)
+    const uint32_t wi = sent ? 0u : w[i];
+    const uint32_t lo = wi & 0x0F0F0F0Fu, hi = (wi >> 4) & 0x0F0F0F0Fu;
+    float f[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const unsigned long long x = pk(__uint_as_float(__byte_perm(lo, 0x4B000000u, 0x7440u | j)),
+                                      __uint_as_float(__byte_perm(hi, 0x4B000000u, 0x7440u | j)));
+      upk(mul2(sub2(x, z2), s2), f[2 * j], f[2 * j + 1]);
+    }
+    if constexpr (sizeof(TOut) == 2) {
       uint32_t u[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const __nv_bfloat162 h2 = __floats2bfloat162_rn(f[8 * i + 2 * k], f[8 * i + 2 * k + 1]);
-        u[k] = *reinterpret_cast<const uint32_t*>(&h2);
+      for (int j = 0; j < 4; ++j) {
+        const __nv_bfloat162 h2 = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+        u[j] = *reinterpret_cast<const uint32_t*>(&h2);
       }
       *reinterpret_cast<uint4*>(dst + 32 * i) = make_uint4(u[0], u[1], u[2], u[3]);
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    } else {
       float4* d4 = reinterpret_cast<float4*>(dst + 32 * i);
-      d4[0] = make_float4(f[8 * i], f[8 * i + 1], f[8 * i + 2], f[8 * i + 3]);
-      d4[1] = make_float4(f[8 * i + 4], f[8 * i + 5], f[8 * i + 6], f[8 * i + 7]);
+      d4[0] = make_float4(f[0], f[1], f[2], f[3]);
+      d4[1] = make_float4(f[4], f[5], f[6], f[7]);
     }
   }
 }
@@ -657,13 +657,16 @@ int kvr_launch_dequant_pages(const Pool& pool, const int32_t* bt, int bt_stride,
   }
   int cl = 0;
   while ((16 << cl) < pool.P) ++cl;
-  const bool fast = pool.d == 128 && pool.T == 16 && (16 << cl) == pool.P && (pool.cell_bytes & 15) == 0 &&
+  const bool fast = pool.d == 128 && pool.T == 16 && (16 << cl) == pool.P && (pool.cell_bytes & 15) == 0 && batch <= 65535 &&
                     ((reinterpret_cast<uintptr_t>(k_out) | reinterpret_cast<uintptr_t>(v_out)) & 15) == 0;
   if (fast && (out_dtype == KVR_BF16 || out_dtype == KVR_F32)) {
-    const int64_t cells = (int64_t)batch * ((max_len + 15) / 16) * pool.H;
+    const int64_t cells = (int64_t)((max_len + 15) / 16) * pool.H;  // per sequence
     const int g = (int)((cells * 4 + 7) / 8);  // four warps per cell, eight warps per block
+    int hl = 0;
+    while ((1 << hl) < pool.H) ++hl;
+    if ((1 << hl) != pool.H) hl = -1;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(g);
+    cfg.gridDim = dim3(g, batch);
     cfg.blockDim = dim3(256);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -673,10 +676,10 @@ int kvr_launch_dequant_pages(const Pool& pool, const int32_t* bt, int bt_stride,
     cfg.numAttrs = 1;
     cudaError_t e;
     if (out_dtype == KVR_BF16)
-      e = cudaLaunchKernelEx(&cfg, dequant_cells_kernel<__nv_bfloat16>, pool, bt, bt_stride, lens, batch, max_len, cl,
+      e = cudaLaunchKernelEx(&cfg, dequant_cells_kernel<__nv_bfloat16>, pool, bt, bt_stride, lens, max_len, cl, hl,
                              (__nv_bfloat16*)k_out, (__nv_bfloat16*)v_out);
     else
-      e = cudaLaunchKernelEx(&cfg, dequant_cells_kernel<float>, pool, bt, bt_stride, lens, batch, max_len, cl,
+      e = cudaLaunchKernelEx(&cfg, dequant_cells_kernel<float>, pool, bt, bt_stride, lens, max_len, cl, hl,
                              (float*)k_out, (float*)v_out);
     return e == cudaSuccess ? 0 : KVR_ERR_CUDA;
   }

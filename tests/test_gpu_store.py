@@ -275,18 +275,20 @@ def test_read_sequence_matches_oracle(golden):
 
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
-@pytest.mark.parametrize("page_tokens", [16, 32])
-def test_fast_dequant_pages_vs_f64(rng, dtype, page_tokens):
+@pytest.mark.parametrize("page_tokens,kv_heads", [(16, 8), (32, 8), (16, 3)])
+def test_fast_dequant_pages_vs_f64(rng, dtype, page_tokens, kv_heads):
     """K4 serving path (d 128, 16-token cells): bf16 / f32 flatten-dequant of ragged
-    sequences == the exact f64 dequant rounded to the output type (<= 1 ulp)."""
-    layout = HeadLayout(num_q_heads=32, num_kv_heads=8, head_dim=128, rot_order=128, page_tokens=page_tokens)
+    sequences == the exact f64 dequant rounded to the output type (<= 1 ulp); a
+    power-of-two and an odd kv-head count (the kernel's shift / division index paths)."""
+    layout = HeadLayout(num_q_heads=4 * kv_heads, num_kv_heads=kv_heads, head_dim=128, rot_order=128,
+                        page_tokens=page_tokens)
     spec = RotationSpec(order=128, signs=make_signs(0, 0, 128, 128))
     t = PageTable(layout, precision=INT4, num_pages=64)
     lens = [37, 1, 100, 5]
     for s, n in enumerate(lens):
         t.create_sequence(s)
-        k = torch.tensor(rng.standard_normal((n, 8, 128)), dtype=torch.bfloat16)
-        v = torch.tensor(rng.standard_normal((n, 8, 128)), dtype=torch.bfloat16)
+        k = torch.tensor(rng.standard_normal((n, kv_heads, 128)), dtype=torch.bfloat16)
+        v = torch.tensor(rng.standard_normal((n, kv_heads, 128)), dtype=torch.bfloat16)
         k[0, 0] = 3.0  # constant row: a sentinel (zp 0xFF) row when stored unrotated (sequence 3)
         t.append_batch([s] * n, k.cuda(), v.cuda(), spec=spec if s < 3 else None)
     seqs = list(range(len(lens)))
