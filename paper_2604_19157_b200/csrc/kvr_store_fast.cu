@@ -380,18 +380,26 @@ KVR_DEV void mma_tile(const uint8_t* buf, uint8_t* stage, const uint2* smask, co
   }
   if constexpr (!ROT) {
     if (__any_sync(0xffffffffu, (fl[0] | fl[1]) != 0u)) {
-      // plain rows: y = x exactly -> the flagged bytes by exact FMA sign tests, in-thread
+      // plain rows: y = x exactly -> the flagged bytes by exact FMA sign tests, in-thread, each on
+      // its input pair re-read from the tile in shared memory (byte k = element pair (row,
+      // 16 (k / 2) + 8 (k % 2) + 2 t), SW128 chunk swizzle), so a lane loops over its own flagged
+      // bytes only (v[] stays in registers: no dynamic index into it)
 #pragma unroll
       for (int rh = 0; rh < 2; ++rh) {
-        uint8_t* srow = stage + (g + 8 * rh) * MS_ROW + t;
+        const int row = g + 8 * rh;
+        uint8_t* srow = stage + row * MS_ROW + t;
+        uint32_t f = fl[rh];
+        if (f == 0u) continue;
         const float inv = 1.0f / rq[rh].s32, zf = (float)rq[rh].z;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {  // static indices keep v[] in registers
-          if (!((fl[rh] >> k) & 1u)) continue;
-          float a0, a1;
-          upk(v[k >> 1][k & 1][rh], a0, a1);
-          srow[4 * k] = (uint8_t)(plain_code_exact(a0, rq[rh].s32, inv, zf) |
-                                  (plain_code_exact(a1, rq[rh].s32, inv, zf) << 4));
+        const uint8_t* xrow = buf + row * 128 + 4 * t;
+        while (f) {
+          const int k = __ffs(f) - 1;
+          f &= f - 1;
+          const int b = k >> 1, chunk = 2 * (b & 3) + (k & 1);
+          const float2 x = b16x2_to_f2<F16>(
+              *reinterpret_cast<const uint32_t*>(xrow + (b >> 2) * FS_SUB_BYTES + ((chunk ^ (row & 7)) << 4)));
+          srow[4 * k] = (uint8_t)(plain_code_exact(x.x, rq[rh].s32, inv, zf) |
+                                  (plain_code_exact(x.y, rq[rh].s32, inv, zf) << 4));
         }
       }
     }
@@ -1269,9 +1277,9 @@ int kvr_launch_store_fast(const void* k, const void* v, int in_dtype, int64_t n_
   // B blocks, 576 threads -- and the per-row latency of one epilogue thread per row dominate)
   const int64_t tiles = 2 * ((n_tok * pool.H + 127) / 128);
   const int sms = kvr_num_sms() > 0 ? kvr_num_sms() : 148;
-  // plain twins (no rotation anywhere) switch earlier: bf16 rows hit exact ties of x / s often and the
-  // tcgen05 kernel spreads their exact fixes over the warp (C1: 13.4 vs 15.9 us on the mma.sync kernel)
-  const int64_t tc_from = (rot_k || rot_v) ? 4 * (int64_t)sms : (int64_t)sms;
+  // (plain twins alike: bf16 rows hit exact ties of x / s often, and the mma.sync kernel re-reads only
+  // the flagged pairs from shared memory -- C1 plain 14.8 -> 11.2 us, below the rotated 11.3 us)
+  const int64_t tc_from = 4 * (int64_t)sms;
   if (k1_use_tc() && (tiles >= tc_from || k1_forced_tc)) {
     switch (order) {
       case 128: return f16 ? launch_tc_impl<128, true, false>(k, v, n_tok, slots, pool, rot_k, rot_v, s, has, flags, st)
