@@ -42,11 +42,11 @@ for rep in sorted(f for f in os.listdir(OUT) if f.endswith(".ncu-rep")):
             vals[k] = v[i]
             lines.append(f"  {k:78s} {v[i]:>14s} {u[i]}")
     if "decode" in rep and "merge" not in rep:
-        rd = float(vals.get("dram__bytes_read.sum", "0").replace(",", ""))
-        wr = float(vals.get("dram__bytes_write.sum", "0").replace(",", ""))
-        ur = u[h.index("dram__bytes_read.sum")]
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(ur, 1)
-        traffic["decode_c2_dram_bytes_per_launch"] = int((rd + wr) * scale)
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+        def nbytes(k):  # each metric in its own unit (ncu picks byte / Kbyte / Mbyte per value)
+            return float(vals.get(k, "0").replace(",", "")) * scale.get(u[h.index(k)], 1) if k in h else 0.0
+        traffic["decode_c2_dram_bytes_per_launch"] = int(nbytes("dram__bytes_read.sum") + nbytes("dram__bytes_write.sum"))
         traffic["source"] = f"profiles/{tag}_ncu_summary.txt ({rep}, dram__bytes_read.sum + dram__bytes_write.sum)"
 lc = os.path.join(OUT, "launches.csv")
 if os.path.exists(lc):
