@@ -593,7 +593,8 @@ struct K1Cfg {
   static constexpr int OFF_CODES = OFF_BAR + 256;               // code staging [groups][128 rows][16 words], swizzled
   static constexpr int OFF_FIXQ = OFF_CODES + NGRP * TM * 64;   // per epilogue warp: queue of flagged words
   static constexpr int FIXQ = LEARNED ? 512 : 1024;            // bytes per warp: learned rows queue <= 8 words each
-  static constexpr int SMEM = OFF_FIXQ + NEPI * FIXQ + 1024;    // + 1 KB alignment slack (SW128 atoms: 1024-B bases)
+  static constexpr int OFF_SLOT = OFF_FIXQ + NEPI * FIXQ;     // learned: per epilogue thread its row's slot id
+  static constexpr int SMEM = OFF_SLOT + (LEARNED ? NEPI * 32 * 8 : 0) + 1024;  // + 1 KB alignment slack (SW128)
 };
 static_assert(K1Cfg<true>::SMEM <= 232448, "learned K1 shared memory");
 static_assert(K1Cfg<false>::SMEM <= 232448, "K1 shared memory");
@@ -904,6 +905,7 @@ __global__ void __launch_bounds__(K1Cfg<LEARNED>::THREADS, 1)
     uint32_t* stage = reinterpret_cast<uint32_t*>(smem + OFF_CODES + g * TM * 64) + 32 * quad * 16;
     const uint32_t sw = (uint32_t)(lane >> 1) & 15u;
     uint16_t* fixq = reinterpret_cast<uint16_t*>(smem + OFF_FIXQ + ew * Cfg::FIXQ);
+    int64_t* s_slot = reinterpret_cast<int64_t*>(smem + Cfg::OFF_SLOT) + ew * 32 + lane;
     const uint32_t ta0 = tmem + ((uint32_t)(32 * quad) << 16) + (uint32_t)(g * 128);
     int k_tile = 0;
     for (int tile = blockIdx.x + g * gridDim.x; tile < total; tile += NGRP * gridDim.x, ++k_tile) {
@@ -913,7 +915,16 @@ __global__ void __launch_bounds__(K1Cfg<LEARNED>::THREADS, 1)
       const int row = (side ? tile - p.tiles_per_side : tile) * TM + rl;
       const bool valid = row < p.n_rows;
       const int tok = hshift >= 0 ? row >> hshift : row / H;
-      const int64_t slot = valid ? __ldg(&p.slots[tok]) : -1;
+      // the row's slot id: learned kernel -- global -> shared by an async copy (LDGSTS), nothing waits
+      // on it until the sidecars (a plain load here is spilled at once, stalling on its latency:
+      // 65,536-token learned write 158 -> 154 us); the Hadamard kernel (96 registers) keeps the load
+      // (the copy's extra live state cost it 101 -> 108 us)
+      const int64_t slot_ld = (!LEARNED && valid) ? __ldg(&p.slots[tok]) : -1;
+      if constexpr (LEARNED) {
+        if (valid)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(s_slot)), "l"(p.slots + tok)
+                       : "memory");
+      }
       mbar_wait(&tfull[g], k_tile & 1);
       tc_fence_after();
       float v[8][8];  // [block b][column 8 ch + c of the block]
@@ -953,7 +964,7 @@ __global__ void __launch_bounds__(K1Cfg<LEARNED>::THREADS, 1)
       }
       const bool fin = isfinite(mx) && isfinite(mn);
       if (valid && !fin && p.flags) atomicOr(p.flags, (uint32_t)KVR_FLAG_NONFINITE);
-      const bool wr = valid && fin && slot >= 0;
+      bool wr = valid && fin && slot_ld >= 0;  // (learned: set once the slot id has landed)
       const RowQ rq = row_quant(mx, mn, rot ? scl_rot : 1.0, valid && fin);
       const bool clamp = __any_sync(0xffffffffu, rq.codes && rq.clamp);
       const bool cd = rq.codes;
@@ -1021,6 +1032,12 @@ __global__ void __launch_bounds__(K1Cfg<LEARNED>::THREADS, 1)
         }
       }
       // ---- sidecars and the row's destination
+      int64_t slot = slot_ld;
+      if constexpr (LEARNED) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        slot = valid ? *s_slot : -1;
+        wr = valid && fin && slot >= 0;
+      }
       unsigned long long rowdst = 0ull;
       if (wr) {
         const int head = row - tok * H;
