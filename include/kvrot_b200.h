@@ -33,6 +33,8 @@
  *                               (rotation.py:171-184) applied to queries / outputs
  *   kvr_rotate_quantize_store_learned <- append with a learned spec (rotation.py:118-168 then
  *                               cache.py:235-270), R fused into the write kernel
+ *   kvr_paged_decode_learned <- attention.decode_step on a learned spec (attention.py:50-87,
+ *                               rotation.py:162-184), q T and the value branch's inverse fused
  */
 #ifndef KVROT_B200_H
 #define KVROT_B200_H
@@ -283,6 +285,26 @@ int kvr_paged_decode(const void* q, int32_t q_dtype, const kvr_pool* pool,
                      int32_t batch, int32_t num_q_heads, int32_t max_seq_len, int32_t rot_order,
                      int32_t rotate, int32_t targets, const uint32_t* sign_words, float* out,
                      void* workspace, size_t workspace_bytes, int32_t num_splits, void* stream);
+
+/*
+ * Row f3: paged INT4 decode with a learned rotation fused into the kernel (attention.py:50-87 on
+ * a learned spec, rotation.py:118-168): the query is multiplied by the composed key transform
+ * T = diag(s) H_blk R (compose_transform, rotation.py:171-184) in the kernel's prologue, and the
+ * output goes back through the value branch (value_branch_spec, rotation.py:162-168) before the
+ * store.  Same arguments as kvr_paged_decode, plus
+ *   t_pad    : device f32 [128][129] = T with a row stride of 129 floats (16-B aligned)
+ *   out_mode : 0 keys only (no output transform), 1 values rotated by the Hadamard part only
+ *              (learned_values = False: block Hadamard inverse of rot_order, then sign_words),
+ *              2 values through T as well (learned_values = True: o T^T)
+ * At most 32 splits (the merge runs inside the grid).  d = 128, T = 16, power-of-two pages,
+ * G in {1, 2, 4, 8}: KVR_ERR_UNSUPPORTED otherwise (the caller then rotates the query and the
+ * output itself around kvr_paged_decode, e.g. with kvr_rows_matmul_f64).
+ */
+int kvr_paged_decode_learned(const void* q, int32_t q_dtype, const kvr_pool* pool,
+                             const int32_t* block_table, int32_t bt_stride, const int32_t* seq_lens,
+                             int32_t batch, int32_t num_q_heads, int32_t max_seq_len, const float* t_pad,
+                             int32_t out_mode, int32_t rot_order, const uint32_t* sign_words, float* out,
+                             void* workspace, size_t workspace_bytes, int32_t num_splits, void* stream);
 
 /*
  * Flat full-precision decode (attention.decode_step_fp): q (num_q_heads, d), k / v

@@ -34,6 +34,7 @@ EXPORTED = (
     "kvr_step_ring_create", "kvr_step_ring_set_slot", "kvr_step_ring_run", "kvr_step_ring_destroy",
     "kvr_step_ring_set_copy_stream", "kvr_step_ring_set_decode", "kvr_debug_step_ring_times",
     "kvr_rotate_quantize_store_learned", "kvr_learned_pack_image", "kvr_rows_matmul_f64",
+    "kvr_paged_decode_learned",
 )
 
 
@@ -95,6 +96,8 @@ def _declare(lib):
         "kvr_decode_pick_splits": (_I32, [_I32, _I32, _I32, _I32]),
         "kvr_paged_decode": (_I32, [_P, _I32, ctypes.POINTER(KvrPool), _P, _I32, _P, _I32, _I32, _I32, _I32, _I32,
                                     _I32, _P, _P, _P, _SZ, _I32, _P]),
+        "kvr_paged_decode_learned": (_I32, [_P, _I32, ctypes.POINTER(KvrPool), _P, _I32, _P, _I32, _I32, _I32, _P,
+                                            _I32, _I32, _P, _P, _P, _SZ, _I32, _P]),
         "kvr_decode_step": (_I32, [_P, _I32, _P, _P, _I32, _P, ctypes.POINTER(KvrPool), _P, _I32, _P, _I32, _I32,
                                    _I32, _I32, _I32, _I32, _P, _P, _P, _SZ, _I32, _P, _P]),
     }

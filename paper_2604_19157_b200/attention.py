@@ -22,7 +22,7 @@ from . import _kernels, _lib
 from .cache import INT4, PageTable
 from .errors import EmptySequenceError, NonFiniteInputError, ShapeError
 from .layout import HeadLayout
-from .rotation import RotationSpec, Targets, composed_on, rows_matmul
+from .rotation import RotationSpec, Targets, composed_on, learned_decode_operand, rows_matmul
 
 _Q_CODE = {torch.float32: _lib.KVR_F32, torch.bfloat16: _lib.KVR_BF16, torch.float16: _lib.KVR_F16}
 _KV_CODE = {torch.float64: _lib.KVR_F64, **_Q_CODE}
@@ -174,11 +174,27 @@ class DecodePlan:
 
     def _run_learned(self, q: torch.Tensor, spec: RotationSpec, out: torch.Tensor,
                      lens: Optional[torch.Tensor] = None) -> torch.Tensor:
-        """Row f3: the query through the composed T = diag(s) H_blk R (one f64
-        row-matmul launch, f32 out), the INT4 decode kernel on the pre-rotated query,
-        then the value branch's T^T on the output (one launch) (attention.py:63-85)."""
+        """Row f3 (attention.py:63-85 on a learned spec): one kvr_paged_decode_learned launch -- the
+        query through the composed T = diag(s) H_blk R in the kernel's prologue, the value branch's
+        inverse before the store.  Geometries that kernel does not take: the query through T (one
+        f64 row-matmul launch, f32 out), the INT4 decode on the pre-rotated query, then the value
+        branch's T^T on the output (one launch)."""
         lay = self.table.layout
         dev = self.table.device
+        if (self.table.precision == INT4 and lay.head_dim == 128 and os.environ.get("KVR_LEARNED_DECODE", "fused")
+                == "fused"):
+            # one launch: q T in the kernel's prologue, the value branch's inverse before the store
+            t_pad, mode = learned_decode_operand(spec, lay, dev)
+            if not q.is_contiguous():
+                q = q.contiguous()
+            rc = _lib.lib().kvr_paged_decode_learned(
+                _kernels.ptr(q), _Q_CODE[q.dtype], ctypes.byref(self.table.desc), _kernels.ptr(self.bt),
+                self.bt.shape[1], _kernels.ptr(lens), len(self.seqs), lay.num_q_heads, self.max_len,
+                _kernels.ptr(t_pad), mode, spec.order, spec.sign_words(lay.head_dim), _kernels.ptr(out),
+                _kernels.ptr(self.ws), self.ws.numel(), self.splits, _kernels.stream_ptr())
+            if rc != _lib.KVR_ERR_UNSUPPORTED:
+                _lib.check(rc)
+                return out
         qr = getattr(self, "_lq", None)
         if qr is None or qr.shape != q.shape:
             qr = self._lq = torch.empty(q.shape, dtype=torch.float32, device=dev)

@@ -634,6 +634,43 @@ int kvr_paged_decode(const void* q, int32_t q_dtype, const kvr_pool* pool, const
   return check_launch("paged_decode");
 }
 
+int kvr_paged_decode_learned(const void* q, int32_t q_dtype, const kvr_pool* pool, const int32_t* block_table,
+                             int32_t bt_stride, const int32_t* seq_lens, int32_t batch, int32_t num_q_heads,
+                             int32_t max_seq_len, const float* t_pad, int32_t out_mode, int32_t rot_order,
+                             const uint32_t* sign_words, float* out, void* workspace, size_t workspace_bytes,
+                             int32_t num_splits, void* stream) {
+  Pool pl;
+  if (int rc = to_pool(pool, pl)) return rc;
+  if (batch < 0 || num_q_heads < 1 || num_q_heads % pl.H != 0)
+    return fail(KVR_ERR_SHAPE, "num_q_heads=%d is not a multiple of num_kv_heads=%d", num_q_heads, pl.H);
+  if (!t_pad || (reinterpret_cast<uintptr_t>(t_pad) & 15)) return fail(KVR_ERR_ARG, "t_pad must be 16-B aligned");
+  if (out_mode < 0 || out_mode > 2) return fail(KVR_ERR_ARG, "out_mode=%d (0, 1 or 2)", out_mode);
+  if (batch == 0) return KVR_OK;
+  if (max_seq_len < 0 || (int64_t)bt_stride * pl.P < max_seq_len)
+    return fail(KVR_ERR_SHAPE, "max_seq_len=%d exceeds bt_stride=%d pages of %d tokens", max_seq_len, bt_stride, pl.P);
+  if (q_dtype != KVR_F32 && q_dtype != KVR_BF16 && q_dtype != KVR_F16)
+    return fail(KVR_ERR_ARG, "q dtype %d unsupported (F32/BF16/F16)", q_dtype);
+  const int G = num_q_heads / pl.H;
+  if (pl.prec != KVR_PREC_INT4 || pl.d != 128 || pl.T != 16 || (pl.P & (pl.P - 1)) ||
+      !(G == 1 || G == 2 || G == 4 || G == 8))
+    return fail(KVR_ERR_UNSUPPORTED, "paged_decode_learned: INT4, d = 128, power-of-two pages, G in 1/2/4/8");
+  Signs s;
+  int has = 0;
+  if (out_mode == 1) {
+    if (int rc = check_order(pl.d, rot_order)) return rc;
+    if (int rc = make_signs(sign_words, pl.d, s, has)) return rc;
+  } else {
+    rot_order = 1;
+    if (int rc = make_signs(nullptr, pl.d, s, has)) return rc;
+  }
+  const int rc = kvr_launch_decode(q, q_dtype, pl, block_table, bt_stride, seq_lens, batch, num_q_heads, max_seq_len,
+                                   128, 0, 0, s, has, out, workspace, workspace_bytes, num_splits, (cudaStream_t)stream,
+                                   nullptr, nullptr, 0, nullptr, nullptr, 0, t_pad, out_mode, rot_order);
+  if (rc == KVR_ERR_ARG) return fail(rc, "decode workspace too small");
+  if (rc) return fail(rc, "paged_decode_learned: unsupported geometry (d=%d, P=%d, G=%d)", pl.d, pl.P, G);
+  return check_launch("paged_decode_learned");
+}
+
 int kvr_decode_step(const void* q, int32_t q_dtype, const void* new_k, const void* new_v, int32_t kv_dtype,
                     const int64_t* new_slot, const kvr_pool* pool, const int32_t* block_table, int32_t bt_stride,
                     const int32_t* seq_lens, int32_t batch, int32_t num_q_heads, int32_t max_seq_len,

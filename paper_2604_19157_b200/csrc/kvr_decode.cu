@@ -71,6 +71,12 @@ struct DecodeParams {
   int meta_post_wait;   // lengths / slot ids come from the previous grid: read them after the wait
   uint32_t f16x2_1024;  // 0x64006400 (fp16x2 1024.0) from the parameter bank: an opaque operand lets
                         // ptxas fuse (x & mask) | 1024 into one LOP3 (two immediates need two)
+  // row f3, learned rotation fused into the decode (the ORDER = 0 instantiation): the composed
+  // T = diag(s) H_blk R as f32 [128][LT_STRIDE] (bulk-copied into shared memory before the wait);
+  // the query is multiplied by T in the prologue, the output mapped back by lq_out: 0 none
+  // (KEYS_ONLY), 1 the value branch's block Hadamard inverse (order lq_order, the signs), 2 T^T
+  const float* lq;
+  int lq_out, lq_order;
 };
 
 KVR_DEV unsigned long long clk64() {
@@ -473,7 +479,17 @@ constexpr int SM_QROT = SM_OBUF + 4096;                               // fp32 ro
 constexpr int SM_VNEW = SM_QROT + 4096;                               // new token's V row [128] (APPEND)
 constexpr int SM_MISC = SM_VNEW + 512;                               // sumq[8] ksc[8] tot[8] flag lse[8]
 constexpr int SM_TOTAL = SM_MISC + 256;
+// learned instantiation only: T [128][129] f32 (row stride 129 floats: both the q T column walk and
+// the o T^T row walk hit 32 distinct banks) and its mbarrier
+constexpr int LT_STRIDE = 129;
+constexpr int LT_BYTES = 128 * LT_STRIDE * 4;  // 66,048 (a multiple of 16: one bulk copy)
+constexpr int SM_LT = SM_TOTAL;
+constexpr int SM_LTBAR = SM_LT + LT_BYTES;
+constexpr int SM_TOTAL_LQ = SM_LTBAR + 16;
+static_assert(SM_LT % 16 == 0, "bulk-copy destination");
+static_assert(1024 + SM_TOTAL_LQ <= 232448, "learned decode shared memory");
 size_t decode_smem_bytes() { return 1024 + SM_TOTAL; }
+size_t decode_smem_bytes_lq() { return 1024 + SM_TOTAL_LQ; }
 
 // Fragments of one staged cell: k_scale[16] | v_scale[16] | K codes [16][64] |
 // V codes [16][64] | k_zp[16] | v_zp[16]
@@ -511,11 +527,52 @@ KVR_DEV void load_cell_rest(CellFrag& f, const uint8_t* st, int r, int i) {
 // rotation of the value branch (o @ H_blk @ diag(signs)) as an fp32 butterfly in
 // registers / shuffles, then a 16-B store per lane.  `row` is o in natural order.
 template <int ORDER>
-KVR_DEV void emit_head(const DecodeParams& p, uint32_t sgw, int b, int h, int j, const float* row, int lane) {
+KVR_DEV void emit_head(const DecodeParams& p, uint32_t sgw, int b, int h, int j, const float* row, int lane,
+                       const float* s_t = nullptr) {
+  float* orow = p.out + ((int64_t)b * p.nq + (int64_t)h * p.G + j) * 128;
   float x[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) x[u] = row[4 * lane + u];
-  if (p.rotate && p.rot_v) {
+  if constexpr (ORDER == 0) {  // row f3 (learned R fused): the output transform of the value branch
+    if (p.lq_out == 2) {
+      // o T^T: lane owns outputs n = lane + 32 m, y_n = sum_k o_k T[n][k] (T rows in shared memory)
+      float ya[4] = {0.f, 0.f, 0.f, 0.f}, yb[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+      for (int k = 0; k < 128; k += 2) {
+        const float o0 = row[k], o1 = row[k + 1];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          ya[m] = fmaf(o0, s_t[(lane + 32 * m) * LT_STRIDE + k], ya[m]);
+          yb[m] = fmaf(o1, s_t[(lane + 32 * m) * LT_STRIDE + k + 1], yb[m]);
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < 4; ++m) orow[lane + 32 * m] = ya[m] + yb[m];
+      return;
+    }
+    if (p.lq_out == 1) {  // the block Hadamard inverse at the runtime order, then the signs
+      const float a0 = x[0] + x[1], a1 = x[0] - x[1], a2 = x[2] + x[3], a3 = x[2] - x[3];
+      x[0] = a0 + a2;
+      x[1] = a1 + a3;
+      x[2] = a0 - a2;
+      x[3] = a1 - a3;
+#pragma unroll 1
+      for (int k = 0; (4 << k) < p.lq_order; ++k) {
+        const float sgn = ((lane >> k) & 1) ? -1.f : 1.f;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float o = __shfl_xor_sync(0xffffffffu, x[u], 1 << k);
+          x[u] = fmaf(sgn, x[u], o);
+        }
+      }
+      const float inv = rsqrtf((float)p.lq_order);  // a power of two: exact
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        x[u] *= inv;
+        if ((sgw >> (4 * (lane & 7) + u)) & 1u) x[u] = -x[u];
+      }
+    }
+  } else if (p.rotate && p.rot_v) {
     const float a0 = x[0] + x[1], a1 = x[0] - x[1], a2 = x[2] + x[3], a3 = x[2] - x[3];
     x[0] = a0 + a2;
     x[1] = a1 + a3;
@@ -537,8 +594,7 @@ KVR_DEV void emit_head(const DecodeParams& p, uint32_t sgw, int b, int h, int j,
       if ((sgw >> (4 * (lane & 7) + u)) & 1u) x[u] = -x[u];
     }
   }
-  float4* dst = reinterpret_cast<float4*>(p.out + ((int64_t)b * p.nq + (int64_t)h * p.G + j) * 128) + lane;
-  *dst = make_float4(x[0], x[1], x[2], x[3]);
+  reinterpret_cast<float4*>(orow)[lane] = make_float4(x[0], x[1], x[2], x[3]);
 }
 
 // K2+K3.  grid (kv head, split, sequence); NWARPS warps, one CTA per SM.  With
@@ -633,9 +689,21 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
   // bank before the dependency wait (0 = no flips)
   const uint32_t sgw = p.has_signs ? signs.w[lane >> 3] : 0u;
   if (threadIdx.x < NWARPS * RING_CELLS) mbar_init(&bars[threadIdx.x], 1);
+  // row f3 (learned instantiation): T is a parameter of the rotation (immutable), so its bulk copy
+  // goes out before the dependency wait
+  float* s_t = reinterpret_cast<float*>(sm + SM_LT);
+  uint64_t* ltbar = reinterpret_cast<uint64_t*>(sm + SM_LTBAR);
+  if constexpr (ORDER == 0)
+    if (threadIdx.x == NWARPS * RING_CELLS) mbar_init(ltbar, 1);
   reinterpret_cast<uint2*>(sfrag)[threadIdx.x] = make_uint2(0u, 0u);  // 4 KB of query digits (padding = 0)
   fence_mbar_init();
   __syncthreads();
+  if constexpr (ORDER == 0) {
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(ltbar, (uint32_t)LT_BYTES);
+      bulk_g2s(s_t, p.lq, (uint32_t)LT_BYTES, ltbar);
+    }
+  }
   const int len_raw = *s_len;
   const int64_t new_slot = APPEND ? *s_slot : -1;
 
@@ -729,9 +797,38 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       x[u] = qx[u];
-      if (p.rotate && ((sgw >> (4 * (lane & 7) + u)) & 1u)) x[u] = -x[u];
+      if (ORDER != 0 && p.rotate && ((sgw >> (4 * (lane & 7) + u)) & 1u)) x[u] = -x[u];
     }
-    if (p.rotate) {
+    if constexpr (ORDER == 0) {
+      // row f3: q' = q T (T = diag(s) H_blk R composed, rotation.py:171-184) in fp32 from shared
+      // memory: lane owns n = lane + 32 m while it sums over k (row stride 129: conflict-free), then
+      // the lanes trade back to dims 4 l .. 4 l + 3 through the head's row of s_qrot
+      float* s_x = s_qrot + j * 128;
+      *reinterpret_cast<float4*>(s_x + 4 * lane) = make_float4(x[0], x[1], x[2], x[3]);
+      __syncwarp();
+      mbar_wait(ltbar, 0);
+      float ya[4] = {0.f, 0.f, 0.f, 0.f}, yb[4] = {0.f, 0.f, 0.f, 0.f};
+      if (j < G) {
+#pragma unroll 4
+        for (int k = 0; k < 128; k += 2) {
+          const float x0 = s_x[k], x1 = s_x[k + 1];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            ya[m] = fmaf(x0, s_t[k * LT_STRIDE + lane + 32 * m], ya[m]);
+            yb[m] = fmaf(x1, s_t[(k + 1) * LT_STRIDE + lane + 32 * m], yb[m]);
+          }
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int m = 0; m < 4; ++m) s_x[lane + 32 * m] = ya[m] + yb[m];
+      __syncwarp();
+      const float4 y4 = *reinterpret_cast<const float4*>(s_x + 4 * lane);
+      x[0] = y4.x;
+      x[1] = y4.y;
+      x[2] = y4.z;
+      x[3] = y4.w;
+    } else if (p.rotate) {
       const float a0 = x[0] + x[1], a1 = x[0] - x[1], a2 = x[2] + x[3], a3 = x[2] - x[3];
       x[0] = a0 + a2;
       x[1] = a1 + a3;
@@ -1258,7 +1355,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
       }
     }
     __syncthreads();
-    if (warp < G && warp % S == rank) emit_head<ORDER>(p, sgw, b, h, warp, omerge + warp * 128, lane);
+    if (warp < G && warp % S == rank) emit_head<ORDER>(p, sgw, b, h, warp, omerge + warp * 128, lane, s_t);
     KVR_STAMP(9);  // merged + stored
     cluster_sync_relaxed();  // every CTA's partial stays readable until all merges are done
     KVR_STAMP(10);
@@ -1333,7 +1430,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
       if (sg == 0) obuf[dd] = tot > 0.f ? acc / tot : 0.f;
     }
     __syncthreads();  // the merged row is in obuf
-    if (warp == 0) emit_head<ORDER>(p, sgw, b, h, j, obuf, lane);
+    if (warp == 0) emit_head<ORDER>(p, sgw, b, h, j, obuf, lane, s_t);
     if (threadIdx.x == 0) p.ws_epoch[((int64_t)b * H + h) * 8 + j] = want;  // read again only by the next launch
     KVR_STAMP(9);  // merged + stored
     return;
@@ -1395,14 +1492,14 @@ __global__ void __launch_bounds__(NWARPS * 32, 1)
       obuf[j * 128 + dd] = ot;
     }
     __syncthreads();
-    if (warp < G) emit_head<ORDER>(p, sgw, b, h, warp, obuf + warp * 128, lane);
+    if (warp < G) emit_head<ORDER>(p, sgw, b, h, warp, obuf + warp * 128, lane, s_t);
     if (threadIdx.x == 0) p.ws_cnt[(int64_t)b * H + h] = 0u;  // read again only after this grid completes
     KVR_STAMP(9);  // merged + stored
     return;
   }
   __syncthreads();
   // ---- output: one warp per q head
-  if (warp < G) emit_head<ORDER>(p, sgw, b, h, warp, obuf + warp * 128, lane);
+  if (warp < G) emit_head<ORDER>(p, sgw, b, h, warp, obuf + warp * 128, lane, s_t);
   KVR_STAMP(10);
 }
 
@@ -2070,7 +2167,7 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
                       const int32_t* lens, int batch, int nq, int max_len, int order, int rotate, int rot_v,
                       const Signs& s, int has, float* out, void* ws, size_t ws_bytes, int splits, cudaStream_t st,
                       const void* new_k, const void* new_v, int new_dtype, const int64_t* new_slot,
-                      uint32_t* flags, int q_host_staged) {
+                      uint32_t* flags, int q_host_staged, const float* lq, int lq_out, int lq_order) {
   DecodeParams p{};
   p.q_pre_wait = q_host_staged == 1;
   p.meta_post_wait = q_host_staged == 2;
@@ -2113,10 +2210,15 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
   const bool tma_ok = pow2 && pool.prec == KVR_PREC_INT4 && pool.d == 128 && pool.T == 16 &&
                       (p.G == 1 || p.G == 2 || p.G == 4 || p.G == 8) &&
                       (reinterpret_cast<uintptr_t>(pool.base) & 15) == 0 && (pool.cell_bytes & 15) == 0;
+  if (lq && !tma_ok) return KVR_ERR_UNSUPPORTED;  // row f3 fused only in the TMA kernel
   if (tma_ok) {
     if (splits <= 0) splits = kvr_pick_splits(batch, pool.H, max_len, pool.P);
     if (splits > MAX_SPLITS) splits = MAX_SPLITS;
-    if (splits > 1 && kvr_decode_ws_bytes(batch, pool.H, nq, 128, splits) > ws_bytes) return KVR_ERR_ARG;
+    if (lq && splits > MERGE_INLINE_MAX) splits = MERGE_INLINE_MAX;  // row f3: merged in-grid (the merge kernel has no T)
+    // the partials' space is required; the flag-in-data merge's words only where the caller sized
+    // the workspace for them (merge_ll below checks that they fit)
+    if (splits > 1 && ws_cnt_bytes(batch, pool.H) + (size_t)batch * pool.H * splits * 8 * 129 * sizeof(float) > ws_bytes)
+      return KVR_ERR_ARG;
     p.splits = splits;
     p.split_tiles = (((max_len + 15) >> 4) + splits - 1) / splits;
     const size_t units = (size_t)batch * pool.H * splits * 8;
@@ -2124,14 +2226,24 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
     p.ws_epoch = p.ws_cnt + (size_t)batch * pool.H;
     p.ws_lse = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + ws_cnt_bytes(batch, pool.H));
     p.ws_o = p.ws_lse + units;
+    size_t ll_end;
     {
       const size_t base = (ws_cnt_bytes(batch, pool.H) + units * sizeof(float) * 129 + 255) & ~size_t(255);
       p.ll_lse = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(ws) + base);
       p.ll_o = p.ll_lse + (size_t)batch * pool.H * 8 * 32;
+      ll_end = base + ws_ll_bytes(batch, pool.H);
+    }
+    if (lq) {  // row f3 fused: a merge inside the decode grid (the merge kernel has no T)
+      if (new_slot) return KVR_ERR_UNSUPPORTED;
+      p.lq = lq;
+      p.lq_out = lq_out;
+      p.lq_order = lq_order;
+      p.rotate = 0;
+      p.rot_v = 0;
     }
     dim3 grid(pool.H, splits, batch);
     const int ord = rotate ? order : 128;
-    const size_t smem = decode_smem_bytes();
+    const size_t smem = lq ? decode_smem_bytes_lq() : decode_smem_bytes();
     int cl = 0;
     while ((16 << cl) < pool.P) ++cl;
     p.cps_log2 = cl;
@@ -2144,8 +2256,9 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
 #endif
     p.merge_inline = KVR_MERGE_INLINE && !p.use_cluster && splits > 1 && splits <= MERGE_INLINE_MAX;
     // flag-in-data merge when the grid is one wave (the merger CTAs spin on the others' words)
-    p.merge_ll = KVR_MERGE_LL && p.merge_inline && ws_has_ll(batch, pool.H, splits) &&
+    p.merge_ll = KVR_MERGE_LL && p.merge_inline && ws_has_ll(batch, pool.H, splits) && ll_end <= ws_bytes &&
                  (long)batch * pool.H * splits <= (kvr_num_sms() > 0 ? kvr_num_sms() : 148) && p.G <= 8;
+    if (lq) return p.G == 8 ? launch_sel<2, 0, false>(grid, smem, st, p, sg) : launch_sel<1, 0, false>(grid, smem, st, p, sg);
     if (new_slot)
       return p.G == 8 ? launch_tma<2, true>(p, sg, grid, smem, ord, st) : launch_tma<1, true>(p, sg, grid, smem, ord, st);
     return p.G == 8 ? launch_tma<2, false>(p, sg, grid, smem, ord, st) : launch_tma<1, false>(p, sg, grid, smem, ord, st);

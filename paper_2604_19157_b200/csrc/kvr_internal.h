@@ -51,7 +51,11 @@ int kvr_launch_decode(const void* q, int q_dtype, const kvr::Pool& pool, const i
                       const int32_t* lens, int batch, int nq, int max_len, int order, int rotate, int rot_v,
                       const kvr::Signs& s, int has, float* out, void* ws, size_t ws_bytes, int splits,
                       cudaStream_t st, const void* new_k = nullptr, const void* new_v = nullptr, int new_dtype = 0,
-                      const int64_t* new_slot = nullptr, uint32_t* flags = nullptr, int q_host_staged = 0);
+                      const int64_t* new_slot = nullptr, uint32_t* flags = nullptr, int q_host_staged = 0,
+                      const float* lq = nullptr, int lq_out = 0, int lq_order = 0);
+// lq (row f3): the composed learned transform T as f32 [128][129] (decode_tma_kernel<., 0, .>), the
+// query multiplied by it in the prologue; lq_out: 0 no output transform, 1 block Hadamard inverse of
+// order lq_order with the signs, 2 T^T
 // q_host_staged: 0 plain; 1 the query is host-staged (read before the wait); 2 lengths / slot ids
 // are written by the preceding grid (read after the wait; no pre-wait cell requests)
 

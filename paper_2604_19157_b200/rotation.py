@@ -179,6 +179,23 @@ def learned_store_operands(spec: RotationSpec, layout: HeadLayout, device):
     return cache[key]
 
 
+def learned_decode_operand(spec: RotationSpec, layout: HeadLayout, device):
+    """Row f3, fused decode operand (memoised per device and layout): the composed key
+    transform T = diag(s) H_blk R (compose_transform, rotation.py:171-184) as f32 with a row
+    stride of 129 floats (kvr_paged_decode_learned), and the output mode of the value branch
+    (value_branch_spec, rotation.py:162-168): 0 none, 1 the Hadamard part only, 2 T itself."""
+    cache = spec.__dict__.setdefault("_learned_dec", {})
+    key = (str(torch.device(device)), layout.head_dim, layout.rot_order)
+    if key not in cache:
+        t = compose_transform(spec, layout)
+        pad = np.zeros((t.shape[0], t.shape[1] + 1), dtype=np.float32)
+        pad[:, :t.shape[1]] = t
+        vb = value_branch_spec(spec)
+        mode = 0 if vb is None else (2 if vb.learned is not None else 1)
+        cache[key] = (torch.from_numpy(pad).to(device), mode)
+    return cache[key]
+
+
 def rotate_kv_learned(k: torch.Tensor, v: torch.Tensor, layout: HeadLayout, spec: RotationSpec):
     """Row f3 (learned R composed after the Hadamard), unfused on the device: the
     K rows through the full transform, the V rows through value_branch_spec

@@ -107,6 +107,19 @@ def test_learned_entry_points_validate_without_device(libpath):
     a2 = list(args)
     a2[5] = ctypes.byref(bf)
     assert lib.kvr_rotate_quantize_store_learned(*a2, dummy, dummy, None, None) == 3  # BF16 pool
+    # the fused learned decode: null / misaligned T, out_mode, order (mode 1), BF16 pool, G = 3
+    dargs = (dummy, _lib.KVR_BF16, ctypes.byref(pool), dummy, 4, dummy, 1, 32, 64)
+    tail = (128, None, dummy, dummy, 1 << 20, 0, None)
+    assert lib.kvr_paged_decode_learned(*dargs, None, 2, *tail) == 5  # null T
+    assert lib.kvr_paged_decode_learned(*dargs, ctypes.c_void_p(264), 2, *tail) == 5  # misaligned T
+    assert lib.kvr_paged_decode_learned(*dargs, dummy, 3, *tail) == 5  # out_mode
+    assert lib.kvr_paged_decode_learned(*dargs, dummy, 1, 48, *tail[1:]) == 2  # Hadamard order
+    d_bf = list(dargs)
+    d_bf[2] = ctypes.byref(bf)
+    assert lib.kvr_paged_decode_learned(*d_bf, dummy, 2, *tail) == 3  # BF16 pool: the row-matmul route
+    d_g3 = list(dargs)
+    d_g3[7] = 24
+    assert lib.kvr_paged_decode_learned(*d_g3, dummy, 2, *tail) == 3  # G = 3
     # rows_matmul: shape, size, aliasing and null checks
     assert lib.kvr_rows_matmul_f64(dummy, _lib.KVR_F64, dummy, dummy, _lib.KVR_F64, -1, 128, None) == 1
     assert lib.kvr_rows_matmul_f64(dummy, _lib.KVR_F64, dummy, ctypes.c_void_p(512), _lib.KVR_F64, 4, 1024,

@@ -273,3 +273,32 @@ def test_learned_store_geometries_and_dtypes(P, H, dt):
         assert np.max(np.abs(gs - sk) / np.abs(sk)) <= 1e-5
     print(f"learned P={P} H={H} {dt}: nibble mismatches {mism} of {total}")
     assert mism <= total * 1e-4
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+@pytest.mark.parametrize("targets,learned_values", [(Targets.KEYS_AND_VALUES, False), (Targets.KEYS_AND_VALUES, True),
+                                                    (Targets.KEYS_ONLY, False)])
+def test_learned_fused_decode_matches_unfused(monkeypatch, G, targets, learned_values):
+    """kvr_paged_decode_learned (q T in the kernel's prologue, the value branch's inverse before
+    the store) == the unfused route (f64 row-matmul launches around the plain decode) for every
+    merge path: one split, a cluster, the flag-in-data merge, and a split count above 32 (clamped)."""
+    H, d, P = 2, 128, 16
+    lens = [37, 2000, 700]
+    layout = HeadLayout(num_q_heads=G * H, num_kv_heads=H, head_dim=d, rot_order=64, page_tokens=P)
+    t = PageTable(layout, num_pages=sum((L + P - 1) // P for L in lens) + 2)
+    spec = RotationSpec(order=64, signs=make_signs(5, 0, d, 64), learned=_orth(d, 13), targets=targets,
+                        learned_values=learned_values)
+    rng = np.random.default_rng(G)
+    for s, L in enumerate(lens):
+        t.create_sequence(s)
+        t.append_batch([s] * L, torch.tensor(rng.standard_normal((L, H, d))), torch.tensor(rng.standard_normal((L, H, d))),
+                       spec=spec, check=False)
+    q = torch.tensor(rng.standard_normal((len(lens), G * H, d)), dtype=torch.float32).cuda()
+    for splits in (1, 4, 16, 64):
+        plan = DecodePlan(t, list(range(len(lens))), num_splits=splits)
+        monkeypatch.setenv("KVR_LEARNED_DECODE", "fused")
+        fused = plan.run(q, spec).clone()
+        monkeypatch.setenv("KVR_LEARNED_DECODE", "unfused")
+        ref = plan.run(q, spec).clone()
+        err = float((fused - ref).abs().max() / ref.abs().max())
+        assert err < 2e-5, (splits, err)

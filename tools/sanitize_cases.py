@@ -50,8 +50,9 @@ oh = torch.empty(1, H * G, D).pin_memory()
 for _ in range(12):
     plan.step(qh, kh, vh, spec, out=oh, graph=True)
 torch.cuda.synchronize()
-# row f3: the learned-R K1 (tcgen05, T in shared memory; V plain / Hadamard / T) and the
-# row-matmul query / output transforms around the decode
+# row f3: the learned-R K1 (tcgen05, T in shared memory; V plain / Hadamard / T) and the fused
+# learned decode (T bulk-copied into shared memory; q T in the prologue, the value branch's inverse
+# in every merge path: single CTA, cluster, flag-in-data merge, clamped split count)
 from paper_2604_19157_b200 import Targets  # noqa: E402
 
 qr_, rr_ = np.linalg.qr(np.random.default_rng(5).standard_normal((D, D)))
@@ -62,7 +63,8 @@ for tg, lv in ((Targets.KEYS_AND_VALUES, False), (Targets.KEYS_AND_VALUES, True)
     t.alloc.seq_pages[0] = []
     t.alloc.free = list(range(t.num_pages))
     t.store_slots(k, v, torch.from_numpy(t.alloc.reserve(0, L)).to(dev), lspec)
-    DecodePlan(t, [0], num_splits=12).run(q, lspec)
+    for splits in (1, 4, 12, 48):
+        DecodePlan(t, [0], num_splits=splits).run(q, lspec)
     torch.cuda.synchronize()
 # BF16 pool: the tuned decode (TMA cells, split-K + merge)
 from paper_2604_19157_b200.cache import BF16  # noqa: E402
