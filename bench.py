@@ -290,7 +290,7 @@ def run_ours(args, rank, world, local_rank):
     t_k2p = timed(lambda i: k2(sets[i % R], None), n_k) / n_k
     # row f3 at C2: a learned spec (same signs, an orthogonal R, learned_values) -- the fused learned
     # decode (q T in the kernel's prologue, o T^T before the store: one launch), and the serving
-    # step (new token through the exact f64 transform + store, then that decode).  Same bytes read;
+    # step (the new token through the fused learned K1, then that decode).  Same bytes read;
     # the values decoded are not meaningful (the pool was written with the Hadamard spec).
     qm_, rm_ = np.linalg.qr(np.random.default_rng(7).standard_normal((D, D)))
     lspec = RotationSpec(order=ORDER, signs=spec.signs, learned=qm_ * np.sign(np.diag(rm_)), learned_values=True)
@@ -299,7 +299,7 @@ def run_ours(args, rank, world, local_rank):
     learned_c2 = {"decode_us": round(t_k2l * 1e3, 3), "step_us": round(t_fl * 1e3, 3),
                   "hadamard_decode_us": round(t_k2 * 1e3, 3), "hadamard_step_us": round(t_fused * 1e3, 3),
                   "launches_decode": "one kvr_paged_decode_learned (q T in the prologue, o T^T in the merge)",
-                  "launches_step": "rows_matmul x 2 (the new K / V rows through T / T_v, f64) + exact store + the fused learned decode"}
+                  "launches_step": "the fused learned K1 (store_tc_kernel<LEARNED>, the new token) + the fused learned decode"}
     print(f"[bench] learned R at C2 {learned_c2}", file=sys.stderr, flush=True)
     # restore the rotated token in every set (the plain / learned twins overwrote slot L)
     for s in sets:

@@ -232,10 +232,14 @@ class DecodePlan:
             spec = None
         rotate = spec is not None
         if (rotate and spec.learned is not None) or not self.fused_ok:
-            # row f3 (learned R) and geometries without the one-launch kernel: the
-            # store kernel (exact f64 arithmetic, as the fused writer), then the decode
+            # row f3 (learned R) and geometries without the one-launch kernel: the store kernel,
+            # then the decode.  Hadamard / plain rows: exact f64 arithmetic, as the fused writer.
+            # Learned rows: the fused learned K1 where it applies (bf16, d = 128) -- the same
+            # one-step-at-a-boundary bar as the exact route, whose dense f64 product also sums in
+            # its own order (rotation.py:140-141 leaves that order to the BLAS)
             dev = table.device
-            table.store_slots(k_new.to(dev), v_new.to(dev), slots.to(dev), spec, exact=True)
+            learned = rotate and spec.learned is not None
+            table.store_slots(k_new.to(dev), v_new.to(dev), slots.to(dev), spec, exact=not learned)
             res = self.run(q.to(dev), spec, out if out.is_cuda else None, lens=lens.to(dev))
             if res is not out:
                 out.copy_(res, non_blocking=True)
