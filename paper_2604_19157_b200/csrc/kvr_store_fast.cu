@@ -608,6 +608,7 @@ struct TcStoreParams {
   int32_t n_rows;          // n_tok * H per side
   int32_t tiles_per_side;  // ceil(n_rows / 128)
   int32_t rot_k, rot_v;    // tile modes: 0 plain, 1 block Hadamard, 2 learned (T)
+  int32_t exact_rows;      // learned: rows with a code near a boundary redone whole (reference (s, z))
   int32_t log2P;
   const uint4* t_img;      // learned: the SW128 image of T's three bf16 parts (kvr_learned_pack), 96 KB
   const double* rt;        // learned: R^T, f64 [128 n][128 k], for the exact recomputation
@@ -749,6 +750,86 @@ __device__ __noinline__ uint32_t warp_learned_word(const uint16_t* xrow, const S
   const int j = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);  // this lane's element 8 w + j
   const uint32_t c = (lane & 3) ? 0u : code_f64(t, s64, z) << (4 * j);
   return __reduce_or_sync(0xffffffffu, c);
+}
+
+// Row f3, one whole learned row exactly (warp-cooperative): y = (x diag(s) H_blk) R in f64 for all
+// 16 words (the butterfly once, then word by word the transposing reduction above), the
+// reference's (s, z) from y's exact extremes (row_quant's arithmetic on f64 extremes), and the 16
+// code words under them into the row's staging words (lane 0; word w at w ^ swz).  Returns the
+// scale slot and zero point to store.  Used for every learned row with a code near a boundary:
+// the fast path's f32 extremes can move s by a few ulps, and a code that close to a boundary is
+// then only right under the reference's own (s, z).
+template <int ORDER>
+__device__ __noinline__ void warp_learned_row(const uint16_t* xrow, const Signs& sg, const double* rt, uint32_t* srow,
+                                              uint32_t swz, float& scale_out, uint32_t& zp_out) {
+  const int lane = threadIdx.x & 31;
+  const uint2 q = *reinterpret_cast<const uint2*>(xrow + 4 * lane);
+  double h[4];
+  const uint32_t xw[2] = {q.x, q.y};
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const uint32_t bits = (u & 1) ? (xw[u >> 1] >> 16) : (xw[u >> 1] & 0xFFFFu);
+    h[u] = (double)__uint_as_float(bits << 16);
+  }
+  warp_fwht_f64<ORDER>(h, sg);
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  double yv[16];
+#pragma unroll 1
+  for (int w = 0; w < 16; ++w) {
+    double y[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double2* rp = reinterpret_cast<const double2*>(rt + (size_t)(8 * w + j) * 128 + 4 * lane);
+      const double2 r0 = __ldg(rp), r1 = __ldg(rp + 1);
+      y[j] = fma(h[3], r1.y, fma(h[2], r1.x, fma(h[1], r0.y, h[0] * r0.x)));
+    }
+    double z4[4], z2[2];
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const double keep = b4 ? y[jj + 4] : y[jj], give = b4 ? y[jj] : y[jj + 4];
+      z4[jj] = keep + __shfl_xor_sync(0xffffffffu, give, 16);
+    }
+#pragma unroll
+    for (int jj = 0; jj < 2; ++jj) {
+      const double keep = b3 ? z4[jj + 2] : z4[jj], give = b3 ? z4[jj] : z4[jj + 2];
+      z2[jj] = keep + __shfl_xor_sync(0xffffffffu, give, 8);
+    }
+    double t = (b2 ? z2[1] : z2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? z2[0] : z2[1], 4);
+    t += __shfl_xor_sync(0xffffffffu, t, 2);
+    t += __shfl_xor_sync(0xffffffffu, t, 1);
+    yv[w] = t;  // element 8 w + j(lane), the same on the 4 lanes of a group
+  }
+  double mx = yv[0], mn = yv[0];
+#pragma unroll
+  for (int w = 1; w < 16; ++w) {
+    mx = fmax(mx, yv[w]);
+    mn = fmin(mn, yv[w]);
+  }
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  }
+  const float s32 = (float)div_rn_recip(mx - mn, 15.0, 1.0 / 15.0);
+  const int j = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
+  if (s32 == 0.0f) {  // constant row: the offset in the scale slot, zp 0xFF, codes 0
+    scale_out = (float)mn;
+    zp_out = 0xFFu;
+    if (lane == 0)
+      for (int w = 0; w < 16; ++w) srow[w ^ swz] = 0u;
+    return;
+  }
+  const double s64 = (double)s32;
+  double z = round_half_away(div_rn_recip(-mn, s64, __drcp_rn(s64)));
+  z = z < 0.0 ? 0.0 : (z > 15.0 ? 15.0 : z);
+  scale_out = s32;
+  zp_out = (uint32_t)z;
+#pragma unroll 1
+  for (int w = 0; w < 16; ++w) {
+    const uint32_t c = (lane & 3) ? 0u : code_f64(yv[w], s64, z) << (4 * j);
+    const uint32_t word = __reduce_or_sync(0xffffffffu, c);
+    if (lane == 0) srow[w ^ swz] = word;
+  }
 }
 
 template <int ORDER, bool F16, bool LEARNED>
@@ -1039,40 +1120,70 @@ __global__ void __launch_bounds__(K1Cfg<LEARNED>::THREADS, 1)
         wr = valid && fin && slot >= 0;
       }
       unsigned long long rowdst = 0ull;
+      float* sc_slot = nullptr;
+      uint8_t* zp_slot = nullptr;
       if (wr) {
         const int head = row - tok * H;
         const int64_t page = slot >> p.log2P;
         const int sip = (int)(slot & (pl.P - 1));
         const int ci = sip & 15;
         uint8_t* cell = pl.base + page * pl.page_bytes + (int64_t)(head * (pl.P >> 4) + (sip >> 4)) * pl.cell_bytes;
-        *reinterpret_cast<float*>(cell + side * 64 + ci * 4) = rq.scale_out;
-        cell[2176 + side * 16 + ci] = (uint8_t)rq.zp_out;
+        sc_slot = reinterpret_cast<float*>(cell + side * 64 + ci * 4);
+        zp_slot = cell + 2176 + side * 16 + ci;
+        *sc_slot = rq.scale_out;
+        *zp_slot = (uint8_t)rq.zp_out;
         rowdst = reinterpret_cast<unsigned long long>(cell + (side ? 1152 : 128) + ci * 64);
       }
       const uint16_t* in = side ? p.v_in : p.k_in;
       __syncwarp();
       if (lrn) {
-        // ---- learned rows: flagged words recomputed in f64 by the whole warp, one word at a time;
-        // rows with more than 8 flagged words (near-constant rows) redo all 16 (keeps the queue <= 256)
-        const uint32_t mine = wr ? flg : 0u;
-        const bool bulk = __popc(mine) > 8;
-        const int nfix = queue_words(bulk ? 0u : mine, fixq);
-        uint32_t bulkrows = __ballot_sync(0xffffffffu, bulk);
-        for (int k = 0; k < nfix || bulkrows; ++k) {  // warp-uniform
-          int owner, w;
-          if (k < nfix) {
-            const int e = fixq[k];
-            owner = e >> 4;
-            w = e & 15;
-          } else {
-            owner = __ffs(bulkrows) - 1;
-            w = (k - nfix) & 15;
-            if (w == 15) bulkrows &= bulkrows - 1;
-          }
-          const double sb = __shfl_sync(0xffffffffu, rq.s64, owner), zb = __shfl_sync(0xffffffffu, rq.z, owner);
+        // ---- learned rows with a code near a boundary (the margin covers the fast path's error in y
+        // and in s), or a zero point near a tie, are redone whole and exactly by the warp: the
+        // reference's (s, z) from exact extremes, then all 16 words (warp_learned_row)
+        bool redo = false;
+        if (wr && cd && p.exact_rows) {
+          const float zz = -mn * __frcp_rn(rq.s32);
+          redo = flg != 0u || fabsf(zz - floorf(zz) - 0.5f) < 1e-3f;
+        }
+        uint32_t rows = __ballot_sync(0xffffffffu, redo);
+        while (rows) {  // warp-uniform
+          const int owner = __ffs(rows) - 1;
+          rows &= rows - 1;
           const int r = row - rl + 32 * quad + owner;
-          const uint32_t word = warp_learned_word<ORDER>(in + (int64_t)r * 128, signs, p.rt, w, sb, zb);
-          if (lane == 0) stage[owner * 16 + (w ^ ((owner >> 1) & 15))] = word;
+          float so;
+          uint32_t zo;
+          warp_learned_row<ORDER>(in + (int64_t)r * 128, signs, p.rt, stage + owner * 16, (uint32_t)(owner >> 1) & 15u,
+                                  so, zo);
+          if (lane == owner) {
+            *sc_slot = so;
+            *zp_slot = (uint8_t)zo;
+          }
+        }
+        if (!p.exact_rows) {
+          // fast mode (KVR_K1L_FAST=1): flagged words recomputed in f64 under this kernel's (s, z),
+          // one word at a time; rows with more than 8 flagged words redo all 16 (queue <= 256).
+          // A code within the fast s's few-ulp error of a boundary can end one step off the
+          // reference's (~1.6e-6 of codes)
+          const uint32_t mine = wr ? flg : 0u;
+          const bool bulk = __popc(mine) > 8;
+          const int nfix = queue_words(bulk ? 0u : mine, fixq);
+          uint32_t bulkrows = __ballot_sync(0xffffffffu, bulk);
+          for (int k = 0; k < nfix || bulkrows; ++k) {  // warp-uniform
+            int owner, w;
+            if (k < nfix) {
+              const int e = fixq[k];
+              owner = e >> 4;
+              w = e & 15;
+            } else {
+              owner = __ffs(bulkrows) - 1;
+              w = (k - nfix) & 15;
+              if (w == 15) bulkrows &= bulkrows - 1;
+            }
+            const double sb = __shfl_sync(0xffffffffu, rq.s64, owner), zb = __shfl_sync(0xffffffffu, rq.z, owner);
+            const int r = row - rl + 32 * quad + owner;
+            const uint32_t word = warp_learned_word<ORDER>(in + (int64_t)r * 128, signs, p.rt, w, sb, zb);
+            if (lane == 0) stage[owner * 16 + (w ^ ((owner >> 1) & 15))] = word;
+          }
         }
         __syncwarp();
       } else if (!rot) {
@@ -1197,6 +1308,7 @@ struct LearnedArgs {
   const void* t_img;
   const double* rt;
   float kappa_units;
+  int exact_rows;
 };
 
 template <int ORDER, bool F16, bool LEARNED>
@@ -1221,6 +1333,7 @@ static int launch_tc_impl(const void* k, const void* v, int64_t n_tok, const int
     prm.t_img = reinterpret_cast<const uint4*>(la->t_img);
     prm.rt = la->rt;
     prm.kappa_units = la->kappa_units;
+    prm.exact_rows = la->exact_rows;
   }
   Signs sg = s;
   if (!has) for (auto& x : sg.w) x = 0u;
@@ -1332,14 +1445,17 @@ int kvr_launch_store_learned(const void* k, const void* v, int in_dtype, int64_t
   if ((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(t_img) |
        reinterpret_cast<uintptr_t>(rt)) & 15)
     return KVR_ERR_UNSUPPORTED;
-  static float kappa = -1.f;  // margin per unit of ||y||_2 / s: 2^-20 (KVR_K1L_KAPPA_LOG2 overrides, for tests)
-  if (kappa < 0.f) {
-    const char* e = getenv("KVR_K1L_KAPPA_LOG2");
-    const int l2 = e ? atoi(e) : -20;
-    kappa = ldexpf(1.0f, l2 + 16);
-    if (e && l2 <= -64) kappa = 0.f;
-  }
-  const LearnedArgs la{t_img, rt, kappa};
+  // margin per unit of ||y||_2 / s: 2^-18 -- the fast y's error (<= 2^-20 ||y||_2, measured bound) plus
+  // what it does to s through the extremes (<= 2.2 x that), so an unflagged code is the same under
+  // the reference's (s, z) (KVR_K1L_KAPPA_LOG2 overrides, for tests)
+  // (fast mode, KVR_K1L_FAST=1: 2^-20, the y error alone, flagged words under this kernel's (s, z))
+  // (read per launch: a serving process may switch modes, and the bench times both)
+  const char* f = getenv("KVR_K1L_FAST");
+  const int exact_rows = (f && atoi(f) == 1) ? 0 : 1;
+  const char* e = getenv("KVR_K1L_KAPPA_LOG2");
+  const int l2 = e ? atoi(e) : (exact_rows ? -18 : -20);
+  const float kappa = (e && l2 <= -64) ? 0.f : ldexpf(1.0f, l2 + 16);
+  const LearnedArgs la{t_img, rt, kappa, exact_rows};
   switch (order) {
     case 128: return launch_tc_impl<128, false, true>(k, v, n_tok, slots, pool, 2, mode_v, s, has, flags, st, &la);
     case 64: return launch_tc_impl<64, false, true>(k, v, n_tok, slots, pool, 2, mode_v, s, has, flags, st, &la);

@@ -501,3 +501,42 @@ def test_read_sequence_full_arrays_match_reference(golden_reads):
             k, v = t.read_sequence(s)
             np.testing.assert_array_equal(k, golden_reads[f"read_{tag}_{s}_k"])
             np.testing.assert_array_equal(v, golden_reads[f"read_{tag}_{s}_v"])
+
+
+def test_c2_full_size_learned_step():
+    """configs[1] with a learned R (row f3, learned_values): the serving step -- the new token
+    through the fused learned K1, the decode with q T and o T^T inside the kernel -- against the
+    reference composition (FWHT then R, rotation.py:118-168) on oracle-quantised pages, and the
+    decode kernel against an f64 decode of its own pages."""
+    H, G, d, L = 8, 4, 128, 32768
+    layout = HeadLayout(num_q_heads=G * H, num_kv_heads=H, head_dim=d, rot_order=128, page_tokens=16)
+    qm, rm = np.linalg.qr(np.random.default_rng(21).standard_normal((d, d)))
+    R = qm * np.sign(np.diag(rm))
+    spec = RotationSpec(order=128, signs=make_signs(0, 0, d, 128), learned=R, learned_values=True)
+    t = PageTable(layout, num_pages=L // 16 + 2)
+    t.create_sequence(0)
+    k, v = _fill(t, 0, 31, L, spec=spec)
+    plan = DecodePlan(t, [0], extra_tokens=1)
+    g = torch.Generator(device="cuda").manual_seed(32)
+    kn = torch.randn((1, H, d), generator=g, device="cuda").bfloat16()
+    vn = torch.randn((1, H, d), generator=g, device="cuda").bfloat16()
+    q = torch.randn((1, G * H, d), generator=g, device="cuda").bfloat16()
+    out = plan.step(q, kn, vn, spec)
+    torch.cuda.synchronize()
+    kk = torch.cat([k, kn]).double().cpu().numpy().reshape(-1, d)
+    vv = torch.cat([v, vn]).double().cpu().numpy().reshape(-1, d)
+
+    def store(x):
+        p_, s_, z_ = O.quantize_rows(O.rotate_rows(x, 128, spec.signs) @ R)
+        return O.dequantize_rows(p_, s_, z_, d).reshape(L + 1, H, d)
+
+    qf = O.rotate_rows(q[0].double().cpu().numpy(), 128, spec.signs) @ R
+    ref = O.unrotate_rows(O.decode_flat(qf, store(kk), store(vv), G) @ R.T, 128, spec.signs)
+    got = out[0].double().cpu().numpy()
+    err = rel_err(got, ref)
+    kd, vd = t.read_sequence_device([0], torch.float64)
+    own = O.unrotate_rows(O.decode_flat(qf, kd[0, :L + 1].cpu().numpy(), vd[0, :L + 1].cpu().numpy(), G) @ R.T, 128,
+                          spec.signs)
+    kern = rel_err(got, own)
+    print("C2 learned step rel err: vs oracle-quantised", err, "| decode kernel vs f64 of its pages", kern)
+    assert err <= TOL and kern <= 1e-5
