@@ -832,7 +832,7 @@ __device__ __noinline__ void warp_learned_row(const uint16_t* xrow, const Signs&
   }
 }
 
-template <int ORDER, bool F16, bool LEARNED>
+template <int ORDER, bool F16, bool LEARNED, bool XR = false>
 __global__ void __launch_bounds__(K1Cfg<LEARNED>::THREADS, 1)
     store_tc_kernel(const __grid_constant__ TcStoreParams p, const __grid_constant__ CUtensorMap map_k,
                     const __grid_constant__ CUtensorMap map_v, const __grid_constant__ Signs signs) {
@@ -1140,26 +1140,28 @@ __global__ void __launch_bounds__(K1Cfg<LEARNED>::THREADS, 1)
         // ---- learned rows with a code near a boundary (the margin covers the fast path's error in y
         // and in s), or a zero point near a tie, are redone whole and exactly by the warp: the
         // reference's (s, z) from exact extremes, then all 16 words (warp_learned_row)
-        bool redo = false;
-        if (wr && cd && p.exact_rows) {
-          const float zz = -mn * __frcp_rn(rq.s32);
-          redo = flg != 0u || fabsf(zz - floorf(zz) - 0.5f) < 1e-3f;
-        }
-        uint32_t rows = __ballot_sync(0xffffffffu, redo);
-        while (rows) {  // warp-uniform
-          const int owner = __ffs(rows) - 1;
-          rows &= rows - 1;
-          const int r = row - rl + 32 * quad + owner;
-          float so;
-          uint32_t zo;
-          warp_learned_row<ORDER>(in + (int64_t)r * 128, signs, p.rt, stage + owner * 16, (uint32_t)(owner >> 1) & 15u,
-                                  so, zo);
-          if (lane == owner) {
-            *sc_slot = so;
-            *zp_slot = (uint8_t)zo;
+        if constexpr (XR) {
+          bool redo = false;
+          if (wr && cd) {
+            const float zz = -mn * __frcp_rn(rq.s32);
+            redo = flg != 0u || fabsf(zz - floorf(zz) - 0.5f) < 1e-3f;
+          }
+          uint32_t rows = __ballot_sync(0xffffffffu, redo);
+          while (rows) {  // warp-uniform
+            const int owner = __ffs(rows) - 1;
+            rows &= rows - 1;
+            const int r = row - rl + 32 * quad + owner;
+            float so;
+            uint32_t zo;
+            warp_learned_row<ORDER>(in + (int64_t)r * 128, signs, p.rt, stage + owner * 16, (uint32_t)(owner >> 1) & 15u,
+                                    so, zo);
+            if (lane == owner) {
+              *sc_slot = so;
+              *zp_slot = (uint8_t)zo;
+            }
           }
         }
-        if (!p.exact_rows) {
+        if constexpr (!XR) {
           // fast mode (KVR_K1L_FAST=1): flagged words recomputed in f64 under this kernel's (s, z),
           // one word at a time; rows with more than 8 flagged words redo all 16 (queue <= 256).
           // A code within the fast s's few-ulp error of a boundary can end one step off the
@@ -1311,7 +1313,7 @@ struct LearnedArgs {
   int exact_rows;
 };
 
-template <int ORDER, bool F16, bool LEARNED>
+template <int ORDER, bool F16, bool LEARNED, bool XR = false>
 static int launch_tc_impl(const void* k, const void* v, int64_t n_tok, const int64_t* slots, const Pool& pool,
                           int rot_k, int rot_v, const Signs& s, int has, uint32_t* flags, cudaStream_t st,
                           const LearnedArgs* la = nullptr) {
@@ -1344,7 +1346,7 @@ static int launch_tc_impl(const void* k, const void* v, int64_t n_tok, const int
   if (kvr_encode_tensor_map_2d(&mv, v, 128, (uint64_t)prm.n_rows, 256, 64, Cfg::TM, CU_TENSOR_MAP_SWIZZLE_128B) !=
       CUDA_SUCCESS)
     return KVR_ERR_CUDA;
-  auto kern = store_tc_kernel<ORDER, F16, LEARNED>;
+  auto kern = store_tc_kernel<ORDER, F16, LEARNED, XR>;
   static bool attr_set[KVR_MAX_DEVICES];
   const int dev = kvr_current_device();
   if (!attr_set[dev]) {
@@ -1457,10 +1459,17 @@ int kvr_launch_store_learned(const void* k, const void* v, int in_dtype, int64_t
   const float kappa = (e && l2 <= -64) ? 0.f : ldexpf(1.0f, l2 + 16);
   const LearnedArgs la{t_img, rt, kappa, exact_rows};
   switch (order) {
-    case 128: return launch_tc_impl<128, false, true>(k, v, n_tok, slots, pool, 2, mode_v, s, has, flags, st, &la);
-    case 64: return launch_tc_impl<64, false, true>(k, v, n_tok, slots, pool, 2, mode_v, s, has, flags, st, &la);
-    case 32: return launch_tc_impl<32, false, true>(k, v, n_tok, slots, pool, 2, mode_v, s, has, flags, st, &la);
-    case 16: return launch_tc_impl<16, false, true>(k, v, n_tok, slots, pool, 2, mode_v, s, has, flags, st, &la);
+    // one instantiation per mode (the exact-row redo's registers cost the fast mode ~20 % when both
+    // paths sit in one kernel)
+#define KVR_LEARNED_CASE(O)                                                                                    \
+  case O:                                                                                                      \
+    return exact_rows ? launch_tc_impl<O, false, true, true>(k, v, n_tok, slots, pool, 2, mode_v, s, has, flags, st, &la) \
+                      : launch_tc_impl<O, false, true, false>(k, v, n_tok, slots, pool, 2, mode_v, s, has, flags, st, &la);
+    KVR_LEARNED_CASE(128)
+    KVR_LEARNED_CASE(64)
+    KVR_LEARNED_CASE(32)
+    KVR_LEARNED_CASE(16)
+#undef KVR_LEARNED_CASE
   }
   return KVR_ERR_UNSUPPORTED;
 }
