@@ -608,7 +608,6 @@ struct TcStoreParams {
   int32_t n_rows;          // n_tok * H per side
   int32_t tiles_per_side;  // ceil(n_rows / 128)
   int32_t rot_k, rot_v;    // tile modes: 0 plain, 1 block Hadamard, 2 learned (T)
-  int32_t exact_rows;      // learned: rows with a code near a boundary redone whole (reference (s, z))
   int32_t log2P;
   const uint4* t_img;      // learned: the SW128 image of T's three bf16 parts (kvr_learned_pack), 96 KB
   const double* rt;        // learned: R^T, f64 [128 n][128 k], for the exact recomputation
@@ -1310,7 +1309,6 @@ struct LearnedArgs {
   const void* t_img;
   const double* rt;
   float kappa_units;
-  int exact_rows;
 };
 
 template <int ORDER, bool F16, bool LEARNED, bool XR = false>
@@ -1335,7 +1333,6 @@ static int launch_tc_impl(const void* k, const void* v, int64_t n_tok, const int
     prm.t_img = reinterpret_cast<const uint4*>(la->t_img);
     prm.rt = la->rt;
     prm.kappa_units = la->kappa_units;
-    prm.exact_rows = la->exact_rows;
   }
   Signs sg = s;
   if (!has) for (auto& x : sg.w) x = 0u;
@@ -1457,7 +1454,7 @@ int kvr_launch_store_learned(const void* k, const void* v, int in_dtype, int64_t
   const char* e = getenv("KVR_K1L_KAPPA_LOG2");
   const int l2 = e ? atoi(e) : (exact_rows ? -18 : -20);
   const float kappa = (e && l2 <= -64) ? 0.f : ldexpf(1.0f, l2 + 16);
-  const LearnedArgs la{t_img, rt, kappa, exact_rows};
+  const LearnedArgs la{t_img, rt, kappa};
   switch (order) {
     // one instantiation per mode (the exact-row redo's registers cost the fast mode ~20 % when both
     // paths sit in one kernel)
