@@ -228,8 +228,11 @@ int kvr_rotate_quantize_store(const void* k, const void* v, int32_t in_dtype, in
  * Row f3, K1 with a learned R fused: y = x diag(s) H_blk R (rotation.py:118-142) for the K
  * rows and for V per value_branch_spec (rotation.py:162-168: learned_values=1 the same T,
  * 0 the Hadamard part only; targets KVR_KEYS_ONLY leaves V plain).  One tcgen05 kernel: T as
- * three bf16 parts in shared memory (24 mantissa bits), fp32 accumulation in TMEM, codes
- * within a margin of a rounding boundary recomputed in f64 (FWHT then R).
+ * three bf16 parts in shared memory (24 mantissa bits), fp32 accumulation in TMEM.  A row with
+ * a code within the margin of a rounding boundary (or a zero point near a tie) is redone whole
+ * in f64 (FWHT then R) under the reference's own scale and zero point, so codes and zero points
+ * equal the reference composition's.  KVR_K1L_FAST=1 (environment, read per call) recomputes only
+ * the flagged 8-code words under this kernel's scale: ~6x faster, ~1.5e-6 of codes one step off.
  *   t_img : device image of T, 98,304 bytes (kvr_learned_pack_image)
  *   r_t   : device R^T, f64 [d][d] row-major (r_t[n * d + k] = R[k][n])
  * Only bf16 rows, d = 128, T = 16, power-of-two pages: KVR_ERR_UNSUPPORTED otherwise (the
