@@ -43,5 +43,7 @@ if "--ncu" in sys.argv:
     t.store_slots(k, v, slots, spec_l)
     torch.cuda.synchronize()
     sys.exit(0)
-print(f"tokens {n_tok} kappa_log2 {os.environ.get('KVR_K1L_KAPPA_LOG2', '-17')}: learned {bench(spec_l):.2f} us, "
+fast = os.environ.get("KVR_K1L_FAST") == "1"
+kl = os.environ.get("KVR_K1L_KAPPA_LOG2", "-20" if fast else "-18")
+print(f"tokens {n_tok} mode {'fast' if fast else 'exact rows'} kappa_log2 {kl}: learned {bench(spec_l):.2f} us, "
       f"hadamard {bench(spec_h):.2f} us")
