@@ -453,6 +453,9 @@ constexpr int RING_CELLS = 4;    // cells in flight per warp (NSTG stages of C c
 #ifndef KVR_PREWAIT_GROUPS
 #define KVR_PREWAIT_GROUPS 1
 #endif
+#ifndef KVR_PREWAIT_GROUPS_LL
+#define KVR_PREWAIT_GROUPS_LL 2
+#endif
 #ifndef KVR_EVICT_FIRST
 #define KVR_EVICT_FIRST 1
 #endif
@@ -2258,6 +2261,10 @@ int kvr_launch_decode(const void* q, int q_dtype, const Pool& pool, const int32_
     // flag-in-data merge when the grid is one wave (the merger CTAs spin on the others' words)
     p.merge_ll = KVR_MERGE_LL && p.merge_inline && ws_has_ll(batch, pool.H, splits) && ll_end <= ws_bytes &&
                  (long)batch * pool.H * splits <= (kvr_num_sms() > 0 ? kvr_num_sms() : 148) && p.G <= 8;
+    // the one-wave flag-in-data grids (C2-like: a short stream per CTA, the step a latency chain) take
+    // their whole ring before the wait (C2 step 14.1 -> 13.9 us); the long streams keep one group
+    // (a full-ring burst there queues the query load behind it: C5 1M +2 %)
+    if (p.pre_groups > 0 && p.merge_ll) p.pre_groups = KVR_PREWAIT_GROUPS_LL;
     if (lq) return p.G == 8 ? launch_sel<2, 0, false>(grid, smem, st, p, sg) : launch_sel<1, 0, false>(grid, smem, st, p, sg);
     if (new_slot)
       return p.G == 8 ? launch_tma<2, true>(p, sg, grid, smem, ord, st) : launch_tma<1, true>(p, sg, grid, smem, ord, st);
